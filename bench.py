@@ -1,0 +1,384 @@
+"""bench.py -- one step of the selected-CI hot path (QiankunNet-cuSCI,
+arXiv 2604.15768) on N B200s:
+
+    for each parent batch of this rank's shard:
+        gen_coupled(batch, integrals, eps)      # coupled configs + H_ij (a1-a7)
+        dedup_global(records.keys)              # global de-dup (a8-a11), NCCL when N > 1
+        merge_space(unique_pool, U_batch)       # GPU-resident union of the unique set
+    merge_space(space_pool, unique_pool)        # S <- S u C (a12)
+
+Workload (default, --workload n2): the N2 cc-pVDZ-like configuration of
+BASELINE.json (56 spin orbitals, 14 electrons, 10^6 parents, synthetic
+D2h-like integrals, eps = 0); parents are sharded across ranks by hash owner
+(strong scaling: fixed total work).  Prints ONE JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "coupled configs/sec (with H_ij) and unique configs/sec after global dedup, 1/2/4/8 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="n2")
+    ap.add_argument("--parents", type=int, default=None, help="override the workload's parent count")
+    ap.add_argument("--batch", type=int, default=None, help="parents per gen_coupled call")
+    ap.add_argument("--eps", type=float, default=0.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=None, help="parents in the oracle's bounded sample")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.idx = device_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- distributed
+def dist_setup(gpus: int):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != gpus:
+        raise SystemExit(f"--gpus {gpus} but WORLD_SIZE={world}")
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+    return rank, world, local, pg
+
+
+def bcast_bytes(pg, payload: bytes | None, rank: int) -> bytes:
+    if pg is None:
+        return payload
+    obj = [payload if rank == 0 else None]
+    pg.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def allreduce_max(pg, x: float) -> float:
+    if pg is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    return float(t.item())
+
+
+def allreduce_sum(pg, x: float) -> float:
+    if pg is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    pg.all_reduce(t, op=pg.ReduceOp.SUM)
+    return float(t.item())
+
+
+def barrier(pg):
+    if pg is not None:
+        pg.barrier()
+
+
+# ----------------------------------------------------------------------------- oracle (cpu baseline)
+def oracle_sample(wl, ints, par, n_sample: int):
+    """The oracle as it stands, single host thread, on a bounded sample of the
+    workload: the first n_sample parents through gen -> dedup -> merge."""
+    import oracle
+    sample = par[:n_sample]
+    t0 = time.perf_counter()
+    rec = oracle.gen_coupled(wl.m, wl.n_alpha, wl.n_beta, sample, ints, 0.0)
+    u = oracle.dedup(rec["keys"], wl.words)
+    s2, ins = oracle.merge(sample, u, wl.words)
+    dt = time.perf_counter() - t0
+    return len(rec["src"]), len(u), dt
+
+
+def default_cpu_sample(wl) -> int:
+    return {"lih": 225, "h2o": 4000, "h2o_dense": 1000, "n2": 1000, "c2h4": 40, "m120": 4}.get(wl, 100)
+
+
+def run_reference(args):
+    """--impl reference: the oracle (the one reference this tier has), timed as
+    it stands on the host cores, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import synth
+    # bounded: ~15 s of oracle work per step at --steps 5, shrunk for longer runs
+    n_sample = args.cpu_sample or max(1, int(default_cpu_sample(args.workload) * min(1.0, 5.0 / max(1, args.steps))))
+    wl, ints, par = synth.workload_inputs(args.workload, n_parents=max(n_sample, 1) if args.parents is None else args.parents)
+    for _ in range(args.warmup):
+        oracle_sample(wl, ints, par, max(1, n_sample // 10))
+    recs, uniq, times = 0, 0, []
+    for _ in range(args.steps):
+        r, u, dt = oracle_sample(wl, ints, par, n_sample)
+        recs, uniq = r, u
+        times.append(dt)
+    t = sum(times) / len(times)
+    value = recs / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "coupled configs/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{wl.name} ({args.workload})", "m": wl.m, "n_alpha": wl.n_alpha,
+                   "n_beta": wl.n_beta, "point_group_irreps": wl.g, "parents": n_sample, "eps": 0.0},
+        "unique_configs_per_s": uniq / t,
+        "cpu_baseline": {"value": value, "unit": "coupled configs/s", "cores": 1, "kind": "oracle",
+                         "sample": f"{n_sample} parents (first distinct sampler draws) of the {args.workload} workload through "
+                                   f"oracle gen -> std::set dedup -> set_union merge ({recs} records, {uniq} unique)"},
+        "e2e": {"value": value, "unit": "coupled configs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- ours
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+
+    import paper_2604_15768_b200 as P
+    import synth
+
+    rank, world, local, pg = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    nid = bcast_bytes(pg, P.Context.nccl_unique_id() if (world > 1 and rank == 0) else None, rank)
+    ctx = P.Context(local, rank, world, nccl_id=nid)
+    stream = ctx.stream
+
+    wl, ints, par_all = synth.workload_inputs(args.workload, n_parents=args.parents)
+    sp = P.Space(wl.m, wl.n_alpha, wl.n_beta)
+    W = wl.words
+    di = P.DeviceIntegrals(ints.h, ints.eri, dev)
+    # shard the parent set by hash owner (the same owner function as the pool)
+    mine = np.array_split(par_all, world)[rank]
+    shard = ctx.dedup_global(sp, torch.from_numpy(mine).to(dev))   # parents owned by this rank (sorted)
+    n_par = int(shard.shape[0])
+    batch = args.batch or {"n2": 250_000, "c2h4": 20_000}.get(args.workload, max(1, n_par))
+    batch = max(1, min(batch, n_par))
+    batches = [(i, min(i + batch, n_par)) for i in range(0, n_par, batch)]
+    # plan: exact record counts per batch (buffer sizing; outside the timed region)
+    counts = [ctx.gen_coupled_count(sp, shard[a:b], di, args.eps) for a, b in batches]
+    cap = max(counts) if counts else 1
+    keys_buf = torch.empty((cap, W), dtype=torch.uint64, device=dev)
+    hij_buf = torch.empty(cap, dtype=torch.float64, device=dev)
+    src_buf = torch.empty(cap, dtype=torch.int32, device=dev)
+    out = P.Records(keys_buf, hij_buf, src_buf, None, cap)
+    shard_host = shard.cpu().numpy()
+    shard_pinned = torch.from_numpy(shard_host).pin_memory()
+
+    def step(parents_dev, e2e=False):
+        """one pass of the hot path; returns (records, unique, space_size)."""
+        nrec = 0
+        upool = ctx.pool(sp, 1 << 20)
+        for (a, b) in batches:
+            rec = ctx.gen_coupled(sp, parents_dev[a:b], di, args.eps, out=out)
+            nrec += rec.count
+            u = ctx.dedup_global(sp, rec.keys)
+            ctx.merge_space(upool, u)
+            del u
+        spool = ctx.pool(sp, 1 << 20)
+        ctx.merge_space(spool, parents_dev)
+        ctx.merge_space(spool, upool.keys())
+        n_unique, n_space = len(upool), len(spool)
+        upool.close()
+        spool.close()
+        return nrec, n_unique, n_space
+
+    # warm-up
+    for _ in range(args.warmup):
+        step(shard)
+    torch.cuda.synchronize()
+
+    # ---------------- timed region (device-resident inputs)
+    clocks = ClockSampler(local)
+    clocks.start()
+    ctx.profile(True)
+    ctx.profile_read()
+    launches0 = ctx.kernel_launches
+    barrier(pg)
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    tot_rec = tot_uni = 0
+    for _ in range(args.steps):
+        r, u, s = step(shard)
+        tot_rec += r
+        tot_uni += u
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier(pg)
+    ms_local = ev0.elapsed_time(ev1)
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    launches = ctx.kernel_launches - launches0
+    clk = clocks.stop()
+    ms = allreduce_max(pg, ms_local)
+    recs_all = allreduce_sum(pg, tot_rec)
+    uni_all = allreduce_sum(pg, tot_uni)
+    value = recs_all / (ms / 1e3)
+    unique_rate = uni_all / (ms / 1e3)
+
+    # ---------------- e2e: host parents (pinned) -> device inside the region, count read back
+    e2e = None
+    if not args.no_e2e:
+        barrier(pg)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        er = 0
+        for _ in range(args.steps):
+            pd = torch.empty_like(shard)
+            pd.copy_(shard_pinned, non_blocking=True)
+            r, u, s = step(pd, e2e=True)
+            res = torch.tensor([r, u, s], dtype=torch.int64).to(dev).cpu()   # result read back (D2H)
+            er += int(res[0])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier(pg)
+        ems = allreduce_max(pg, e0.elapsed_time(e1))
+        e2e = {"value": allreduce_sum(pg, er) / (ems / 1e3), "unit": "coupled configs/s",
+               "h2d_bytes_per_step": int(shard_pinned.numel() * 8 + ints.h.nbytes * 0),
+               "d2h_bytes_per_step": 24}
+
+    # ---------------- roofline of the dominant kernel class
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    dom = max(prof.items(), key=lambda kv: kv[1][0]) if prof else ("none", (0.0, 0))
+    rec_bytes = 8 * W + 8 + 4
+    # algorithmic bytes per step for each kernel class
+    per_step_rec = tot_rec / max(args.steps, 1)
+    alg = {
+        "gen": per_step_rec * rec_bytes + n_par * 8 * W,
+        "hash_filter": per_step_rec * 8 * W,
+    }
+    dname, (dms, dlaunch) = dom
+    roof = None
+    if dname in alg and dlaunch:
+        per_launch_bytes = alg[dname] * args.steps / dlaunch
+        per_launch_s = dms / dlaunch / 1e3
+        achieved = per_launch_bytes / per_launch_s / 1e9
+        roof = {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": None, "peak_source": peak_src}
+    gen_ms, gen_l = prof.get("gen", (0.0, 0))
+    gen_bytes = alg["gen"] * args.steps
+    gen_roof = None
+    if gen_l:
+        ach = gen_bytes / (gen_ms / 1e3) / 1e9
+        gen_roof = {"achieved": ach, "frac": ach / hbm_peak, "records_per_s_kernel": tot_rec / (gen_ms / 1e3)}
+    if roof is None and gen_roof is not None:
+        roof = {"bound": "hbm", "kernel": "gen", "achieved": gen_roof["achieved"], "peak": hbm_peak, "unit": "GB/s",
+                "frac": gen_roof["frac"], "traffic": None, "peak_source": peak_src}
+
+    # ---------------- cpu baseline (oracle, rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        n_sample = args.cpu_sample or default_cpu_sample(args.workload)
+        _, _, par_s = synth.workload_inputs(args.workload, n_parents=n_sample)
+        r, u, dt = oracle_sample(wl, ints, par_s, n_sample)
+        cpu = {"value": r / dt, "unit": "coupled configs/s", "cores": 1, "kind": "oracle",
+               "sample": f"{n_sample} parents (first distinct sampler draws) of the workload through oracle gen -> std::set dedup -> "
+                         f"set_union merge ({r} records, {u} unique, {dt:.1f} s)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "coupled configs/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{wl.name} ({args.workload})", "m": wl.m, "n_alpha": wl.n_alpha,
+                       "n_beta": wl.n_beta, "point_group_irreps": wl.g, "parents": int(len(par_all)),
+                       "parents_per_batch": batch, "eps": args.eps, "records_per_step": int(recs_all / args.steps),
+                       "unique_per_step": int(uni_all / args.steps),
+                       "parallelism": f"dp{world} (hash-owner shards, NCCL all-to-all-v)",
+                       "l2": "inputs larger than L2 (records per batch >> 126 MB)"},
+            "unique_configs_per_s": unique_rate,
+            "redundancy": 1.0 - uni_all / max(recs_all, 1),
+            "roofline": roof,
+            "gen_kernel": gen_roof,
+            "kernel_ms_per_step": {k: v[0] / args.steps for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if pg is not None:
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

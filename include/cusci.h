@@ -1,0 +1,194 @@
+/* cusci.h -- C ABI of libcusci, the B200-native (sm_100a) selected-CI hot path
+ * of QiankunNet-cuSCI (arXiv 2604.15768):
+ *
+ *     gen_coupled(parents, integrals, threshold) -> dedup_global(configs) -> merge_space(space, new)
+ *
+ * Citations: "P:L" = /reference PAPER.md line L, "S:L" = SPEC.md line L.
+ *
+ * Conventions (readings r1-r9):
+ *   - A configuration (determinant) over m spin orbitals is `words` uint64
+ *     words, words = 1 if m <= 64 else 2 (m <= 128).  Spin orbital t lives in
+ *     word t/64 at bit t%64.  Spin orbitals are interleaved:
+ *     t = 2P + sigma, sigma 0 = alpha, 1 = beta; P = t/2 is the spatial index.
+ *   - Key arrays are row-major [n][words]; keys are ordered as one big
+ *     unsigned integer with word (words-1) most significant.
+ *   - Integrals are real fp64: h[K*K] (symmetric, row-major) and the
+ *     two-electron integrals (PQ|RS) in chemist notation, 8-fold packed:
+ *       ij = max(P,Q)(max(P,Q)+1)/2 + min(P,Q);  idx = max(ij,kl)(max(ij,kl)+1)/2 + min(ij,kl).
+ *
+ * Memory: unless stated otherwise every array pointer is a DEVICE pointer on
+ * the context's device.  Every call is ordered on the context's CUDA stream;
+ * calls that return a count synchronise that stream before returning.
+ * Inputs are caller-owned and read-only during the call; the library never
+ * frees caller memory.  Outputs of dedup_global / merge_space(inserted) are
+ * allocated with the context's allocator callback (cudaMallocAsync when no
+ * callback is given) and ownership passes to the caller (free with the
+ * matching free callback, or cusci_free when none was given).
+ *
+ * Errors: every entry point returning int returns 0 on success or one of the
+ * CUSCI_E_* codes below; cusci_last_error(ctx) returns a one-line message.
+ * A context that returned CUSCI_E_NCCL or CUSCI_E_CUDA is unusable
+ * (the communicator has been aborted); destroy it.
+ */
+#ifndef CUSCI_H
+#define CUSCI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CUSCI_OK 0
+#define CUSCI_E_INVALID_ARG 1    /* m not in [2,128]; words mismatch; n_alpha+n_beta > m; eps < 0 or NaN; NULL required pointer */
+#define CUSCI_E_INVALID_PARENT 2 /* a parent with a bit >= m or spin popcounts != (n_alpha, n_beta) */
+#define CUSCI_E_CAPACITY 3       /* output capacity too small: *count holds the true total; retry with a larger buffer */
+#define CUSCI_E_CUDA 4           /* CUDA runtime error */
+#define CUSCI_E_NCCL 5           /* NCCL error (communicator aborted; all ranks report it) */
+#define CUSCI_E_OOM 6            /* device scratch allocation failed */
+
+typedef struct cusci_ctx cusci_ctx;    /* device, stream, NCCL comm, allocator, workspace, cached Hamiltonian prep */
+typedef struct cusci_pool cusci_pool;  /* GPU-resident owned shard of the configuration space S (sorted, unique) */
+
+typedef struct {
+  int32_t m;        /* spin orbitals, 2 <= m <= 128, m even (m = 2K) */
+  int32_t n_alpha;  /* electrons on even (alpha) spin orbitals */
+  int32_t n_beta;   /* electrons on odd (beta) spin orbitals */
+  int32_t words;    /* must equal (m <= 64 ? 1 : 2) */
+} cusci_space;
+
+typedef struct {
+  int32_t n_spatial;  /* K = m/2 */
+  const double* h;    /* device, [K*K] */
+  const double* eri;  /* device, packed 8-fold, [npair(npair+1)/2], npair = K(K+1)/2 */
+} cusci_integrals;
+
+typedef struct {
+  uint64_t* keys;     /* device, [capacity][words]   target configuration j          (required) */
+  double* hij;        /* device, [capacity]          H_ij (fp64), |H_ij| > threshold (required) */
+  uint32_t* src;      /* device, [capacity]          index of the parent i in `parents` (nullable) */
+  int8_t* phase;      /* device, [capacity]          fermionic phase +-1 of the excitation (nullable) */
+  uint64_t capacity;  /* records the buffers hold */
+  uint64_t count;     /* OUT (host): number of records produced (the true total on CUSCI_E_CAPACITY) */
+} cusci_records;
+
+typedef struct {
+  uint64_t* keys;   /* device, [count][words]; allocated by the library, owned by the caller */
+  uint64_t count;
+} cusci_keys;
+
+/* Allocator callbacks (e.g. backed by the torch caching allocator).  alloc must
+ * return a device pointer aligned to >= 256 bytes, usable on `stream`, or NULL. */
+typedef void* (*cusci_alloc_fn)(size_t bytes, void* stream, void* user);
+typedef void (*cusci_free_fn)(void* ptr, void* user);
+
+/* ---- lifecycle ------------------------------------------------------------ */
+
+/* Writes a fresh 128-byte NCCL unique id to host memory `out128` (call on rank
+ * 0, then broadcast it to all ranks, e.g. with torch.distributed). */
+int cusci_nccl_unique_id(void* out128);
+
+/* Create a context on `device` for rank `rank` of `world` (world >= 1).
+ * nccl_unique_id: host pointer to the 128-byte id (required iff world > 1;
+ * collective over all ranks when world > 1).  cuda_stream: a cudaStream_t on
+ * `device` (NULL = a library-owned non-blocking stream).  alloc/free: output
+ * allocator (both NULL = cudaMallocAsync / cudaFreeAsync on the stream). */
+int cusci_init(cusci_ctx** ctx, int device, int rank, int world, const void* nccl_unique_id,
+               void* cuda_stream, cusci_alloc_fn alloc, cusci_free_fn free_fn, void* alloc_user);
+void cusci_finalize(cusci_ctx* ctx);
+const char* cusci_last_error(const cusci_ctx* ctx);
+/* Drop the cached Hamiltonian prep (call after mutating integrals in place). */
+void cusci_invalidate_integrals(cusci_ctx* ctx);
+/* Free a library-allocated output when the context has no free callback. */
+void cusci_free(cusci_ctx* ctx, void* ptr);
+/* Number of kernels this context has launched (instrumentation). */
+uint64_t cusci_kernel_launches(const cusci_ctx* ctx);
+/* Per-kernel-class CUDA-event profiler (instrumentation for bench.py): when
+ * enabled, every library launch is bracketed by an event pair on the context
+ * stream.  cusci_profile_read synchronises the stream, writes the summed
+ * milliseconds and launch counts per class into ms[n_tags] / launches[n_tags]
+ * (class ids: 0 prep, 1 validate, 2 gen, 3 hash filter, 4 owner scatter,
+ * 5 radix upsweep, 6 radix downsweep, 7 scan, 8 unique, 9 merge split,
+ * 10 merge tile, 11 sorted check, 12 NCCL exchange, 13 memset) and clears the log. */
+void cusci_profile_enable(cusci_ctx* ctx, int on);
+int cusci_profile_read(cusci_ctx* ctx, double* ms, uint64_t* launches, int n_tags);
+
+/* ---- step 1: coupled generation ------------------------------------------ */
+
+/* Upper bound on the records gen_coupled can emit for n_parents parents: the
+ * dense closed form per parent, sum_s n_s v_s + sum_s C(n_s,2) C(v_s,2)
+ * + n_a v_a n_b v_b, times n_parents (SURVEY 8 "closed forms"). Host only. */
+uint64_t gen_coupled_bound(const cusci_space* sp, uint64_t n_parents);
+
+/* For every parent i (device, [n_parents][words]) emit every configuration j
+ * of the coupled set C_i (Eq. 4): all spin-conserving single
+ * (p->a) and double (p<q -> a<b) excitations, with the Slater-Condon element
+ * (Sec 4.2.1)
+ *     single: H = ph * (h_PA + sum_{k in occ(i)\p, ascending} [(PA|KK) - [s_k = s_p] (PK|KA)])
+ *     double: H = ph * <pq||ab>,  <pq||ab> = d1 - d2 | d1 | -d2 with
+ *             d1 = (PA|QB) [s_p=s_a, s_q=s_b], d2 = (PB|QA) [s_p=s_b, s_q=s_a]
+ * and ph the fermionic phase of sequential singles p->a then q->b,
+ * keeping the record iff |H| > threshold (strict; Alg. 1 line 12).
+ * The diagonal is not emitted.  Records are written compactly (no gaps)
+ * into `out`; the order of parents' record blocks is unspecified, the records
+ * of one parent are contiguous.  threshold >= 0 (NaN rejected).
+ * Parents are validated on device before anything is written
+ * (CUSCI_E_INVALID_PARENT, the message names the first bad index).
+ * If the total exceeds out->capacity, nothing beyond capacity is written,
+ * out->count = true total and CUSCI_E_CAPACITY is returned.
+ * The Hamiltonian prep (pair tables) is built on first use and cached per
+ * (h, eri, K, threshold). */
+int gen_coupled(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* parents, uint64_t n_parents,
+                const cusci_integrals* ints, double threshold, cusci_records* out);
+
+/* Exact record count gen_coupled would produce (no records written). */
+int gen_coupled_count(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* parents, uint64_t n_parents,
+                      const cusci_integrals* ints, double threshold, uint64_t* count);
+
+/* ---- step 2: global de-duplication (COLLECTIVE when world > 1) ------------ */
+
+/* Global de-duplication of the union over all ranks of `configs` (device,
+ * [n][words]) (Sec 2.2; Sec 4.1.1): local unique filter
+ * (P:380-382), hash-owner partition owner(j) = floor(mix(j) * world / 2^64)
+ * (DESIGN.md r9), one all-to-all exchange over NCCL, local radix sort
+ * + unique.  On return owned_unique holds, sorted ascending, exactly the
+ * distinct keys j of the global union with owner(j) == rank.  Every rank must
+ * call it with the same cusci_space; argument errors are agreed across ranks
+ * before any data moves. */
+int dedup_global(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* configs, uint64_t n,
+                 cusci_keys* owned_unique);
+
+/* The two local halves of dedup_global, exposed for logical-rank tests and
+ * custom transports:
+ *   dedup_partition: local unique filter + owner partition into n_owners bins;
+ *     bins->keys holds the bins back to back (bin r first at offset
+ *     sum_{r'<r} counts[r']); counts (HOST, [n_owners]) receives the sizes.
+ *   dedup_finalize: sort + unique of a received buffer (device, [n][words]). */
+int dedup_partition(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* configs, uint64_t n,
+                    int n_owners, cusci_keys* bins, uint64_t* counts);
+int dedup_finalize(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* keys, uint64_t n,
+                   cusci_keys* unique_sorted);
+
+/* ---- step 3: the GPU-resident configuration pool --------------------------- */
+
+/* Create an empty pool (capacity = initial key capacity; it grows). */
+int cusci_pool_create(cusci_ctx* ctx, const cusci_space* sp, uint64_t capacity, cusci_pool** out);
+/* Read-only view of the pool's sorted unique keys; valid until the next merge_space. */
+int cusci_pool_view(const cusci_pool* pool, const uint64_t** keys, uint64_t* count);
+/* Copy the pool's keys into dst (device, capacity_keys >= count), stream-ordered. */
+int cusci_pool_copy(const cusci_pool* pool, uint64_t* dst, uint64_t capacity_keys);
+void cusci_pool_destroy(cusci_pool* pool);
+
+/* S <- S u new (Sec 2.2).  new_keys (device,
+ * [n_new][words]) must be sorted ascending and unique (as returned by
+ * dedup_global on this rank; CUSCI_E_INVALID_ARG otherwise).  If `inserted`
+ * is non-NULL it receives new \ S_old, sorted.  Local: the pool shard and the
+ * new keys share the owner function, so no communication is needed. */
+int merge_space(cusci_ctx* ctx, cusci_pool* space, const uint64_t* new_keys, uint64_t n_new,
+                cusci_keys* inserted);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CUSCI_H */

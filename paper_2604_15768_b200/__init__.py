@@ -1,0 +1,307 @@
+"""paper_2604_15768_b200 -- B200-native selected-CI hot path (QiankunNet-cuSCI,
+arXiv 2604.15768): gen_coupled -> dedup_global -> merge_space.
+
+Thin Python binding over the C ABI of libcusci.so (include/cusci.h): argument
+marshalling only, every step runs in the library's sm_100a kernels.  PyTorch
+supplies device memory (through the allocator callback), streams and process
+groups.  There is no CPU fallback: importing this package on a machine without
+the built library raises, and every call needs a CUDA device.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+from ._lib import CUSCI_ERRORS, CusciError, lib, LIB_PATH  # noqa: F401
+
+__all__ = ["Space", "DeviceIntegrals", "Context", "Pool", "Records", "CusciError", "LIB_PATH",
+           "gen_coupled_bound"]
+
+
+class _Space(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_int32), ("n_alpha", ctypes.c_int32), ("n_beta", ctypes.c_int32),
+                ("words", ctypes.c_int32)]
+
+
+class _Integrals(ctypes.Structure):
+    _fields_ = [("n_spatial", ctypes.c_int32), ("h", ctypes.c_void_p), ("eri", ctypes.c_void_p)]
+
+
+class _Records(ctypes.Structure):
+    _fields_ = [("keys", ctypes.c_void_p), ("hij", ctypes.c_void_p), ("src", ctypes.c_void_p),
+                ("phase", ctypes.c_void_p), ("capacity", ctypes.c_uint64), ("count", ctypes.c_uint64)]
+
+
+class _Keys(ctypes.Structure):
+    _fields_ = [("keys", ctypes.c_void_p), ("count", ctypes.c_uint64)]
+
+
+class Space:
+    """m spin orbitals (interleaved alpha/beta), n_alpha / n_beta electrons."""
+
+    def __init__(self, m: int, n_alpha: int, n_beta: int):
+        self.m, self.n_alpha, self.n_beta = int(m), int(n_alpha), int(n_beta)
+        self.words = 1 if self.m <= 64 else 2
+
+    def _c(self) -> _Space:
+        return _Space(self.m, self.n_alpha, self.n_beta, self.words)
+
+    def __repr__(self):
+        return f"Space(m={self.m}, n_alpha={self.n_alpha}, n_beta={self.n_beta}, words={self.words})"
+
+
+class DeviceIntegrals:
+    """h [K,K] and packed (PQ|RS) as float64 CUDA tensors (kept alive here)."""
+
+    def __init__(self, h, eri, device="cuda"):
+        self.h = torch.as_tensor(h, dtype=torch.float64).to(device).contiguous()
+        self.eri = torch.as_tensor(eri, dtype=torch.float64).to(device).contiguous()
+        self.n_spatial = int(self.h.shape[0])
+
+    def _c(self) -> _Integrals:
+        return _Integrals(self.n_spatial, self.h.data_ptr(), self.eri.data_ptr())
+
+
+def gen_coupled_bound(space: Space, n_parents: int) -> int:
+    sp = space._c()
+    return int(lib().gen_coupled_bound(ctypes.byref(sp), int(n_parents)))
+
+
+class Records:
+    """Output of gen_coupled: keys uint64 [count, W], hij float64 [count],
+    src uint32-as-int32 [count] (or None), phase int8 [count] (or None)."""
+
+    def __init__(self, keys, hij, src, phase, count):
+        self.keys, self.hij, self.src, self.phase, self.count = keys, hij, src, phase, count
+
+
+_ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+_FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p)
+
+
+def _as_u64_2d(t: torch.Tensor, W: int) -> torch.Tensor:
+    if t.dtype != torch.uint64:
+        raise TypeError("configuration keys must be torch.uint64")
+    if not t.is_cuda:
+        raise ValueError("configuration keys must be a CUDA tensor")
+    return t.reshape(-1, W).contiguous()
+
+
+class Context:
+    """One library context per (process, GPU): stream, NCCL communicator,
+    output allocator (torch caching allocator), cached Hamiltonian prep."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
+                 stream: torch.cuda.Stream | None = None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2604_15768_b200 needs a CUDA device (no CPU fallback)")
+        self.device = torch.device("cuda", device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self._live: dict[int, torch.Tensor] = {}
+
+        def _alloc(nbytes, _stream, _user):
+            try:
+                with torch.cuda.stream(self.stream):
+                    t = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
+            except RuntimeError:
+                return None
+            p = t.data_ptr()
+            self._live[p] = t
+            return p
+
+        def _free(ptr, _user):
+            self._live.pop(ptr, None)
+
+        self._alloc_cb = _ALLOC_FN(_alloc)
+        self._free_cb = _FREE_FN(_free)
+        idbuf = None
+        if world > 1:
+            if nccl_id is None or len(nccl_id) != 128:
+                raise ValueError("world > 1 needs the 128-byte NCCL unique id")
+            idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        ctx = ctypes.c_void_p()
+        rc = lib().cusci_init(ctypes.byref(ctx), device, rank, world, idbuf, ctypes.c_void_p(self.stream.cuda_stream),
+                              self._alloc_cb, self._free_cb, None)
+        if rc != 0:
+            raise CusciError(rc, "cusci_init failed")
+        self._ctx = ctx
+        self.rank, self.world = rank, world
+
+    # ------------------------------------------------------------------ plumbing
+    def close(self):
+        if getattr(self, "_ctx", None):
+            lib().cusci_finalize(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc: int, what: str):
+        if rc != 0:
+            msg = lib().cusci_last_error(self._ctx).decode(errors="replace")
+            raise CusciError(rc, f"{what}: {msg}")
+
+    def _take(self, ptr: int | None, count: int, W: int) -> torch.Tensor:
+        if not ptr:
+            return torch.empty((0, W), dtype=torch.uint64, device=self.device)
+        t = self._live.pop(ptr)
+        return t.view(torch.uint64)[: count * W].view(count, W)
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(lib().cusci_kernel_launches(self._ctx))
+
+    def profile(self, on: bool = True):
+        """Enable/disable the library's per-kernel-class CUDA-event profiler."""
+        lib().cusci_profile_enable(self._ctx, 1 if on else 0)
+
+    def profile_read(self) -> dict:
+        """{kernel class: (milliseconds, launches)} since the last read."""
+        from ._lib import PROFILE_TAGS
+        n = len(PROFILE_TAGS)
+        ms = (ctypes.c_double * n)()
+        cnt = (ctypes.c_uint64 * n)()
+        self._check(lib().cusci_profile_read(self._ctx, ms, cnt, n), "cusci_profile_read")
+        return {t: (ms[i], int(cnt[i])) for i, t in enumerate(PROFILE_TAGS) if cnt[i]}
+
+    def invalidate_integrals(self):
+        lib().cusci_invalidate_integrals(self._ctx)
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        rc = lib().cusci_nccl_unique_id(buf)
+        if rc != 0:
+            raise CusciError(rc, "ncclGetUniqueId failed")
+        return buf.raw
+
+    # ------------------------------------------------------------------ step 1
+    def gen_coupled(self, space: Space, parents: torch.Tensor, ints: DeviceIntegrals, threshold: float = 0.0,
+                    capacity: int | None = None, with_src: bool = True, with_phase: bool = False,
+                    out: Records | None = None) -> Records:
+        """Coupled configurations of every parent with H_ij (include/cusci.h gen_coupled).
+        `out` (optional) supplies preallocated buffers (keys [cap, W], hij [cap], src, phase)."""
+        W = space.words
+        par = _as_u64_2d(parents, W)
+        n = par.shape[0]
+        if out is None:
+            if capacity is None:
+                capacity = self.gen_coupled_count(space, par, ints, threshold)
+            cap = int(capacity)
+            keys = torch.empty((cap, W), dtype=torch.uint64, device=self.device)
+            hij = torch.empty(cap, dtype=torch.float64, device=self.device)
+            src = torch.empty(cap, dtype=torch.int32, device=self.device) if with_src else None
+            phase = torch.empty(cap, dtype=torch.int8, device=self.device) if with_phase else None
+        else:
+            keys, hij, src, phase = out.keys, out.hij, out.src, out.phase
+            cap = int(keys.shape[0])
+        rec = _Records(keys.data_ptr(), hij.data_ptr(), src.data_ptr() if src is not None else None,
+                       phase.data_ptr() if phase is not None else None, cap, 0)
+        sp, ci = space._c(), ints._c()
+        rc = lib().gen_coupled(self._ctx, ctypes.byref(sp), ctypes.c_void_p(par.data_ptr()), n, ctypes.byref(ci),
+                               float(threshold), ctypes.byref(rec))
+        self._check(rc, "gen_coupled")
+        c = int(rec.count)
+        return Records(keys[:c], hij[:c], src[:c] if src is not None else None,
+                       phase[:c] if phase is not None else None, c)
+
+    def gen_coupled_count(self, space: Space, parents: torch.Tensor, ints: DeviceIntegrals,
+                          threshold: float = 0.0) -> int:
+        par = _as_u64_2d(parents, space.words)
+        cnt = ctypes.c_uint64(0)
+        sp, ci = space._c(), ints._c()
+        rc = lib().gen_coupled_count(self._ctx, ctypes.byref(sp), ctypes.c_void_p(par.data_ptr()), par.shape[0],
+                                     ctypes.byref(ci), float(threshold), ctypes.byref(cnt))
+        self._check(rc, "gen_coupled_count")
+        return int(cnt.value)
+
+    # ------------------------------------------------------------------ step 2
+    def dedup_global(self, space: Space, configs: torch.Tensor) -> torch.Tensor:
+        """Sorted unique keys owned by this rank (collective when world > 1)."""
+        W = space.words
+        cfg = _as_u64_2d(configs, W)
+        k = _Keys()
+        sp = space._c()
+        rc = lib().dedup_global(self._ctx, ctypes.byref(sp), ctypes.c_void_p(cfg.data_ptr()), cfg.shape[0],
+                                ctypes.byref(k))
+        self._check(rc, "dedup_global")
+        return self._take(k.keys, int(k.count), W)
+
+    def dedup_partition(self, space: Space, configs: torch.Tensor, n_owners: int):
+        """(bins [sum counts, W] back to back by owner, counts list)."""
+        W = space.words
+        cfg = _as_u64_2d(configs, W)
+        k = _Keys()
+        counts = (ctypes.c_uint64 * n_owners)()
+        sp = space._c()
+        rc = lib().dedup_partition(self._ctx, ctypes.byref(sp), ctypes.c_void_p(cfg.data_ptr()), cfg.shape[0],
+                                   n_owners, ctypes.byref(k), counts)
+        self._check(rc, "dedup_partition")
+        return self._take(k.keys, int(k.count), W), [int(c) for c in counts]
+
+    def dedup_finalize(self, space: Space, keys: torch.Tensor) -> torch.Tensor:
+        W = space.words
+        cfg = _as_u64_2d(keys, W)
+        k = _Keys()
+        sp = space._c()
+        rc = lib().dedup_finalize(self._ctx, ctypes.byref(sp), ctypes.c_void_p(cfg.data_ptr()), cfg.shape[0],
+                                  ctypes.byref(k))
+        self._check(rc, "dedup_finalize")
+        return self._take(k.keys, int(k.count), W)
+
+    # ------------------------------------------------------------------ step 3
+    def pool(self, space: Space, capacity: int = 1 << 20) -> "Pool":
+        return Pool(self, space, capacity)
+
+    def merge_space(self, pool: "Pool", new_keys: torch.Tensor, want_inserted: bool = False):
+        W = pool.space.words
+        nk = _as_u64_2d(new_keys, W)
+        k = _Keys()
+        rc = lib().merge_space(self._ctx, pool._pool, ctypes.c_void_p(nk.data_ptr()), nk.shape[0],
+                               ctypes.byref(k) if want_inserted else None)
+        self._check(rc, "merge_space")
+        if want_inserted:
+            return self._take(k.keys, int(k.count), W)
+        return None
+
+
+class Pool:
+    """GPU-resident sorted unique configuration shard (library owned)."""
+
+    def __init__(self, ctx: Context, space: Space, capacity: int):
+        self.ctx, self.space = ctx, space
+        p = ctypes.c_void_p()
+        sp = space._c()
+        ctx._check(lib().cusci_pool_create(ctx._ctx, ctypes.byref(sp), int(capacity), ctypes.byref(p)),
+                   "cusci_pool_create")
+        self._pool = p
+
+    def __len__(self) -> int:
+        ptr, cnt = ctypes.c_void_p(), ctypes.c_uint64()
+        lib().cusci_pool_view(self._pool, ctypes.byref(ptr), ctypes.byref(cnt))
+        return int(cnt.value)
+
+    def keys(self) -> torch.Tensor:
+        """A copy of the pool's keys (uint64 [count, W])."""
+        ptr, cnt = ctypes.c_void_p(), ctypes.c_uint64()
+        lib().cusci_pool_view(self._pool, ctypes.byref(ptr), ctypes.byref(cnt))
+        n, W = int(cnt.value), self.space.words
+        out = torch.empty((n, W), dtype=torch.uint64, device=self.ctx.device)
+        self.ctx._check(lib().cusci_pool_copy(self._pool, ctypes.c_void_p(out.data_ptr()), n), "cusci_pool_copy")
+        return out
+
+    def close(self):
+        if getattr(self, "_pool", None):
+            lib().cusci_pool_destroy(self._pool)
+            self._pool = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,84 @@
+"""Loader for libcusci.so: ctypes signatures of include/cusci.h.  Fails loudly
+if the library is missing (there is no fallback implementation)."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcusci.so")
+
+CUSCI_ERRORS = {0: "OK", 1: "E_INVALID_ARG", 2: "E_INVALID_PARENT", 3: "E_CAPACITY", 4: "E_CUDA", 5: "E_NCCL",
+                6: "E_OOM"}
+
+# every symbol include/cusci.h declares
+EXPORTS = ["cusci_nccl_unique_id", "cusci_init", "cusci_finalize", "cusci_last_error", "cusci_invalidate_integrals",
+           "cusci_free", "cusci_kernel_launches", "cusci_profile_enable", "cusci_profile_read", "gen_coupled_bound", "gen_coupled", "gen_coupled_count",
+           "dedup_global", "dedup_partition", "dedup_finalize", "cusci_pool_create", "cusci_pool_view",
+           "cusci_pool_copy", "cusci_pool_destroy", "merge_space"]
+
+
+PROFILE_TAGS = ["prep", "validate", "gen", "hash_filter", "owner_scatter", "radix_upsweep", "radix_downsweep",
+                "scan", "unique", "merge_split", "merge_tile", "sorted_check", "nccl_exchange", "memset"]
+
+
+class CusciError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{CUSCI_ERRORS.get(code, code)}] {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2604_15768_b200.build` "
+                          "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i32, u64, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_uint64, ctypes.c_size_t
+    P = ctypes.POINTER
+    L.cusci_nccl_unique_id.argtypes = [vp]
+    L.cusci_nccl_unique_id.restype = i32
+    L.cusci_init.argtypes = [P(vp), i32, i32, i32, vp, vp, vp, vp, vp]
+    L.cusci_init.restype = i32
+    L.cusci_finalize.argtypes = [vp]
+    L.cusci_finalize.restype = None
+    L.cusci_last_error.argtypes = [vp]
+    L.cusci_last_error.restype = ctypes.c_char_p
+    L.cusci_invalidate_integrals.argtypes = [vp]
+    L.cusci_invalidate_integrals.restype = None
+    L.cusci_free.argtypes = [vp, vp]
+    L.cusci_free.restype = None
+    L.cusci_kernel_launches.argtypes = [vp]
+    L.cusci_kernel_launches.restype = u64
+    L.cusci_profile_enable.argtypes = [vp, i32]
+    L.cusci_profile_enable.restype = None
+    L.cusci_profile_read.argtypes = [vp, P(ctypes.c_double), P(u64), i32]
+    L.cusci_profile_read.restype = i32
+    L.gen_coupled_bound.argtypes = [vp, u64]
+    L.gen_coupled_bound.restype = u64
+    L.gen_coupled.argtypes = [vp, vp, vp, u64, vp, ctypes.c_double, vp]
+    L.gen_coupled.restype = i32
+    L.gen_coupled_count.argtypes = [vp, vp, vp, u64, vp, ctypes.c_double, P(u64)]
+    L.gen_coupled_count.restype = i32
+    L.dedup_global.argtypes = [vp, vp, vp, u64, vp]
+    L.dedup_global.restype = i32
+    L.dedup_partition.argtypes = [vp, vp, vp, u64, i32, vp, vp]
+    L.dedup_partition.restype = i32
+    L.dedup_finalize.argtypes = [vp, vp, vp, u64, vp]
+    L.dedup_finalize.restype = i32
+    L.cusci_pool_create.argtypes = [vp, vp, u64, P(vp)]
+    L.cusci_pool_create.restype = i32
+    L.cusci_pool_view.argtypes = [vp, P(vp), P(u64)]
+    L.cusci_pool_view.restype = i32
+    L.cusci_pool_copy.argtypes = [vp, vp, u64]
+    L.cusci_pool_copy.restype = i32
+    L.cusci_pool_destroy.argtypes = [vp]
+    L.cusci_pool_destroy.restype = None
+    L.merge_space.argtypes = [vp, vp, vp, u64, vp]
+    L.merge_space.restype = i32
+    _lib = L
+    return L

@@ -1,0 +1,287 @@
+// C-ABI lifecycle, errors, memory plumbing (include/cusci.h).
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+
+#include "internal.cuh"
+
+namespace cusci {
+
+int set_error(cusci_ctx* ctx, int code, const char* fmt, ...) {
+  if (ctx) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    ctx->err = buf;
+  }
+  return code;
+}
+
+Scratch::~Scratch() {
+  for (void* p : ptrs) cudaFreeAsync(p, ctx->stream);
+}
+
+int Scratch::get(size_t bytes, void** p) {
+  if (bytes == 0) bytes = 256;
+  void* q = nullptr;
+  cudaError_t e = cudaMallocFromPoolAsync(&q, bytes, ctx->pool, ctx->stream);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_error(ctx, CUSCI_E_OOM, "scratch allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
+  }
+  ptrs.push_back(q);
+  *p = q;
+  return CUSCI_OK;
+}
+
+int out_alloc(cusci_ctx* ctx, size_t bytes, void** p) {
+  if (bytes == 0) bytes = 256;
+  void* q = nullptr;
+  if (ctx->alloc) {
+    q = ctx->alloc(bytes, (void*)ctx->stream, ctx->alloc_user);
+  } else {
+    cudaError_t e = cudaMallocFromPoolAsync(&q, bytes, ctx->pool, ctx->stream);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      q = nullptr;
+    }
+  }
+  if (!q) return set_error(ctx, CUSCI_E_OOM, "output allocation of %zu bytes failed", bytes);
+  *p = q;
+  return CUSCI_OK;
+}
+
+void out_free(cusci_ctx* ctx, void* p) {
+  if (!p) return;
+  if (ctx->free_fn) ctx->free_fn(p, ctx->alloc_user);
+  else cudaFreeAsync(p, ctx->stream);
+}
+
+int check_space(cusci_ctx* ctx, const cusci_space* sp) {
+  if (!sp) return set_error(ctx, CUSCI_E_INVALID_ARG, "space is NULL");
+  if (sp->m < 2 || sp->m > 128 || (sp->m & 1))
+    return set_error(ctx, CUSCI_E_INVALID_ARG, "m=%d not an even number in [2,128]", sp->m);
+  int W = sp->m <= 64 ? 1 : 2;
+  if (sp->words != W) return set_error(ctx, CUSCI_E_INVALID_ARG, "words=%d but m=%d needs %d", sp->words, sp->m, W);
+  if (sp->n_alpha < 0 || sp->n_beta < 0 || sp->n_alpha > sp->m / 2 || sp->n_beta > sp->m / 2)
+    return set_error(ctx, CUSCI_E_INVALID_ARG, "electron counts (%d,%d) invalid for m=%d", sp->n_alpha, sp->n_beta, sp->m);
+  return CUSCI_OK;
+}
+
+int read_u64(cusci_ctx* ctx, const uint64_t* dev, uint64_t* host, int count) {
+  uint64_t* pinned = (uint64_t*)ctx->host_pinned;
+  if (count > 512) return set_error(ctx, CUSCI_E_INVALID_ARG, "read_u64 count too large");
+  CUSCI_CUDA(ctx, cudaMemcpyAsync(pinned, dev, sizeof(uint64_t) * count, cudaMemcpyDeviceToHost, ctx->stream));
+  CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  memcpy(host, pinned, sizeof(uint64_t) * count);
+  return CUSCI_OK;
+}
+
+static cudaEvent_t ev_get(cusci_ctx* ctx) {
+  if (!ctx->ev_free.empty()) {
+    cudaEvent_t e = ctx->ev_free.back();
+    ctx->ev_free.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+Prof::Prof(cusci_ctx* c, int t) : ctx(c), tag(t) {
+  if (!ctx->profiling) return;
+  a = ev_get(ctx);
+  cudaEventRecord(a, ctx->stream);
+}
+
+Prof::~Prof() {
+  if (!a) return;
+  cudaEvent_t b = ev_get(ctx);
+  cudaEventRecord(b, ctx->stream);
+  ctx->prof.push_back(ProfRec{tag, a, b});
+}
+
+}  // namespace cusci
+
+using namespace cusci;
+
+extern "C" {
+
+int cusci_nccl_unique_id(void* out128) {
+  if (!out128) return CUSCI_E_INVALID_ARG;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return CUSCI_E_NCCL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId must be 128 bytes");
+  memcpy(out128, &id, sizeof(id));
+  return CUSCI_OK;
+}
+
+int cusci_init(cusci_ctx** out, int device, int rank, int world, const void* nccl_unique_id, void* cuda_stream,
+               cusci_alloc_fn alloc, cusci_free_fn free_fn, void* alloc_user) {
+  if (!out) return CUSCI_E_INVALID_ARG;
+  *out = nullptr;
+  if (world < 1 || rank < 0 || rank >= world) return CUSCI_E_INVALID_ARG;
+  if (world > 1 && !nccl_unique_id) return CUSCI_E_INVALID_ARG;
+  if ((alloc == nullptr) != (free_fn == nullptr)) return CUSCI_E_INVALID_ARG;
+  cusci_ctx* ctx = new cusci_ctx;
+  ctx->device = device;
+  ctx->rank = rank;
+  ctx->world = world;
+  ctx->alloc = alloc;
+  ctx->free_fn = free_fn;
+  ctx->alloc_user = alloc_user;
+  auto fail = [&](int code) {
+    cusci_finalize(ctx);
+    return code;
+  };
+  if (cudaSetDevice(device) != cudaSuccess) return fail(CUSCI_E_CUDA);
+  cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (cuda_stream) {
+    ctx->stream = (cudaStream_t)cuda_stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) return fail(CUSCI_E_CUDA);
+    ctx->own_stream = true;
+  }
+  cudaMemPoolProps props = {};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = device;
+  if (cudaMemPoolCreate(&ctx->pool, &props) != cudaSuccess) return fail(CUSCI_E_CUDA);
+  uint64_t thresh = UINT64_MAX;
+  cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &thresh);
+  if (cudaMallocHost(&ctx->host_pinned, 4096) != cudaSuccess) return fail(CUSCI_E_CUDA);
+  if (world > 1) {
+    ncclUniqueId id;
+    memcpy(&id, nccl_unique_id, sizeof(id));
+    if (ncclCommInitRank(&ctx->comm, world, id, rank) != ncclSuccess) {
+      ctx->comm = nullptr;
+      return fail(CUSCI_E_NCCL);
+    }
+  }
+  *out = ctx;
+  return CUSCI_OK;
+}
+
+static void prep_release(cusci_ctx* ctx) {
+  if (ctx->prep.block) cudaFree(ctx->prep.block);
+  ctx->prep = Prep{};
+}
+
+void cusci_finalize(cusci_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  prep_release(ctx);
+  if (ctx->comm) {
+    if (ctx->broken) ncclCommAbort(ctx->comm);
+    else ncclCommDestroy(ctx->comm);
+  }
+  for (auto& r : ctx->prof) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : ctx->ev_free) cudaEventDestroy(e);
+  if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
+  if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* cusci_last_error(const cusci_ctx* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+
+void cusci_invalidate_integrals(cusci_ctx* ctx) {
+  if (!ctx) return;
+  cudaStreamSynchronize(ctx->stream);
+  prep_release(ctx);
+}
+
+void cusci_free(cusci_ctx* ctx, void* ptr) {
+  if (ctx && ptr) out_free(ctx, ptr);
+}
+
+uint64_t cusci_kernel_launches(const cusci_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+void cusci_profile_enable(cusci_ctx* ctx, int on) {
+  if (ctx) ctx->profiling = on != 0;
+}
+
+int cusci_profile_read(cusci_ctx* ctx, double* ms, uint64_t* launches, int n_tags) {
+  if (!ctx || !ms || !launches) return CUSCI_E_INVALID_ARG;
+  CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  for (int t = 0; t < n_tags; t++) {
+    ms[t] = 0;
+    launches[t] = 0;
+  }
+  for (const ProfRec& r : ctx->prof) {
+    float e = 0;
+    cudaEventElapsedTime(&e, r.a, r.b);
+    if (r.tag < n_tags) {
+      ms[r.tag] += e;
+      launches[r.tag]++;
+    }
+    ctx->ev_free.push_back(r.a);
+    ctx->ev_free.push_back(r.b);
+  }
+  ctx->prof.clear();
+  return CUSCI_OK;
+}
+
+static uint64_t binom2(uint64_t n) { return n < 2 ? 0 : n * (n - 1) / 2; }
+
+uint64_t gen_coupled_bound(const cusci_space* sp, uint64_t n_parents) {
+  if (!sp) return 0;
+  uint64_t K = (uint64_t)sp->m / 2;
+  uint64_t na = sp->n_alpha, nb = sp->n_beta, va = K - na, vb = K - nb;
+  uint64_t per = na * va + nb * vb + binom2(na) * binom2(va) + binom2(nb) * binom2(vb) + na * va * nb * vb;
+  return per * n_parents;
+}
+
+// ------------------------------------------------------------------ pool
+int cusci_pool_create(cusci_ctx* ctx, const cusci_space* sp, uint64_t capacity, cusci_pool** out) {
+  if (!ctx || !out) return CUSCI_E_INVALID_ARG;
+  CUSCI_TRY(check_space(ctx, sp));
+  cusci_pool* p = new cusci_pool;
+  p->ctx = ctx;
+  p->sp = *sp;
+  p->cap = capacity < 1024 ? 1024 : capacity;
+  for (int b = 0; b < 2; b++) {
+    if (cudaMallocFromPoolAsync((void**)&p->buf[b], p->cap * sp->words * 8, ctx->pool, ctx->stream) != cudaSuccess) {
+      cudaGetLastError();
+      cusci_pool_destroy(p);
+      return set_error(ctx, CUSCI_E_OOM, "pool allocation failed");
+    }
+  }
+  *out = p;
+  return CUSCI_OK;
+}
+
+int cusci_pool_view(const cusci_pool* pool, const uint64_t** keys, uint64_t* count) {
+  if (!pool || !keys || !count) return CUSCI_E_INVALID_ARG;
+  *keys = pool->buf[pool->cur];
+  *count = pool->count;
+  return CUSCI_OK;
+}
+
+int cusci_pool_copy(const cusci_pool* pool, uint64_t* dst, uint64_t capacity_keys) {
+  if (!pool || (!dst && pool->count)) return CUSCI_E_INVALID_ARG;
+  cusci_ctx* ctx = pool->ctx;
+  if (capacity_keys < pool->count)
+    return set_error(ctx, CUSCI_E_CAPACITY, "pool copy: %llu keys > capacity %llu", (unsigned long long)pool->count,
+                     (unsigned long long)capacity_keys);
+  if (pool->count)
+    CUSCI_CUDA(ctx, cudaMemcpyAsync(dst, pool->buf[pool->cur], pool->count * pool->sp.words * 8,
+                                    cudaMemcpyDeviceToDevice, ctx->stream));
+  return CUSCI_OK;
+}
+
+void cusci_pool_destroy(cusci_pool* pool) {
+  if (!pool) return;
+  for (int b = 0; b < 2; b++)
+    if (pool->buf[b]) cudaFreeAsync(pool->buf[b], pool->ctx->stream);
+  cudaStreamSynchronize(pool->ctx->stream);
+  delete pool;
+}
+
+}  // extern "C"

@@ -1,0 +1,245 @@
+// Internal definitions shared by the libcusci translation units (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/cusci.h"
+
+namespace cusci {
+
+constexpr int kWarp = 32;
+constexpr unsigned kFull = 0xffffffffu;
+
+// ------------------------------------------------------------------ status
+struct Status {
+  int code = CUSCI_OK;
+};
+
+// ------------------------------------------------------------------ scratch
+// Scratch memory comes from a context-owned CUDA memory pool (stream-ordered
+// cudaMallocFromPoolAsync, release threshold = infinity), so steady-state
+// calls reuse cached blocks and never hit the driver allocator.  A Scratch
+// object frees everything it handed out (stream-ordered) when it goes out of
+// scope.
+// Cached Hamiltonian prep: built on device from (h, eri).
+struct Prep {
+  const double* h = nullptr;
+  const double* eri = nullptr;
+  int K = 0;
+  double eps = -1.0;
+  uint64_t fingerprint = 0;
+  bool valid = false;
+  // pair rows over spin-orbital pairs p<q, row id = q(q-1)/2 + p
+  uint32_t* rowptr = nullptr;   // [npq + 1]
+  uint16_t* ab = nullptr;       // [nnz]  a | b << 8   (a < b)
+  double* v = nullptr;          // [nnz]  <pq||ab> (d1-d2 | d1 | -d2), |v| > eps
+  uint64_t nnz = 0;
+  // singles candidates per spin orbital p: targets a (same spin, a != p) with
+  // any nonzero constituent integral
+  uint32_t* srowptr = nullptr;  // [m + 1]
+  uint8_t* sa = nullptr;        // [snnz]
+  uint64_t snnz = 0;
+  double* topp = nullptr;       // [K][K][K]  (PA|KK)
+  double* tsame = nullptr;      // [K][K][K]  (PA|KK) - (PK|KA)
+  void* block = nullptr;        // single cudaMalloc holding all of the above
+  size_t block_bytes = 0;
+};
+
+// kernel classes for the optional per-launch event profiler (cusci_profile_*)
+enum ProfTag {
+  PT_PREP = 0, PT_VALIDATE, PT_GEN, PT_HASH, PT_SCATTER, PT_RADIX_UP, PT_RADIX_DOWN, PT_SCAN, PT_UNIQUE,
+  PT_MERGE_SPLIT, PT_MERGE_TILE, PT_CHECK, PT_NCCL, PT_MEMSET, PT_COUNT
+};
+struct ProfRec {
+  int tag;
+  cudaEvent_t a, b;
+};
+
+}  // namespace cusci
+
+struct cusci_ctx {
+  int device = 0;
+  int rank = 0;
+  int world = 1;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  ncclComm_t comm = nullptr;
+  bool broken = false;
+  cusci_alloc_fn alloc = nullptr;
+  cusci_free_fn free_fn = nullptr;
+  void* alloc_user = nullptr;
+  cudaMemPool_t pool = nullptr;
+  cusci::Prep prep;
+  void* host_pinned = nullptr;  // small pinned staging (counts, flags)
+  uint64_t launches = 0;
+  int num_sms = 148;
+  bool profiling = false;
+  std::vector<cusci::ProfRec> prof;
+  std::vector<cudaEvent_t> ev_free;
+  std::string err;
+};
+
+struct cusci_pool {
+  cusci_ctx* ctx = nullptr;
+  cusci_space sp{};
+  uint64_t* buf[2] = {nullptr, nullptr};
+  uint64_t cap = 0;  // keys per buffer
+  int cur = 0;
+  uint64_t count = 0;
+};
+
+namespace cusci {
+
+int set_error(cusci_ctx* ctx, int code, const char* fmt, ...);
+
+#define CUSCI_CUDA(ctx, call)                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess) {                                                               \
+      (ctx)->broken = true;                                                                \
+      return ::cusci::set_error((ctx), CUSCI_E_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call, \
+                                cudaGetErrorString(e_));                                   \
+    }                                                                                      \
+  } while (0)
+
+#define CUSCI_TRY(expr)        \
+  do {                         \
+    int rc_ = (expr);          \
+    if (rc_ != CUSCI_OK) return rc_; \
+  } while (0)
+
+#define CUSCI_LAUNCH_CHECK(ctx)                  \
+  do {                                           \
+    (ctx)->launches++;                           \
+    CUSCI_CUDA((ctx), cudaPeekAtLastError());    \
+  } while (0)
+
+// launch a kernel under the profiler scope of class `tag`
+#define CUSCI_LAUNCH(ctx, tag, ...)              \
+  do {                                           \
+    ::cusci::Prof pf_((ctx), (tag));             \
+    __VA_ARGS__;                                 \
+    CUSCI_LAUNCH_CHECK(ctx);                     \
+  } while (0)
+
+// Profiler scope: when ctx->profiling, records a CUDA event pair on the
+// context stream around the enclosed launches (tagged by kernel class).
+struct Prof {
+  cusci_ctx* ctx;
+  int tag;
+  cudaEvent_t a = nullptr;
+  Prof(cusci_ctx* c, int t);
+  ~Prof();
+};
+
+// scratch (stream-ordered, from the context pool)
+struct Scratch {
+  cusci_ctx* ctx;
+  std::vector<void*> ptrs;
+  explicit Scratch(cusci_ctx* c) : ctx(c) {}
+  ~Scratch();
+  // returns CUSCI_OK or CUSCI_E_OOM (with message); zero-byte requests give a valid dummy
+  int get(size_t bytes, void** p);
+  template <typename T> int get_t(size_t count, T** p) { return get(count * sizeof(T), (void**)p); }
+};
+
+// output allocation through the context's allocator
+int out_alloc(cusci_ctx* ctx, size_t bytes, void** p);
+void out_free(cusci_ctx* ctx, void* p);
+
+int check_space(cusci_ctx* ctx, const cusci_space* sp);
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// ------------------------------------------------------------------ keys
+template <int W> struct KeyT;
+template <> struct KeyT<1> {
+  uint64_t w0;
+};
+template <> struct alignas(16) KeyT<2> {
+  uint64_t w0, w1;
+};
+
+template <int W> __device__ __forceinline__ KeyT<W> load_key(const uint64_t* base, uint64_t i);
+template <> __device__ __forceinline__ KeyT<1> load_key<1>(const uint64_t* base, uint64_t i) {
+  return KeyT<1>{base[i]};
+}
+template <> __device__ __forceinline__ KeyT<2> load_key<2>(const uint64_t* base, uint64_t i) {
+  ulonglong2 v = reinterpret_cast<const ulonglong2*>(base)[i];
+  return KeyT<2>{v.x, v.y};
+}
+template <int W> __device__ __forceinline__ void store_key(uint64_t* base, uint64_t i, const KeyT<W>& k);
+template <> __device__ __forceinline__ void store_key<1>(uint64_t* base, uint64_t i, const KeyT<1>& k) {
+  base[i] = k.w0;
+}
+template <> __device__ __forceinline__ void store_key<2>(uint64_t* base, uint64_t i, const KeyT<2>& k) {
+  reinterpret_cast<ulonglong2*>(base)[i] = make_ulonglong2(k.w0, k.w1);
+}
+__device__ __forceinline__ bool key_eq(const KeyT<1>& a, const KeyT<1>& b) { return a.w0 == b.w0; }
+__device__ __forceinline__ bool key_eq(const KeyT<2>& a, const KeyT<2>& b) { return a.w0 == b.w0 && a.w1 == b.w1; }
+__device__ __forceinline__ bool key_lt(const KeyT<1>& a, const KeyT<1>& b) { return a.w0 < b.w0; }
+__device__ __forceinline__ bool key_lt(const KeyT<2>& a, const KeyT<2>& b) {
+  return a.w1 < b.w1 || (a.w1 == b.w1 && a.w0 < b.w0);
+}
+__device__ __forceinline__ bool key_le(const KeyT<1>& a, const KeyT<1>& b) { return a.w0 <= b.w0; }
+__device__ __forceinline__ bool key_le(const KeyT<2>& a, const KeyT<2>& b) { return !key_lt(b, a); }
+
+// 8-bit digit d (bits [8d, 8d+8)) of the big integer
+__device__ __forceinline__ uint32_t key_digit(const KeyT<1>& k, int shift) { return (uint32_t)(k.w0 >> shift) & 0xffu; }
+__device__ __forceinline__ uint32_t key_digit(const KeyT<2>& k, int shift) {
+  return (uint32_t)((shift < 64 ? (k.w0 >> shift) : (k.w1 >> (shift - 64)))) & 0xffu;
+}
+
+// splitmix64 finalizer
+__device__ __forceinline__ uint64_t fmix64(uint64_t x) {
+  x ^= x >> 30;
+  x *= 0xBF58476D1CE4E5B9ull;
+  x ^= x >> 27;
+  x *= 0x94D049BB133111EBull;
+  x ^= x >> 31;
+  return x;
+}
+// owner(j) = floor(mix(j) * P / 2^64)   (reading r9)
+__device__ __forceinline__ uint64_t owner_mix(const KeyT<1>& k) { return fmix64(k.w0); }
+__device__ __forceinline__ uint64_t owner_mix(const KeyT<2>& k) {
+  return fmix64(k.w0 ^ fmix64(k.w1 ^ 0x9E3779B97F4A7C15ull));
+}
+template <int W> __device__ __forceinline__ uint32_t owner_of(const KeyT<W>& k, uint32_t P) {
+  return (uint32_t)__umul64hi(owner_mix(k), (uint64_t)P);
+}
+// hash-table slot hash (independent of the owner mix)
+__device__ __forceinline__ uint64_t slot_hash(const KeyT<1>& k) { return fmix64(k.w0 ^ 0xD6E8FEB86659FD93ull); }
+__device__ __forceinline__ uint64_t slot_hash(const KeyT<2>& k) {
+  return fmix64(k.w1 ^ fmix64(k.w0 ^ 0xD6E8FEB86659FD93ull));
+}
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned r;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+  return r;
+}
+
+// ------------------------------------------------------------------ launchers (per .cu)
+int prep_build(cusci_ctx* ctx, const cusci_space* sp, const cusci_integrals* ints, double eps);
+
+// exclusive scan of n values (u32 or u64) in place-safe out; optional device total
+int scan_exclusive_u32(cusci_ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t n);
+int scan_exclusive_u64(cusci_ctx* ctx, const uint64_t* in, uint64_t* out, uint64_t n, uint64_t* total_dev);
+
+// LSD radix sort of keys[n][W] over bits [0, nbits); the sorted keys end in
+// *out_sorted, which is `keys` or `alt` (both [n][W] device buffers).
+int radix_sort_keys(cusci_ctx* ctx, int W, uint64_t* keys, uint64_t* alt, uint64_t n, int nbits,
+                    uint64_t** out_sorted);
+// unique compaction of sorted keys into out; count written to device *n_out_dev
+int unique_sorted_keys(cusci_ctx* ctx, int W, const uint64_t* in, uint64_t n, uint64_t* out,
+                       uint64_t* n_out_dev);
+// sync the stream and read a device u64
+int read_u64(cusci_ctx* ctx, const uint64_t* dev, uint64_t* host, int count = 1);
+
+}  // namespace cusci

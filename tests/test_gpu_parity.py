@@ -1,0 +1,282 @@
+"""GPU parity: the CUDA path (through the C ABI, paper_2604_15768_b200) against
+the oracle, element by element on the same seeded inputs.
+
+Bar (BASELINE.json north_star): configuration sets, counts and phases
+bit-exact; H_ij within 1e-12 relative (we also assert the expected exact
+equality, reading r5)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2604_15768_b200 as P
+    return P
+
+
+@pytest.fixture(scope="module")
+def ctx(P):
+    c = P.Context(0)
+    yield c
+    c.close()
+
+
+def canon(keys, src, *cols):
+    """sort records by (src, key big-integer)"""
+    keys = np.asarray(keys).reshape(len(keys), -1)
+    order = np.lexsort(tuple(keys[:, w] for w in range(keys.shape[1])) + (np.asarray(src),))
+    return (keys[order], np.asarray(src)[order]) + tuple(np.asarray(c)[order] for c in cols)
+
+
+def run_gen(P, ctx, wl_m, na, nb, par, ints, eps):
+    sp = P.Space(wl_m, na, nb)
+    di = P.DeviceIntegrals(ints.h, ints.eri)
+    tpar = torch.from_numpy(par.astype(np.uint64)).cuda()
+    rec = ctx.gen_coupled(sp, tpar, di, eps, with_src=True, with_phase=True)
+    torch.cuda.synchronize()
+    return (rec.keys.cpu().numpy(), rec.src.cpu().numpy().astype(np.uint32), rec.hij.cpu().numpy(),
+            rec.phase.cpu().numpy())
+
+
+def assert_gen_parity(P, ctx, m, na, nb, par, ints, eps=0.0):
+    g_keys, g_src, g_h, g_ph = run_gen(P, ctx, m, na, nb, par, ints, eps)
+    ref = oracle.gen_coupled(m, na, nb, par, ints, eps)
+    assert len(g_src) == len(ref["src"]), "record counts differ"
+    gk, gs, gh, gp = canon(g_keys, g_src, g_h, g_ph)
+    rk, rs, rh, rp = canon(ref["keys"], ref["src"], ref["hij"], ref["phase"])
+    assert np.array_equal(gs, rs) and np.array_equal(gk, rk), "coupled sets differ"
+    assert np.array_equal(gp, rp), "phases differ"
+    rel = np.abs(gh - rh) / np.maximum(np.abs(rh), 1e-300)
+    assert np.all(rel <= 1e-12), f"max rel err {rel.max()}"
+    assert np.array_equal(gh, rh), "H not bit-identical (expected under reading r5)"
+    # per-parent counts
+    assert np.array_equal(np.bincount(gs, minlength=len(par)), np.bincount(rs, minlength=len(par)))
+    return len(gs)
+
+
+@pytest.mark.parametrize("key", ["lih", "lih_g4"])
+def test_gen_lih_full_space(P, ctx, key):
+    wl, ints, par = synth.workload_inputs(key)
+    n = assert_gen_parity(P, ctx, wl.m, wl.n_alpha, wl.n_beta, par, ints)
+    if key == "lih":
+        assert n == 20700
+
+
+def test_gen_h2o_10k(P, ctx):
+    wl, ints, par = synth.workload_inputs("h2o")
+    assert len(par) == 10_000
+    assert_gen_parity(P, ctx, wl.m, wl.n_alpha, wl.n_beta, par, ints)
+
+
+def test_gen_h2o_dense_and_threshold(P, ctx):
+    wl, ints, par = synth.workload_inputs("h2o_dense", n_parents=2000)
+    n0 = assert_gen_parity(P, ctx, wl.m, 5, 5, par, ints, 0.0)
+    assert n0 == 2000 * 2240
+    assert_gen_parity(P, ctx, wl.m, 5, 5, par, ints, 1e-4)
+    assert_gen_parity(P, ctx, wl.m, 5, 5, par, ints, 3e-3)
+
+
+def test_gen_open_shell(P, ctx):
+    ints = synth.make_integrals(9, 2, 77)
+    par = synth.hf_ball_parents(9, 4, 2, 500, 1, 78)
+    assert_gen_parity(P, ctx, 18, 4, 2, par, ints)
+
+
+def test_gen_n2_prefix_and_sample(P, ctx):
+    wl, ints, par = synth.workload_inputs("n2", n_parents=20_000)
+    rng = np.random.default_rng(0)
+    sel = np.sort(rng.choice(len(par), 300, replace=False))
+    assert_gen_parity(P, ctx, wl.m, 7, 7, par[:200], ints)
+    assert_gen_parity(P, ctx, wl.m, 7, 7, par[sel], ints)
+
+
+def test_gen_c2h4_w2(P, ctx):
+    wl, ints, par = synth.workload_inputs("c2h4", n_parents=2000)
+    rng = np.random.default_rng(1)
+    sel = np.sort(rng.choice(len(par), 60, replace=False))
+    assert_gen_parity(P, ctx, wl.m, 8, 8, par[sel], ints)
+
+
+def test_gen_m120_w2(P, ctx):
+    wl, ints, par = synth.workload_inputs("m120", n_parents=40)
+    assert_gen_parity(P, ctx, wl.m, 12, 12, par[:12], ints)
+
+
+def test_gen_m128_dense_word_boundary(P, ctx):
+    ints = synth.make_integrals(64, 1, 5)
+    par = synth.hf_ball_parents(64, 3, 3, 8, 1, 6)
+    assert_gen_parity(P, ctx, 128, 3, 3, par, ints)
+
+
+# ------------------------------------------------------------------ edge cases / errors
+def test_gen_edges_and_errors(P, ctx):
+    wl, ints, par = synth.workload_inputs("h2o", n_parents=100)
+    sp = P.Space(wl.m, 5, 5)
+    di = P.DeviceIntegrals(ints.h, ints.eri)
+    tpar = torch.from_numpy(par).cuda()
+    # empty
+    r = ctx.gen_coupled(sp, tpar[:0], di, 0.0, capacity=10)
+    assert r.count == 0
+    # eps = inf -> nothing
+    assert ctx.gen_coupled_count(sp, tpar, di, float("inf")) == 0
+    # capacity overflow then retry
+    total = ctx.gen_coupled_count(sp, tpar, di, 0.0)
+    with pytest.raises(P.CusciError) as e:
+        ctx.gen_coupled(sp, tpar, di, 0.0, capacity=total - 1)
+    assert e.value.code == 3
+    r = ctx.gen_coupled(sp, tpar, di, 0.0, capacity=total)
+    assert r.count == total
+    # invalid parent: a bit >= m, wrong spin count
+    bad = par.copy()
+    bad[17, 0] |= np.uint64(1 << 40)
+    with pytest.raises(P.CusciError) as e:
+        ctx.gen_coupled(sp, torch.from_numpy(bad).cuda(), di, 0.0, capacity=total)
+    assert e.value.code == 2 and "parent 17" in str(e.value)
+    bad = par.copy()
+    bad[5, 0] ^= np.uint64(1)
+    with pytest.raises(P.CusciError) as e:
+        ctx.gen_coupled_count(sp, torch.from_numpy(bad).cuda(), di, 0.0)
+    assert e.value.code == 2
+    # bad arguments
+    with pytest.raises(P.CusciError) as e:
+        ctx.gen_coupled_count(sp, tpar, di, float("nan"))
+    assert e.value.code == 1
+    with pytest.raises(P.CusciError) as e:
+        ctx.gen_coupled_count(sp, tpar, di, -1.0)
+    assert e.value.code == 1
+    with pytest.raises(P.CusciError) as e:
+        ctx.gen_coupled_count(P.Space(130, 5, 5), tpar, di, 0.0)
+    assert e.value.code == 1
+
+
+def test_gen_full_size_sampled(P, ctx):
+    """N2 at the bench's launch configuration (one batch of 125k parents):
+    sampled parents compared record by record; properties checked for all."""
+    wl, ints, par = synth.workload_inputs("n2", n_parents=125_000)
+    sp = P.Space(wl.m, 7, 7)
+    di = P.DeviceIntegrals(ints.h, ints.eri)
+    tpar = torch.from_numpy(par).cuda()
+    rec = ctx.gen_coupled(sp, tpar, di, 0.0, with_src=True)
+    src = rec.src.cpu().numpy().astype(np.int64)
+    hij = rec.hij.cpu().numpy()
+    assert np.all(np.abs(hij) > 0)
+    rng = np.random.default_rng(3)
+    sel = np.sort(rng.choice(len(par), 40, replace=False))
+    ref = oracle.gen_coupled(wl.m, 7, 7, par[sel], ints, 0.0)
+    keys = rec.keys.cpu().numpy()
+    mask = np.isin(src, sel)
+    remap = {int(s): i for i, s in enumerate(sel)}
+    g_src = np.array([remap[int(s)] for s in src[mask]], dtype=np.uint32)
+    gk, gs, gh = canon(keys[mask], g_src, hij[mask])
+    rk, rs, rh = canon(ref["keys"], ref["src"], ref["hij"])
+    assert np.array_equal(gk, rk) and np.array_equal(gs, rs) and np.array_equal(gh, rh)
+
+
+# ------------------------------------------------------------------ dedup
+def _dedup_gpu(P, ctx, sp, keys):
+    out = ctx.dedup_global(sp, torch.from_numpy(keys).cuda())
+    return out.cpu().numpy()
+
+
+def test_dedup_lih_closure(P, ctx):
+    wl, ints, par = synth.workload_inputs("lih")
+    sp = P.Space(12, 2, 2)
+    di = P.DeviceIntegrals(ints.h, ints.eri)
+    rec = ctx.gen_coupled(sp, torch.from_numpy(par).cuda(), di, 0.0)
+    u = ctx.dedup_global(sp, rec.keys).cpu().numpy()
+    assert np.array_equal(u, par)          # 20,700 records -> the 225 parents
+
+
+@pytest.mark.parametrize("W,n", [(1, 0), (1, 1), (1, 5000), (1, 1_000_003), (2, 700_001)])
+def test_dedup_zipf(P, ctx, W, n):
+    sp = P.Space(64 * W, 1, 1)
+    keys = synth.zipf_keys(max(n, 1), W, 1.1, 1 << 18, seed=11 + W)[:n]
+    got = _dedup_gpu(P, ctx, sp, keys)
+    ref = oracle.dedup(keys, W)
+    assert np.array_equal(got.reshape(-1, W), ref.reshape(-1, W))
+
+
+def test_dedup_generated_stream(P, ctx):
+    wl, ints, par = synth.workload_inputs("h2o")
+    sp = P.Space(wl.m, 5, 5)
+    di = P.DeviceIntegrals(ints.h, ints.eri)
+    rec = ctx.gen_coupled(sp, torch.from_numpy(par).cuda(), di, 0.0)
+    got = ctx.dedup_global(sp, rec.keys).cpu().numpy()
+    ref = oracle.dedup(rec.keys.cpu().numpy(), 1)
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("W,Pn", [(1, 2), (1, 4), (1, 8), (2, 4)])
+def test_dedup_logical_ranks(P, ctx, W, Pn):
+    """P logical ranks on one GPU: partition on each rank, exchange by device
+    copies in the harness, finalize per owner; compare with the oracle's
+    per-owner shards (multi-GPU host logic)."""
+    sp = P.Space(64 * W, 1, 1)
+    allk = synth.zipf_keys(400_000, W, 1.1, 1 << 16, seed=5)
+    parts = np.array_split(allk, Pn)
+    bins = []
+    for r in range(Pn):
+        b, counts = ctx.dedup_partition(sp, torch.from_numpy(parts[r]).cuda(), Pn)
+        offs = np.concatenate([[0], np.cumsum(counts)])
+        bins.append([b[offs[o]:offs[o + 1]] for o in range(Pn)])
+        # each bin holds only its owner's keys, locally unique
+        for o in range(Pn):
+            kb = bins[r][o].cpu().numpy()
+            assert len(np.unique(kb, axis=0)) == len(kb)
+            if len(kb):
+                assert np.all(oracle.owner(kb, W, Pn) == o)
+    total = 0
+    for o in range(Pn):
+        recv = torch.cat([bins[r][o] for r in range(Pn)])
+        got = ctx.dedup_finalize(sp, recv).cpu().numpy()
+        ref = oracle.dedup(allk, W, Pn, o)
+        assert np.array_equal(got.reshape(-1, W), ref.reshape(-1, W))
+        total += len(got)
+    assert total == len(oracle.dedup(allk, W))
+
+
+# ------------------------------------------------------------------ merge
+@pytest.mark.parametrize("W", [1, 2])
+def test_merge_parity(P, ctx, W):
+    rng = np.random.default_rng(2 + W)
+    sp = P.Space(64 * W, 1, 1)
+    S0 = synth.unique_keys(rng.integers(1, 1 << 40, size=(300_000, W), dtype=np.uint64))
+    pool = ctx.pool(sp, capacity=1000)           # forces growth
+    ins0 = ctx.merge_space(pool, torch.from_numpy(S0).cuda(), want_inserted=True).cpu().numpy()
+    assert np.array_equal(ins0, S0) and len(pool) == len(S0)
+    for it in range(3):
+        U = synth.unique_keys(np.concatenate([S0[rng.choice(len(S0), 50_000)],
+                                              rng.integers(1, 1 << 40, size=(80_000, W), dtype=np.uint64)]))
+        before = pool.keys().cpu().numpy()
+        ins = ctx.merge_space(pool, torch.from_numpy(U).cuda(), want_inserted=True).cpu().numpy()
+        ref_s, ref_ins = oracle.merge(before, U, W)
+        assert np.array_equal(pool.keys().cpu().numpy(), ref_s)
+        assert np.array_equal(ins, ref_ins)
+        assert len(pool) == len(before) + len(ins)
+    # idempotence
+    again = ctx.merge_space(pool, torch.from_numpy(U).cuda(), want_inserted=True)
+    assert again.shape[0] == 0
+    # unsorted input rejected
+    with pytest.raises(P.CusciError) as e:
+        ctx.merge_space(pool, torch.from_numpy(U[::-1].copy()).cuda())
+    assert e.value.code == 1
+    pool.close()
+
+
+def test_pipeline_lih_merge_inserts_nothing(P, ctx):
+    wl, ints, par = synth.workload_inputs("lih")
+    sp = P.Space(12, 2, 2)
+    di = P.DeviceIntegrals(ints.h, ints.eri)
+    tp = torch.from_numpy(par).cuda()
+    pool = ctx.pool(sp, 256)
+    ctx.merge_space(pool, tp)
+    rec = ctx.gen_coupled(sp, tp, di, 0.0)
+    u = ctx.dedup_global(sp, rec.keys)
+    ins = ctx.merge_space(pool, u, want_inserted=True)
+    assert ins.shape[0] == 0 and len(pool) == 225
