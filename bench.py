@@ -119,11 +119,16 @@ def bcast_bytes(pg, payload: bytes | None, rank: int) -> bytes:
     return obj[0]
 
 
+def _reduce_device(pg):
+    import torch
+    return "cuda" if pg.get_backend() == "nccl" else "cpu"
+
+
 def allreduce_max(pg, x: float) -> float:
     if pg is None:
         return x
     import torch
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device=_reduce_device(pg))
     pg.all_reduce(t, op=pg.ReduceOp.MAX)
     return float(t.item())
 
@@ -132,7 +137,7 @@ def allreduce_sum(pg, x: float) -> float:
     if pg is None:
         return x
     import torch
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device=_reduce_device(pg))
     pg.all_reduce(t, op=pg.ReduceOp.SUM)
     return float(t.item())
 
@@ -234,23 +239,23 @@ def main():
     shard_host = shard.cpu().numpy()
     shard_pinned = torch.from_numpy(shard_host).pin_memory()
 
+    upool = ctx.pool(sp, 1 << 20)   # union of the unique coupled configurations C
+    spool = ctx.pool(sp, 1 << 20)   # the space S (starts as the parent shard)
+
     def step(parents_dev, e2e=False):
         """one pass of the hot path; returns (records, unique, space_size)."""
         nrec = 0
-        upool = ctx.pool(sp, 1 << 20)
+        upool.clear()
+        spool.clear()
         for (a, b) in batches:
             rec = ctx.gen_coupled(sp, parents_dev[a:b], di, args.eps, out=out)
             nrec += rec.count
             u = ctx.dedup_global(sp, rec.keys)
             ctx.merge_space(upool, u)
             del u
-        spool = ctx.pool(sp, 1 << 20)
         ctx.merge_space(spool, parents_dev)
-        ctx.merge_space(spool, upool.keys())
-        n_unique, n_space = len(upool), len(spool)
-        upool.close()
-        spool.close()
-        return nrec, n_unique, n_space
+        ctx.merge_pool(spool, upool)
+        return nrec, len(upool), len(spool)
 
     # warm-up
     for _ in range(args.warmup):

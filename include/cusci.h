@@ -131,8 +131,8 @@ uint64_t gen_coupled_bound(const cusci_space* sp, uint64_t n_parents);
  * and ph the fermionic phase of sequential singles p->a then q->b,
  * keeping the record iff |H| > threshold (strict; Alg. 1 line 12).
  * The diagonal is not emitted.  Records are written compactly (no gaps)
- * into `out`; the order of parents' record blocks is unspecified, the records
- * of one parent are contiguous.  threshold >= 0 (NaN rejected).
+ * into `out` in an unspecified order (src identifies the parent; compare
+ * record sets after sorting by (src, key)).  threshold >= 0 (NaN rejected).
  * Parents are validated on device before anything is written
  * (CUSCI_E_INVALID_PARENT, the message names the first bad index).
  * If the total exceeds out->capacity, nothing beyond capacity is written,
@@ -176,6 +176,8 @@ int dedup_finalize(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* keys, 
 int cusci_pool_create(cusci_ctx* ctx, const cusci_space* sp, uint64_t capacity, cusci_pool** out);
 /* Read-only view of the pool's sorted unique keys; valid until the next merge_space. */
 int cusci_pool_view(const cusci_pool* pool, const uint64_t** keys, uint64_t* count);
+/* Empty the pool (keeps its buffers, so a reused pool never reallocates). */
+int cusci_pool_clear(cusci_pool* pool);
 /* Copy the pool's keys into dst (device, capacity_keys >= count), stream-ordered. */
 int cusci_pool_copy(const cusci_pool* pool, uint64_t* dst, uint64_t capacity_keys);
 void cusci_pool_destroy(cusci_pool* pool);

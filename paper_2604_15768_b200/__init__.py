@@ -258,6 +258,17 @@ class Context:
     def pool(self, space: Space, capacity: int = 1 << 20) -> "Pool":
         return Pool(self, space, capacity)
 
+    def merge_pool(self, dst: "Pool", src: "Pool", want_inserted: bool = False):
+        """dst <- dst u src, reading src's keys in place (no copy)."""
+        ptr, cnt = src.view()
+        k = _Keys()
+        rc = lib().merge_space(self._ctx, dst._pool, ctypes.c_void_p(ptr), cnt,
+                               ctypes.byref(k) if want_inserted else None)
+        self._check(rc, "merge_space")
+        if want_inserted:
+            return self._take(k.keys, int(k.count), dst.space.words)
+        return None
+
     def merge_space(self, pool: "Pool", new_keys: torch.Tensor, want_inserted: bool = False):
         W = pool.space.words
         nk = _as_u64_2d(new_keys, W)
@@ -285,6 +296,15 @@ class Pool:
         ptr, cnt = ctypes.c_void_p(), ctypes.c_uint64()
         lib().cusci_pool_view(self._pool, ctypes.byref(ptr), ctypes.byref(cnt))
         return int(cnt.value)
+
+    def view(self):
+        """(device pointer, count) of the pool's keys, valid until the next merge."""
+        ptr, cnt = ctypes.c_void_p(), ctypes.c_uint64()
+        lib().cusci_pool_view(self._pool, ctypes.byref(ptr), ctypes.byref(cnt))
+        return ptr.value or 0, int(cnt.value)
+
+    def clear(self):
+        self.ctx._check(lib().cusci_pool_clear(self._pool), "cusci_pool_clear")
 
     def keys(self) -> torch.Tensor:
         """A copy of the pool's keys (uint64 [count, W])."""

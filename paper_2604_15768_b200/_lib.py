@@ -14,7 +14,7 @@ CUSCI_ERRORS = {0: "OK", 1: "E_INVALID_ARG", 2: "E_INVALID_PARENT", 3: "E_CAPACI
 EXPORTS = ["cusci_nccl_unique_id", "cusci_init", "cusci_finalize", "cusci_last_error", "cusci_invalidate_integrals",
            "cusci_free", "cusci_kernel_launches", "cusci_profile_enable", "cusci_profile_read", "gen_coupled_bound", "gen_coupled", "gen_coupled_count",
            "dedup_global", "dedup_partition", "dedup_finalize", "cusci_pool_create", "cusci_pool_view",
-           "cusci_pool_copy", "cusci_pool_destroy", "merge_space"]
+           "cusci_pool_copy", "cusci_pool_clear", "cusci_pool_destroy", "merge_space"]
 
 
 PROFILE_TAGS = ["prep", "validate", "gen", "hash_filter", "owner_scatter", "radix_upsweep", "radix_downsweep",
@@ -74,6 +74,8 @@ def lib():
     L.cusci_pool_create.restype = i32
     L.cusci_pool_view.argtypes = [vp, P(vp), P(u64)]
     L.cusci_pool_view.restype = i32
+    L.cusci_pool_clear.argtypes = [vp]
+    L.cusci_pool_clear.restype = i32
     L.cusci_pool_copy.argtypes = [vp, vp, u64]
     L.cusci_pool_copy.restype = i32
     L.cusci_pool_destroy.argtypes = [vp]

@@ -1,4 +1,5 @@
 // C-ABI lifecycle, errors, memory plumbing (include/cusci.h).
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -19,20 +20,65 @@ int set_error(cusci_ctx* ctx, int code, const char* fmt, ...) {
   return code;
 }
 
+static void arena_release_all(cusci_ctx* ctx) {
+  Arena& A = ctx->arena;
+  for (auto& sg : A.segs) cudaFree(sg.base);
+  A.segs.clear();
+  A.cur = A.off = A.used = 0;
+}
+
+Scratch::Scratch(cusci_ctx* c) : ctx(c) {
+  Arena& A = ctx->arena;
+  if (A.depth == 0) {
+    if (A.segs.size() > 1) {  // consolidate into one segment of the observed peak
+      cudaStreamSynchronize(ctx->stream);
+      arena_release_all(ctx);
+      void* q = nullptr;
+      if (cudaMalloc(&q, A.peak) == cudaSuccess) A.segs.push_back({(char*)q, A.peak});
+      else cudaGetLastError();
+    }
+    A.cur = A.off = A.used = 0;
+  }
+  A.depth++;
+  m_cur = A.cur;
+  m_off = A.off;
+  m_used = A.used;
+}
+
 Scratch::~Scratch() {
-  for (void* p : ptrs) cudaFreeAsync(p, ctx->stream);
+  Arena& A = ctx->arena;
+  A.cur = m_cur;
+  A.off = m_off;
+  A.used = m_used;
+  A.depth--;
 }
 
 int Scratch::get(size_t bytes, void** p) {
-  if (bytes == 0) bytes = 256;
-  void* q = nullptr;
-  cudaError_t e = cudaMallocFromPoolAsync(&q, bytes, ctx->pool, ctx->stream);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    return set_error(ctx, CUSCI_E_OOM, "scratch allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
+  Arena& A = ctx->arena;
+  bytes = align256(bytes ? bytes : 256);
+  while (A.cur < A.segs.size() && A.off + bytes > A.segs[A.cur].cap) {
+    A.cur++;
+    A.off = 0;
   }
-  ptrs.push_back(q);
-  *p = q;
+  if (A.cur >= A.segs.size()) {
+    size_t want = std::max(bytes, std::max(A.peak, (size_t)64 << 20));
+    void* q = nullptr;
+    if (cudaMalloc(&q, want) != cudaSuccess) {
+      cudaGetLastError();
+      want = bytes;
+      if (cudaMalloc(&q, want) != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(ctx, CUSCI_E_OOM, "scratch allocation of %zu bytes failed", bytes);
+      }
+    }
+    A.segs.push_back({(char*)q, want});
+    A.cur = A.segs.size() - 1;
+    A.off = 0;
+  }
+  *p = A.segs[A.cur].base + A.off;
+  A.off += bytes;
+  A.used += bytes;
+  if (A.used > A.peak) A.peak = A.used;
   return CUSCI_OK;
 }
 
@@ -174,6 +220,7 @@ void cusci_finalize(cusci_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   prep_release(ctx);
+  arena_release_all(ctx);
   if (ctx->comm) {
     if (ctx->broken) ncclCommAbort(ctx->comm);
     else ncclCommDestroy(ctx->comm);
@@ -261,6 +308,12 @@ int cusci_pool_view(const cusci_pool* pool, const uint64_t** keys, uint64_t* cou
   if (!pool || !keys || !count) return CUSCI_E_INVALID_ARG;
   *keys = pool->buf[pool->cur];
   *count = pool->count;
+  return CUSCI_OK;
+}
+
+int cusci_pool_clear(cusci_pool* pool) {
+  if (!pool) return CUSCI_E_INVALID_ARG;
+  pool->count = 0;
   return CUSCI_OK;
 }
 

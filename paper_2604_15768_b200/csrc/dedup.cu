@@ -4,13 +4,14 @@
 // generation").
 //
 // B200 design:
-//   a8+a9  one kernel: open-addressing hash filter (load <= 0.5, empty slot = 0,
-//          64-bit atomicCAS for W=1, 128-bit atom.cas.b128 for W=2) keeps the
-//          first copy of each key; survivors are appended with one warp-
-//          aggregated atomic per warp step, and per-owner counts are
-//          accumulated (owner(j) = floor(mix(j) P / 2^64), DESIGN.md r9)
-//          with match_any aggregation; a scatter kernel then writes the
-//          survivors into P contiguous owner bins.
+//   a8+a9  keys are scattered into buckets bucket(j) = owner(j) * 2^s + top s
+//          bits of a bijective 64-bit mix (owner(j) = floor(mix(j) P / 2^64),
+//          DESIGN.md r9), ~1024 keys per bucket (histogram + scatter with
+//          L2-resident per-bucket atomics); one CTA per bucket then removes
+//          duplicates with an open-addressing hash table in SHARED memory
+//          (32-bit atomicCAS, linear probing): the random probes never touch
+//          HBM.  Survivors of the buckets of owner r form contiguous owner
+//          bin r (P = 1: one atomic append per bucket).
 //   a10    counts all-to-all then one payload all-to-all-v over NCCL grouped
 //          ncclSend/ncclRecv (NVLink/NVSwitch); one host sync for the sizes.
 //   a11    LSD radix sort over the m significant key bits + adjacent-unique
@@ -26,104 +27,152 @@ namespace {
 
 constexpr int kHashThreads = 256;
 
-__device__ __forceinline__ void cas128(uint64_t* addr, uint64_t c0, uint64_t c1, uint64_t v0, uint64_t v1,
-                                       uint64_t& o0, uint64_t& o1) {
+// ---------------------------------------------------------------- bucket dedup
+// After the onesweep passes the keys are ordered by bucket(j) = the top `bits`
+// bits of the owner mix (a bijective 64-bit mix), ~<= 4096 keys per bucket.
+// Each CTA takes ranges of 64 Ki positions and processes the buckets that
+// START in its range: it streams a bucket's keys in rounds of 256 through an
+// open-addressing hash table held in SHARED memory (the keys themselves are
+// the slots: 64-bit atomicCAS, or ATOMS.CAS.128 for W=2; empty = 0, key 0 is
+// tracked by a flag; linear probing on the low bits of an independent mix).
+// The first copy of each key is appended to `out` (one atomic per warp-round).
+// If a bucket holds more distinct keys than the table can take, the table is
+// flushed and restarted; the duplicates that then survive are removed by the
+// final sort + unique, so the result stays exact.
+template <int W> struct SDCfg {
+  static constexpr int TS = W == 1 ? 8192 : 4096;  // slots (64 KB)
+  static constexpr size_t SMEM = (size_t)TS * sizeof(KeyT<W>);
+  static constexpr uint32_t FILL_LIMIT = (TS * 3) / 4;
+  static constexpr uint64_t RANGE = 1ull << 16;
+};
+
+__device__ __forceinline__ uint64_t cas_slot(KeyT<1>* slot, const KeyT<1>& k, KeyT<1>& old) {
+  old.w0 = atomicCAS(reinterpret_cast<unsigned long long*>(&slot->w0), 0ull, (unsigned long long)k.w0);
+  return 0;
+}
+__device__ __forceinline__ uint64_t cas_slot(KeyT<2>* slot, const KeyT<2>& k, KeyT<2>& old) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(slot);
+  uint64_t o0, o1;
   asm volatile(
       "{\n\t.reg .b128 c, v, o;\n\t"
       "mov.b128 c, {%2, %3};\n\t"
       "mov.b128 v, {%4, %5};\n\t"
-      "atom.global.cas.b128 o, [%6], c, v;\n\t"
+      "atom.shared.cas.b128 o, [%6], c, v;\n\t"
       "mov.b128 {%0, %1}, o;\n\t}"
       : "=l"(o0), "=l"(o1)
-      : "l"(c0), "l"(c1), "l"(v0), "l"(v1), "l"(addr)
+      : "l"(0ull), "l"(0ull), "l"(k.w0), "l"(k.w1), "r"(sa)
       : "memory");
+  old.w0 = o0;
+  old.w1 = o1;
+  return 0;
 }
+__device__ __forceinline__ bool key_zero(const KeyT<1>& k) { return k.w0 == 0; }
+__device__ __forceinline__ bool key_zero(const KeyT<2>& k) { return (k.w0 | k.w1) == 0; }
 
-// returns true iff this thread inserted k (first copy)
-__device__ __forceinline__ bool hash_insert(uint64_t* table, uint64_t mask, const KeyT<1>& k) {
-  uint64_t slot = slot_hash(k) & mask;
-  for (;;) {
-    uint64_t cur = __ldcg(table + slot);
-    if (cur == k.w0) return false;
-    if (cur == 0) {
-      const uint64_t old = atomicCAS((unsigned long long*)(table + slot), 0ull, (unsigned long long)k.w0);
-      if (old == 0) return true;
-      if (old == k.w0) return false;
-    }
-    slot = (slot + 1) & mask;
-  }
-}
-
-__device__ __forceinline__ bool hash_insert(uint64_t* table, uint64_t mask, const KeyT<2>& k) {
-  uint64_t slot = slot_hash(k) & mask;
-  for (;;) {
-    const ulonglong2 cur = __ldcg(reinterpret_cast<const ulonglong2*>(table) + slot);
-    if (cur.x == k.w0 && cur.y == k.w1) return false;
-    if (cur.x == 0 && cur.y == 0) {
-      uint64_t o0, o1;
-      cas128(table + 2 * slot, 0, 0, k.w0, k.w1, o0, o1);
-      if (o0 == 0 && o1 == 0) return true;
-      if (o0 == k.w0 && o1 == k.w1) return false;
-    }
-    slot = (slot + 1) & mask;
-  }
+template <int W>
+__device__ __forceinline__ uint32_t bucket_id(const KeyT<W>& k, int bits) {
+  return bits ? (uint32_t)(owner_mix(k) >> (64 - bits)) : 0u;
 }
 
 template <int W>
-__global__ void __launch_bounds__(kHashThreads) hash_filter_kernel(const uint64_t* __restrict__ in, uint64_t n,
-                                                                  uint64_t* __restrict__ table, uint64_t mask,
-                                                                  uint64_t* __restrict__ out,
-                                                                  unsigned long long* __restrict__ counters,
-                                                                  uint32_t n_owners) {
-  // counters[0] = survivors, counters[1 + r] = survivors owned by r
-  const unsigned lane = lane_id();
-  const uint64_t warp_global = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t base = warp_global * 32; base < n; base += nwarps * 32) {
-    const uint64_t idx = base + lane;
-    bool keep = false;
-    KeyT<W> k{};
-    if (idx < n) {
-      k = load_key<W>(in, idx);
-      keep = hash_insert(table, mask, k);
+__device__ __forceinline__ bool table_insert(KeyT<W>* tab, const KeyT<W>& k, int* s_zero, uint32_t* s_fill) {
+  constexpr uint32_t TS = SDCfg<W>::TS;
+  if (key_zero(k)) return atomicExch(s_zero, 1) == 0;
+  uint32_t h = (uint32_t)slot_hash(k) & (TS - 1);
+  for (uint32_t probe = 0; probe < TS; probe++) {
+    const KeyT<W> cur = tab[h];
+    if (key_eq(cur, k)) return false;
+    if (key_zero(cur)) {
+      KeyT<W> old;
+      cas_slot(&tab[h], k, old);
+      if (key_zero(old)) {
+        atomicAdd(s_fill, 1u);
+        return true;
+      }
+      if (key_eq(old, k)) return false;
     }
-    const unsigned bal = __ballot_sync(kFull, keep);
-    if (bal == 0) continue;
-    unsigned long long wbase = 0;
-    if (lane == 0) wbase = atomicAdd(&counters[0], (unsigned long long)__popc(bal));
-    wbase = __shfl_sync(kFull, wbase, 0);
-    if (keep) store_key<W>(out, wbase + __popc(bal & lanemask_lt()), k);
-    if (n_owners > 1) {
-      const uint32_t o = keep ? owner_of<W>(k, n_owners) : 0xffffffffu;
-      const unsigned peers = __match_any_sync(kFull, o);
-      if (keep && lane == (unsigned)(__ffs(peers) - 1)) atomicAdd(&counters[1 + o], (unsigned long long)__popc(peers));
-    }
+    h = (h + 1) & (TS - 1);
   }
+  return true;  // table full: pass through (removed later by sort + unique)
 }
 
 template <int W>
-__global__ void __launch_bounds__(kHashThreads) owner_scatter_kernel(const uint64_t* __restrict__ in, uint64_t n,
-                                                                    uint64_t* __restrict__ bins,
-                                                                    unsigned long long* __restrict__ cursor,
-                                                                    uint32_t n_owners) {
+__global__ void __launch_bounds__(kHashThreads) sorted_dedup_kernel(const uint64_t* __restrict__ keys, uint64_t n,
+                                                                   int bits, uint64_t* __restrict__ out,
+                                                                   unsigned long long* __restrict__ counters) {
+  extern __shared__ __align__(16) unsigned char sd_smem[];
+  KeyT<W>* tab = reinterpret_cast<KeyT<W>*>(sd_smem);
+  constexpr uint32_t TS = SDCfg<W>::TS;
+  constexpr int IT = 8;  // keys per thread per round (all loads issued first)
+  const uint32_t RND = IT * kHashThreads;
+  __shared__ int s_zero;
+  __shared__ uint32_t s_fill, s_first;
   const unsigned lane = lane_id();
-  const uint64_t warp_global = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t base = warp_global * 32; base < n; base += nwarps * 32) {
-    const uint64_t idx = base + lane;
-    const bool valid = idx < n;
-    KeyT<W> k{};
-    uint32_t o = 0xffffffffu;
-    if (valid) {
-      k = load_key<W>(in, idx);
-      o = owner_of<W>(k, n_owners);
+  const uint64_t range = SDCfg<W>::RANGE;
+  for (uint64_t r = blockIdx.x; r * range < n; r += gridDim.x) {
+    const uint64_t lo = r * range, hi = std::min(n, lo + range);
+    // first bucket start >= lo: skip the tail of the bucket that began before lo
+    uint64_t pos = lo;
+    if (lo > 0) {
+      const uint32_t bprev = bucket_id<W>(load_key<W>(keys, lo - 1), bits);
+      for (;;) {
+        const uint64_t j = pos + threadIdx.x;
+        const bool same = j < n && bucket_id<W>(load_key<W>(keys, j), bits) == bprev;
+        const int c = __syncthreads_count(same);
+        pos += c;
+        if (c < (int)blockDim.x || pos >= hi) break;
+      }
     }
-    const unsigned peers = __match_any_sync(kFull, o);
-    const unsigned leader = __ffs(peers) - 1;
-    unsigned long long b = 0;
-    if (valid && lane == leader) b = atomicAdd(&cursor[o], (unsigned long long)__popc(peers));
-    b = __shfl_sync(kFull, b, leader);
-    if (valid) store_key<W>(bins, b + __popc(peers & lanemask_lt()), k);
+    while (pos < hi) {
+      const uint32_t b = bucket_id<W>(load_key<W>(keys, pos), bits);
+      bool fresh = true;
+      for (;;) {
+        KeyT<W> k[IT];
+        bool inb[IT];
+#pragma unroll
+        for (int u = 0; u < IT; u++) {
+          const uint64_t j = pos + (uint64_t)u * kHashThreads + threadIdx.x;
+          if (j < n) k[u] = load_key<W>(keys, j);
+        }
+        if (fresh) {
+          for (uint32_t i = threadIdx.x; i < TS; i += blockDim.x) tab[i] = KeyT<W>{};
+          if (threadIdx.x == 0) {
+            s_zero = 0;
+            s_fill = 0;
+          }
+          fresh = false;
+        }
+        if (threadIdx.x == 0) s_first = RND;
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < IT; u++) {
+          const uint64_t j = pos + (uint64_t)u * kHashThreads + threadIdx.x;
+          inb[u] = j < n && bucket_id<W>(k[u], bits) == b;
+          if (!inb[u]) atomicMin(&s_first, (uint32_t)(u * kHashThreads + threadIdx.x));
+        }
+#pragma unroll
+        for (int u = 0; u < IT; u++) {
+          const bool keep = inb[u] && table_insert<W>(tab, k[u], &s_zero, &s_fill);
+          const unsigned bal = __ballot_sync(kFull, keep);
+          if (bal) {
+            unsigned long long wb = 0;
+            if (lane == 0) wb = atomicAdd(&counters[0], (unsigned long long)__popc(bal));
+            wb = __shfl_sync(kFull, wb, 0);
+            if (keep) store_key<W>(out, wb + __popc(bal & lanemask_lt()), k[u]);
+          }
+        }
+        __syncthreads();
+        const uint32_t c = s_first;
+        pos += c;
+        if (c < RND) break;
+        if (s_fill > SDCfg<W>::FILL_LIMIT) {  // too many distinct keys: restart the table
+          fresh = true;
+          if (threadIdx.x == 0) atomicAdd(&counters[1], 1ull);
+        }
+        __syncthreads();
+      }
+      __syncthreads();
+    }
   }
 }
 
@@ -149,46 +198,68 @@ int agree_status(cusci_ctx* ctx, int local) {
   return *(int*)ctx->host_pinned;
 }
 
+// local unique filter (a8) + owner partition (a9): survivors of the bucket
+// dedup, grouped into contiguous owner bins (P > 1: one onesweep pass with
+// digit = owner over the survivors only).  bins_out holds >= n keys.
 template <int W>
-int partition_impl(cusci_ctx* ctx, const uint64_t* configs, uint64_t n, int P, uint64_t* bins_out /*[n][W] device*/,
+int partition_impl(cusci_ctx* ctx, const uint64_t* configs, uint64_t n, int P, uint64_t* bins_out,
                    uint64_t* counts /*host [P]*/, uint64_t* total) {
   Scratch s(ctx);
-  uint64_t cap = 1024;
-  while (cap < 2 * n) cap <<= 1;
-  uint64_t* table;
+  for (int r = 0; r < P; r++) counts[r] = 0;
+  *total = 0;
+  if (n == 0) return CUSCI_OK;
+  // bucket bits: <= ~capacity/2 keys per bucket even with no redundancy
+  const uint64_t per_bucket = (uint64_t)SDCfg<W>::TS / 2;
+  int bits = 0;
+  while ((n >> bits) > per_bucket && bits < 27) bits++;
+  uint64_t *b0, *b1, *surv;
   unsigned long long* ctr;
-  CUSCI_TRY(s.get_t(cap * W, &table));
-  CUSCI_TRY(s.get_t(1 + P, &ctr));
-  {
-    Prof pf(ctx, PT_MEMSET);
-    CUSCI_CUDA(ctx, cudaMemsetAsync(table, 0, cap * W * sizeof(uint64_t), ctx->stream));
+  CUSCI_TRY(s.get_t(n * W, &b0));
+  CUSCI_TRY(s.get_t(n * W, &b1));
+  CUSCI_TRY(s.get_t(2, &ctr));
+  CUSCI_CUDA(ctx, cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), ctx->stream));
+  const uint64_t* sorted = configs;
+  if (bits) {
+    DigitSpecs specs{};
+    // LSD over the top `bits` bits of the owner mix, <= 9 bits per pass
+    const int npass = (bits + 8) / 9;
+    const int per = (bits + npass - 1) / npass;
+    for (int q = 0, lowbit = 64 - bits; q < npass; q++) {
+      const int nb = std::min(per, 64 - lowbit);
+      specs.d[specs.n++] = DigitSpec{1, lowbit, nb, 0u};
+      lowbit += nb;
+    }
+    CUSCI_TRY(onesweep_passes(ctx, W, configs, b0, b1, n, specs, &sorted, nullptr));
   }
-  CUSCI_CUDA(ctx, cudaMemsetAsync(ctr, 0, (1 + P) * sizeof(unsigned long long), ctx->stream));
-  const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + kHashThreads - 1) / kHashThreads,
-                                                                             (uint64_t)ctx->num_sms * 8));
-  uint64_t* surv = bins_out;
-  if (P > 1) CUSCI_TRY(s.get_t(n * W, &surv));
-  CUSCI_LAUNCH(ctx, PT_HASH, hash_filter_kernel<W><<<blocks, kHashThreads, 0, ctx->stream>>>(configs, n, table, cap - 1, surv, ctr, (uint32_t)P));
-  uint64_t hc[1 + 512];
-  CUSCI_TRY(read_u64(ctx, (const uint64_t*)ctr, hc, 1 + P));
+  surv = (P == 1) ? bins_out : ((sorted == b0) ? b1 : b0);
+  static bool attr_set[3] = {false, false, false};
+  if (!attr_set[W]) {
+    CUSCI_CUDA(ctx, cudaFuncSetAttribute(sorted_dedup_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)SDCfg<W>::SMEM));
+    attr_set[W] = true;
+  }
+  const uint64_t nranges = (n + SDCfg<W>::RANGE - 1) / SDCfg<W>::RANGE;
+  const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(nranges, (uint64_t)ctx->num_sms * 3));
+  CUSCI_LAUNCH(ctx, PT_HASH, sorted_dedup_kernel<W><<<blocks, kHashThreads, SDCfg<W>::SMEM, ctx->stream>>>(sorted, n, bits, surv, ctr));
+  uint64_t hc[2];
+  CUSCI_TRY(read_u64(ctx, (const uint64_t*)ctr, hc, 2));
   *total = hc[0];
   if (P == 1) {
     counts[0] = hc[0];
     return CUSCI_OK;
   }
-  uint64_t off = 0;
-  for (int r = 0; r < P; r++) {
-    counts[r] = hc[1 + r];
-    ((uint64_t*)ctx->host_pinned)[r] = off;
-    off += hc[1 + r];
-  }
-  CUSCI_CUDA(ctx, cudaMemcpyAsync(ctr, ctx->host_pinned, P * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
-  const uint64_t ns = hc[0];
-  if (ns) {
-    const unsigned b2 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((ns + kHashThreads - 1) / kHashThreads,
-                                                                           (uint64_t)ctx->num_sms * 8));
-    CUSCI_LAUNCH(ctx, PT_SCATTER, owner_scatter_kernel<W><<<b2, kHashThreads, 0, ctx->stream>>>(surv, ns, bins_out, ctr, (uint32_t)P));
-  }
+  // owner bins: one stable pass over the survivors with digit = owner
+  DigitSpecs os{};
+  int obits = 1;
+  while ((1 << obits) < P) obits++;
+  os.d[os.n++] = DigitSpec{2, 0, obits, (uint32_t)P};
+  std::vector<uint64_t> h0((size_t)1 << obits);
+  const uint64_t* binned = surv;
+  uint64_t* spare = (surv == b0) ? b1 : b0;
+  CUSCI_TRY(onesweep_passes(ctx, W, surv, bins_out, spare, hc[0], os, &binned, h0.data()));
+  if (binned != bins_out && hc[0])
+    CUSCI_CUDA(ctx, cudaMemcpyAsync(bins_out, binned, hc[0] * W * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  for (int r = 0; r < P; r++) counts[r] = h0[r];
   return CUSCI_OK;
 }
 

@@ -5,24 +5,30 @@
 // B200 design: a persistent grid of warps pulls work
 // units (parent, contiguous range of excitation rows) from a global counter.
 // Per unit one warp
-//   a1  loads the parent (one 8/16-byte broadcast load) and builds its sorted
-//       occupied list in shared memory with ballots + popc (no loops over bits
-//       per lane);
-//   a2  walks its rows: row r < n is the singles row of occupied orbital
-//       occ[r] (targets from the singles candidate table), row r >= n is the
-//       pair row of occupied pair (occ[x], occ[y]), x < y, read from the
-//       prescreened CSR pair table (a0) 32 entries per step, coalesced;
-//   a3  forms the target key with XORs;
-//   a4  the phase from popc over masked ranges (sequential singles p->a, q->b);
-//   a5  H from the table value (doubles) or the sequential sum over occ(i)\p
+//   a1  loads the parent (one 8/16-byte broadcast load), builds its sorted
+//       occupied list in shared memory with ballots + popc, and the prefix-
+//       parity mask PP (bit t = parity of the occupied orbitals below t);
+//   a2  row 0 = all singles of the parent, flattened across occupied
+//       orbitals (a warp scan over the per-orbital candidate counts + a
+//       shuffle binary search gives each lane its (p, a)); rows 1.. = the
+//       occupied pairs (occ[x] < occ[y]), each read from the prescreened CSR
+//       pair table (a0), 32 entries (16 B each, one 128-bit load) per step;
+//   a3  target key = (parent ^ p ^ q) ^ abmask;
+//   a4  phase of sequential singles p->a, q->b in closed form:
+//         parity = (x + y + 1) ^ M(a) ^ M(b),  M = PP ^ above(p) ^ above(q)
+//       (singles: parity = x ^ PP(a) ^ [a > p]) -- one popc per record;
+//   a5  H = +-v from the table (doubles) or the sequential sum over occ(i)\p
 //       of the [K][P][A] tables (singles, same order as the definition);
-//   a6  keeps |H| > eps (doubles: already folded into the table);
-//   a7  counts survivors in a first sweep, reserves exactly that many output
-//       slots with ONE atomicAdd per unit, then re-sweeps and writes survivors
-//       compacted with ballot/popc offsets: every store instruction of the warp
-//       covers consecutive records (coalesced), there are no gaps, and no
-//       per-record atomics (the paper's "one atomicAdd per block").
+//   a6  keeps |H| > eps (doubles: folded into the table at build time);
+//   a7  survivors are compacted with ballot/popc into a per-warp staging
+//       buffer in shared memory; when it is nearly full the warp reserves
+//       exactly its fill with ONE atomicAdd and copies it out with fully
+//       coalesced stores (the paper's "one atomicAdd per block", as a
+//       per-384-record flush).  No count pass, no gaps; record order is
+//       unspecified (reading r6).
+#include <algorithm>
 #include <cmath>
+#include <cstring>
 
 #include "internal.cuh"
 
@@ -33,16 +39,21 @@ constexpr int kGenThreads = 256;
 constexpr int kGenWarps = kGenThreads / 32;
 constexpr unsigned long long kNoError = ~0ull;
 
+template <int W> struct GenCfg {
+  static constexpr int STAGE = W == 1 ? 384 : 192;  // staged records per warp (3-5 CTAs/SM)
+  static constexpr size_t BYTES_PER_REC = sizeof(KeyT<W>) + 8 + 4 + 1;
+  static constexpr size_t SMEM = (size_t)kGenWarps * STAGE * BYTES_PER_REC;
+};
+
 struct GenArgs {
   const uint64_t* parents;
   uint64_t n_parents;
   int m, n_elec, K;
   uint32_t units_per_parent;
-  uint32_t rows_per_parent;
+  uint32_t rows_per_parent;  // 1 (all singles) + n(n-1)/2 pair rows
   uint64_t n_units;
   const uint32_t* rowptr;
-  const uint16_t* ab;
-  const double* v;
+  const PairEnt* ent;
   const uint32_t* srowptr;
   const uint8_t* sa;
   const double* topp;
@@ -54,7 +65,7 @@ struct GenArgs {
   uint32_t* src;
   int8_t* phase;
   uint64_t capacity;
-  unsigned long long* counter;    // [0] = records reserved, [1] = unit work counter, [2] = first bad parent
+  unsigned long long* counter;  // [0] records, [1] unit work counter, [2] first bad parent
   int count_only;
 };
 
@@ -63,24 +74,54 @@ __device__ __forceinline__ bool occ_bit(const KeyT<1>& k, int t) { return (k.w0 
 __device__ __forceinline__ bool occ_bit(const KeyT<2>& k, int t) {
   return t < 64 ? ((k.w0 >> t) & 1ull) : ((k.w1 >> (t - 64)) & 1ull);
 }
-__device__ __forceinline__ void flip2(KeyT<1>& k, int s, int t) { k.w0 ^= (1ull << s) ^ (1ull << t); }
-__device__ __forceinline__ void flip2(KeyT<2>& k, int s, int t) {
-  if (s < 64) k.w0 ^= 1ull << s; else k.w1 ^= 1ull << (s - 64);
-  if (t < 64) k.w0 ^= 1ull << t; else k.w1 ^= 1ull << (t - 64);
+__device__ __forceinline__ KeyT<1> bitk1(int t) { return KeyT<1>{1ull << t}; }
+__device__ __forceinline__ KeyT<2> bitk2(int t) {
+  return t < 64 ? KeyT<2>{1ull << t, 0ull} : KeyT<2>{0ull, 1ull << (t - 64)};
 }
-// bits < t, t in [0, 64]
-__device__ __forceinline__ uint64_t below64(int t) { return t >= 64 ? ~0ull : ((1ull << t) - 1ull); }
-// parity of the occupied orbitals strictly between x and y
-__device__ __forceinline__ uint32_t parity_between(const KeyT<1>& k, int x, int y) {
-  const int lo = min(x, y), hi = max(x, y);
-  const uint64_t mask = below64(hi) & ~below64(lo + 1);
-  return __popcll(k.w0 & mask) & 1u;
+template <int W> __device__ __forceinline__ KeyT<W> bitk(int t);
+template <> __device__ __forceinline__ KeyT<1> bitk<1>(int t) { return bitk1(t); }
+template <> __device__ __forceinline__ KeyT<2> bitk<2>(int t) { return bitk2(t); }
+__device__ __forceinline__ KeyT<1> kxor(const KeyT<1>& a, const KeyT<1>& b) { return KeyT<1>{a.w0 ^ b.w0}; }
+__device__ __forceinline__ KeyT<2> kxor(const KeyT<2>& a, const KeyT<2>& b) { return KeyT<2>{a.w0 ^ b.w0, a.w1 ^ b.w1}; }
+__device__ __forceinline__ bool kdisjoint(const KeyT<1>& a, const KeyT<1>& b) { return (a.w0 & b.w0) == 0; }
+__device__ __forceinline__ bool kdisjoint(const KeyT<2>& a, const KeyT<2>& b) {
+  return ((a.w0 & b.w0) | (a.w1 & b.w1)) == 0;
 }
-__device__ __forceinline__ uint32_t parity_between(const KeyT<2>& k, int x, int y) {
-  const int lo = min(x, y), hi = max(x, y);
-  const uint64_t m0 = below64(min(hi, 64)) & ~below64(min(lo + 1, 64));
-  const uint64_t m1 = below64(max(hi - 64, 0)) & ~below64(max(lo + 1 - 64, 0));
-  return (__popcll(k.w0 & m0) + __popcll(k.w1 & m1)) & 1u;
+__device__ __forceinline__ uint32_t kparity_and(const KeyT<1>& a, const KeyT<1>& b) { return __popcll(a.w0 & b.w0) & 1u; }
+__device__ __forceinline__ uint32_t kparity_and(const KeyT<2>& a, const KeyT<2>& b) {
+  return (__popcll(a.w0 & b.w0) ^ __popcll(a.w1 & b.w1)) & 1u;
+}
+// bits strictly above t
+template <int W> __device__ __forceinline__ KeyT<W> abovek(int t);
+template <> __device__ __forceinline__ KeyT<1> abovek<1>(int t) { return KeyT<1>{t >= 63 ? 0ull : (~0ull << (t + 1))}; }
+template <> __device__ __forceinline__ KeyT<2> abovek<2>(int t) {
+  if (t < 63) return KeyT<2>{~0ull << (t + 1), ~0ull};
+  if (t == 63) return KeyT<2>{0ull, ~0ull};
+  return KeyT<2>{0ull, t >= 127 ? 0ull : (~0ull << (t - 63))};
+}
+// exclusive prefix parity: bit t = parity of popc(k & bits below t)
+__device__ __forceinline__ uint64_t prefix_xor_incl(uint64_t x) {
+  x ^= x << 1;
+  x ^= x << 2;
+  x ^= x << 4;
+  x ^= x << 8;
+  x ^= x << 16;
+  x ^= x << 32;
+  return x;
+}
+__device__ __forceinline__ KeyT<1> prefix_parity(const KeyT<1>& k) { return KeyT<1>{prefix_xor_incl(k.w0) << 1}; }
+__device__ __forceinline__ KeyT<2> prefix_parity(const KeyT<2>& k) {
+  const uint64_t lo = prefix_xor_incl(k.w0);
+  const uint64_t carry = (lo >> 63) ? ~0ull : 0ull;  // parity of the whole of word 0
+  const uint64_t hi = prefix_xor_incl(k.w1);
+  return KeyT<2>{lo << 1, (hi << 1) ^ carry};
+}
+// table entry -> abmask: stored (W = 1) or built from (a, b) (W = 2)
+__device__ __forceinline__ void ent_mask(uint64_t x, KeyT<1>& m) { m.w0 = x; }
+__device__ __forceinline__ void ent_mask(uint64_t x, KeyT<2>& m) {
+  const KeyT<2> ma = bitk2((int)(x & 0xff)), mb = bitk2((int)((x >> 8) & 0xff));
+  m.w0 = ma.w0 | mb.w0;
+  m.w1 = ma.w1 | mb.w1;
 }
 
 template <int W>
@@ -103,114 +144,215 @@ __global__ void validate_kernel(const uint64_t* __restrict__ parents, uint64_t n
   }
 }
 
-// one warp processes the rows [r0, r1) of parent s; pass 0 counts, pass 1 emits
+// per-warp staging buffer in shared memory
 template <int W>
-__device__ __forceinline__ uint32_t process_rows(const GenArgs& a, const KeyT<W>& par, const uint8_t* occ, uint64_t s,
-                                                 uint32_t r0, uint32_t r1, bool emit, uint64_t cursor) {
+struct Stage {
+  KeyT<W>* key;
+  double* h;
+  uint32_t* src;
+  int8_t* ph;
+  uint32_t n;  // warp-uniform fill
+};
+
+template <int W>
+__device__ __forceinline__ void stage_flush(const GenArgs& a, Stage<W>& st) {
+  if (st.n == 0) return;
+  const unsigned lane = lane_id();
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(&a.counter[0], (unsigned long long)st.n);
+  base = __shfl_sync(kFull, base, 0);
+  if (base + st.n <= a.capacity) {
+    for (uint32_t i = lane; i < st.n; i += 32) {
+      store_key<W>(a.keys, base + i, st.key[i]);
+      a.hij[base + i] = st.h[i];
+    }
+    if (a.src)
+      for (uint32_t i = lane; i < st.n; i += 32) a.src[base + i] = st.src[i];
+    if (a.phase)
+      for (uint32_t i = lane; i < st.n; i += 32) a.phase[base + i] = st.ph[i];
+  }
+  __syncwarp();
+  st.n = 0;
+}
+
+// append the lanes' survivors (ballot `bal`) to the stage
+template <int W>
+__device__ __forceinline__ void stage_put(const GenArgs& a, Stage<W>& st, unsigned bal, bool keep, const KeyT<W>& key,
+                                          double H, uint32_t s, uint32_t par) {
+  if (st.n + 32 > (uint32_t)GenCfg<W>::STAGE) stage_flush<W>(a, st);
+  if (keep) {
+    const uint32_t i = st.n + __popc(bal & lanemask_lt());
+    st.key[i] = key;
+    st.h[i] = H;
+    st.src[i] = s;
+    st.ph[i] = par ? -1 : 1;
+  }
+  __syncwarp();
+  st.n += __popc(bal);
+}
+
+__device__ __forceinline__ uint32_t warp_incl_scan_u32(uint32_t v) {
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(kFull, v, o);
+    if ((int)lane_id() >= o) v += t;
+  }
+  return v;
+}
+
+// row 0: all singles of parent s (flattened over occupied orbitals)
+template <int W>
+__device__ __forceinline__ uint32_t do_singles(const GenArgs& a, const KeyT<W>& par, const KeyT<W>& PP,
+                                               const uint8_t* occ, uint32_t s, Stage<W>& st, bool emit) {
   const unsigned lane = lane_id();
   const int n = a.n_elec;
-  uint32_t total = 0;
-  // decode the first pair row
-  int x = 0, y = 1;
-  if (r1 > (uint32_t)n) {
-    uint32_t k = r0 > (uint32_t)n ? r0 - n : 0;
-    while (k >= (uint32_t)(n - 1 - x)) {
-      k -= (uint32_t)(n - 1 - x);
-      x++;
+  uint32_t total_kept = 0;
+  for (int xc = 0; xc < n; xc += 32) {
+    const int xl = xc + (int)lane;
+    int p = 0;
+    uint32_t c0 = 0, c = 0;
+    if (xl < n) {
+      p = occ[xl];
+      c0 = __ldg(a.srowptr + p);
+      c = __ldg(a.srowptr + p + 1) - c0;
     }
-    y = x + 1 + (int)k;
-  }
-  for (uint32_t r = r0; r < r1; r++) {
-    if (r < (uint32_t)n) {
-      // ---------------- singles row: p = occ[r]
-      const int p = occ[r];
-      const int P = p >> 1;
-      const uint32_t c0 = __ldg(a.srowptr + p), c1 = __ldg(a.srowptr + p + 1);
-      for (uint32_t c = c0; c < c1; c += 32) {
-        const uint32_t ci = c + lane;
-        bool keep = false;
-        int t = 0;
-        double H = 0.0;
-        uint32_t ph = 0;
-        if (ci < c1) {
-          t = __ldg(a.sa + ci);
-          if (!occ_bit(par, t)) {
-            const int A = t >> 1;
-            double v = __ldg(a.h + P * a.K + A);
-            for (int xx = 0; xx < n; xx++) {
-              const int kk = occ[xx];
-              if (kk == p) continue;
-              const size_t o = ((size_t)(kk >> 1) * a.K + P) * a.K + A;
-              const double tv = ((kk & 1) == (p & 1)) ? __ldg(a.tsame + o) : __ldg(a.topp + o);
-              v = __dadd_rn(v, tv);
-            }
-            ph = parity_between(par, p, t);
-            H = ph ? -v : v;
-            keep = fabs(H) > a.eps;
+    const uint32_t incl = warp_incl_scan_u32(c);
+    const uint32_t total = __shfl_sync(kFull, incl, 31);
+    for (uint32_t f0 = 0; f0 < total; f0 += 32) {
+      const uint32_t f = f0 + lane;
+      // owner lane L of candidate f = number of lanes whose inclusive count <= f
+      int L = 0;
+#pragma unroll
+      for (int b = 16; b >= 1; b >>= 1) {
+        const uint32_t v = __shfl_sync(kFull, incl, L + b - 1);
+        if (v <= f) L += b;
+      }
+      L = min(L, 31);
+      const int pL = __shfl_sync(kFull, p, L);
+      const uint32_t c0L = __shfl_sync(kFull, c0, L);
+      const uint32_t exL = __shfl_sync(kFull, incl, L) - __shfl_sync(kFull, c, L);
+      bool keep = false;
+      double H = 0.0;
+      uint32_t ph = 0;
+      int t = pL;
+      if (f < total) {
+        t = __ldg(a.sa + c0L + (f - exL));
+        if (!occ_bit(par, t)) {
+          const int P = pL >> 1, A = t >> 1;
+          double v = __ldg(a.h + P * a.K + A);
+          for (int xx = 0; xx < n; xx++) {
+            const int kk = occ[xx];
+            if (kk == pL) continue;
+            const size_t o = ((size_t)(kk >> 1) * a.K + P) * a.K + A;
+            const double tv = ((kk & 1) == (pL & 1)) ? __ldg(a.tsame + o) : __ldg(a.topp + o);
+            v = __dadd_rn(v, tv);
           }
+          // parity = c(p) + c(a) + [a > p], c(p) = index of p in occ
+          ph = (uint32_t)((xc + L) & 1) ^ (uint32_t)occ_bit(PP, t) ^ (uint32_t)(t > pL);
+          H = ph ? -v : v;
+          keep = fabs(H) > a.eps;
         }
-        const unsigned bal = __ballot_sync(kFull, keep);
-        if (emit && keep) {
-          const uint64_t pos = cursor + total + __popc(bal & lanemask_lt());
-          KeyT<W> j = par;
-          flip2(j, p, t);
-          store_key<W>(a.keys, pos, j);
-          a.hij[pos] = H;
-          if (a.src) a.src[pos] = (uint32_t)s;
-          if (a.phase) a.phase[pos] = ph ? -1 : 1;
-        }
-        total += __popc(bal);
       }
-    } else {
-      // ---------------- pair row (p, q) = (occ[x], occ[y])
-      const int p = occ[x], q = occ[y];
-      const uint32_t row = (uint32_t)q * (q - 1) / 2 + p;
-      const uint32_t e0 = __ldg(a.rowptr + row), e1 = __ldg(a.rowptr + row + 1);
-      KeyT<W> base = par;
-      flip2(base, p, q);
-      for (uint32_t e = e0; e < e1; e += 32) {
-        const uint32_t ei = e + lane;
-        bool keep = false;
-        int ta = 0, tb = 0;
-        if (ei < e1) {
-          const uint32_t abv = __ldg(a.ab + ei);
-          ta = abv & 0xff;
-          tb = abv >> 8;
-          keep = !occ_bit(par, ta) && !occ_bit(par, tb);
-        }
-        const unsigned bal = __ballot_sync(kFull, keep);
-        if (emit && keep) {
-          const double v = __ldg(a.v + ei);
-          // sequential singles p->a on i, then q->b on i' = i ^ p ^ a
-          KeyT<W> i1 = par;
-          flip2(i1, p, ta);
-          const uint32_t ph = parity_between(par, p, ta) ^ parity_between(i1, q, tb);
-          const uint64_t pos = cursor + total + __popc(bal & lanemask_lt());
-          KeyT<W> j = base;
-          flip2(j, ta, tb);
-          store_key<W>(a.keys, pos, j);
-          a.hij[pos] = ph ? -v : v;
-          if (a.src) a.src[pos] = (uint32_t)s;
-          if (a.phase) a.phase[pos] = ph ? -1 : 1;
-        }
-        total += __popc(bal);
+      const unsigned bal = __ballot_sync(kFull, keep);
+      if (emit) {
+        const KeyT<W> j = kxor(par, kxor(bitk<W>(pL), bitk<W>(t)));
+        stage_put<W>(a, st, bal, keep, j, H, s, ph);
       }
-      if (++y == n) {
-        x++;
-        y = x + 1;
-      }
+      total_kept += __popc(bal);
     }
   }
-  return total;
+  return total_kept;
+}
+
+// pair rows [r0, r1) (1-based over the occupied pairs) of parent s.
+// Latency hiding: two 32-entry chunks (two 128-bit loads per lane) are in
+// flight per step, and the next row's CSR bounds are loaded while the current
+// row is processed.
+template <int W>
+__device__ __forceinline__ void pair_chunk(const GenArgs& a, const ulonglong2& raw, bool valid, const KeyT<W>& par,
+                                           const KeyT<W>& base, const KeyT<W>& M, uint32_t rc, uint32_t s,
+                                           Stage<W>& st, bool emit, uint32_t& total_kept) {
+  KeyT<W> abm{};
+  ent_mask(raw.x, abm);
+  const bool keep = valid && kdisjoint(par, abm);
+  const unsigned bal = __ballot_sync(kFull, keep);
+  if (emit) {
+    const double v = __longlong_as_double((long long)raw.y);
+    const uint32_t ph = rc ^ kparity_and(M, abm);
+    stage_put<W>(a, st, bal, keep, kxor(base, abm), ph ? -v : v, s, ph);
+  }
+  total_kept += __popc(bal);
+}
+
+template <int W>
+__device__ __forceinline__ uint32_t do_pairs(const GenArgs& a, const KeyT<W>& par, const KeyT<W>& PP,
+                                             const uint8_t* occ, uint32_t s, uint32_t r0, uint32_t r1, Stage<W>& st,
+                                             bool emit) {
+  const unsigned lane = lane_id();
+  const int n = a.n_elec;
+  uint32_t total_kept = 0;
+  uint32_t k = r0 - 1;  // decode pair index -> (x, y), x < y
+  int x = 0;
+  while (k >= (uint32_t)(n - 1 - x)) {
+    k -= (uint32_t)(n - 1 - x);
+    x++;
+  }
+  int y = x + 1 + (int)k;
+  const ulonglong2* ent = reinterpret_cast<const ulonglong2*>(a.ent);
+  int p = occ[x], q = occ[y];
+  uint32_t row = (uint32_t)q * (q - 1) / 2 + p;
+  uint32_t e0 = __ldg(a.rowptr + row), e1 = __ldg(a.rowptr + row + 1);
+  for (uint32_t r = r0; r < r1; r++) {
+    // next row's bounds, issued early
+    int nx = x, ny = y + 1;
+    if (ny == n) {
+      nx++;
+      ny = nx + 1;
+    }
+    uint32_t ne0 = 0, ne1 = 0;
+    int np_ = 0, nq = 0;
+    if (r + 1 < r1) {
+      np_ = occ[nx];
+      nq = occ[ny];
+      const uint32_t nrow = (uint32_t)nq * (nq - 1) / 2 + np_;
+      ne0 = __ldg(a.rowptr + nrow);
+      ne1 = __ldg(a.rowptr + nrow + 1);
+    }
+    const KeyT<W> base = kxor(par, kxor(bitk<W>(p), bitk<W>(q)));
+    const KeyT<W> M = kxor(PP, kxor(abovek<W>(p), abovek<W>(q)));
+    const uint32_t rc = (uint32_t)(x + y + 1) & 1u;
+    for (uint32_t e = e0; e < e1; e += 64) {
+      const uint32_t i0 = e + lane, i1 = e + 32 + lane;
+      const ulonglong2 raw0 = i0 < e1 ? __ldg(ent + i0) : make_ulonglong2(~0ull, 0ull);
+      const ulonglong2 raw1 = i1 < e1 ? __ldg(ent + i1) : make_ulonglong2(~0ull, 0ull);
+      pair_chunk<W>(a, raw0, i0 < e1, par, base, M, rc, s, st, emit, total_kept);
+      if (e + 32 < e1) pair_chunk<W>(a, raw1, i1 < e1, par, base, M, rc, s, st, emit, total_kept);
+    }
+    x = nx;
+    y = ny;
+    p = np_;
+    q = nq;
+    e0 = ne0;
+    e1 = ne1;
+  }
+  return total_kept;
 }
 
 template <int W>
 __global__ void __launch_bounds__(kGenThreads) gen_kernel(const GenArgs a) {
+  extern __shared__ __align__(16) unsigned char gsm[];
   __shared__ uint8_t occ_s[kGenWarps][128];
   __shared__ unsigned long long unit_s[kGenWarps];
   if (a.counter[2] != kNoError) return;  // invalid parent: write nothing
   const int w = threadIdx.x >> 5;
   const unsigned lane = lane_id();
+  constexpr int S = GenCfg<W>::STAGE;
+  const bool emit = !a.count_only;
+  Stage<W> st;
+  st.key = reinterpret_cast<KeyT<W>*>(gsm) + (size_t)w * S;
+  st.h = reinterpret_cast<double*>(gsm + (size_t)kGenWarps * S * sizeof(KeyT<W>)) + (size_t)w * S;
+  st.src = reinterpret_cast<uint32_t*>(gsm + (size_t)kGenWarps * S * (sizeof(KeyT<W>) + 8)) + (size_t)w * S;
+  st.ph = reinterpret_cast<int8_t*>(gsm + (size_t)kGenWarps * S * (sizeof(KeyT<W>) + 12)) + (size_t)w * S;
+  st.n = 0;
   uint8_t* occ = occ_s[w];
   for (;;) {
     if (lane == 0) unit_s[w] = atomicAdd(&a.counter[1], 1ull);
@@ -235,17 +377,15 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(const GenArgs a) {
       nocc += __popc(bal);
     }
     __syncwarp();
-    const uint32_t cnt = process_rows<W>(a, par, occ, s, r0, r1, false, 0);
-    if (cnt == 0 || a.count_only) {
-      if (lane == 0 && cnt) atomicAdd(&a.counter[0], (unsigned long long)cnt);
-      continue;
-    }
-    unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(&a.counter[0], (unsigned long long)cnt);
-    base = __shfl_sync(kFull, base, 0);
-    if (base + cnt <= a.capacity) process_rows<W>(a, par, occ, s, r0, r1, true, base);
+    const KeyT<W> PP = prefix_parity(par);
+    uint32_t cnt = 0;
+    if (r0 == 0 && r1 > 0) cnt += do_singles<W>(a, par, PP, occ, (uint32_t)s, st, emit);
+    const uint32_t pr0 = r0 == 0 ? 1 : r0;
+    if (r1 > pr0) cnt += do_pairs<W>(a, par, PP, occ, (uint32_t)s, pr0, r1, st, emit);
+    if (!emit && lane == 0 && cnt) atomicAdd(&a.counter[0], (unsigned long long)cnt);
     __syncwarp();
   }
+  if (emit) stage_flush<W>(a, st);
 }
 
 int gen_impl(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* parents, uint64_t n_parents,
@@ -289,18 +429,16 @@ int gen_impl(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* parents, uin
   a.m = sp->m;
   a.n_elec = n;
   a.K = ints->n_spatial;
-  a.rows_per_parent = (uint32_t)(n + n * (n - 1) / 2);
-  const uint64_t target_units = (uint64_t)ctx->num_sms * 64 * 4;
+  a.rows_per_parent = (uint32_t)(1 + n * (n - 1) / 2);
+  const uint64_t target_units = (uint64_t)ctx->num_sms * 16 * 4;
   uint64_t U = (target_units + n_parents - 1) / n_parents;
   if (U < 1) U = 1;
   if (U > a.rows_per_parent) U = a.rows_per_parent;
-  if (a.rows_per_parent == 0) U = 1;
   a.units_per_parent = (uint32_t)U;
   a.n_units = n_parents * U;
   const Prep& pr = ctx->prep;
   a.rowptr = pr.rowptr;
-  a.ab = pr.ab;
-  a.v = pr.v;
+  a.ent = pr.ent;
   a.srowptr = pr.srowptr;
   a.sa = pr.sa;
   a.topp = pr.topp;
@@ -316,11 +454,26 @@ int gen_impl(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* parents, uin
   }
   a.counter = counter;
   a.count_only = count_only ? 1 : 0;
-  const unsigned blocks = (unsigned)ctx->num_sms * (2048 / kGenThreads);
+  static bool attr_set[3] = {false, false, false};
+  if (!attr_set[W]) {
+    if (W == 1)
+      CUSCI_CUDA(ctx, cudaFuncSetAttribute(gen_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GenCfg<1>::SMEM));
+    else
+      CUSCI_CUDA(ctx, cudaFuncSetAttribute(gen_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GenCfg<2>::SMEM));
+    attr_set[W] = true;
+  }
+  const size_t smem = W == 1 ? GenCfg<1>::SMEM : GenCfg<2>::SMEM;
+  static int per_sm[3] = {0, 0, 0};
+  if (!per_sm[W]) {
+    if (W == 1) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[W], gen_kernel<1>, kGenThreads, smem);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[W], gen_kernel<2>, kGenThreads, smem);
+    if (per_sm[W] < 1) per_sm[W] = 1;
+  }
+  const unsigned blocks = (unsigned)(ctx->num_sms * per_sm[W]);
   if (W == 1)
-    CUSCI_LAUNCH(ctx, PT_GEN, gen_kernel<1><<<blocks, kGenThreads, 0, ctx->stream>>>(a));
+    CUSCI_LAUNCH(ctx, PT_GEN, gen_kernel<1><<<blocks, kGenThreads, smem, ctx->stream>>>(a));
   else
-    CUSCI_LAUNCH(ctx, PT_GEN, gen_kernel<2><<<blocks, kGenThreads, 0, ctx->stream>>>(a));
+    CUSCI_LAUNCH(ctx, PT_GEN, gen_kernel<2><<<blocks, kGenThreads, smem, ctx->stream>>>(a));
   unsigned long long res[4];
   CUSCI_CUDA(ctx, cudaMemcpyAsync(ctx->host_pinned, counter, sizeof(res), cudaMemcpyDeviceToHost, ctx->stream));
   CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));

@@ -21,12 +21,33 @@ struct Status {
   int code = CUSCI_OK;
 };
 
-// ------------------------------------------------------------------ scratch
-// Scratch memory comes from a context-owned CUDA memory pool (stream-ordered
-// cudaMallocFromPoolAsync, release threshold = infinity), so steady-state
-// calls reuse cached blocks and never hit the driver allocator.  A Scratch
-// object frees everything it handed out (stream-ordered) when it goes out of
-// scope.
+// ------------------------------------------------------------------ scratch arena
+// Scratch memory is bump-allocated from a context-owned, grow-only device
+// arena (a list of cudaMalloc'd segments).  Scratch scopes nest LIFO; a scope
+// releases its bytes when it ends (all work is ordered on the context stream,
+// so the bytes can be reused by later launches without a sync).  When a call
+// needed more than one segment, the next top-level call synchronises the
+// stream and replaces the segments by one segment of the observed peak, so the
+// steady state performs no device allocation at all.
+struct Arena {
+  struct Seg {
+    char* base;
+    size_t cap;
+  };
+  std::vector<Seg> segs;
+  size_t cur = 0;    // active segment
+  size_t off = 0;    // bump offset in segs[cur]
+  size_t used = 0;   // bytes live across segments
+  size_t peak = 0;   // high-water mark
+  int depth = 0;     // live Scratch scopes
+};
+// pair-table entry (16 B, one 128-bit load): x = occupation mask 2^a | 2^b
+// (m <= 64) or a | b << 8 (m > 64); v = <pq||ab>
+struct __align__(16) PairEnt {
+  uint64_t x;
+  double v;
+};
+
 // Cached Hamiltonian prep: built on device from (h, eri).
 struct Prep {
   const double* h = nullptr;
@@ -37,8 +58,7 @@ struct Prep {
   bool valid = false;
   // pair rows over spin-orbital pairs p<q, row id = q(q-1)/2 + p
   uint32_t* rowptr = nullptr;   // [npq + 1]
-  uint16_t* ab = nullptr;       // [nnz]  a | b << 8   (a < b)
-  double* v = nullptr;          // [nnz]  <pq||ab> (d1-d2 | d1 | -d2), |v| > eps
+  PairEnt* ent = nullptr;       // [nnz]  (a < b, <pq||ab> = d1-d2 | d1 | -d2), |v| > eps
   uint64_t nnz = 0;
   // singles candidates per spin orbital p: targets a (same spin, a != p) with
   // any nonzero constituent integral
@@ -75,6 +95,7 @@ struct cusci_ctx {
   cusci_free_fn free_fn = nullptr;
   void* alloc_user = nullptr;
   cudaMemPool_t pool = nullptr;
+  cusci::Arena arena;
   cusci::Prep prep;
   void* host_pinned = nullptr;  // small pinned staging (counts, flags)
   uint64_t launches = 0;
@@ -141,8 +162,8 @@ struct Prof {
 // scratch (stream-ordered, from the context pool)
 struct Scratch {
   cusci_ctx* ctx;
-  std::vector<void*> ptrs;
-  explicit Scratch(cusci_ctx* c) : ctx(c) {}
+  size_t m_cur, m_off, m_used;
+  explicit Scratch(cusci_ctx* c);
   ~Scratch();
   // returns CUSCI_OK or CUSCI_E_OOM (with message); zero-byte requests give a valid dummy
   int get(size_t bytes, void** p);
@@ -195,6 +216,15 @@ __device__ __forceinline__ uint32_t key_digit(const KeyT<2>& k, int shift) {
   return (uint32_t)((shift < 64 ? (k.w0 >> shift) : (k.w1 >> (shift - 64)))) & 0xffu;
 }
 
+// bits [shift, shift+32) of the big integer (shift < 64W)
+__device__ __forceinline__ uint32_t key_digit_bits(const KeyT<1>& k, int shift) { return (uint32_t)(k.w0 >> shift); }
+__device__ __forceinline__ uint32_t key_digit_bits(const KeyT<2>& k, int shift) {
+  if (shift >= 64) return (uint32_t)(k.w1 >> (shift - 64));
+  const uint64_t lo = k.w0 >> shift;
+  const uint64_t hi = shift ? (k.w1 << (64 - shift)) : 0ull;
+  return (uint32_t)(lo | hi);
+}
+
 // splitmix64 finalizer
 __device__ __forceinline__ uint64_t fmix64(uint64_t x) {
   x ^= x >> 30;
@@ -225,6 +255,48 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return r;
 }
 
+// block-wide exclusive scan of one u32 per thread (smem: >= 33 words); returns
+// this thread's exclusive prefix and the block total
+__device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t v, uint32_t* smem, uint32_t& total) {
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  uint32_t inc = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+    if ((int)lane_id() >= o) inc += t;
+  }
+  if (lane_id() == 31) smem[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    const uint32_t sv = (int)lane_id() < nw ? smem[lane_id()] : 0u;
+    uint32_t si = sv;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, si, o);
+      if ((int)lane_id() >= o) si += t;
+    }
+    if ((int)lane_id() < nw) smem[lane_id()] = si - sv;
+    if (lane_id() == 31) smem[32] = si;
+  }
+  __syncthreads();
+  const uint32_t r = smem[w] + inc - v;
+  total = smem[32];
+  __syncthreads();
+  return r;
+}
+
+// radix pass digit: mode 0 = key bits [shift, shift+bits), 1 = owner-mix bits,
+// 2 = owner(j) among P (bits = ceil(log2 P))
+struct DigitSpec {
+  int mode;
+  int shift;
+  int bits;
+  uint32_t P;
+};
+constexpr int kMaxPasses = 8;
+struct DigitSpecs {
+  DigitSpec d[kMaxPasses];
+  int n;
+};
+
 // ------------------------------------------------------------------ launchers (per .cu)
 int prep_build(cusci_ctx* ctx, const cusci_space* sp, const cusci_integrals* ints, double eps);
 
@@ -232,6 +304,12 @@ int prep_build(cusci_ctx* ctx, const cusci_space* sp, const cusci_integrals* int
 int scan_exclusive_u32(cusci_ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t n);
 int scan_exclusive_u64(cusci_ctx* ctx, const uint64_t* in, uint64_t* out, uint64_t n, uint64_t* total_dev);
 
+// Onesweep LSD passes: pass 0 reads `in` and writes buf0, then the passes
+// alternate buf0 <-> buf1; *out points at the buffer holding the result (`in`
+// itself if every pass was trivial).  hist0 (host, optional, [2^bits of pass 0])
+// receives pass 0's digit histogram.
+int onesweep_passes(cusci_ctx* ctx, int W, const uint64_t* in, uint64_t* buf0, uint64_t* buf1, uint64_t n,
+                    const DigitSpecs& specs, const uint64_t** out, uint64_t* hist0);
 // LSD radix sort of keys[n][W] over bits [0, nbits); the sorted keys end in
 // *out_sorted, which is `keys` or `alt` (both [n][W] device buffers).
 int radix_sort_keys(cusci_ctx* ctx, int W, uint64_t* keys, uint64_t* alt, uint64_t n, int nbits,

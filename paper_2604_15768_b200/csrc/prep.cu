@@ -81,7 +81,7 @@ __global__ void pair_count_kernel(const double* __restrict__ eri, int m, double 
 // ordered fill: the block walks candidates in chunks of blockDim, block-scans
 // the keep flags and appends in candidate order (rows sorted by (b, a)).
 __global__ void pair_fill_kernel(const double* __restrict__ eri, int m, double eps, const uint32_t* __restrict__ rowptr,
-                                 uint16_t* __restrict__ ab, double* __restrict__ vout) {
+                                 PairEnt* __restrict__ ent) {
   const int row = blockIdx.x;
   int q = (int)((1.0 + sqrt(1.0 + 8.0 * (double)row)) * 0.5);
   while (q * (q - 1) / 2 > row) q--;
@@ -112,8 +112,10 @@ __global__ void pair_fill_kernel(const double* __restrict__ eri, int m, double e
     }
     if (keep) {
       const uint32_t pos = base + off + __popc(bal & lanemask_lt());
-      ab[pos] = (uint16_t)(a | (b << 8));
-      vout[pos] = v;
+      PairEnt e;
+      e.x = m <= 64 ? ((1ull << a) | (1ull << b)) : (uint64_t)(a | (b << 8));
+      e.v = v;
+      ent[pos] = e;
     }
     __syncthreads();
     if (threadIdx.x == 0) base += tot;
@@ -210,7 +212,7 @@ int prep_build(cusci_ctx* ctx, const cusci_space* sp, const cusci_integrals* int
   nnz32 = *(uint32_t*)ctx->host_pinned;
   const size_t nnz = nnz32;
   const size_t kkk = (size_t)K * K * K;
-  // one block: rowptr | srowptr | v | topp | tsame | ab | sa
+  // one block: rowptr | srowptr | ent | topp | tsame | sa
   size_t off = 0;
   auto place = [&](size_t bytes) {
     size_t o = off;
@@ -219,10 +221,9 @@ int prep_build(cusci_ctx* ctx, const cusci_space* sp, const cusci_integrals* int
   };
   const size_t o_rowptr = place(sizeof(uint32_t) * (npq + 1));
   const size_t o_srow = place(sizeof(uint32_t) * (m + 1));
-  const size_t o_v = place(sizeof(double) * (nnz ? nnz : 1));
+  const size_t o_ent = place(sizeof(PairEnt) * (nnz ? nnz : 1));
   const size_t o_topp = place(sizeof(double) * kkk);
   const size_t o_tsame = place(sizeof(double) * kkk);
-  const size_t o_ab = place(sizeof(uint16_t) * (nnz ? nnz : 1));
   const size_t o_sa = place((size_t)m * m);
   void* block = nullptr;
   if (cudaMalloc(&block, off) != cudaSuccess) {
@@ -234,16 +235,15 @@ int prep_build(cusci_ctx* ctx, const cusci_space* sp, const cusci_integrals* int
   pr.block_bytes = off;
   pr.rowptr = (uint32_t*)(b8 + o_rowptr);
   pr.srowptr = (uint32_t*)(b8 + o_srow);
-  pr.v = (double*)(b8 + o_v);
+  pr.ent = (PairEnt*)(b8 + o_ent);
   pr.topp = (double*)(b8 + o_topp);
   pr.tsame = (double*)(b8 + o_tsame);
-  pr.ab = (uint16_t*)(b8 + o_ab);
   pr.sa = (uint8_t*)(b8 + o_sa);
   pr.nnz = nnz;
   CUSCI_CUDA(ctx, cudaMemcpyAsync(pr.rowptr, rowptr_tmp, sizeof(uint32_t) * (npq + 1), cudaMemcpyDeviceToDevice,
                                   ctx->stream));
   if (nnz) {
-    CUSCI_LAUNCH(ctx, PT_PREP, pair_fill_kernel<<<npq, 256, 0, ctx->stream>>>(ints->eri, m, eps, pr.rowptr, pr.ab, pr.v));
+    CUSCI_LAUNCH(ctx, PT_PREP, pair_fill_kernel<<<npq, 256, 0, ctx->stream>>>(ints->eri, m, eps, pr.rowptr, pr.ent));
   }
   CUSCI_LAUNCH(ctx, PT_PREP, singles_tables_kernel<<<dim3(K, K), 64, 0, ctx->stream>>>(ints->h, ints->eri, K, pr.topp, pr.tsame, nz));
   CUSCI_LAUNCH(ctx, PT_PREP, singles_rows_kernel<<<1, 32, 0, ctx->stream>>>(nz, K, pr.srowptr, pr.sa));

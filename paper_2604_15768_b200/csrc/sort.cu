@@ -103,106 +103,6 @@ int scan_impl(cusci_ctx* ctx, const T* in, T* out, uint64_t n, T* total_dev) {
   return CUSCI_OK;
 }
 
-// ------------------------------------------------------------------ radix sort
-constexpr int kRadixThreads = 256;
-constexpr int kRadixWarps = kRadixThreads / 32;
-template <int W> struct RadixCfg;
-template <> struct RadixCfg<1> { static constexpr int ITEMS = 16; };
-template <> struct RadixCfg<2> { static constexpr int ITEMS = 8; };
-
-// per-tile digit histogram -> hist[digit * ntiles + tile]
-template <int W>
-__global__ void __launch_bounds__(kRadixThreads) radix_upsweep(const uint64_t* __restrict__ keys, uint64_t n, int shift,
-                                                            uint32_t* __restrict__ hist, uint32_t ntiles) {
-  constexpr int ITEMS = RadixCfg<W>::ITEMS;
-  constexpr int TILE = kRadixThreads * ITEMS;
-  __shared__ uint32_t h[256];
-  h[threadIdx.x] = 0;
-  __syncthreads();
-  const uint64_t base = (uint64_t)blockIdx.x * TILE;
-#pragma unroll
-  for (int i = 0; i < ITEMS; i++) {
-    const uint64_t idx = base + (uint64_t)i * kRadixThreads + threadIdx.x;
-    const bool valid = idx < n;
-    uint32_t d = 256;
-    if (valid) d = key_digit(load_key<W>(keys, idx), shift);
-    const unsigned peers = __match_any_sync(kFull, d);
-    if (valid && (lane_id() == (unsigned)(__ffs(peers) - 1))) atomicAdd(&h[d], (uint32_t)__popc(peers));
-  }
-  __syncthreads();
-  hist[(size_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
-}
-
-template <int W>
-__global__ void __launch_bounds__(kRadixThreads) radix_downsweep(const uint64_t* __restrict__ in, uint64_t* __restrict__ out,
-                                                              uint64_t n, int shift, const uint32_t* __restrict__ offs,
-                                                              uint32_t ntiles) {
-  constexpr int ITEMS = RadixCfg<W>::ITEMS;
-  constexpr int TILE = kRadixThreads * ITEMS;
-  constexpr int WCHUNK = ITEMS * 32;
-  __shared__ uint32_t whist[kRadixWarps][256];
-  __shared__ uint32_t tstart[256];
-  __shared__ uint32_t gbase[256];
-  __shared__ uint32_t red[33];
-  __shared__ KeyT<W> skeys[TILE];
-  const int w = threadIdx.x >> 5;
-  const unsigned lane = lane_id();
-#pragma unroll
-  for (int i = 0; i < kRadixWarps; i++) whist[i][threadIdx.x] = 0;
-  __syncthreads();
-  const uint64_t base = (uint64_t)blockIdx.x * TILE;
-  KeyT<W> k[ITEMS];
-  uint32_t rank[ITEMS], dig[ITEMS];
-#pragma unroll
-  for (int i = 0; i < ITEMS; i++) {
-    const uint64_t idx = base + (uint64_t)w * WCHUNK + (uint64_t)i * 32 + lane;
-    if (idx < n) {
-      k[i] = load_key<W>(in, idx);
-      dig[i] = key_digit(k[i], shift);
-    } else {
-      dig[i] = 256;
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < ITEMS; i++) {
-    const uint32_t d = dig[i];
-    const unsigned peers = __match_any_sync(kFull, d);
-    uint32_t before = 0;
-    if (d < 256) before = whist[w][d];
-    rank[i] = before + __popc(peers & lanemask_lt());
-    __syncwarp();
-    if (d < 256 && lane == (unsigned)(__ffs(peers) - 1)) whist[w][d] = before + __popc(peers);
-    __syncwarp();
-  }
-  __syncthreads();
-  // per digit: exclusive prefix across warps, tile total, tile-local start
-  uint32_t acc = 0;
-#pragma unroll
-  for (int i = 0; i < kRadixWarps; i++) {
-    const uint32_t t = whist[i][threadIdx.x];
-    whist[i][threadIdx.x] = acc;
-    acc += t;
-  }
-  uint32_t tot;
-  const uint32_t st = block_excl_scan<uint32_t>(acc, red, tot);
-  tstart[threadIdx.x] = st;
-  gbase[threadIdx.x] = offs[(size_t)threadIdx.x * ntiles + blockIdx.x];
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < ITEMS; i++) {
-    const uint32_t d = dig[i];
-    if (d < 256) skeys[tstart[d] + whist[w][d] + rank[i]] = k[i];
-  }
-  __syncthreads();
-  const uint64_t rem = n - base;
-  const int cnt = rem < (uint64_t)TILE ? (int)rem : TILE;
-  for (int j = threadIdx.x; j < cnt; j += kRadixThreads) {
-    const KeyT<W> key = skeys[j];
-    const uint32_t d = key_digit(key, shift);
-    store_key<W>(out, (uint64_t)gbase[d] + (uint32_t)j - tstart[d], key);
-  }
-}
-
 // ------------------------------------------------------------------ unique
 constexpr int kUniqThreads = 256;
 constexpr int kUniqItems = 8;
@@ -263,36 +163,6 @@ int scan_exclusive_u32(cusci_ctx* ctx, const uint32_t* in, uint32_t* out, uint64
 }
 int scan_exclusive_u64(cusci_ctx* ctx, const uint64_t* in, uint64_t* out, uint64_t n, uint64_t* total_dev) {
   return scan_impl<uint64_t>(ctx, in, out, n, total_dev);
-}
-
-template <int W>
-static int radix_sort_impl(cusci_ctx* ctx, uint64_t* keys, uint64_t* alt, uint64_t n, int nbits, uint64_t** out_sorted) {
-  *out_sorted = keys;
-  if (n <= 1) return CUSCI_OK;
-  if (n >= (1ull << 32)) return set_error(ctx, CUSCI_E_INVALID_ARG, "radix sort: n=%llu exceeds 2^32", (unsigned long long)n);
-  constexpr int TILE = kRadixThreads * RadixCfg<W>::ITEMS;
-  const uint32_t ntiles = (uint32_t)((n + TILE - 1) / TILE);
-  Scratch s(ctx);
-  uint32_t *hist, *offs;
-  CUSCI_TRY(s.get_t((size_t)256 * ntiles, &hist));
-  CUSCI_TRY(s.get_t((size_t)256 * ntiles, &offs));
-  uint64_t* src = keys;
-  uint64_t* dst = alt;
-  for (int shift = 0; shift < nbits; shift += 8) {
-    CUSCI_LAUNCH(ctx, PT_RADIX_UP, radix_upsweep<W><<<ntiles, kRadixThreads, 0, ctx->stream>>>(src, n, shift, hist, ntiles));
-    CUSCI_TRY(scan_exclusive_u32(ctx, hist, offs, (uint64_t)256 * ntiles));
-    CUSCI_LAUNCH(ctx, PT_RADIX_DOWN, radix_downsweep<W><<<ntiles, kRadixThreads, 0, ctx->stream>>>(src, dst, n, shift, offs, ntiles));
-    uint64_t* t = src;
-    src = dst;
-    dst = t;
-  }
-  *out_sorted = src;
-  return CUSCI_OK;
-}
-
-int radix_sort_keys(cusci_ctx* ctx, int W, uint64_t* keys, uint64_t* alt, uint64_t n, int nbits, uint64_t** out_sorted) {
-  return W == 1 ? radix_sort_impl<1>(ctx, keys, alt, n, nbits, out_sorted)
-                : radix_sort_impl<2>(ctx, keys, alt, n, nbits, out_sorted);
 }
 
 template <int W>

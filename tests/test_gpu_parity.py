@@ -280,3 +280,30 @@ def test_pipeline_lih_merge_inserts_nothing(P, ctx):
     u = ctx.dedup_global(sp, rec.keys)
     ins = ctx.merge_space(pool, u, want_inserted=True)
     assert ins.shape[0] == 0 and len(pool) == 225
+
+
+def test_radix_multi_portion_subprocess():
+    """The onesweep passes chain <= 2^28-key portions on the device; shrink the
+    portion to 2^16 keys (CUSCI_PORTION_LOG2) to exercise that path at small n."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import paper_2604_15768_b200 as P, oracle, synth
+ctx = P.Context(0)
+for W, m, n in [(1, 56, 300_000), (1, 26, 200_001), (2, 96, 150_000), (2, 120, 70_001)]:
+    rng = np.random.default_rng(n)
+    base = rng.integers(1, 1 << min(m, 62), size=(max(1, n // 4), W), dtype=np.uint64)
+    if W == 2:
+        base[:, 1] &= np.uint64((1 << (m - 64)) - 1)
+    keys = base[rng.integers(0, len(base), size=n)]
+    sp = P.Space(m, 1, 1)
+    got = ctx.dedup_global(sp, torch.from_numpy(keys).cuda()).cpu().numpy()
+    assert np.array_equal(got.reshape(-1, W), oracle.dedup(keys, W).reshape(-1, W)), (W, m, n)
+print("OK")
+''' % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CUSCI_PORTION_LOG2="16")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
