@@ -38,10 +38,11 @@ namespace {
 constexpr int kGenThreads = 256;
 constexpr int kGenWarps = kGenThreads / 32;
 constexpr unsigned long long kNoError = ~0ull;
+constexpr int kChunks = 4;  // 32-entry chunks (128-bit loads per lane) in flight per step
 
 template <int W> struct GenCfg {
   static constexpr int STAGE = W == 1 ? 384 : 192;  // staged records per warp (3-5 CTAs/SM)
-  static constexpr size_t BYTES_PER_REC = sizeof(KeyT<W>) + 8 + 4 + 1;
+  static constexpr size_t BYTES_PER_REC = (W == 1 ? 16 : 24) + 4 + 1;
   static constexpr size_t SMEM = (size_t)kGenWarps * STAGE * BYTES_PER_REC;
 };
 
@@ -144,17 +145,36 @@ __global__ void validate_kernel(const uint64_t* __restrict__ parents, uint64_t n
   }
 }
 
-// per-warp staging buffer in shared memory
+// per-warp staging buffer in shared memory: kh = (key, H) interleaved
+// (one 16-byte store per record at W=1), src, phase (only if requested)
+template <int W> struct StRec;
+template <> struct __align__(16) StRec<1> {
+  uint64_t k0;
+  double h;
+};
+template <> struct __align__(8) StRec<2> {
+  uint64_t k0, k1;
+  double h;
+};
 template <int W>
 struct Stage {
-  KeyT<W>* key;
-  double* h;
+  StRec<W>* kh;
   uint32_t* src;
   int8_t* ph;
   uint32_t n;  // warp-uniform fill
 };
+__device__ __forceinline__ void st_put(StRec<1>& r, const KeyT<1>& k, double h) {
+  *reinterpret_cast<ulonglong2*>(&r) = make_ulonglong2(k.w0, (unsigned long long)__double_as_longlong(h));
+}
+__device__ __forceinline__ void st_put(StRec<2>& r, const KeyT<2>& k, double h) {
+  r.k0 = k.w0;
+  r.k1 = k.w1;
+  r.h = h;
+}
+__device__ __forceinline__ KeyT<1> st_key(const StRec<1>& r) { return KeyT<1>{r.k0}; }
+__device__ __forceinline__ KeyT<2> st_key(const StRec<2>& r) { return KeyT<2>{r.k0, r.k1}; }
 
-template <int W>
+template <int W, int MODE>
 __device__ __forceinline__ void stage_flush(const GenArgs& a, Stage<W>& st) {
   if (st.n == 0) return;
   const unsigned lane = lane_id();
@@ -163,12 +183,13 @@ __device__ __forceinline__ void stage_flush(const GenArgs& a, Stage<W>& st) {
   base = __shfl_sync(kFull, base, 0);
   if (base + st.n <= a.capacity) {
     for (uint32_t i = lane; i < st.n; i += 32) {
-      store_key<W>(a.keys, base + i, st.key[i]);
-      a.hij[base + i] = st.h[i];
+      const StRec<W> r = st.kh[i];
+      store_key<W>(a.keys, base + i, st_key(r));
+      a.hij[base + i] = r.h;
     }
     if (a.src)
       for (uint32_t i = lane; i < st.n; i += 32) a.src[base + i] = st.src[i];
-    if (a.phase)
+    if (MODE == 2)
       for (uint32_t i = lane; i < st.n; i += 32) a.phase[base + i] = st.ph[i];
   }
   __syncwarp();
@@ -176,16 +197,15 @@ __device__ __forceinline__ void stage_flush(const GenArgs& a, Stage<W>& st) {
 }
 
 // append the lanes' survivors (ballot `bal`) to the stage
-template <int W>
+template <int W, int MODE>
 __device__ __forceinline__ void stage_put(const GenArgs& a, Stage<W>& st, unsigned bal, bool keep, const KeyT<W>& key,
                                           double H, uint32_t s, uint32_t par) {
-  if (st.n + 32 > (uint32_t)GenCfg<W>::STAGE) stage_flush<W>(a, st);
+  if (st.n + 32 > (uint32_t)GenCfg<W>::STAGE) stage_flush<W, MODE>(a, st);
   if (keep) {
     const uint32_t i = st.n + __popc(bal & lanemask_lt());
-    st.key[i] = key;
-    st.h[i] = H;
+    st_put(st.kh[i], key, H);
     st.src[i] = s;
-    st.ph[i] = par ? -1 : 1;
+    if (MODE == 2) st.ph[i] = par ? -1 : 1;
   }
   __syncwarp();
   st.n += __popc(bal);
@@ -200,9 +220,10 @@ __device__ __forceinline__ uint32_t warp_incl_scan_u32(uint32_t v) {
 }
 
 // row 0: all singles of parent s (flattened over occupied orbitals)
-template <int W>
+template <int W, int MODE>
 __device__ __forceinline__ uint32_t do_singles(const GenArgs& a, const KeyT<W>& par, const KeyT<W>& PP,
-                                               const uint8_t* occ, uint32_t s, Stage<W>& st, bool emit) {
+                                               const uint8_t* occ, uint32_t s, Stage<W>& st) {
+  constexpr bool emit = MODE != 0;
   const unsigned lane = lane_id();
   const int n = a.n_elec;
   uint32_t total_kept = 0;
@@ -255,9 +276,10 @@ __device__ __forceinline__ uint32_t do_singles(const GenArgs& a, const KeyT<W>& 
       const unsigned bal = __ballot_sync(kFull, keep);
       if (emit) {
         const KeyT<W> j = kxor(par, kxor(bitk<W>(pL), bitk<W>(t)));
-        stage_put<W>(a, st, bal, keep, j, H, s, ph);
+        stage_put<W, MODE>(a, st, bal, keep, j, H, s, ph);
+      } else {
+        total_kept += __popc(bal);
       }
-      total_kept += __popc(bal);
     }
   }
   return total_kept;
@@ -267,26 +289,28 @@ __device__ __forceinline__ uint32_t do_singles(const GenArgs& a, const KeyT<W>& 
 // Latency hiding: two 32-entry chunks (two 128-bit loads per lane) are in
 // flight per step, and the next row's CSR bounds are loaded while the current
 // row is processed.
-template <int W>
+template <int W, int MODE>
 __device__ __forceinline__ void pair_chunk(const GenArgs& a, const ulonglong2& raw, bool valid, const KeyT<W>& par,
                                            const KeyT<W>& base, const KeyT<W>& M, uint32_t rc, uint32_t s,
-                                           Stage<W>& st, bool emit, uint32_t& total_kept) {
+                                           Stage<W>& st, uint32_t& total_kept) {
   KeyT<W> abm{};
   ent_mask(raw.x, abm);
   const bool keep = valid && kdisjoint(par, abm);
   const unsigned bal = __ballot_sync(kFull, keep);
-  if (emit) {
-    const double v = __longlong_as_double((long long)raw.y);
+  if (MODE != 0) {
     const uint32_t ph = rc ^ kparity_and(M, abm);
-    stage_put<W>(a, st, bal, keep, kxor(base, abm), ph ? -v : v, s, ph);
+    // H = +-v: flip the sign bit (exact)
+    const double H = __longlong_as_double((long long)(raw.y ^ ((unsigned long long)ph << 63)));
+    stage_put<W, MODE>(a, st, bal, keep, kxor(base, abm), H, s, ph);
+  } else {
+    total_kept += __popc(bal);
   }
-  total_kept += __popc(bal);
 }
 
-template <int W>
+template <int W, int MODE>
 __device__ __forceinline__ uint32_t do_pairs(const GenArgs& a, const KeyT<W>& par, const KeyT<W>& PP,
-                                             const uint8_t* occ, uint32_t s, uint32_t r0, uint32_t r1, Stage<W>& st,
-                                             bool emit) {
+                                             const uint8_t* occ, const ulonglong2* bm, uint32_t s, uint32_t r0,
+                                             uint32_t r1, Stage<W>& st) {
   const unsigned lane = lane_id();
   const int n = a.n_elec;
   uint32_t total_kept = 0;
@@ -317,15 +341,26 @@ __device__ __forceinline__ uint32_t do_pairs(const GenArgs& a, const KeyT<W>& pa
       ne0 = __ldg(a.rowptr + nrow);
       ne1 = __ldg(a.rowptr + nrow + 1);
     }
-    const KeyT<W> base = kxor(par, kxor(bitk<W>(p), bitk<W>(q)));
-    const KeyT<W> M = kxor(PP, kxor(abovek<W>(p), abovek<W>(q)));
+    KeyT<W> base, M;
+    if constexpr (W == 1) {  // per-occupied {2^p, above(p)} precomputed once per unit
+      const ulonglong2 bx = bm[x], by = bm[y];
+      base = KeyT<W>{par.w0 ^ bx.x ^ by.x};
+      M = KeyT<W>{PP.w0 ^ bx.y ^ by.y};
+    } else {
+      base = kxor(par, kxor(bitk<W>(p), bitk<W>(q)));
+      M = kxor(PP, kxor(abovek<W>(p), abovek<W>(q)));
+    }
     const uint32_t rc = (uint32_t)(x + y + 1) & 1u;
-    for (uint32_t e = e0; e < e1; e += 64) {
-      const uint32_t i0 = e + lane, i1 = e + 32 + lane;
-      const ulonglong2 raw0 = i0 < e1 ? __ldg(ent + i0) : make_ulonglong2(~0ull, 0ull);
-      const ulonglong2 raw1 = i1 < e1 ? __ldg(ent + i1) : make_ulonglong2(~0ull, 0ull);
-      pair_chunk<W>(a, raw0, i0 < e1, par, base, M, rc, s, st, emit, total_kept);
-      if (e + 32 < e1) pair_chunk<W>(a, raw1, i1 < e1, par, base, M, rc, s, st, emit, total_kept);
+    for (uint32_t e = e0; e < e1; e += 32 * kChunks) {
+      ulonglong2 raw[kChunks];
+#pragma unroll
+      for (int u = 0; u < kChunks; u++) {
+        const uint32_t i = e + 32 * u + lane;
+        raw[u] = i < e1 ? __ldg(ent + i) : make_ulonglong2(~0ull, 0ull);
+      }
+#pragma unroll
+      for (int u = 0; u < kChunks; u++)
+        if (e + 32 * u < e1) pair_chunk<W, MODE>(a, raw[u], e + 32 * u + lane < e1, par, base, M, rc, s, st, total_kept);
     }
     x = nx;
     y = ny;
@@ -337,21 +372,21 @@ __device__ __forceinline__ uint32_t do_pairs(const GenArgs& a, const KeyT<W>& pa
   return total_kept;
 }
 
-template <int W>
-__global__ void __launch_bounds__(kGenThreads) gen_kernel(const GenArgs a) {
+template <int W, int MODE>
+__global__ void __launch_bounds__(kGenThreads, 3) gen_kernel(const GenArgs a) {
   extern __shared__ __align__(16) unsigned char gsm[];
   __shared__ uint8_t occ_s[kGenWarps][128];
+  __shared__ ulonglong2 bm_s[kGenWarps][W == 1 ? 64 : 1];
   __shared__ unsigned long long unit_s[kGenWarps];
   if (a.counter[2] != kNoError) return;  // invalid parent: write nothing
   const int w = threadIdx.x >> 5;
   const unsigned lane = lane_id();
   constexpr int S = GenCfg<W>::STAGE;
-  const bool emit = !a.count_only;
+  constexpr bool emit = MODE != 0;
   Stage<W> st;
-  st.key = reinterpret_cast<KeyT<W>*>(gsm) + (size_t)w * S;
-  st.h = reinterpret_cast<double*>(gsm + (size_t)kGenWarps * S * sizeof(KeyT<W>)) + (size_t)w * S;
-  st.src = reinterpret_cast<uint32_t*>(gsm + (size_t)kGenWarps * S * (sizeof(KeyT<W>) + 8)) + (size_t)w * S;
-  st.ph = reinterpret_cast<int8_t*>(gsm + (size_t)kGenWarps * S * (sizeof(KeyT<W>) + 12)) + (size_t)w * S;
+  st.kh = reinterpret_cast<StRec<W>*>(gsm) + (size_t)w * S;
+  st.src = reinterpret_cast<uint32_t*>(gsm + (size_t)kGenWarps * S * sizeof(StRec<W>)) + (size_t)w * S;
+  st.ph = reinterpret_cast<int8_t*>(gsm + (size_t)kGenWarps * S * (sizeof(StRec<W>) + 4)) + (size_t)w * S;
   st.n = 0;
   uint8_t* occ = occ_s[w];
   for (;;) {
@@ -376,16 +411,22 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(const GenArgs a) {
       if (b) occ[nocc + __popc(bal & lanemask_lt())] = (uint8_t)t;
       nocc += __popc(bal);
     }
+    if constexpr (W == 1) {
+      for (uint32_t x = lane; x < nocc; x += 32) {
+        const int t = occ[x];
+        bm_s[w][x] = make_ulonglong2(1ull << t, t >= 63 ? 0ull : (~0ull << (t + 1)));
+      }
+    }
     __syncwarp();
     const KeyT<W> PP = prefix_parity(par);
     uint32_t cnt = 0;
-    if (r0 == 0 && r1 > 0) cnt += do_singles<W>(a, par, PP, occ, (uint32_t)s, st, emit);
+    if (r0 == 0 && r1 > 0) cnt += do_singles<W, MODE>(a, par, PP, occ, (uint32_t)s, st);
     const uint32_t pr0 = r0 == 0 ? 1 : r0;
-    if (r1 > pr0) cnt += do_pairs<W>(a, par, PP, occ, (uint32_t)s, pr0, r1, st, emit);
+    if (r1 > pr0) cnt += do_pairs<W, MODE>(a, par, PP, occ, bm_s[w], (uint32_t)s, pr0, r1, st);
     if (!emit && lane == 0 && cnt) atomicAdd(&a.counter[0], (unsigned long long)cnt);
     __syncwarp();
   }
-  if (emit) stage_flush<W>(a, st);
+  if (emit) stage_flush<W, MODE>(a, st);
 }
 
 int gen_impl(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* parents, uint64_t n_parents,
@@ -454,26 +495,19 @@ int gen_impl(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* parents, uin
   }
   a.counter = counter;
   a.count_only = count_only ? 1 : 0;
-  static bool attr_set[3] = {false, false, false};
-  if (!attr_set[W]) {
-    if (W == 1)
-      CUSCI_CUDA(ctx, cudaFuncSetAttribute(gen_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GenCfg<1>::SMEM));
-    else
-      CUSCI_CUDA(ctx, cudaFuncSetAttribute(gen_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GenCfg<2>::SMEM));
-    attr_set[W] = true;
+  const int mode = count_only ? 0 : (out->phase ? 2 : 1);
+  const size_t smem = mode == 0 ? 0 : (W == 1 ? GenCfg<1>::SMEM : GenCfg<2>::SMEM);
+  void (*kern)(const GenArgs) = nullptr;
+  if (W == 1) kern = mode == 0 ? gen_kernel<1, 0> : (mode == 1 ? gen_kernel<1, 1> : gen_kernel<1, 2>);
+  else kern = mode == 0 ? gen_kernel<2, 0> : (mode == 1 ? gen_kernel<2, 1> : gen_kernel<2, 2>);
+  static int per_sm[3][3] = {{0}};
+  if (!per_sm[W][mode]) {
+    CUSCI_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[W][mode], kern, kGenThreads, smem);
+    if (per_sm[W][mode] < 1) per_sm[W][mode] = 1;
   }
-  const size_t smem = W == 1 ? GenCfg<1>::SMEM : GenCfg<2>::SMEM;
-  static int per_sm[3] = {0, 0, 0};
-  if (!per_sm[W]) {
-    if (W == 1) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[W], gen_kernel<1>, kGenThreads, smem);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[W], gen_kernel<2>, kGenThreads, smem);
-    if (per_sm[W] < 1) per_sm[W] = 1;
-  }
-  const unsigned blocks = (unsigned)(ctx->num_sms * per_sm[W]);
-  if (W == 1)
-    CUSCI_LAUNCH(ctx, PT_GEN, gen_kernel<1><<<blocks, kGenThreads, smem, ctx->stream>>>(a));
-  else
-    CUSCI_LAUNCH(ctx, PT_GEN, gen_kernel<2><<<blocks, kGenThreads, smem, ctx->stream>>>(a));
+  const unsigned blocks = (unsigned)(ctx->num_sms * per_sm[W][mode]);
+  CUSCI_LAUNCH(ctx, PT_GEN, kern<<<blocks, kGenThreads, smem, ctx->stream>>>(a));
   unsigned long long res[4];
   CUSCI_CUDA(ctx, cudaMemcpyAsync(ctx->host_pinned, counter, sizeof(res), cudaMemcpyDeviceToHost, ctx->stream));
   CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
