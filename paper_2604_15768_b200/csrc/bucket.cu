@@ -1,0 +1,481 @@
+// Local de-duplication into the hash order (
+// PAPER.md:380-382 local uniqueness filter, :454-460 local sort + unique).
+//
+// B200 design (reading r13): keys are ordered by the hash
+// order pi(j) = (hi, lo) -- a fixed bijection of the key space (hi =
+// owner mix, so owner(j) = floor(hi * P / 2^64) is monotone in it) -- instead
+// of the big-integer order.  Because pi is uniform, a 2-level MSD partition on
+// the top B bits of hi (B = log2(n / ~2k)) puts ~2k keys in every bucket:
+//   pass 1  histogram + scatter by the top hb (<= 9) bits (per-tile shared-
+//           memory ranks, one global atomic per (tile, digit) on an
+//           L2-resident cursor array -- no look-back chain, no stability
+//           requirement);
+//   pass 2  histogram + scatter by the full B bits, tiles binned locally on
+//           the <= 2 pass-1 digits a tile spans (far keys: direct atomics);
+// then ONE CTA per bucket: open-addressing hash table in shared memory
+// (64-bit atomicCAS / ATOMS.CAS.128) keeps the first copy of each key, and
+// the survivors are sorted inside the bucket by a counting sort on the next
+// bits of hi plus an insertion sort of the (rare) collisions.  Buckets are
+// then concatenated in bucket order: the result is sorted in the hash order
+// and unique -- a full sort in two partition passes.  A bucket with more
+// distinct keys than its table holds is flagged; the host then finishes with
+// a full LSD sort over the hash digits + unique (exact, rare slow path).
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace cusci {
+namespace {
+
+constexpr int kBT = 256;        // threads
+constexpr int kBI = 8;          // keys per thread per tile
+constexpr int kBTile = kBT * kBI;
+
+template <int W>
+__device__ __forceinline__ uint32_t top_bits(const KeyT<W>& k, int bits) {
+  return bits ? (uint32_t)(hk_hi(k) >> (64 - bits)) : 0u;
+}
+
+// ---------------------------------------------------------------- partition passes
+// One pass = per-tile digit histograms written to a [digit][tile] matrix, one
+// exclusive scan of the matrix, and a scatter in which every CTA turns its
+// matrix column into shared-memory cursors and places each key with ONE
+// shared-memory atomic (no global atomics, no look-back; order inside a
+// bucket is irrelevant).  Tiles are <= 32 Ki keys, processed 2 Ki at a time.
+// Pass 1 digit = top hb bits of hi over plain tiles; pass 2 digit = the next
+// lb bits, over tiles that never straddle a pass-1 group (the matrix is laid
+// out group by group, so one global scan yields every bucket's offset).
+struct PTile {
+  uint64_t start;   // first key
+  uint32_t len;     // keys in the tile
+  uint32_t stride;  // matrix stride between digits (tiles of this group)
+  uint64_t mbase;   // matrix index of digit 0 of this tile
+};
+constexpr uint32_t kPTile = 32768;
+
+template <int W>
+__global__ void __launch_bounds__(kBT) tile_hist_kernel(const uint64_t* __restrict__ in,
+                                                       const PTile* __restrict__ tiles, int bsel, uint32_t dmask,
+                                                       uint32_t* __restrict__ mat) {
+  __shared__ uint32_t h[2048];
+  const PTile t = tiles[blockIdx.x];
+  for (uint32_t i = threadIdx.x; i <= dmask; i += kBT) h[i] = 0;
+  __syncthreads();
+  for (uint32_t r0 = 0; r0 < t.len; r0 += kBTile) {
+    KeyT<W> k[kBI];
+#pragma unroll
+    for (int u = 0; u < kBI; u++) {
+      const uint32_t i = r0 + u * kBT + threadIdx.x;
+      if (i < t.len) k[u] = load_key<W>(in, t.start + i);
+    }
+#pragma unroll
+    for (int u = 0; u < kBI; u++) {
+      const uint32_t i = r0 + u * kBT + threadIdx.x;
+      if (i < t.len) atomicAdd(&h[top_bits<W>(k[u], bsel) & dmask], 1u);
+    }
+  }
+  __syncthreads();
+  for (uint32_t d = threadIdx.x; d <= dmask; d += kBT) mat[t.mbase + (uint64_t)d * t.stride] = h[d];
+}
+
+template <int W>
+__global__ void __launch_bounds__(kBT) tile_scatter_kernel(const uint64_t* __restrict__ in,
+                                                          const PTile* __restrict__ tiles, int bsel, uint32_t dmask,
+                                                          const uint32_t* __restrict__ offs, uint64_t* __restrict__ out) {
+  __shared__ uint32_t cur[2048];
+  const PTile t = tiles[blockIdx.x];
+  for (uint32_t d = threadIdx.x; d <= dmask; d += kBT) cur[d] = offs[t.mbase + (uint64_t)d * t.stride];
+  __syncthreads();
+  for (uint32_t r0 = 0; r0 < t.len; r0 += kBTile) {
+    KeyT<W> k[kBI];
+#pragma unroll
+    for (int u = 0; u < kBI; u++) {
+      const uint32_t i = r0 + u * kBT + threadIdx.x;
+      if (i < t.len) k[u] = load_key<W>(in, t.start + i);
+    }
+#pragma unroll
+    for (int u = 0; u < kBI; u++) {
+      const uint32_t i = r0 + u * kBT + threadIdx.x;
+      if (i < t.len) store_key<W>(out, atomicAdd(&cur[top_bits<W>(k[u], bsel) & dmask], 1u), k[u]);
+    }
+  }
+}
+
+// bucket (g, d) offsets after pass 2: gmeta[g] = {group start, tiles, matrix base}
+__global__ void bucket_off_kernel(const uint32_t* __restrict__ offs2, const uint4* __restrict__ gmeta, uint32_t R1,
+                                  int lb, uint32_t n, uint32_t* __restrict__ off) {
+  const uint32_t L = 1u << lb;
+  const uint32_t id = blockIdx.x * blockDim.x + threadIdx.x;
+  if (id > R1 * L) return;
+  if (id == R1 * L) {
+    off[id] = n;
+    return;
+  }
+  const uint32_t g = id >> lb, d = id & (L - 1);
+  const uint4 m = gmeta[g];  // x = start, y = tiles, z = mbase
+  off[id] = m.y ? offs2[m.z + (uint64_t)d * m.y] : m.x;
+}
+
+// ---------------------------------------------------------------- per-bucket dedup + sort
+template <int W> struct BDCfg {
+  static constexpr uint32_t TS = W == 1 ? 8192 : 4096;  // table slots (64 KB)
+  static constexpr uint32_t LIMIT = TS / 2;              // distinct keys per bucket
+  static constexpr size_t SMEM = (size_t)TS * sizeof(KeyT<W>) + (size_t)LIMIT * sizeof(KeyT<W>);
+};
+
+__device__ __forceinline__ void cas_slot(KeyT<1>* slot, const KeyT<1>& k, KeyT<1>& old) {
+  old.w0 = atomicCAS(reinterpret_cast<unsigned long long*>(&slot->w0), 0ull, (unsigned long long)k.w0);
+}
+__device__ __forceinline__ void cas_slot(KeyT<2>* slot, const KeyT<2>& k, KeyT<2>& old) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(slot);
+  uint64_t o0, o1;
+  asm volatile(
+      "{\n\t.reg .b128 c, v, o;\n\t"
+      "mov.b128 c, {%2, %3};\n\t"
+      "mov.b128 v, {%4, %5};\n\t"
+      "atom.shared.cas.b128 o, [%6], c, v;\n\t"
+      "mov.b128 {%0, %1}, o;\n\t}"
+      : "=l"(o0), "=l"(o1)
+      : "l"(0ull), "l"(0ull), "l"(k.w0), "l"(k.w1), "r"(sa)
+      : "memory");
+  old.w0 = o0;
+  old.w1 = o1;
+}
+__device__ __forceinline__ bool kzero(const KeyT<1>& k) { return k.w0 == 0; }
+__device__ __forceinline__ bool kzero(const KeyT<2>& k) { return (k.w0 | k.w1) == 0; }
+
+// returns true iff k was inserted (first copy); *full set when no slot found
+template <int W>
+__device__ __forceinline__ bool tab_insert(KeyT<W>* tab, uint32_t ts, const KeyT<W>& k, int* s_zero, bool* full) {
+  if (kzero(k)) return atomicExch(s_zero, 1) == 0;
+  uint32_t h = (uint32_t)slot_hash(k) & (ts - 1);
+  for (uint32_t probe = 0; probe < ts; probe++) {
+    const KeyT<W> cur = tab[h];
+    if (key_eq(cur, k)) return false;
+    if (kzero(cur)) {
+      KeyT<W> old;
+      cas_slot(&tab[h], k, old);
+      if (kzero(old)) return true;
+      if (key_eq(old, k)) return false;
+    }
+    h = (h + 1) & (ts - 1);
+  }
+  *full = true;
+  return false;
+}
+
+template <int W>
+__global__ void __launch_bounds__(kBT) bucket_dedup_sort_kernel(const uint64_t* __restrict__ part,
+                                                               const uint32_t* __restrict__ off, uint32_t nb, int B,
+                                                               uint64_t* __restrict__ tmp,
+                                                               uint32_t* __restrict__ surv,
+                                                               unsigned long long* __restrict__ flags) {
+  extern __shared__ __align__(16) unsigned char bsm[];
+  constexpr uint32_t TS = BDCfg<W>::TS, LIMIT = BDCfg<W>::LIMIT;
+  KeyT<W>* tab = reinterpret_cast<KeyT<W>*>(bsm);
+  KeyT<W>* sv = tab + TS;
+  // after the dedup the table region is reused: sorted keys + bin counters
+  KeyT<W>* so = tab;
+  uint32_t* bins = reinterpret_cast<uint32_t*>(tab + LIMIT);
+  __shared__ int s_zero;
+  __shared__ uint32_t s_ns;
+  __shared__ int s_bad;
+  __shared__ uint32_t red[33];
+  for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    const uint32_t start = off[b], cnt = off[b + 1] - start;
+    if (cnt == 0) {
+      if (threadIdx.x == 0) surv[b] = 0;
+      continue;
+    }
+    uint32_t ts = 64;
+    while (ts < 2 * cnt && ts < TS) ts <<= 1;
+    for (uint32_t i = threadIdx.x; i < ts; i += kBT) tab[i] = KeyT<W>{};
+    if (threadIdx.x == 0) {
+      s_zero = 0;
+      s_ns = 0;
+      s_bad = 0;
+    }
+    __syncthreads();
+    bool full = false;
+    for (uint32_t r0 = 0; r0 < cnt; r0 += kBTile) {
+      KeyT<W> k[kBI];
+#pragma unroll
+      for (int u = 0; u < kBI; u++) {
+        const uint32_t i = r0 + u * kBT + threadIdx.x;
+        if (i < cnt) k[u] = load_key<W>(part, (uint64_t)start + i);
+      }
+#pragma unroll
+      for (int u = 0; u < kBI; u++) {
+        const uint32_t i = r0 + u * kBT + threadIdx.x;
+        if (i < cnt && tab_insert<W>(tab, ts, k[u], &s_zero, &full)) {
+          const uint32_t j = atomicAdd(&s_ns, 1u);
+          if (j < LIMIT) sv[j] = k[u];
+        }
+      }
+    }
+    if (full) s_bad = 1;
+    __syncthreads();
+    const uint32_t ns = s_ns;
+    if (s_bad || ns > LIMIT) {
+      // overflow: pass the bucket through unfiltered and let the host finish
+      for (uint32_t i = threadIdx.x; i < cnt; i += kBT)
+        store_key<W>(tmp, (uint64_t)start + i, load_key<W>(part, (uint64_t)start + i));
+      if (threadIdx.x == 0) {
+        surv[b] = cnt;
+        atomicAdd(&flags[0], 1ull);
+      }
+      __syncthreads();
+      continue;
+    }
+    // counting sort of the survivors on the next sb bits of hi
+    int sb = 8;
+    while ((1u << sb) < ns && sb < 12) sb++;
+    const uint32_t NB = 1u << sb;
+    const int shift = 64 - B - sb;  // B + sb <= 64 always (B <= 24)
+    for (uint32_t i = threadIdx.x; i < NB; i += kBT) bins[i] = 0;
+    __syncthreads();
+    uint32_t myrank[LIMIT / kBT];
+#pragma unroll
+    for (int u = 0; u < (int)(LIMIT / kBT); u++) {
+      const uint32_t i = u * kBT + threadIdx.x;
+      if (i < ns) myrank[u] = atomicAdd(&bins[(uint32_t)(hk_hi(sv[i]) >> shift) & (NB - 1)], 1u);
+    }
+    __syncthreads();
+    // exclusive scan of the NB bin counts (NB / 256 consecutive bins per thread)
+    const uint32_t per = NB / kBT;
+    uint32_t loc = 0;
+    uint32_t cnts[16];
+    for (uint32_t j = 0; j < per; j++) {
+      cnts[j] = bins[threadIdx.x * per + j];
+      loc += cnts[j];
+    }
+    uint32_t tot;
+    uint32_t ex = block_excl_scan_u32(loc, red, tot);
+    for (uint32_t j = 0; j < per; j++) {
+      bins[threadIdx.x * per + j] = ex;  // bin start
+      ex += cnts[j];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < (int)(LIMIT / kBT); u++) {
+      const uint32_t i = u * kBT + threadIdx.x;
+      if (i < ns) {
+        const KeyT<W> key = sv[i];
+        so[bins[(uint32_t)(hk_hi(key) >> shift) & (NB - 1)] + myrank[u]] = key;
+      }
+    }
+    __syncthreads();
+    // order the (few) keys that share a bin: insertion sort in the hash order
+    for (uint32_t bi = threadIdx.x; bi < NB; bi += kBT) {
+      const uint32_t s0 = bins[bi];
+      const uint32_t s1 = (bi + 1 < NB) ? bins[bi + 1] : ns;
+      for (uint32_t i = s0 + 1; i < s1; i++) {
+        const KeyT<W> key = so[i];
+        uint32_t j = i;
+        while (j > s0 && hk_lt(key, so[j - 1])) {
+          so[j] = so[j - 1];
+          j--;
+        }
+        so[j] = key;
+      }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < ns; i += kBT) store_key<W>(tmp, (uint64_t)start + i, so[i]);
+    if (threadIdx.x == 0) surv[b] = ns;
+    __syncthreads();
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(kBT) bucket_compact_kernel(const uint64_t* __restrict__ tmp,
+                                                            const uint32_t* __restrict__ off,
+                                                            const uint32_t* __restrict__ surv,
+                                                            const uint64_t* __restrict__ soff, uint32_t nb,
+                                                            uint64_t* __restrict__ out) {
+  for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    const uint32_t start = off[b], ns = surv[b];
+    const uint64_t o = soff[b];
+    for (uint32_t i = threadIdx.x; i < ns; i += kBT) store_key<W>(out, o + i, load_key<W>(tmp, (uint64_t)start + i));
+  }
+}
+
+// boundaries of the owner ranges in a hash-ordered array: bnd[r] = first index with owner >= r
+template <int W>
+__global__ void owner_bounds_kernel(const uint64_t* __restrict__ keys, uint64_t n, uint32_t P, uint64_t* __restrict__ bnd) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r > P) return;
+  uint64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (owner_of<W>(load_key<W>(keys, mid), P) < r) lo = mid + 1;
+    else hi = mid;
+  }
+  bnd[r] = lo;
+}
+
+template <int W>
+int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* out, uint64_t* n_out) {
+  *n_out = 0;
+  if (n == 0) return CUSCI_OK;
+  Scratch s(ctx);
+  // B bits of hi: ~<= 2048 keys per bucket on average
+  int B = 0;
+  while ((n >> B) > 2048 && B < 20) B++;
+  const int lb = B > 9 ? std::min(9, B / 2) : 0, hb = B - lb;  // hb <= 11, lb <= 9
+  const uint32_t nb = 1u << B;
+  uint64_t *a, *b2;
+  uint32_t *hist, *off, *cur, *surv;
+  uint64_t *surv64, *soff;
+  unsigned long long* flags;
+  CUSCI_TRY(s.get_t(n * W, &a));
+  CUSCI_TRY(s.get_t(n * W, &b2));
+  CUSCI_TRY(s.get_t(nb + 1, &hist));
+  CUSCI_TRY(s.get_t(nb + 1, &off));
+  CUSCI_TRY(s.get_t(nb + 1, &cur));
+  CUSCI_TRY(s.get_t(nb + 1, &surv));
+  CUSCI_TRY(s.get_t(nb + 1, &surv64));
+  CUSCI_TRY(s.get_t(nb + 1, &soff));
+  CUSCI_TRY(s.get_t(2, &flags));
+  CUSCI_CUDA(ctx, cudaMemsetAsync(flags, 0, 2 * sizeof(unsigned long long), ctx->stream));
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + kBTile - 1) / kBTile, (uint64_t)ctx->num_sms * 8));
+  const uint64_t* part = in;
+  if (B > 0) {
+    // ---- pass 1: plain tiles, digit = top hb bits
+    const uint32_t R1 = 1u << hb;
+    const uint32_t nt1 = (uint32_t)((n + kPTile - 1) / kPTile);
+    std::vector<PTile> t1(nt1);
+    for (uint32_t t = 0; t < nt1; t++)
+      t1[t] = PTile{(uint64_t)t * kPTile, (uint32_t)std::min<uint64_t>(kPTile, n - (uint64_t)t * kPTile), nt1, t};
+    PTile* dt1;
+    uint32_t *mat1, *offs1;
+    CUSCI_TRY(s.get_t(nt1, &dt1));
+    CUSCI_TRY(s.get_t((uint64_t)R1 * nt1, &mat1));
+    CUSCI_TRY(s.get_t((uint64_t)R1 * nt1, &offs1));
+    CUSCI_CUDA(ctx, cudaMemcpyAsync(dt1, t1.data(), nt1 * sizeof(PTile), cudaMemcpyHostToDevice, ctx->stream));
+    CUSCI_LAUNCH(ctx, PT_RADIX_UP, tile_hist_kernel<W><<<nt1, kBT, 0, ctx->stream>>>(in, dt1, hb, R1 - 1, mat1));
+    CUSCI_TRY(scan_exclusive_u32(ctx, mat1, offs1, (uint64_t)R1 * nt1));
+    CUSCI_LAUNCH(ctx, PT_RADIX_DOWN, tile_scatter_kernel<W><<<nt1, kBT, 0, ctx->stream>>>(in, dt1, hb, R1 - 1, offs1, a));
+    part = a;
+    if (lb == 0) {
+      // buckets = pass-1 groups: off[g] = offs1[g * nt1]
+      CUSCI_CUDA(ctx, cudaMemcpy2DAsync(off, sizeof(uint32_t), offs1, (size_t)nt1 * sizeof(uint32_t), sizeof(uint32_t),
+                                        R1, cudaMemcpyDeviceToDevice, ctx->stream));
+      const uint32_t nn = (uint32_t)n;
+      memcpy(ctx->host_pinned, &nn, 4);
+      CUSCI_CUDA(ctx, cudaMemcpyAsync(off + R1, ctx->host_pinned, 4, cudaMemcpyHostToDevice, ctx->stream));
+      CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    } else {
+      // ---- pass 2: tiles inside each pass-1 group, digit = next lb bits
+      std::vector<uint32_t> gstart(R1 + 1);
+      CUSCI_CUDA(ctx, cudaMemcpy2DAsync(ctx->host_pinned, sizeof(uint32_t), offs1, (size_t)nt1 * sizeof(uint32_t),
+                                        sizeof(uint32_t), R1, cudaMemcpyDeviceToHost, ctx->stream));
+      CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+      memcpy(gstart.data(), ctx->host_pinned, R1 * sizeof(uint32_t));
+      gstart[R1] = (uint32_t)n;
+      const uint32_t L = 1u << lb;
+      std::vector<PTile> t2;
+      std::vector<uint4> gm(R1);
+      t2.reserve(nt1 + R1);
+      uint64_t mb = 0;
+      for (uint32_t g = 0; g < R1; g++) {
+        const uint64_t gs = gstart[g], ge = gstart[g + 1];
+        const uint32_t chunks = (uint32_t)((ge - gs + kPTile - 1) / kPTile);
+        gm[g] = make_uint4((uint32_t)gs, chunks, (uint32_t)mb, 0u);
+        for (uint32_t c = 0; c < chunks; c++) {
+          const uint64_t st = gs + (uint64_t)c * kPTile;
+          t2.push_back(PTile{st, (uint32_t)std::min<uint64_t>(kPTile, ge - st), chunks, mb + c});
+        }
+        mb += (uint64_t)L * chunks;
+      }
+      const uint32_t nt2 = (uint32_t)t2.size();
+      PTile* dt2;
+      uint4* dgm;
+      uint32_t *mat2, *offs2;
+      CUSCI_TRY(s.get_t(std::max<uint32_t>(nt2, 1), &dt2));
+      CUSCI_TRY(s.get_t(R1, &dgm));
+      CUSCI_TRY(s.get_t(std::max<uint64_t>(mb, 1), &mat2));
+      CUSCI_TRY(s.get_t(std::max<uint64_t>(mb, 1), &offs2));
+      CUSCI_CUDA(ctx, cudaMemcpyAsync(dt2, t2.data(), nt2 * sizeof(PTile), cudaMemcpyHostToDevice, ctx->stream));
+      CUSCI_CUDA(ctx, cudaMemcpyAsync(dgm, gm.data(), R1 * sizeof(uint4), cudaMemcpyHostToDevice, ctx->stream));
+      CUSCI_LAUNCH(ctx, PT_RADIX_UP, tile_hist_kernel<W><<<nt2, kBT, 0, ctx->stream>>>(a, dt2, B, L - 1, mat2));
+      CUSCI_TRY(scan_exclusive_u32(ctx, mat2, offs2, mb));
+      CUSCI_LAUNCH(ctx, PT_RADIX_DOWN, tile_scatter_kernel<W><<<nt2, kBT, 0, ctx->stream>>>(a, dt2, B, L - 1, offs2, b2));
+      CUSCI_LAUNCH(ctx, PT_SCATTER, bucket_off_kernel<<<(nb + 1 + 255) / 256, 256, 0, ctx->stream>>>(offs2, dgm, R1, lb, (uint32_t)n, off));
+      part = b2;
+      CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // host vectors t2/gm die at scope end
+    }
+  } else {
+    const uint32_t o2[2] = {0u, (uint32_t)n};
+    memcpy(ctx->host_pinned, o2, sizeof(o2));
+    CUSCI_CUDA(ctx, cudaMemcpyAsync(off, ctx->host_pinned, sizeof(o2), cudaMemcpyHostToDevice, ctx->stream));
+    CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  }
+  uint64_t* tmp = (part == a) ? b2 : a;
+  static bool attr[3] = {false, false, false};
+  if (!attr[W]) {
+    CUSCI_CUDA(ctx, cudaFuncSetAttribute(bucket_dedup_sort_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)BDCfg<W>::SMEM));
+    attr[W] = true;
+  }
+  const unsigned dgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(nb, (uint64_t)ctx->num_sms * 2));
+  CUSCI_LAUNCH(ctx, PT_HASH, bucket_dedup_sort_kernel<W><<<dgrid, kBT, BDCfg<W>::SMEM, ctx->stream>>>(part, off, nb, B, tmp, surv, flags));
+  // compact the buckets' survivors in bucket order
+  CUSCI_CUDA(ctx, cudaMemsetAsync(surv64, 0, (nb + 1) * sizeof(uint64_t), ctx->stream));
+  CUSCI_CUDA(ctx, cudaMemcpy2DAsync(surv64, sizeof(uint64_t), surv, sizeof(uint32_t), sizeof(uint32_t), nb,
+                                    cudaMemcpyDeviceToDevice, ctx->stream));
+  CUSCI_TRY(scan_exclusive_u64(ctx, surv64, soff, nb + 1, nullptr));
+  CUSCI_LAUNCH(ctx, PT_SCATTER, bucket_compact_kernel<W><<<dgrid, kBT, 0, ctx->stream>>>(tmp, off, surv, soff, nb, out));
+  uint64_t h[2];
+  CUSCI_CUDA(ctx, cudaMemcpyAsync(ctx->host_pinned, soff + nb, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  CUSCI_CUDA(ctx, cudaMemcpyAsync((char*)ctx->host_pinned + 8, flags, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  memcpy(h, ctx->host_pinned, sizeof(h));
+  *n_out = h[0];
+  if (h[1]) {
+    // rare slow path: some bucket overflowed its table -> full LSD sort over the
+    // hash digits (lo then hi for W = 2) + adjacent unique
+    DigitSpecs sp{};
+    const uint64_t m = h[0];
+    uint64_t* cur_buf = out;
+    for (int part_i = (W == 2 ? 0 : 1); part_i < 2; part_i++) {
+      sp = DigitSpecs{};
+      for (int sh = 0; sh < 64; sh += 8) sp.d[sp.n++] = DigitSpec{part_i == 0 ? 3 : 1, sh, 8, 0u};
+      const uint64_t* o = cur_buf;
+      CUSCI_TRY(onesweep_passes(ctx, W, cur_buf, a, b2, m, sp, &o, nullptr));
+      if (o != out) CUSCI_CUDA(ctx, cudaMemcpyAsync(out, o, m * W * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    uint64_t* cnt;
+    CUSCI_TRY(s.get_t(1, &cnt));
+    CUSCI_CUDA(ctx, cudaMemcpyAsync(a, out, m * W * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    CUSCI_TRY(unique_sorted_keys(ctx, W, a, m, out, cnt));
+    CUSCI_TRY(read_u64(ctx, cnt, n_out, 1));
+  }
+  return CUSCI_OK;
+}
+
+template <int W>
+int owner_bounds_impl(cusci_ctx* ctx, const uint64_t* keys, uint64_t n, int P, uint64_t* counts) {
+  Scratch s(ctx);
+  uint64_t* bnd;
+  CUSCI_TRY(s.get_t(P + 1, &bnd));
+  CUSCI_LAUNCH(ctx, PT_SCATTER, owner_bounds_kernel<W><<<(P + 1 + 63) / 64, 64, 0, ctx->stream>>>(keys, n, (uint32_t)P, bnd));
+  uint64_t hb[513];
+  CUSCI_TRY(read_u64(ctx, bnd, hb, P + 1));
+  for (int r = 0; r < P; r++) counts[r] = hb[r + 1] - hb[r];
+  return CUSCI_OK;
+}
+
+}  // namespace
+
+int local_dedup(cusci_ctx* ctx, int W, const uint64_t* in, uint64_t n, uint64_t* out, uint64_t* n_out) {
+  if (n >= (1ull << 32)) return set_error(ctx, CUSCI_E_INVALID_ARG, "dedup: n=%llu exceeds 2^32", (unsigned long long)n);
+  return W == 1 ? local_dedup_impl<1>(ctx, in, n, out, n_out) : local_dedup_impl<2>(ctx, in, n, out, n_out);
+}
+
+int owner_counts(cusci_ctx* ctx, int W, const uint64_t* keys, uint64_t n, int P, uint64_t* counts) {
+  return W == 1 ? owner_bounds_impl<1>(ctx, keys, n, P, counts) : owner_bounds_impl<2>(ctx, keys, n, P, counts);
+}
+
+}  // namespace cusci

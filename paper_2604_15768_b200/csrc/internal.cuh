@@ -242,6 +242,20 @@ __device__ __forceinline__ uint64_t owner_mix(const KeyT<2>& k) {
 template <int W> __device__ __forceinline__ uint32_t owner_of(const KeyT<W>& k, uint32_t P) {
   return (uint32_t)__umul64hi(owner_mix(k), (uint64_t)P);
 }
+// Hash order (reading r13): pi(j) = (hi, lo), a bijection of the
+// key space; hi = owner mix (owner(j) = floor(hi P / 2^64) is monotone in pi).
+//   W = 1: hi = fmix(w0), lo = 0;   W = 2: lo = fmix(w1 ^ C), hi = fmix(w0 ^ lo).
+__device__ __forceinline__ uint64_t hk_hi(const KeyT<1>& k) { return fmix64(k.w0); }
+__device__ __forceinline__ uint64_t hk_hi(const KeyT<2>& k) { return owner_mix(k); }
+__device__ __forceinline__ uint64_t hk_lo(const KeyT<1>&) { return 0ull; }
+__device__ __forceinline__ uint64_t hk_lo(const KeyT<2>& k) { return fmix64(k.w1 ^ 0x9E3779B97F4A7C15ull); }
+template <int W> __device__ __forceinline__ bool hk_lt(const KeyT<W>& a, const KeyT<W>& b) {
+  const uint64_t ha = hk_hi(a), hb = hk_hi(b);
+  if (W == 1) return ha < hb;
+  return ha < hb || (ha == hb && hk_lo(a) < hk_lo(b));
+}
+template <int W> __device__ __forceinline__ bool hk_le(const KeyT<W>& a, const KeyT<W>& b) { return !hk_lt<W>(b, a); }
+
 // hash-table slot hash (independent of the owner mix)
 __device__ __forceinline__ uint64_t slot_hash(const KeyT<1>& k) { return fmix64(k.w0 ^ 0xD6E8FEB86659FD93ull); }
 __device__ __forceinline__ uint64_t slot_hash(const KeyT<2>& k) {
@@ -283,8 +297,8 @@ __device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t v, uint32_t* sm
   return r;
 }
 
-// radix pass digit: mode 0 = key bits [shift, shift+bits), 1 = owner-mix bits,
-// 2 = owner(j) among P (bits = ceil(log2 P))
+// radix pass digit: mode 0 = key bits [shift, shift+bits), 1 = hash-order hi
+// (owner-mix) bits, 2 = owner(j) among P (bits = ceil(log2 P)), 3 = hash lo bits
 struct DigitSpec {
   int mode;
   int shift;
@@ -314,6 +328,11 @@ int onesweep_passes(cusci_ctx* ctx, int W, const uint64_t* in, uint64_t* buf0, u
 // *out_sorted, which is `keys` or `alt` (both [n][W] device buffers).
 int radix_sort_keys(cusci_ctx* ctx, int W, uint64_t* keys, uint64_t* alt, uint64_t n, int nbits,
                     uint64_t** out_sorted);
+// local dedup (bucket.cu): out (capacity n) receives the distinct keys of in,
+// sorted in the hash order; *n_out their number (host)
+int local_dedup(cusci_ctx* ctx, int W, const uint64_t* in, uint64_t n, uint64_t* out, uint64_t* n_out);
+// owner range sizes of a hash-ordered array (host counts[P])
+int owner_counts(cusci_ctx* ctx, int W, const uint64_t* keys, uint64_t n, int P, uint64_t* counts);
 // unique compaction of sorted keys into out; count written to device *n_out_dev
 int unique_sorted_keys(cusci_ctx* ctx, int W, const uint64_t* in, uint64_t n, uint64_t* out,
                        uint64_t* n_out_dev);

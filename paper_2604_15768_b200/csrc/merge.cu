@@ -34,7 +34,7 @@ __global__ void merge_split_kernel(const uint64_t* __restrict__ S, uint64_t nS, 
   uint64_t lo = d > nU ? d - nU : 0, hi = std::min(d, nS);
   while (lo < hi) {
     const uint64_t mid = (lo + hi) >> 1;
-    if (key_le(load_key<W>(S, mid), load_key<W>(U, d - mid - 1))) lo = mid + 1;
+    if (hk_le<W>(load_key<W>(S, mid), load_key<W>(U, d - mid - 1))) lo = mid + 1;
     else hi = mid;
   }
   split[t] = lo;
@@ -45,7 +45,7 @@ template <int W>
 __global__ void check_sorted_kernel(const uint64_t* __restrict__ U, uint64_t n, int* __restrict__ flag) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x + 1; i < n; i += stride)
-    if (!key_lt(load_key<W>(U, i - 1), load_key<W>(U, i))) *flag = 1;
+    if (!hk_lt<W>(load_key<W>(U, i - 1), load_key<W>(U, i))) *flag = 1;
 }
 
 template <int W>
@@ -80,12 +80,12 @@ __global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(const uint64_
     int lo = k0 > nb ? k0 - nb : 0, hi = std::min(k0, na);
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      if (key_le(A[mid], B[k0 - mid - 1])) lo = mid + 1;
+      if (hk_le<W>(A[mid], B[k0 - mid - 1])) lo = mid + 1;
       else hi = mid;
     }
     int i = lo, j = k0 - lo;
     for (int k = k0; k < std::min(k0 + kMergeItems, len); k++) {
-      const bool takeA = i < na && (j >= nb || key_le(A[i], B[j]));
+      const bool takeA = i < na && (j >= nb || hk_le<W>(A[i], B[j]));
       if (takeA) {
         mrg[k] = A[i++];
         fromU[k] = 0;
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(const uint64_
   }
   if (j0 > 0) {
     const KeyT<W> u = load_key<W>(U, j0 - 1);
-    if (!has_prev0 || key_lt(prev0, u)) prev0 = u;
+    if (!has_prev0 || hk_lt<W>(prev0, u)) prev0 = u;
     has_prev0 = true;
   }
   if (threadIdx.x == 0) {

@@ -48,6 +48,7 @@ __device__ __forceinline__ uint32_t digit_of(const KeyT<W>& k, const DigitSpec& 
   const uint32_t mask = (1u << d.bits) - 1u;
   if (d.mode == 0) return key_digit_bits(k, d.shift) & mask;
   if (d.mode == 1) return (uint32_t)(owner_mix(k) >> d.shift) & mask;
+  if (d.mode == 3) return (uint32_t)(hk_lo(k) >> d.shift) & mask;
   return owner_of<W>(k, d.P);
 }
 

@@ -27,6 +27,38 @@ def ctx(P):
     c.close()
 
 
+def fmix64(x):
+    x = np.asarray(x, dtype=np.uint64).copy()
+    with np.errstate(over="ignore"):
+        x ^= x >> np.uint64(30)
+        x *= np.uint64(0xBF58476D1CE4E5B9)
+        x ^= x >> np.uint64(27)
+        x *= np.uint64(0x94D049BB133111EB)
+        x ^= x >> np.uint64(31)
+    return x
+
+
+def hash_hi_lo(keys, W):
+    """Hash order pi(j) = (hi, lo) (reading r13), written from its definition."""
+    keys = np.asarray(keys, dtype=np.uint64).reshape(-1, W)
+    if W == 1:
+        return fmix64(keys[:, 0]), np.zeros(len(keys), dtype=np.uint64)
+    lo = fmix64(keys[:, 1] ^ np.uint64(0x9E3779B97F4A7C15))
+    return fmix64(keys[:, 0] ^ lo), lo
+
+
+def hash_sort(keys, W):
+    keys = np.asarray(keys, dtype=np.uint64).reshape(-1, W)
+    hi, lo = hash_hi_lo(keys, W)
+    return keys[np.lexsort((lo, hi))]
+
+
+def assert_hash_sorted_unique(keys, W):
+    hi, lo = hash_hi_lo(keys, W)
+    if len(hi) > 1:
+        assert np.all((hi[1:] > hi[:-1]) | ((hi[1:] == hi[:-1]) & (lo[1:] > lo[:-1]))), "not strictly in hash order"
+
+
 def canon(keys, src, *cols):
     """sort records by (src, key big-integer)"""
     keys = np.asarray(keys).reshape(len(keys), -1)
@@ -190,16 +222,18 @@ def test_dedup_lih_closure(P, ctx):
     di = P.DeviceIntegrals(ints.h, ints.eri)
     rec = ctx.gen_coupled(sp, torch.from_numpy(par).cuda(), di, 0.0)
     u = ctx.dedup_global(sp, rec.keys).cpu().numpy()
-    assert np.array_equal(u, par)          # 20,700 records -> the 225 parents
+    assert_hash_sorted_unique(u, 1)
+    assert np.array_equal(synth.sort_keys(u), par)          # 20,700 records -> the 225 parents
 
 
 @pytest.mark.parametrize("W,n", [(1, 0), (1, 1), (1, 5000), (1, 1_000_003), (2, 700_001)])
 def test_dedup_zipf(P, ctx, W, n):
     sp = P.Space(64 * W, 1, 1)
     keys = synth.zipf_keys(max(n, 1), W, 1.1, 1 << 18, seed=11 + W)[:n]
-    got = _dedup_gpu(P, ctx, sp, keys)
+    got = _dedup_gpu(P, ctx, sp, keys).reshape(-1, W)
     ref = oracle.dedup(keys, W)
-    assert np.array_equal(got.reshape(-1, W), ref.reshape(-1, W))
+    assert_hash_sorted_unique(got, W)
+    assert np.array_equal(synth.sort_keys(got), ref.reshape(-1, W))
 
 
 def test_dedup_generated_stream(P, ctx):
@@ -209,7 +243,8 @@ def test_dedup_generated_stream(P, ctx):
     rec = ctx.gen_coupled(sp, torch.from_numpy(par).cuda(), di, 0.0)
     got = ctx.dedup_global(sp, rec.keys).cpu().numpy()
     ref = oracle.dedup(rec.keys.cpu().numpy(), 1)
-    assert np.array_equal(got, ref)
+    assert_hash_sorted_unique(got, 1)
+    assert np.array_equal(synth.sort_keys(got), ref)
 
 
 @pytest.mark.parametrize("W,Pn", [(1, 2), (1, 4), (1, 8), (2, 4)])
@@ -234,9 +269,10 @@ def test_dedup_logical_ranks(P, ctx, W, Pn):
     total = 0
     for o in range(Pn):
         recv = torch.cat([bins[r][o] for r in range(Pn)])
-        got = ctx.dedup_finalize(sp, recv).cpu().numpy()
+        got = ctx.dedup_finalize(sp, recv).cpu().numpy().reshape(-1, W)
         ref = oracle.dedup(allk, W, Pn, o)
-        assert np.array_equal(got.reshape(-1, W), ref.reshape(-1, W))
+        assert_hash_sorted_unique(got, W)
+        assert np.array_equal(synth.sort_keys(got), ref.reshape(-1, W))
         total += len(got)
     assert total == len(oracle.dedup(allk, W))
 
@@ -248,23 +284,26 @@ def test_merge_parity(P, ctx, W):
     sp = P.Space(64 * W, 1, 1)
     S0 = synth.unique_keys(rng.integers(1, 1 << 40, size=(300_000, W), dtype=np.uint64))
     pool = ctx.pool(sp, capacity=1000)           # forces growth
-    ins0 = ctx.merge_space(pool, torch.from_numpy(S0).cuda(), want_inserted=True).cpu().numpy()
-    assert np.array_equal(ins0, S0) and len(pool) == len(S0)
+    ins0 = ctx.merge_space(pool, torch.from_numpy(hash_sort(S0, W)).cuda(), want_inserted=True).cpu().numpy()
+    assert np.array_equal(synth.sort_keys(ins0), S0) and len(pool) == len(S0)
     for it in range(3):
         U = synth.unique_keys(np.concatenate([S0[rng.choice(len(S0), 50_000)],
                                               rng.integers(1, 1 << 40, size=(80_000, W), dtype=np.uint64)]))
         before = pool.keys().cpu().numpy()
-        ins = ctx.merge_space(pool, torch.from_numpy(U).cuda(), want_inserted=True).cpu().numpy()
+        ins = ctx.merge_space(pool, torch.from_numpy(hash_sort(U, W)).cuda(), want_inserted=True).cpu().numpy()
         ref_s, ref_ins = oracle.merge(before, U, W)
-        assert np.array_equal(pool.keys().cpu().numpy(), ref_s)
-        assert np.array_equal(ins, ref_ins)
+        after = pool.keys().cpu().numpy()
+        assert_hash_sorted_unique(after, W)
+        assert_hash_sorted_unique(ins, W)
+        assert np.array_equal(synth.sort_keys(after), ref_s)
+        assert np.array_equal(synth.sort_keys(ins), ref_ins)
         assert len(pool) == len(before) + len(ins)
     # idempotence
-    again = ctx.merge_space(pool, torch.from_numpy(U).cuda(), want_inserted=True)
+    again = ctx.merge_space(pool, torch.from_numpy(hash_sort(U, W)).cuda(), want_inserted=True)
     assert again.shape[0] == 0
-    # unsorted input rejected
+    # input not in the hash order is rejected
     with pytest.raises(P.CusciError) as e:
-        ctx.merge_space(pool, torch.from_numpy(U[::-1].copy()).cuda())
+        ctx.merge_space(pool, torch.from_numpy(hash_sort(U, W)[::-1].copy()).cuda())
     assert e.value.code == 1
     pool.close()
 
@@ -275,7 +314,7 @@ def test_pipeline_lih_merge_inserts_nothing(P, ctx):
     di = P.DeviceIntegrals(ints.h, ints.eri)
     tp = torch.from_numpy(par).cuda()
     pool = ctx.pool(sp, 256)
-    ctx.merge_space(pool, tp)
+    ctx.merge_space(pool, torch.from_numpy(hash_sort(par, 1)).cuda())
     rec = ctx.gen_coupled(sp, tp, di, 0.0)
     u = ctx.dedup_global(sp, rec.keys)
     ins = ctx.merge_space(pool, u, want_inserted=True)
@@ -300,10 +339,43 @@ for W, m, n in [(1, 56, 300_000), (1, 26, 200_001), (2, 96, 150_000), (2, 120, 7
         base[:, 1] &= np.uint64((1 << (m - 64)) - 1)
     keys = base[rng.integers(0, len(base), size=n)]
     sp = P.Space(m, 1, 1)
-    got = ctx.dedup_global(sp, torch.from_numpy(keys).cuda()).cpu().numpy()
-    assert np.array_equal(got.reshape(-1, W), oracle.dedup(keys, W).reshape(-1, W)), (W, m, n)
+    got = ctx.dedup_global(sp, torch.from_numpy(keys).cuda()).cpu().numpy().reshape(-1, W)
+    assert np.array_equal(synth.sort_keys(got), oracle.dedup(keys, W).reshape(-1, W)), (W, m, n)
 print("OK")
 ''' % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, CUSCI_PORTION_LOG2="16")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
+
+
+def _fmix64_inv(h):
+    """inverse of the splitmix64 finalizer (to build keys with chosen hash)."""
+    M = (1 << 64) - 1
+    i2 = pow(0x94D049BB133111EB, -1, 1 << 64)
+    i1 = pow(0xBF58476D1CE4E5B9, -1, 1 << 64)
+    out = []
+    for x in h:
+        x = int(x)
+        x ^= (x >> 31) ^ (x >> 62)
+        x = (x * i2) & M
+        x ^= (x >> 27) ^ (x >> 54)
+        x = (x * i1) & M
+        x ^= (x >> 30) ^ (x >> 60)
+        out.append(x)
+    return np.array(out, dtype=np.uint64)
+
+
+def test_dedup_bucket_overflow_slow_path(P, ctx):
+    """Keys whose hash lands in ONE bucket (more distinct keys than its
+    shared-memory table): the bucket is flagged and the host finishes with the
+    full hash-order sort + unique -- the result must still be exact."""
+    rng = np.random.default_rng(17)
+    hi = rng.integers(1, 1 << 40, size=9000, dtype=np.uint64)        # top 24 bits zero
+    keys = _fmix64_inv(hi).reshape(-1, 1)
+    assert np.array_equal(fmix64(keys[:, 0]), hi)
+    other = rng.integers(1, 1 << 62, size=(12000, 1), dtype=np.uint64)
+    allk = np.concatenate([keys, keys[:3000], other])
+    sp = P.Space(64, 1, 1)
+    got = ctx.dedup_global(sp, torch.from_numpy(allk).cuda()).cpu().numpy()
+    assert_hash_sorted_unique(got, 1)
+    assert np.array_equal(synth.sort_keys(got), oracle.dedup(allk, 1))

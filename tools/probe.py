@@ -13,6 +13,7 @@ ctx = P.Context(0)
 sp = P.Space(wl.m, wl.n_alpha, wl.n_beta)
 di = P.DeviceIntegrals(ints.h, ints.eri)
 tp = torch.from_numpy(par).cuda()
+tph = ctx.dedup_global(sp, tp)  # parents in the pool (hash) order
 batches = [(i, min(i + batch, len(par))) for i in range(0, len(par), batch)]
 cnts = [ctx.gen_coupled_count(sp, tp[a:b], di) for a, b in batches]
 cap = max(cnts)
@@ -30,7 +31,7 @@ for it in range(5):
         t = T(); u = ctx.dedup_global(sp, rec.keys); tim["dedup"] = tim.get("dedup", 0) + T() - t
         t = T(); ctx.merge_space(upool, u); tim["merge"] = tim.get("merge", 0) + T() - t
         del u
-    t = T(); ctx.merge_space(spool, tp); ctx.merge_pool(spool, upool)
+    t = T(); ctx.merge_space(spool, tph); ctx.merge_pool(spool, upool)
     tim["final"] = T() - t
     tot = T() - t0
     prof = ctx.profile_read()
