@@ -91,8 +91,9 @@ int cusci_nccl_unique_id(void* out128);
 
 /* Create a context on `device` for rank `rank` of `world` (world >= 1).
  * nccl_unique_id: host pointer to the 128-byte id (required iff world > 1;
- * collective over all ranks when world > 1).  cuda_stream: a cudaStream_t on
- * `device` (NULL = a library-owned non-blocking stream).  alloc/free: output
+ * collective over all ranks when world > 1).  cuda_stream: the cudaStream_t on
+ * `device` every call is ordered on (NULL = the legacy default stream; pass the
+ * stream the caller's producers and consumers of these buffers use).  alloc/free: output
  * allocator (both NULL = cudaMallocAsync / cudaFreeAsync on the stream). */
 int cusci_init(cusci_ctx** ctx, int device, int rank, int world, const void* nccl_unique_id,
                void* cuda_stream, cusci_alloc_fn alloc, cusci_free_fn free_fn, void* alloc_user);

@@ -184,12 +184,9 @@ int cusci_init(cusci_ctx** out, int device, int rank, int world, const void* ncc
   };
   if (cudaSetDevice(device) != cudaSuccess) return fail(CUSCI_E_CUDA);
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
-  if (cuda_stream) {
-    ctx->stream = (cudaStream_t)cuda_stream;
-  } else {
-    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) return fail(CUSCI_E_CUDA);
-    ctx->own_stream = true;
-  }
+  // NULL = the legacy default stream (the one torch's current_stream() is by default);
+  // every library call is ordered on this stream with the caller's own work.
+  ctx->stream = (cudaStream_t)cuda_stream;
   cudaMemPoolProps props = {};
   props.allocType = cudaMemAllocationTypePinned;
   props.location.type = cudaMemLocationTypeDevice;

@@ -39,27 +39,32 @@ __device__ __forceinline__ uint32_t top_bits(const KeyT<W>& k, int bits) {
 }
 
 // ---------------------------------------------------------------- partition passes
-// One pass = per-tile digit histograms written to a [digit][tile] matrix, one
-// exclusive scan of the matrix, and a scatter in which every CTA turns its
-// matrix column into shared-memory cursors and places each key with ONE
-// shared-memory atomic (no global atomics, no look-back; order inside a
-// bucket is irrelevant).  Tiles are <= 32 Ki keys, processed 2 Ki at a time.
-// Pass 1 digit = top hb bits of hi over plain tiles; pass 2 digit = the next
-// lb bits, over tiles that never straddle a pass-1 group (the matrix is laid
-// out group by group, so one global scan yields every bucket's offset).
+// Segmented MSD passes of <= 8 bits of hi.  A pass = per-tile digit
+// histograms written to a matrix laid out group by group ([group][digit]
+// [tile]), ONE exclusive scan of that matrix (it then holds every (group,
+// digit, tile) output offset), and a scatter: each CTA loads its matrix
+// column as shared-memory cursors and, per 4 Ki-key sub-round, ranks its keys
+// with shared-memory atomics, stages them in digit order in shared memory and
+// writes them out as runs of consecutive addresses (~16 keys = 128 B per
+// digit), so HBM sees full sectors.  No global atomics, no look-back, no
+// stability requirement.  Tiles (<= 32 Ki keys) never straddle a group.
 struct PTile {
   uint64_t start;   // first key
   uint32_t len;     // keys in the tile
-  uint32_t stride;  // matrix stride between digits (tiles of this group)
+  uint32_t stride;  // matrix stride between digits (= tiles of this group)
   uint64_t mbase;   // matrix index of digit 0 of this tile
 };
 constexpr uint32_t kPTile = 32768;
+template <int W> struct SSCfg {
+  static constexpr int ITEMS = W == 1 ? 16 : 8;  // keys per thread per sub-round
+  static constexpr int SUB = kBT * ITEMS;        // 4096 / 2048 keys (32 KB staged)
+};
 
 template <int W>
 __global__ void __launch_bounds__(kBT) tile_hist_kernel(const uint64_t* __restrict__ in,
                                                        const PTile* __restrict__ tiles, int bsel, uint32_t dmask,
                                                        uint32_t* __restrict__ mat) {
-  __shared__ uint32_t h[2048];
+  __shared__ uint32_t h[256];
   const PTile t = tiles[blockIdx.x];
   for (uint32_t i = threadIdx.x; i <= dmask; i += kBT) h[i] = 0;
   __syncthreads();
@@ -84,38 +89,76 @@ template <int W>
 __global__ void __launch_bounds__(kBT) tile_scatter_kernel(const uint64_t* __restrict__ in,
                                                           const PTile* __restrict__ tiles, int bsel, uint32_t dmask,
                                                           const uint32_t* __restrict__ offs, uint64_t* __restrict__ out) {
-  __shared__ uint32_t cur[2048];
+  constexpr int ITEMS = SSCfg<W>::ITEMS, SUB = SSCfg<W>::SUB;
+  __shared__ uint32_t cur[256], cnt[256], lst[256];
+  __shared__ uint32_t red[33];
+  __shared__ KeyT<W> stage[SUB];
+  __shared__ uint8_t sdig[SUB];
   const PTile t = tiles[blockIdx.x];
-  for (uint32_t d = threadIdx.x; d <= dmask; d += kBT) cur[d] = offs[t.mbase + (uint64_t)d * t.stride];
+  const uint32_t R = dmask + 1;
+  for (uint32_t d = threadIdx.x; d < 256; d += kBT) {
+    cur[d] = d < R ? offs[t.mbase + (uint64_t)d * t.stride] : 0u;
+    cnt[d] = 0;
+  }
   __syncthreads();
-  for (uint32_t r0 = 0; r0 < t.len; r0 += kBTile) {
-    KeyT<W> k[kBI];
+  for (uint32_t r0 = 0; r0 < t.len; r0 += SUB) {
+    const uint32_t m = min((uint32_t)SUB, t.len - r0);
+    KeyT<W> k[ITEMS];
+    uint32_t d[ITEMS], rk[ITEMS];
 #pragma unroll
-    for (int u = 0; u < kBI; u++) {
-      const uint32_t i = r0 + u * kBT + threadIdx.x;
-      if (i < t.len) k[u] = load_key<W>(in, t.start + i);
+    for (int u = 0; u < ITEMS; u++) {
+      const uint32_t i = u * kBT + threadIdx.x;
+      if (i < m) k[u] = load_key<W>(in, t.start + r0 + i);
     }
 #pragma unroll
-    for (int u = 0; u < kBI; u++) {
-      const uint32_t i = r0 + u * kBT + threadIdx.x;
-      if (i < t.len) store_key<W>(out, atomicAdd(&cur[top_bits<W>(k[u], bsel) & dmask], 1u), k[u]);
+    for (int u = 0; u < ITEMS; u++) {
+      const uint32_t i = u * kBT + threadIdx.x;
+      if (i < m) {
+        d[u] = top_bits<W>(k[u], bsel) & dmask;
+        rk[u] = atomicAdd(&cnt[d[u]], 1u);
+      }
     }
+    __syncthreads();
+    uint32_t tot;
+    const uint32_t c = cnt[threadIdx.x];
+    const uint32_t ex = block_excl_scan_u32(c, red, tot);
+    lst[threadIdx.x] = ex;
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < ITEMS; u++) {
+      const uint32_t i = u * kBT + threadIdx.x;
+      if (i < m) {
+        const uint32_t pos = lst[d[u]] + rk[u];
+        stage[pos] = k[u];
+        sdig[pos] = (uint8_t)d[u];
+      }
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < m; j += kBT) {
+      const uint32_t dj = sdig[j];
+      store_key<W>(out, (uint64_t)cur[dj] + (j - lst[dj]), stage[j]);
+    }
+    __syncthreads();
+    cur[threadIdx.x] += c;
+    cnt[threadIdx.x] = 0;
+    __syncthreads();
   }
 }
 
-// bucket (g, d) offsets after pass 2: gmeta[g] = {group start, tiles, matrix base}
-__global__ void bucket_off_kernel(const uint32_t* __restrict__ offs2, const uint4* __restrict__ gmeta, uint32_t R1,
-                                  int lb, uint32_t n, uint32_t* __restrict__ off) {
-  const uint32_t L = 1u << lb;
+// group offsets after a pass: for old group g with meta {start, tiles, mbase},
+// new group g*R + d starts at offs[mbase + d * tiles] (or the old start if empty)
+__global__ void group_off_kernel(const uint32_t* __restrict__ offs, const uint4* __restrict__ gmeta, uint32_t G,
+                                 int bits, uint32_t n, uint32_t* __restrict__ off) {
+  const uint32_t R = 1u << bits;
   const uint32_t id = blockIdx.x * blockDim.x + threadIdx.x;
-  if (id > R1 * L) return;
-  if (id == R1 * L) {
+  if (id > G * R) return;
+  if (id == G * R) {
     off[id] = n;
     return;
   }
-  const uint32_t g = id >> lb, d = id & (L - 1);
+  const uint32_t g = id >> bits, d = id & (R - 1);
   const uint4 m = gmeta[g];  // x = start, y = tiles, z = mbase
-  off[id] = m.y ? offs2[m.z + (uint64_t)d * m.y] : m.x;
+  off[id] = m.y ? offs[m.z + (uint64_t)d * m.y] : m.x;
 }
 
 // ---------------------------------------------------------------- per-bucket dedup + sort
@@ -322,8 +365,7 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
   Scratch s(ctx);
   // B bits of hi: ~<= 2048 keys per bucket on average
   int B = 0;
-  while ((n >> B) > 2048 && B < 20) B++;
-  const int lb = B > 9 ? std::min(9, B / 2) : 0, hb = B - lb;  // hb <= 11, lb <= 9
+  while ((n >> B) > 2048 && B < 22) B++;
   const uint32_t nb = 1u << B;
   uint64_t *a, *b2;
   uint32_t *hist, *off, *cur, *surv;
@@ -342,69 +384,57 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
   const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + kBTile - 1) / kBTile, (uint64_t)ctx->num_sms * 8));
   const uint64_t* part = in;
   if (B > 0) {
-    // ---- pass 1: plain tiles, digit = top hb bits
-    const uint32_t R1 = 1u << hb;
-    const uint32_t nt1 = (uint32_t)((n + kPTile - 1) / kPTile);
-    std::vector<PTile> t1(nt1);
-    for (uint32_t t = 0; t < nt1; t++)
-      t1[t] = PTile{(uint64_t)t * kPTile, (uint32_t)std::min<uint64_t>(kPTile, n - (uint64_t)t * kPTile), nt1, t};
-    PTile* dt1;
-    uint32_t *mat1, *offs1;
-    CUSCI_TRY(s.get_t(nt1, &dt1));
-    CUSCI_TRY(s.get_t((uint64_t)R1 * nt1, &mat1));
-    CUSCI_TRY(s.get_t((uint64_t)R1 * nt1, &offs1));
-    CUSCI_CUDA(ctx, cudaMemcpyAsync(dt1, t1.data(), nt1 * sizeof(PTile), cudaMemcpyHostToDevice, ctx->stream));
-    CUSCI_LAUNCH(ctx, PT_RADIX_UP, tile_hist_kernel<W><<<nt1, kBT, 0, ctx->stream>>>(in, dt1, hb, R1 - 1, mat1));
-    CUSCI_TRY(scan_exclusive_u32(ctx, mat1, offs1, (uint64_t)R1 * nt1));
-    CUSCI_LAUNCH(ctx, PT_RADIX_DOWN, tile_scatter_kernel<W><<<nt1, kBT, 0, ctx->stream>>>(in, dt1, hb, R1 - 1, offs1, a));
-    part = a;
-    if (lb == 0) {
-      // buckets = pass-1 groups: off[g] = offs1[g * nt1]
-      CUSCI_CUDA(ctx, cudaMemcpy2DAsync(off, sizeof(uint32_t), offs1, (size_t)nt1 * sizeof(uint32_t), sizeof(uint32_t),
-                                        R1, cudaMemcpyDeviceToDevice, ctx->stream));
-      const uint32_t nn = (uint32_t)n;
-      memcpy(ctx->host_pinned, &nn, 4);
-      CUSCI_CUDA(ctx, cudaMemcpyAsync(off + R1, ctx->host_pinned, 4, cudaMemcpyHostToDevice, ctx->stream));
-      CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    } else {
-      // ---- pass 2: tiles inside each pass-1 group, digit = next lb bits
-      std::vector<uint32_t> gstart(R1 + 1);
-      CUSCI_CUDA(ctx, cudaMemcpy2DAsync(ctx->host_pinned, sizeof(uint32_t), offs1, (size_t)nt1 * sizeof(uint32_t),
-                                        sizeof(uint32_t), R1, cudaMemcpyDeviceToHost, ctx->stream));
-      CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-      memcpy(gstart.data(), ctx->host_pinned, R1 * sizeof(uint32_t));
-      gstart[R1] = (uint32_t)n;
-      const uint32_t L = 1u << lb;
-      std::vector<PTile> t2;
-      std::vector<uint4> gm(R1);
-      t2.reserve(nt1 + R1);
+    // segmented MSD passes of <= 8 bits over the top B bits of hi
+    const int np = (B + 7) / 8;
+    int done = 0;
+    std::vector<uint32_t> gstart{0u, (uint32_t)n};  // current groups (host)
+    uint64_t* dst = a;
+    for (int pi = 0; pi < np; pi++) {
+      const int bits = (B - done + (np - pi) - 1) / (np - pi);  // even split
+      const uint32_t R = 1u << bits;
+      const uint32_t G = (uint32_t)gstart.size() - 1;
+      std::vector<PTile> tl;
+      std::vector<uint4> gm(G);
+      tl.reserve(n / kPTile + G + 1);
       uint64_t mb = 0;
-      for (uint32_t g = 0; g < R1; g++) {
+      for (uint32_t g = 0; g < G; g++) {
         const uint64_t gs = gstart[g], ge = gstart[g + 1];
         const uint32_t chunks = (uint32_t)((ge - gs + kPTile - 1) / kPTile);
         gm[g] = make_uint4((uint32_t)gs, chunks, (uint32_t)mb, 0u);
         for (uint32_t c = 0; c < chunks; c++) {
           const uint64_t st = gs + (uint64_t)c * kPTile;
-          t2.push_back(PTile{st, (uint32_t)std::min<uint64_t>(kPTile, ge - st), chunks, mb + c});
+          tl.push_back(PTile{st, (uint32_t)std::min<uint64_t>(kPTile, ge - st), chunks, mb + c});
         }
-        mb += (uint64_t)L * chunks;
+        mb += (uint64_t)R * chunks;
       }
-      const uint32_t nt2 = (uint32_t)t2.size();
-      PTile* dt2;
+      if (mb >= (1ull << 32)) return set_error(ctx, CUSCI_E_INVALID_ARG, "dedup: partition matrix too large");
+      const uint32_t nt = (uint32_t)tl.size();
+      Scratch ps(ctx);
+      PTile* dtl;
       uint4* dgm;
-      uint32_t *mat2, *offs2;
-      CUSCI_TRY(s.get_t(std::max<uint32_t>(nt2, 1), &dt2));
-      CUSCI_TRY(s.get_t(R1, &dgm));
-      CUSCI_TRY(s.get_t(std::max<uint64_t>(mb, 1), &mat2));
-      CUSCI_TRY(s.get_t(std::max<uint64_t>(mb, 1), &offs2));
-      CUSCI_CUDA(ctx, cudaMemcpyAsync(dt2, t2.data(), nt2 * sizeof(PTile), cudaMemcpyHostToDevice, ctx->stream));
-      CUSCI_CUDA(ctx, cudaMemcpyAsync(dgm, gm.data(), R1 * sizeof(uint4), cudaMemcpyHostToDevice, ctx->stream));
-      CUSCI_LAUNCH(ctx, PT_RADIX_UP, tile_hist_kernel<W><<<nt2, kBT, 0, ctx->stream>>>(a, dt2, B, L - 1, mat2));
-      CUSCI_TRY(scan_exclusive_u32(ctx, mat2, offs2, mb));
-      CUSCI_LAUNCH(ctx, PT_RADIX_DOWN, tile_scatter_kernel<W><<<nt2, kBT, 0, ctx->stream>>>(a, dt2, B, L - 1, offs2, b2));
-      CUSCI_LAUNCH(ctx, PT_SCATTER, bucket_off_kernel<<<(nb + 1 + 255) / 256, 256, 0, ctx->stream>>>(offs2, dgm, R1, lb, (uint32_t)n, off));
-      part = b2;
-      CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // host vectors t2/gm die at scope end
+      uint32_t *mat, *offs, *goff;
+      CUSCI_TRY(ps.get_t(std::max<uint32_t>(nt, 1), &dtl));
+      CUSCI_TRY(ps.get_t(std::max<uint32_t>(G, 1), &dgm));
+      CUSCI_TRY(ps.get_t(std::max<uint64_t>(mb, 1), &mat));
+      CUSCI_TRY(ps.get_t(std::max<uint64_t>(mb, 1), &offs));
+      CUSCI_TRY(ps.get_t((uint64_t)G * R + 1, &goff));
+      CUSCI_CUDA(ctx, cudaMemcpyAsync(dtl, tl.data(), nt * sizeof(PTile), cudaMemcpyHostToDevice, ctx->stream));
+      CUSCI_CUDA(ctx, cudaMemcpyAsync(dgm, gm.data(), G * sizeof(uint4), cudaMemcpyHostToDevice, ctx->stream));
+      const int sel = done + bits;
+      CUSCI_LAUNCH(ctx, PT_RADIX_UP, tile_hist_kernel<W><<<nt, kBT, 0, ctx->stream>>>(part, dtl, sel, R - 1, mat));
+      CUSCI_TRY(scan_exclusive_u32(ctx, mat, offs, mb));
+      CUSCI_LAUNCH(ctx, PT_RADIX_DOWN, tile_scatter_kernel<W><<<nt, kBT, 0, ctx->stream>>>(part, dtl, sel, R - 1, offs, dst));
+      uint32_t* goff_final = (pi == np - 1) ? off : goff;
+      CUSCI_LAUNCH(ctx, PT_SCATTER, group_off_kernel<<<(unsigned)(((uint64_t)G * R + 1 + 255) / 256), 256, 0, ctx->stream>>>(offs, dgm, G, bits, (uint32_t)n, goff_final));
+      if (pi < np - 1) {
+        gstart.resize((size_t)G * R + 1);
+        CUSCI_CUDA(ctx, cudaMemcpyAsync(gstart.data(), goff, gstart.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                                        ctx->stream));
+      }
+      CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // host tables die at scope end
+      part = dst;
+      dst = (dst == a) ? b2 : a;
+      done += bits;
     }
   } else {
     const uint32_t o2[2] = {0u, (uint32_t)n};
