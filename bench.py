@@ -226,7 +226,7 @@ def main():
     mine = np.array_split(par_all, world)[rank]
     shard = ctx.dedup_global(sp, torch.from_numpy(mine).to(dev))   # parents owned by this rank (sorted)
     n_par = int(shard.shape[0])
-    batch = args.batch or {"n2": 250_000, "c2h4": 20_000}.get(args.workload, max(1, n_par))
+    batch = args.batch or {"n2": 500_000, "c2h4": 20_000}.get(args.workload, max(1, n_par))
     batch = max(1, min(batch, n_par))
     batches = [(i, min(i + batch, n_par)) for i in range(0, n_par, batch)]
     # plan: exact record counts per batch (buffer sizing; outside the timed region)
@@ -323,31 +323,37 @@ def main():
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-    dom = max(prof.items(), key=lambda kv: kv[1][0]) if prof else ("none", (0.0, 0))
     rec_bytes = 8 * W + 8 + 4
-    # algorithmic bytes per step for each kernel class (DESIGN.md "Algorithmic bytes")
-    per_step_rec = tot_rec / max(args.steps, 1)
+
+    def dedup_passes(n):  # bucket.cu: B = bits with <= 2048 keys/bucket (cap 22), <= 8-bit passes
+        B = 0
+        while (n >> B) > 2048 and B < 22:
+            B += 1
+        return (B + 7) // 8
+
+    # algorithmic bytes per step for each kernel class (DESIGN.md section 8)
     alg = {
-        "gen": per_step_rec * rec_bytes + n_par * 8 * W,
-        "hash_filter": per_step_rec * 8 * W,
+        "gen": sum(counts) * rec_bytes + n_par * 8 * W,                       # records written + parents read
+        "radix_downsweep": sum(dedup_passes(c) * c * 16 * W for c in counts),  # partition: read + write a key per pass
+        "radix_upsweep": sum(dedup_passes(c) * c * 8 * W for c in counts),     # per-pass histograms: read a key
+        "hash_filter": sum(c * 8 * W for c in counts),                         # bucket dedup: read every key once
     }
-    dname, (dms, dlaunch) = dom
+    kernels = {}
+    for name, (kms, kl) in prof.items():
+        if name in alg and kl:
+            ach = alg[name] * args.steps / (kms / 1e3) / 1e9
+            kernels[name] = {"ms_per_step": kms / args.steps, "achieved_GBs": ach, "frac": ach / hbm_peak}
+    dname = max(prof.items(), key=lambda kv: kv[1][0])[0] if prof else None
+    rname = dname if dname in kernels else (max(kernels, key=lambda k: kernels[k]["ms_per_step"]) if kernels else None)
     roof = None
-    if dname in alg and dlaunch:
-        per_launch_bytes = alg[dname] * args.steps / dlaunch
-        per_launch_s = dms / dlaunch / 1e3
-        achieved = per_launch_bytes / per_launch_s / 1e9
-        roof = {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": None, "peak_source": peak_src}
-    gen_ms, gen_l = prof.get("gen", (0.0, 0))
-    gen_bytes = alg["gen"] * args.steps
+    if rname:
+        roof = {"bound": "hbm", "kernel": rname, "achieved": kernels[rname]["achieved_GBs"], "peak": hbm_peak,
+                "unit": "GB/s", "frac": kernels[rname]["frac"], "traffic": None, "peak_source": peak_src,
+                "dominant_class": dname}
     gen_roof = None
-    if gen_l:
-        ach = gen_bytes / (gen_ms / 1e3) / 1e9
-        gen_roof = {"achieved": ach, "frac": ach / hbm_peak, "records_per_s_kernel": tot_rec / (gen_ms / 1e3)}
-    if roof is None and gen_roof is not None:
-        roof = {"bound": "hbm", "kernel": "gen", "achieved": gen_roof["achieved"], "peak": hbm_peak, "unit": "GB/s",
-                "frac": gen_roof["frac"], "traffic": None, "peak_source": peak_src}
+    if "gen" in kernels:
+        gen_roof = {"achieved": kernels["gen"]["achieved_GBs"], "frac": kernels["gen"]["frac"],
+                    "records_per_s_kernel": tot_rec / (prof["gen"][0] / 1e3)}
 
     # ---------------- cpu baseline (oracle, rank 0, N=1 only)
     cpu = None
@@ -374,6 +380,7 @@ def main():
             "redundancy": 1.0 - uni_all / max(recs_all, 1),
             "roofline": roof,
             "gen_kernel": gen_roof,
+            "kernel_roofline": kernels,
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])},
             "cpu_baseline": cpu,
             "e2e": e2e,

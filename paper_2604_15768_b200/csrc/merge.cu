@@ -2,15 +2,16 @@
 // PAPER.md:311-312 Sec 2.2 "merging them into S", :404-405; abstract :167
 // "GPU-side pooling").
 //
-// B200 design: merge path.  The merged sequence of
-// S (sorted unique) and U (sorted unique), ties S-first, is cut into tiles of
-// kTile outputs by a diagonal binary search per tile boundary; each CTA stages
-// its S and U runs in shared memory, merges them (serial merge of ITEMS
-// outputs per thread from one in-tile diagonal search), drops an element equal
-// to its predecessor (an element of U already in S), and writes S' and
-// inserted = U \ S with block-ordered compaction.  Two sweeps (count, write)
-// with one scan of per-tile counts in between; S' is written to the pool's
-// second buffer and the buffers are swapped (grown geometrically if needed).
+// B200 design: merge path in the pool (hash) order
+// (reading r13).  The merged sequence of S (sorted unique) and U (sorted
+// unique), ties S-first, is cut into tiles of kTile outputs by a diagonal
+// binary search per tile boundary; each CTA stages its S and U runs in shared
+// memory, merges them (serial merge of ITEMS outputs per thread from one
+// in-tile diagonal search), drops an element equal to its predecessor (an
+// element of U already in S), validates U's order, and writes S' and
+// inserted = U \ S at offsets found by decoupled look-back -- ONE sweep over
+// S and U.  S' goes to the pool's second buffer (grown geometrically to the
+// upper bound |S| + |U| when needed) and the buffers are swapped.
 #include <algorithm>
 
 #include "internal.cuh"
@@ -48,14 +49,21 @@ __global__ void check_sorted_kernel(const uint64_t* __restrict__ U, uint64_t n, 
     if (!hk_lt<W>(load_key<W>(U, i - 1), load_key<W>(U, i))) *flag = 1;
 }
 
+// Single sweep: each CTA takes a tile ticket (predecessors are resident),
+// merges its S and U runs in shared memory, drops an element equal to its
+// predecessor, checks that its U run is strictly increasing in the hash order,
+// publishes its (kept, inserted) counts and resolves its output offsets by
+// decoupled look-back over its predecessors' published counts, then writes
+// S' and inserted with block-ordered compaction.
+constexpr uint64_t kMFlagA = 1ull << 62, kMFlagP = 2ull << 62, kMVal = (1ull << 62) - 1;
+
 template <int W>
 __global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(const uint64_t* __restrict__ S, uint64_t nS,
                                                                   const uint64_t* __restrict__ U, uint64_t nU,
-                                                                  const uint64_t* __restrict__ split, int write,
-                                                                  uint64_t* __restrict__ cnt_keep,
-                                                                  uint64_t* __restrict__ cnt_ins,
-                                                                  const uint64_t* __restrict__ off_keep,
-                                                                  const uint64_t* __restrict__ off_ins,
+                                                                  const uint64_t* __restrict__ split,
+                                                                  unsigned long long* __restrict__ status,
+                                                                  unsigned* __restrict__ tile_ctr,
+                                                                  int* __restrict__ bad,
                                                                   uint64_t* __restrict__ out, uint64_t* __restrict__ ins) {
   constexpr int kMergeItems = MergeCfg<W>::ITEMS;
   constexpr int kTile = MergeCfg<W>::TILE;
@@ -64,16 +72,32 @@ __global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(const uint64_
   __shared__ uint8_t fromU[kTile];
   __shared__ uint32_t wk[kMergeThreads / 32], wi[kMergeThreads / 32];
   __shared__ uint64_t run_k, run_i;
-  const uint64_t t = blockIdx.x;
+  __shared__ unsigned s_tile;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  __syncthreads();
+  const uint64_t t = s_tile;
   const uint64_t i0 = split[t], i1 = split[t + 1];
   const uint64_t d0 = t * kTile, d1 = std::min<uint64_t>(d0 + kTile, nS + nU);
   const uint64_t j0 = d0 - i0, j1 = d1 - i1;
-  const int na = (int)(i1 - i0), nb = (int)(j1 - j0), len = na + nb;
+  // an unsorted U can make the merge-path splits inconsistent: flag it and
+  // process nothing (the tile still publishes zero counts for its successors)
+  const bool inval = i1 < i0 || j1 < j0 || (i1 - i0) + (j1 - j0) > (uint64_t)kTile || j1 > nU || i1 > nS;
+  if (inval && threadIdx.x == 0) *bad = 1;
+  const int na = inval ? 0 : (int)(i1 - i0), nb = inval ? 0 : (int)(j1 - j0), len = na + nb;
   for (int x = threadIdx.x; x < na; x += kMergeThreads) ab[x] = load_key<W>(S, i0 + x);
   for (int x = threadIdx.x; x < nb; x += kMergeThreads) ab[na + x] = load_key<W>(U, j0 + x);
   __syncthreads();
   const KeyT<W>* A = ab;
   const KeyT<W>* B = ab + na;
+  // input check: U strictly increasing in the hash order (tile run + left boundary)
+  {
+    bool badu = false;
+    for (int x = threadIdx.x; x < nb; x += kMergeThreads) {
+      if (x > 0) badu |= !hk_lt<W>(B[x - 1], B[x]);
+      else if (j0 > 0 && j0 <= nU) badu |= !hk_lt<W>(load_key<W>(U, j0 - 1), B[0]);
+    }
+    if (badu) *bad = 1;
+  }
   // each thread merges outputs [k0, k0 + ITEMS)
   const int k0 = threadIdx.x * kMergeItems;
   if (k0 < len) {
@@ -98,22 +122,62 @@ __global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(const uint64_
   // predecessor of the tile's first output: the larger of S[i0-1], U[j0-1]
   KeyT<W> prev0{};
   bool has_prev0 = false;
-  if (i0 > 0) {
+  if (!inval && i0 > 0) {
     prev0 = load_key<W>(S, i0 - 1);
     has_prev0 = true;
   }
-  if (j0 > 0) {
+  if (!inval && j0 > 0) {
     const KeyT<W> u = load_key<W>(U, j0 - 1);
     if (!has_prev0 || hk_lt<W>(prev0, u)) prev0 = u;
     has_prev0 = true;
   }
-  if (threadIdx.x == 0) {
-    run_k = write ? off_keep[t] : 0;
-    run_i = write ? off_ins[t] : 0;
-  }
   __syncthreads();
+  // tile counts
   const int w = threadIdx.x >> 5;
   uint32_t ck = 0, ci = 0;
+  for (int r = 0; r < kMergeItems; r++) {
+    const int k = r * kMergeThreads + threadIdx.x;
+    if (k < len) {
+      const bool dup = k > 0 ? key_eq(mrg[k], mrg[k - 1]) : (has_prev0 && key_eq(mrg[0], prev0));
+      ck += !dup;
+      ci += (!dup && fromU[k]);
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    ck += __shfl_xor_sync(kFull, ck, o);
+    ci += __shfl_xor_sync(kFull, ci, o);
+  }
+  if (lane_id() == 0) {
+    wk[w] = ck;
+    wi[w] = ci;
+  }
+  __syncthreads();
+  // publish + look-back (thread 0: kept, thread 32: inserted)
+  volatile unsigned long long* st = status;
+  if (threadIdx.x == 0 || threadIdx.x == 32) {
+    const int which = threadIdx.x == 0 ? 0 : 1;
+    uint64_t mine = 0;
+    for (int x = 0; x < kMergeThreads / 32; x++) mine += which ? wi[x] : wk[x];
+    st[2 * t + which] = (t == 0 ? kMFlagP : kMFlagA) | mine;
+    uint64_t excl = 0;
+    if (t > 0) {
+      int64_t q = (int64_t)t - 1;
+      while (q >= 0) {
+        const uint64_t v = st[2 * q + which];
+        if ((v >> 62) == 0) {
+          __nanosleep(20);
+          continue;
+        }
+        excl += v & kMVal;
+        if ((v >> 62) == 2) break;
+        q--;
+      }
+      st[2 * t + which] = kMFlagP | (excl + mine);
+    }
+    if (which == 0) run_k = excl;
+    else run_i = excl;
+  }
+  __syncthreads();
   for (int r = 0; r < kMergeItems; r++) {
     const int k = r * kMergeThreads + threadIdx.x;
     bool keep = false, isins = false;
@@ -121,11 +185,6 @@ __global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(const uint64_
       const bool dup = k > 0 ? key_eq(mrg[k], mrg[k - 1]) : (has_prev0 && key_eq(mrg[0], prev0));
       keep = !dup;
       isins = keep && fromU[k];
-    }
-    if (!write) {
-      ck += keep;
-      ci += isins;
-      continue;
     }
     const unsigned bk = __ballot_sync(kFull, keep), bi = __ballot_sync(kFull, isins);
     if (lane_id() == 0) {
@@ -151,26 +210,6 @@ __global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(const uint64_
     }
     __syncthreads();
   }
-  if (!write) {
-    for (int o = 16; o; o >>= 1) {
-      ck += __shfl_xor_sync(kFull, ck, o);
-      ci += __shfl_xor_sync(kFull, ci, o);
-    }
-    if (lane_id() == 0) {
-      wk[w] = ck;
-      wi[w] = ci;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint64_t a = 0, b = 0;
-      for (int x = 0; x < kMergeThreads / 32; x++) {
-        a += wk[x];
-        b += wi[x];
-      }
-      cnt_keep[t] = a;
-      cnt_ins[t] = b;
-    }
-  }
 }
 
 template <int W>
@@ -183,17 +222,6 @@ int merge_impl(cusci_ctx* ctx, cusci_pool* pool, const uint64_t* U, uint64_t nU,
     inserted->keys = nullptr;
     inserted->count = 0;
   }
-  if (nU > 1) {
-    int* flag;
-    CUSCI_TRY(s.get_t(1, &flag));
-    CUSCI_CUDA(ctx, cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
-    const unsigned blocks = (unsigned)std::min<uint64_t>((nU + 255) / 256, (uint64_t)ctx->num_sms * 8);
-    CUSCI_LAUNCH(ctx, PT_CHECK, check_sorted_kernel<W><<<blocks, 256, 0, ctx->stream>>>(U, nU, flag));
-    CUSCI_CUDA(ctx, cudaMemcpyAsync(ctx->host_pinned, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    if (*(int*)ctx->host_pinned)
-      return set_error(ctx, CUSCI_E_INVALID_ARG, "merge_space: new_keys must be sorted ascending and unique");
-  }
   if (nU == 0) {
     if (inserted) {
       void* o;
@@ -204,49 +232,68 @@ int merge_impl(cusci_ctx* ctx, cusci_pool* pool, const uint64_t* U, uint64_t nU,
   }
   constexpr int kTile = MergeCfg<W>::TILE;
   const uint64_t ntiles = (total + kTile - 1) / kTile;
-  uint64_t *split, *ck, *ci, *ok, *oi, *tot;
+  uint64_t* split;
+  unsigned long long* status;
+  unsigned* tctr;
+  int* bad;
   CUSCI_TRY(s.get_t(ntiles + 1, &split));
-  CUSCI_TRY(s.get_t(ntiles, &ck));
-  CUSCI_TRY(s.get_t(ntiles, &ci));
-  CUSCI_TRY(s.get_t(ntiles, &ok));
-  CUSCI_TRY(s.get_t(ntiles, &oi));
-  CUSCI_TRY(s.get_t(2, &tot));
-  CUSCI_LAUNCH(ctx, PT_MERGE_SPLIT, merge_split_kernel<W><<<(unsigned)((ntiles + 1 + 255) / 256), 256, 0, ctx->stream>>>(S, nS, U, nU, ntiles, split));
-  CUSCI_LAUNCH(ctx, PT_MERGE_TILE, merge_tile_kernel<W><<<(unsigned)ntiles, kMergeThreads, 0, ctx->stream>>>(S, nS, U, nU, split, 0, ck, ci, nullptr,
-                                                                           nullptr, nullptr, nullptr));
-  CUSCI_TRY(scan_exclusive_u64(ctx, ck, ok, ntiles, tot));
-  CUSCI_TRY(scan_exclusive_u64(ctx, ci, oi, ntiles, tot + 1));
-  uint64_t h[2];
-  CUSCI_TRY(read_u64(ctx, tot, h, 2));
-  const uint64_t n_new = h[0], n_ins = h[1];
-  // destination buffer (grow geometrically)
+  CUSCI_TRY(s.get_t(2 * ntiles, &status));
+  CUSCI_TRY(s.get_t(1, &tctr));
+  CUSCI_TRY(s.get_t(1, &bad));
+  CUSCI_CUDA(ctx, cudaMemsetAsync(status, 0, 2 * ntiles * sizeof(unsigned long long), ctx->stream));
+  CUSCI_CUDA(ctx, cudaMemsetAsync(tctr, 0, sizeof(unsigned), ctx->stream));
+  CUSCI_CUDA(ctx, cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
+  // destination: the pool's other buffer, grown to the upper bound nS + nU if needed
   uint64_t* dst = pool->buf[1 - pool->cur];
-  uint64_t* old_bufs[2] = {nullptr, nullptr};
-  if (n_new > pool->cap) {
-    uint64_t ncap = std::max<uint64_t>(pool->cap * 2, n_new + n_new / 4);
-    uint64_t* nb[2] = {nullptr, nullptr};
+  uint64_t* grown[2] = {nullptr, nullptr};
+  uint64_t ncap = pool->cap;
+  if (total > pool->cap) {
+    ncap = std::max<uint64_t>(pool->cap * 2, total + total / 4);
     for (int b = 0; b < 2; b++) {
-      if (cudaMallocFromPoolAsync((void**)&nb[b], ncap * W * 8, ctx->pool, ctx->stream) != cudaSuccess) {
+      if (cudaMallocFromPoolAsync((void**)&grown[b], ncap * W * 8, ctx->pool, ctx->stream) != cudaSuccess) {
         cudaGetLastError();
-        if (nb[0]) cudaFreeAsync(nb[0], ctx->stream);
+        if (grown[0]) cudaFreeAsync(grown[0], ctx->stream);
         return set_error(ctx, CUSCI_E_OOM, "pool growth to %llu keys failed", (unsigned long long)ncap);
       }
     }
-    old_bufs[0] = pool->buf[0];
-    old_bufs[1] = pool->buf[1];
-    pool->buf[0] = nb[0];
-    pool->buf[1] = nb[1];
-    pool->cap = ncap;
-    pool->cur = 1;  // S still lives in the old buffer; write into buf[0]
-    dst = pool->buf[0];
+    dst = grown[0];
   }
   void* insp = nullptr;
-  if (inserted) CUSCI_TRY(out_alloc(ctx, std::max<uint64_t>(n_ins, 1) * W * 8, &insp));
-  CUSCI_LAUNCH(ctx, PT_MERGE_TILE, merge_tile_kernel<W><<<(unsigned)ntiles, kMergeThreads, 0, ctx->stream>>>(S, nS, U, nU, split, 1, nullptr, nullptr,
-                                                                           ok, oi, dst, (uint64_t*)insp));
-  for (int b = 0; b < 2; b++)
-    if (old_bufs[b]) cudaFreeAsync(old_bufs[b], ctx->stream);
-  pool->cur = (dst == pool->buf[0]) ? 0 : 1;
+  if (inserted) {
+    const int rc = out_alloc(ctx, nU * W * 8, &insp);
+    if (rc != CUSCI_OK) {
+      for (int b = 0; b < 2; b++)
+        if (grown[b]) cudaFreeAsync(grown[b], ctx->stream);
+      return rc;
+    }
+  }
+  CUSCI_LAUNCH(ctx, PT_MERGE_SPLIT, merge_split_kernel<W><<<(unsigned)((ntiles + 1 + 255) / 256), 256, 0, ctx->stream>>>(S, nS, U, nU, ntiles, split));
+  CUSCI_LAUNCH(ctx, PT_MERGE_TILE, merge_tile_kernel<W><<<(unsigned)ntiles, kMergeThreads, 0, ctx->stream>>>(S, nS, U, nU, split, status, tctr, bad, dst, (uint64_t*)insp));
+  // totals = the last tile's inclusive counts; plus the input check flag
+  uint64_t h[3];
+  CUSCI_CUDA(ctx, cudaMemcpyAsync(ctx->host_pinned, status + 2 * (ntiles - 1), 2 * sizeof(uint64_t),
+                                  cudaMemcpyDeviceToHost, ctx->stream));
+  CUSCI_CUDA(ctx, cudaMemcpyAsync((char*)ctx->host_pinned + 16, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  memcpy(h, ctx->host_pinned, 2 * sizeof(uint64_t));
+  const int badflag = *(int*)((char*)ctx->host_pinned + 16);
+  if (badflag) {
+    for (int b = 0; b < 2; b++)
+      if (grown[b]) cudaFreeAsync(grown[b], ctx->stream);
+    if (insp) out_free(ctx, insp);
+    return set_error(ctx, CUSCI_E_INVALID_ARG, "merge_space: new_keys must be sorted in the pool (hash) order and unique");
+  }
+  const uint64_t n_new = h[0] & kMVal, n_ins = h[1] & kMVal;
+  if (grown[0]) {
+    cudaFreeAsync(pool->buf[0], ctx->stream);
+    cudaFreeAsync(pool->buf[1], ctx->stream);
+    pool->buf[0] = grown[0];
+    pool->buf[1] = grown[1];
+    pool->cap = ncap;
+    pool->cur = 0;
+  } else {
+    pool->cur = 1 - pool->cur;
+  }
   pool->count = n_new;
   if (inserted) {
     inserted->keys = (uint64_t*)insp;
