@@ -327,7 +327,7 @@ def main():
 
     def dedup_passes(n):  # bucket.cu: B = bits with <= 2048 keys/bucket (cap 22), <= 8-bit passes
         B = 0
-        while (n >> B) > 2048 and B < 22:
+        while (n >> B) > 1792 and B < 22:
             B += 1
         return (B + 7) // 8
 

@@ -162,10 +162,17 @@ __global__ void group_off_kernel(const uint32_t* __restrict__ offs, const uint4*
 }
 
 // ---------------------------------------------------------------- per-bucket dedup + sort
+// survivor record: the key and its hash-order hi (computed once per key)
+template <int W> struct SvRec {
+  KeyT<W> key;
+  uint64_t hi;
+};
 template <int W> struct BDCfg {
-  static constexpr uint32_t TS = W == 1 ? 8192 : 4096;  // table slots (64 KB)
-  static constexpr uint32_t LIMIT = TS / 2;              // distinct keys per bucket
-  static constexpr size_t SMEM = (size_t)TS * sizeof(KeyT<W>) + (size_t)LIMIT * sizeof(KeyT<W>);
+  static constexpr uint32_t TS = W == 1 ? 4096 : 2048;     // table slots (32 KB)
+  static constexpr uint32_t LIMIT = W == 1 ? 2560 : 1280;  // distinct keys per bucket
+  static constexpr uint32_t NBMAX = 2048;                  // counting-sort bins
+  static constexpr size_t SMEM = (size_t)TS * sizeof(KeyT<W>) + (size_t)LIMIT * sizeof(SvRec<W>);
+  static_assert(LIMIT * 2 + NBMAX * 4 <= TS * sizeof(KeyT<W>), "sort scratch must fit the table");
 };
 
 __device__ __forceinline__ void cas_slot(KeyT<1>* slot, const KeyT<1>& k, KeyT<1>& old) {
@@ -191,9 +198,10 @@ __device__ __forceinline__ bool kzero(const KeyT<2>& k) { return (k.w0 | k.w1) =
 
 // returns true iff k was inserted (first copy); *full set when no slot found
 template <int W>
-__device__ __forceinline__ bool tab_insert(KeyT<W>* tab, uint32_t ts, const KeyT<W>& k, int* s_zero, bool* full) {
+__device__ __forceinline__ bool tab_insert(KeyT<W>* tab, uint32_t ts, const KeyT<W>& k, uint64_t hi, int* s_zero,
+                                           bool* full) {
   if (kzero(k)) return atomicExch(s_zero, 1) == 0;
-  uint32_t h = (uint32_t)slot_hash(k) & (ts - 1);
+  uint32_t h = (uint32_t)hi & (ts - 1);  // low bits of hi: uniform within a bucket
   for (uint32_t probe = 0; probe < ts; probe++) {
     const KeyT<W> cur = tab[h];
     if (key_eq(cur, k)) return false;
@@ -209,125 +217,154 @@ __device__ __forceinline__ bool tab_insert(KeyT<W>* tab, uint32_t ts, const KeyT
   return false;
 }
 
+// A CTA walks a chunk of consecutive buckets and processes them in RUNS:
+// as many consecutive buckets as fit RUN_CAP keys share one table clear, one
+// dedup and one sort (buckets hold ~1-2 Ki keys but often few distinct ones,
+// so per-bucket fixed costs would dominate).  The run's survivors (key + hi,
+// hi computed once per key) are counting-sorted by hi and written at the run's
+// first bucket offset; surv[] gets the run count there and 0 for the run's
+// other buckets, which is what the compaction expects.
 template <int W>
-__global__ void __launch_bounds__(kBT) bucket_dedup_sort_kernel(const uint64_t* __restrict__ part,
-                                                               const uint32_t* __restrict__ off, uint32_t nb, int B,
-                                                               uint64_t* __restrict__ tmp,
-                                                               uint32_t* __restrict__ surv,
-                                                               unsigned long long* __restrict__ flags) {
+__global__ void __launch_bounds__(kBT, 3) bucket_dedup_sort_kernel(const uint64_t* __restrict__ part,
+                                                                  const uint32_t* __restrict__ off, uint32_t nb, int B,
+                                                                  uint32_t chunk, uint64_t* __restrict__ tmp,
+                                                                  uint32_t* __restrict__ surv,
+                                                                  unsigned long long* __restrict__ flags) {
   extern __shared__ __align__(16) unsigned char bsm[];
   constexpr uint32_t TS = BDCfg<W>::TS, LIMIT = BDCfg<W>::LIMIT;
+  constexpr uint32_t RUN_CAP = TS / 2;
+  constexpr int PER_MAX = (LIMIT + kBT - 1) / kBT;
   KeyT<W>* tab = reinterpret_cast<KeyT<W>*>(bsm);
-  KeyT<W>* sv = tab + TS;
-  // after the dedup the table region is reused: sorted keys + bin counters
-  KeyT<W>* so = tab;
-  uint32_t* bins = reinterpret_cast<uint32_t*>(tab + LIMIT);
+  SvRec<W>* sv = reinterpret_cast<SvRec<W>*>(tab + TS);
+  // after the dedup the table region is reused: sorted survivor indices + bin counters
+  uint16_t* so = reinterpret_cast<uint16_t*>(tab);
+  uint32_t* bins = reinterpret_cast<uint32_t*>(so + LIMIT);
   __shared__ int s_zero;
-  __shared__ uint32_t s_ns;
+  __shared__ uint32_t s_ns, s_b1;
   __shared__ int s_bad;
   __shared__ uint32_t red[33];
-  for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {
-    const uint32_t start = off[b], cnt = off[b + 1] - start;
-    if (cnt == 0) {
-      if (threadIdx.x == 0) surv[b] = 0;
-      continue;
-    }
-    uint32_t ts = 64;
-    while (ts < 2 * cnt && ts < TS) ts <<= 1;
-    for (uint32_t i = threadIdx.x; i < ts; i += kBT) tab[i] = KeyT<W>{};
-    if (threadIdx.x == 0) {
-      s_zero = 0;
-      s_ns = 0;
-      s_bad = 0;
-    }
-    __syncthreads();
-    bool full = false;
-    for (uint32_t r0 = 0; r0 < cnt; r0 += kBTile) {
-      KeyT<W> k[kBI];
-#pragma unroll
-      for (int u = 0; u < kBI; u++) {
-        const uint32_t i = r0 + u * kBT + threadIdx.x;
-        if (i < cnt) k[u] = load_key<W>(part, (uint64_t)start + i);
-      }
-#pragma unroll
-      for (int u = 0; u < kBI; u++) {
-        const uint32_t i = r0 + u * kBT + threadIdx.x;
-        if (i < cnt && tab_insert<W>(tab, ts, k[u], &s_zero, &full)) {
-          const uint32_t j = atomicAdd(&s_ns, 1u);
-          if (j < LIMIT) sv[j] = k[u];
-        }
-      }
-    }
-    if (full) s_bad = 1;
-    __syncthreads();
-    const uint32_t ns = s_ns;
-    if (s_bad || ns > LIMIT) {
-      // overflow: pass the bucket through unfiltered and let the host finish
-      for (uint32_t i = threadIdx.x; i < cnt; i += kBT)
-        store_key<W>(tmp, (uint64_t)start + i, load_key<W>(part, (uint64_t)start + i));
+  const uint32_t nchunks = (nb + chunk - 1) / chunk;
+  for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const uint32_t cb1 = min(nb, (c + 1) * chunk);
+    uint32_t b0 = c * chunk;
+    while (b0 < cb1) {
       if (threadIdx.x == 0) {
-        surv[b] = cnt;
-        atomicAdd(&flags[0], 1ull);
+        const uint32_t s0 = off[b0];
+        uint32_t b1 = b0 + 1;
+        while (b1 < cb1 && off[b1 + 1] - s0 <= RUN_CAP) b1++;
+        s_b1 = b1;
+        s_zero = 0;
+        s_ns = 0;
+        s_bad = 0;
       }
       __syncthreads();
-      continue;
-    }
-    // counting sort of the survivors on the next sb bits of hi
-    int sb = 8;
-    while ((1u << sb) < ns && sb < 12) sb++;
-    const uint32_t NB = 1u << sb;
-    const int shift = 64 - B - sb;  // B + sb <= 64 always (B <= 24)
-    for (uint32_t i = threadIdx.x; i < NB; i += kBT) bins[i] = 0;
-    __syncthreads();
-    uint32_t myrank[LIMIT / kBT];
-#pragma unroll
-    for (int u = 0; u < (int)(LIMIT / kBT); u++) {
-      const uint32_t i = u * kBT + threadIdx.x;
-      if (i < ns) myrank[u] = atomicAdd(&bins[(uint32_t)(hk_hi(sv[i]) >> shift) & (NB - 1)], 1u);
-    }
-    __syncthreads();
-    // exclusive scan of the NB bin counts (NB / 256 consecutive bins per thread)
-    const uint32_t per = NB / kBT;
-    uint32_t loc = 0;
-    uint32_t cnts[16];
-    for (uint32_t j = 0; j < per; j++) {
-      cnts[j] = bins[threadIdx.x * per + j];
-      loc += cnts[j];
-    }
-    uint32_t tot;
-    uint32_t ex = block_excl_scan_u32(loc, red, tot);
-    for (uint32_t j = 0; j < per; j++) {
-      bins[threadIdx.x * per + j] = ex;  // bin start
-      ex += cnts[j];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < (int)(LIMIT / kBT); u++) {
-      const uint32_t i = u * kBT + threadIdx.x;
-      if (i < ns) {
-        const KeyT<W> key = sv[i];
-        so[bins[(uint32_t)(hk_hi(key) >> shift) & (NB - 1)] + myrank[u]] = key;
+      const uint32_t b1 = s_b1;
+      const uint32_t start = off[b0], cnt = off[b1] - start;
+      if (cnt == 0) {
+        for (uint32_t x = b0 + threadIdx.x; x < b1; x += kBT) surv[x] = 0;
+        __syncthreads();
+        b0 = b1;
+        continue;
       }
-    }
-    __syncthreads();
-    // order the (few) keys that share a bin: insertion sort in the hash order
-    for (uint32_t bi = threadIdx.x; bi < NB; bi += kBT) {
-      const uint32_t s0 = bins[bi];
-      const uint32_t s1 = (bi + 1 < NB) ? bins[bi + 1] : ns;
-      for (uint32_t i = s0 + 1; i < s1; i++) {
-        const KeyT<W> key = so[i];
-        uint32_t j = i;
-        while (j > s0 && hk_lt(key, so[j - 1])) {
-          so[j] = so[j - 1];
-          j--;
+      uint32_t ts = 64;
+      while (ts < 2 * cnt && ts < TS) ts <<= 1;
+      for (uint32_t i = threadIdx.x; i < ts; i += kBT) tab[i] = KeyT<W>{};
+      __syncthreads();
+      bool full = false;
+      for (uint32_t r0 = 0; r0 < cnt; r0 += kBTile) {
+        KeyT<W> kc[kBI];
+#pragma unroll
+        for (int u = 0; u < kBI; u++) {
+          const uint32_t i = r0 + u * kBT + threadIdx.x;
+          if (i < cnt) kc[u] = load_key<W>(part, (uint64_t)start + i);
         }
-        so[j] = key;
+#pragma unroll
+        for (int u = 0; u < kBI; u++) {
+          const uint32_t i = r0 + u * kBT + threadIdx.x;
+          if (i < cnt) {
+            const uint64_t hi = hk_hi(kc[u]);
+            if (tab_insert<W>(tab, ts, kc[u], hi, &s_zero, &full)) {
+              const uint32_t j = atomicAdd(&s_ns, 1u);
+              if (j < LIMIT) sv[j] = SvRec<W>{kc[u], hi};
+            }
+          }
+        }
       }
+      if (full) s_bad = 1;
+      __syncthreads();
+      const uint32_t ns = s_ns;
+      if (s_bad || ns > LIMIT) {
+        // overflow (one huge bucket): pass it through unfiltered, the host finishes
+        for (uint32_t i = threadIdx.x; i < cnt; i += kBT)
+          store_key<W>(tmp, (uint64_t)start + i, load_key<W>(part, (uint64_t)start + i));
+        for (uint32_t x = b0 + threadIdx.x; x < b1; x += kBT) surv[x] = x == b0 ? cnt : 0u;
+        if (threadIdx.x == 0) atomicAdd(&flags[0], 1ull);
+        __syncthreads();
+        b0 = b1;
+        continue;
+      }
+      // counting sort of the survivors on hi relative to the run's range
+      int sb = 8;
+      while ((1u << sb) < ns && sb < 11) sb++;
+      const uint32_t NB = 1u << sb;
+      int span = 64 - B;  // bits of hi below the bucket id
+      for (uint32_t w = b1 - b0 - 1; w; w >>= 1) span++;
+      const uint64_t base = B ? ((uint64_t)b0 << (64 - B)) : 0ull;
+      const int shift = span > sb ? span - sb : 0;
+      for (uint32_t i = threadIdx.x; i < NB; i += kBT) bins[i] = 0;
+      __syncthreads();
+      uint32_t myrank[PER_MAX];
+#pragma unroll
+      for (int u = 0; u < PER_MAX; u++) {
+        const uint32_t i = u * kBT + threadIdx.x;
+        if (i < ns) myrank[u] = atomicAdd(&bins[(uint32_t)((sv[i].hi - base) >> shift) & (NB - 1)], 1u);
+      }
+      __syncthreads();
+      const uint32_t per = NB / kBT;
+      uint32_t loc = 0;
+      uint32_t cnts[BDCfg<W>::NBMAX / kBT];
+      for (uint32_t j = 0; j < per; j++) {
+        cnts[j] = bins[threadIdx.x * per + j];
+        loc += cnts[j];
+      }
+      uint32_t tot;
+      uint32_t ex = block_excl_scan_u32(loc, red, tot);
+      for (uint32_t j = 0; j < per; j++) {
+        bins[threadIdx.x * per + j] = ex;  // bin start
+        ex += cnts[j];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < PER_MAX; u++) {
+        const uint32_t i = u * kBT + threadIdx.x;
+        if (i < ns) so[bins[(uint32_t)((sv[i].hi - base) >> shift) & (NB - 1)] + myrank[u]] = (uint16_t)i;
+      }
+      __syncthreads();
+      // order the (few) keys that share a bin: insertion sort in the hash order
+      for (uint32_t bi = threadIdx.x; bi < NB; bi += kBT) {
+        const uint32_t s0 = bins[bi];
+        const uint32_t s1 = (bi + 1 < NB) ? bins[bi + 1] : ns;
+        for (uint32_t i = s0 + 1; i < s1; i++) {
+          const uint16_t x = so[i];
+          const uint64_t hx = sv[x].hi;
+          uint32_t j = i;
+          while (j > s0) {
+            const uint16_t y = so[j - 1];
+            const uint64_t hy = sv[y].hi;
+            const bool lt = W == 1 ? hx < hy : (hx < hy || (hx == hy && hk_lo(sv[x].key) < hk_lo(sv[y].key)));
+            if (!lt) break;
+            so[j] = y;
+            j--;
+          }
+          so[j] = x;
+        }
+      }
+      __syncthreads();
+      for (uint32_t i = threadIdx.x; i < ns; i += kBT) store_key<W>(tmp, (uint64_t)start + i, sv[so[i]].key);
+      for (uint32_t x = b0 + threadIdx.x; x < b1; x += kBT) surv[x] = x == b0 ? ns : 0u;
+      __syncthreads();
+      b0 = b1;
     }
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < ns; i += kBT) store_key<W>(tmp, (uint64_t)start + i, so[i]);
-    if (threadIdx.x == 0) surv[b] = ns;
-    __syncthreads();
   }
 }
 
@@ -365,7 +402,7 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
   Scratch s(ctx);
   // B bits of hi: ~<= 2048 keys per bucket on average
   int B = 0;
-  while ((n >> B) > 2048 && B < 22) B++;
+  while ((n >> B) > 1792 && B < 22) B++;  // <= LIMIT distinct keys per bucket w.h.p.
   const uint32_t nb = 1u << B;
   uint64_t *a, *b2;
   uint32_t *hist, *off, *cur, *surv;
@@ -449,8 +486,15 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
                                          (int)BDCfg<W>::SMEM));
     attr[W] = true;
   }
-  const unsigned dgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(nb, (uint64_t)ctx->num_sms * 2));
-  CUSCI_LAUNCH(ctx, PT_HASH, bucket_dedup_sort_kernel<W><<<dgrid, kBT, BDCfg<W>::SMEM, ctx->stream>>>(part, off, nb, B, tmp, surv, flags));
+  static int dper[3] = {0, 0, 0};
+  if (!dper[W]) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&dper[W], bucket_dedup_sort_kernel<W>, kBT, BDCfg<W>::SMEM);
+    if (dper[W] < 1) dper[W] = 1;
+  }
+  const uint32_t chunk = 64;  // consecutive buckets per CTA work item
+  const uint32_t nchunks = (nb + chunk - 1) / chunk;
+  const unsigned dgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(nchunks, (uint64_t)ctx->num_sms * dper[W]));
+  CUSCI_LAUNCH(ctx, PT_HASH, bucket_dedup_sort_kernel<W><<<dgrid, kBT, BDCfg<W>::SMEM, ctx->stream>>>(part, off, nb, B, chunk, tmp, surv, flags));
   // compact the buckets' survivors in bucket order
   CUSCI_CUDA(ctx, cudaMemsetAsync(surv64, 0, (nb + 1) * sizeof(uint64_t), ctx->stream));
   CUSCI_CUDA(ctx, cudaMemcpy2DAsync(surv64, sizeof(uint64_t), surv, sizeof(uint32_t), sizeof(uint32_t), nb,
