@@ -68,8 +68,8 @@ __global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(const uint64_
   constexpr int kMergeItems = MergeCfg<W>::ITEMS;
   constexpr int kTile = MergeCfg<W>::TILE;
   __shared__ KeyT<W> ab[kTile];     // S run then U run
-  __shared__ KeyT<W> mrg[kTile];    // merged tile
-  __shared__ uint8_t fromU[kTile];
+  __shared__ uint64_t abh[kTile];   // their hash-order hi (computed once per element)
+  __shared__ uint16_t mrg[kTile];   // merged tile as indices into ab (>= na: from U)
   __shared__ uint32_t wk[kMergeThreads / 32], wi[kMergeThreads / 32];
   __shared__ uint64_t run_k, run_i;
   __shared__ unsigned s_tile;
@@ -84,17 +84,29 @@ __global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(const uint64_
   const bool inval = i1 < i0 || j1 < j0 || (i1 - i0) + (j1 - j0) > (uint64_t)kTile || j1 > nU || i1 > nS;
   if (inval && threadIdx.x == 0) *bad = 1;
   const int na = inval ? 0 : (int)(i1 - i0), nb = inval ? 0 : (int)(j1 - j0), len = na + nb;
-  for (int x = threadIdx.x; x < na; x += kMergeThreads) ab[x] = load_key<W>(S, i0 + x);
-  for (int x = threadIdx.x; x < nb; x += kMergeThreads) ab[na + x] = load_key<W>(U, j0 + x);
+  for (int x = threadIdx.x; x < na; x += kMergeThreads) {
+    const KeyT<W> k = load_key<W>(S, i0 + x);
+    ab[x] = k;
+    abh[x] = hk_hi(k);
+  }
+  for (int x = threadIdx.x; x < nb; x += kMergeThreads) {
+    const KeyT<W> k = load_key<W>(U, j0 + x);
+    ab[na + x] = k;
+    abh[na + x] = hk_hi(k);
+  }
   __syncthreads();
-  const KeyT<W>* A = ab;
-  const KeyT<W>* B = ab + na;
+  // hash-order comparisons on the staged elements: hi first, lo only on a tie (W = 2)
+  auto le = [&](int x, int y) -> bool {
+    const uint64_t hx = abh[x], hy = abh[y];
+    if (W == 1 || hx != hy) return hx <= hy;
+    return hk_lo(ab[x]) <= hk_lo(ab[y]);
+  };
   // input check: U strictly increasing in the hash order (tile run + left boundary)
   {
     bool badu = false;
     for (int x = threadIdx.x; x < nb; x += kMergeThreads) {
-      if (x > 0) badu |= !hk_lt<W>(B[x - 1], B[x]);
-      else if (j0 > 0 && j0 <= nU) badu |= !hk_lt<W>(load_key<W>(U, j0 - 1), B[0]);
+      if (x > 0) badu |= le(na + x, na + x - 1);
+      else if (j0 > 0 && j0 <= nU) badu |= !hk_lt<W>(load_key<W>(U, j0 - 1), ab[na]);
     }
     if (badu) *bad = 1;
   }
@@ -104,19 +116,13 @@ __global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(const uint64_
     int lo = k0 > nb ? k0 - nb : 0, hi = std::min(k0, na);
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      if (hk_le<W>(A[mid], B[k0 - mid - 1])) lo = mid + 1;
+      if (le(mid, na + k0 - mid - 1)) lo = mid + 1;
       else hi = mid;
     }
     int i = lo, j = k0 - lo;
     for (int k = k0; k < std::min(k0 + kMergeItems, len); k++) {
-      const bool takeA = i < na && (j >= nb || hk_le<W>(A[i], B[j]));
-      if (takeA) {
-        mrg[k] = A[i++];
-        fromU[k] = 0;
-      } else {
-        mrg[k] = B[j++];
-        fromU[k] = 1;
-      }
+      const bool takeA = i < na && (j >= nb || le(i, na + j));
+      mrg[k] = (uint16_t)(takeA ? i++ : na + j++);
     }
   }
   // predecessor of the tile's first output: the larger of S[i0-1], U[j0-1]
@@ -138,9 +144,9 @@ __global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(const uint64_
   for (int r = 0; r < kMergeItems; r++) {
     const int k = r * kMergeThreads + threadIdx.x;
     if (k < len) {
-      const bool dup = k > 0 ? key_eq(mrg[k], mrg[k - 1]) : (has_prev0 && key_eq(mrg[0], prev0));
+      const bool dup = k > 0 ? key_eq(ab[mrg[k]], ab[mrg[k - 1]]) : (has_prev0 && key_eq(ab[mrg[0]], prev0));
       ck += !dup;
-      ci += (!dup && fromU[k]);
+      ci += (!dup && mrg[k] >= na);
     }
   }
   for (int o = 16; o; o >>= 1) {
@@ -182,9 +188,9 @@ __global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(const uint64_
     const int k = r * kMergeThreads + threadIdx.x;
     bool keep = false, isins = false;
     if (k < len) {
-      const bool dup = k > 0 ? key_eq(mrg[k], mrg[k - 1]) : (has_prev0 && key_eq(mrg[0], prev0));
+      const bool dup = k > 0 ? key_eq(ab[mrg[k]], ab[mrg[k - 1]]) : (has_prev0 && key_eq(ab[mrg[0]], prev0));
       keep = !dup;
-      isins = keep && fromU[k];
+      isins = keep && mrg[k] >= na;
     }
     const unsigned bk = __ballot_sync(kFull, keep), bi = __ballot_sync(kFull, isins);
     if (lane_id() == 0) {
@@ -201,8 +207,8 @@ __global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(const uint64_
       tk += wk[x];
       ti += wi[x];
     }
-    if (keep) store_key<W>(out, run_k + ok + __popc(bk & lanemask_lt()), mrg[k]);
-    if (isins && ins) store_key<W>(ins, run_i + oi + __popc(bi & lanemask_lt()), mrg[k]);
+    if (keep) store_key<W>(out, run_k + ok + __popc(bk & lanemask_lt()), ab[mrg[k]]);
+    if (isins && ins) store_key<W>(ins, run_i + oi + __popc(bi & lanemask_lt()), ab[mrg[k]]);
     __syncthreads();
     if (threadIdx.x == 0) {
       run_k += tk;
