@@ -85,18 +85,21 @@ __global__ void __launch_bounds__(kBT) tile_hist_kernel(const uint64_t* __restri
   for (uint32_t d = threadIdx.x; d <= dmask; d += kBT) mat[t.mbase + (uint64_t)d * t.stride] = h[d];
 }
 
+constexpr int kST = 512;  // scatter threads (2 CTAs / SM at <= 64 registers)
 template <int W>
-__global__ void __launch_bounds__(kBT) tile_scatter_kernel(const uint64_t* __restrict__ in,
-                                                          const PTile* __restrict__ tiles, int bsel, uint32_t dmask,
-                                                          const uint32_t* __restrict__ offs, uint64_t* __restrict__ out) {
-  constexpr int ITEMS = SSCfg<W>::ITEMS, SUB = SSCfg<W>::SUB;
+__global__ void __launch_bounds__(kST, 2) tile_scatter_kernel(const uint64_t* __restrict__ in,
+                                                             const PTile* __restrict__ tiles, int bsel, uint32_t dmask,
+                                                             const uint32_t* __restrict__ offs, uint64_t* __restrict__ out) {
+  constexpr int ITEMS = SSCfg<W>::SUB / kST;
+  constexpr int SUB = SSCfg<W>::SUB;
   __shared__ uint32_t cur[256], cnt[256], lst[256];
   __shared__ uint32_t red[33];
   __shared__ KeyT<W> stage[SUB];
   __shared__ uint8_t sdig[SUB];
   const PTile t = tiles[blockIdx.x];
   const uint32_t R = dmask + 1;
-  for (uint32_t d = threadIdx.x; d < 256; d += kBT) {
+  if (threadIdx.x < 256) {
+    const uint32_t d = threadIdx.x;
     cur[d] = d < R ? offs[t.mbase + (uint64_t)d * t.stride] : 0u;
     cnt[d] = 0;
   }
@@ -104,43 +107,46 @@ __global__ void __launch_bounds__(kBT) tile_scatter_kernel(const uint64_t* __res
   for (uint32_t r0 = 0; r0 < t.len; r0 += SUB) {
     const uint32_t m = min((uint32_t)SUB, t.len - r0);
     KeyT<W> k[ITEMS];
-    uint32_t d[ITEMS], rk[ITEMS];
+    uint32_t dr[ITEMS];  // digit << 16 | rank within the sub-round
 #pragma unroll
     for (int u = 0; u < ITEMS; u++) {
-      const uint32_t i = u * kBT + threadIdx.x;
+      const uint32_t i = u * kST + threadIdx.x;
       if (i < m) k[u] = load_key<W>(in, t.start + r0 + i);
     }
 #pragma unroll
     for (int u = 0; u < ITEMS; u++) {
-      const uint32_t i = u * kBT + threadIdx.x;
+      const uint32_t i = u * kST + threadIdx.x;
       if (i < m) {
-        d[u] = top_bits<W>(k[u], bsel) & dmask;
-        rk[u] = atomicAdd(&cnt[d[u]], 1u);
+        const uint32_t d = top_bits<W>(k[u], bsel) & dmask;
+        dr[u] = (d << 16) | atomicAdd(&cnt[d], 1u);
       }
     }
     __syncthreads();
     uint32_t tot;
-    const uint32_t c = cnt[threadIdx.x];
+    const uint32_t c = threadIdx.x < 256 ? cnt[threadIdx.x] : 0u;
     const uint32_t ex = block_excl_scan_u32(c, red, tot);
-    lst[threadIdx.x] = ex;
+    if (threadIdx.x < 256) lst[threadIdx.x] = ex;
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < ITEMS; u++) {
-      const uint32_t i = u * kBT + threadIdx.x;
+      const uint32_t i = u * kST + threadIdx.x;
       if (i < m) {
-        const uint32_t pos = lst[d[u]] + rk[u];
+        const uint32_t d = dr[u] >> 16;
+        const uint32_t pos = lst[d] + (dr[u] & 0xffffu);
         stage[pos] = k[u];
-        sdig[pos] = (uint8_t)d[u];
+        sdig[pos] = (uint8_t)d;
       }
     }
     __syncthreads();
-    for (uint32_t j = threadIdx.x; j < m; j += kBT) {
+    for (uint32_t j = threadIdx.x; j < m; j += kST) {
       const uint32_t dj = sdig[j];
       store_key<W>(out, (uint64_t)cur[dj] + (j - lst[dj]), stage[j]);
     }
     __syncthreads();
-    cur[threadIdx.x] += c;
-    cnt[threadIdx.x] = 0;
+    if (threadIdx.x < 256) {
+      cur[threadIdx.x] += c;
+      cnt[threadIdx.x] = 0;
+    }
     __syncthreads();
   }
 }
@@ -460,7 +466,7 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
       const int sel = done + bits;
       CUSCI_LAUNCH(ctx, PT_RADIX_UP, tile_hist_kernel<W><<<nt, kBT, 0, ctx->stream>>>(part, dtl, sel, R - 1, mat));
       CUSCI_TRY(scan_exclusive_u32(ctx, mat, offs, mb));
-      CUSCI_LAUNCH(ctx, PT_RADIX_DOWN, tile_scatter_kernel<W><<<nt, kBT, 0, ctx->stream>>>(part, dtl, sel, R - 1, offs, dst));
+      CUSCI_LAUNCH(ctx, PT_RADIX_DOWN, tile_scatter_kernel<W><<<nt, kST, 0, ctx->stream>>>(part, dtl, sel, R - 1, offs, dst));
       uint32_t* goff_final = (pi == np - 1) ? off : goff;
       CUSCI_LAUNCH(ctx, PT_SCATTER, group_off_kernel<<<(unsigned)(((uint64_t)G * R + 1 + 255) / 256), 256, 0, ctx->stream>>>(offs, dgm, G, bits, (uint32_t)n, goff_final));
       if (pi < np - 1) {
