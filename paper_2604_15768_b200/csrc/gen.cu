@@ -41,7 +41,7 @@ constexpr unsigned long long kNoError = ~0ull;
 constexpr int kChunks = 4;  // 32-entry chunks (128-bit loads per lane) in flight per step
 
 template <int W> struct GenCfg {
-  static constexpr int STAGE = W == 1 ? 384 : 192;  // staged records per warp (3-5 CTAs/SM)
+  static constexpr int STAGE = W == 1 ? 256 : 192;  // staged records per warp (4 CTAs/SM)
   static constexpr size_t BYTES_PER_REC = (W == 1 ? 16 : 24) + 4 + 1;
   static constexpr size_t SMEM = (size_t)kGenWarps * STAGE * BYTES_PER_REC;
 };
@@ -373,7 +373,7 @@ __device__ __forceinline__ uint32_t do_pairs(const GenArgs& a, const KeyT<W>& pa
 }
 
 template <int W, int MODE>
-__global__ void __launch_bounds__(kGenThreads, 3) gen_kernel(const GenArgs a) {
+__global__ void __launch_bounds__(kGenThreads, 4) gen_kernel(const GenArgs a) {
   extern __shared__ __align__(16) unsigned char gsm[];
   __shared__ uint8_t occ_s[kGenWarps][128];
   __shared__ ulonglong2 bm_s[kGenWarps][W == 1 ? 64 : 1];
