@@ -182,13 +182,20 @@ __device__ __forceinline__ void stage_flush(const GenArgs& a, Stage<W>& st) {
   if (lane == 0) base = atomicAdd(&a.counter[0], (unsigned long long)st.n);
   base = __shfl_sync(kFull, base, 0);
   if (base + st.n <= a.capacity) {
-    for (uint32_t i = lane; i < st.n; i += 32) {
-      const StRec<W> r = st.kh[i];
-      store_key<W>(a.keys, base + i, st_key(r));
-      a.hij[base + i] = r.h;
+    if (a.src) {
+      for (uint32_t i = lane; i < st.n; i += 32) {
+        const StRec<W> r = st.kh[i];
+        store_key<W>(a.keys, base + i, st_key(r));
+        a.hij[base + i] = r.h;
+        a.src[base + i] = st.src[i];
+      }
+    } else {
+      for (uint32_t i = lane; i < st.n; i += 32) {
+        const StRec<W> r = st.kh[i];
+        store_key<W>(a.keys, base + i, st_key(r));
+        a.hij[base + i] = r.h;
+      }
     }
-    if (a.src)
-      for (uint32_t i = lane; i < st.n; i += 32) a.src[base + i] = st.src[i];
     if (MODE == 2)
       for (uint32_t i = lane; i < st.n; i += 32) a.phase[base + i] = st.ph[i];
   }
@@ -342,10 +349,10 @@ __device__ __forceinline__ uint32_t do_pairs(const GenArgs& a, const KeyT<W>& pa
       ne1 = __ldg(a.rowptr + nrow + 1);
     }
     KeyT<W> base, M;
-    if constexpr (W == 1) {  // per-occupied {2^p, above(p)} precomputed once per unit
+    if constexpr (W == 1) {  // per-occupied {2^p, PP ^ above(p)} precomputed once per unit
       const ulonglong2 bx = bm[x], by = bm[y];
       base = KeyT<W>{par.w0 ^ bx.x ^ by.x};
-      M = KeyT<W>{PP.w0 ^ bx.y ^ by.y};
+      M = KeyT<W>{bx.y ^ by.y ^ PP.w0};  // (PP^above p)^(PP^above q)^PP = PP^above p^above q
     } else {
       base = kxor(par, kxor(bitk<W>(p), bitk<W>(q)));
       M = kxor(PP, kxor(abovek<W>(p), abovek<W>(q)));
@@ -376,7 +383,7 @@ template <int W, int MODE>
 __global__ void __launch_bounds__(kGenThreads, 4) gen_kernel(const GenArgs a) {
   extern __shared__ __align__(16) unsigned char gsm[];
   __shared__ uint8_t occ_s[kGenWarps][128];
-  __shared__ ulonglong2 bm_s[kGenWarps][W == 1 ? 64 : 1];
+  __shared__ ulonglong2 bm_s[kGenWarps][W == 1 ? 64 : 1];  // {2^p, PP ^ above(p)} per occupied index
   __shared__ unsigned long long unit_s[kGenWarps];
   if (a.counter[2] != kNoError) return;  // invalid parent: write nothing
   const int w = threadIdx.x >> 5;
@@ -411,14 +418,14 @@ __global__ void __launch_bounds__(kGenThreads, 4) gen_kernel(const GenArgs a) {
       if (b) occ[nocc + __popc(bal & lanemask_lt())] = (uint8_t)t;
       nocc += __popc(bal);
     }
+    const KeyT<W> PP = prefix_parity(par);
     if constexpr (W == 1) {
       for (uint32_t x = lane; x < nocc; x += 32) {
         const int t = occ[x];
-        bm_s[w][x] = make_ulonglong2(1ull << t, t >= 63 ? 0ull : (~0ull << (t + 1)));
+        bm_s[w][x] = make_ulonglong2(1ull << t, PP.w0 ^ (t >= 63 ? 0ull : (~0ull << (t + 1))));
       }
     }
     __syncwarp();
-    const KeyT<W> PP = prefix_parity(par);
     uint32_t cnt = 0;
     if (r0 == 0 && r1 > 0) cnt += do_singles<W, MODE>(a, par, PP, occ, (uint32_t)s, st);
     const uint32_t pr0 = r0 == 0 ? 1 : r0;
