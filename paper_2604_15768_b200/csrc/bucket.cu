@@ -249,15 +249,18 @@ __global__ void __launch_bounds__(kBT, 3) bucket_dedup_sort_kernel(const uint64_
   __shared__ uint32_t s_ns, s_b1;
   __shared__ int s_bad;
   __shared__ uint32_t red[33];
+  __shared__ uint32_t soff[kBT + 1];  // the chunk's bucket offsets (one coalesced load)
   const uint32_t nchunks = (nb + chunk - 1) / chunk;
   for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-    const uint32_t cb1 = min(nb, (c + 1) * chunk);
-    uint32_t b0 = c * chunk;
+    const uint32_t cb0 = c * chunk, cb1 = min(nb, (c + 1) * chunk);
+    for (uint32_t x = threadIdx.x; x <= cb1 - cb0; x += kBT) soff[x] = off[cb0 + x];
+    __syncthreads();
+    uint32_t b0 = cb0;
     while (b0 < cb1) {
       if (threadIdx.x == 0) {
-        const uint32_t s0 = off[b0];
+        const uint32_t s0 = soff[b0 - cb0];
         uint32_t b1 = b0 + 1;
-        while (b1 < cb1 && off[b1 + 1] - s0 <= RUN_CAP) b1++;
+        while (b1 < cb1 && soff[b1 + 1 - cb0] - s0 <= RUN_CAP) b1++;
         s_b1 = b1;
         s_zero = 0;
         s_ns = 0;
@@ -265,7 +268,7 @@ __global__ void __launch_bounds__(kBT, 3) bucket_dedup_sort_kernel(const uint64_
       }
       __syncthreads();
       const uint32_t b1 = s_b1;
-      const uint32_t start = off[b0], cnt = off[b1] - start;
+      const uint32_t start = soff[b0 - cb0], cnt = soff[b1 - cb0] - start;
       if (cnt == 0) {
         for (uint32_t x = b0 + threadIdx.x; x < b1; x += kBT) surv[x] = 0;
         __syncthreads();
@@ -497,7 +500,7 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&dper[W], bucket_dedup_sort_kernel<W>, kBT, BDCfg<W>::SMEM);
     if (dper[W] < 1) dper[W] = 1;
   }
-  const uint32_t chunk = 64;  // consecutive buckets per CTA work item
+  const uint32_t chunk = 128;  // consecutive buckets per CTA work item (<= kBT)
   const uint32_t nchunks = (nb + chunk - 1) / chunk;
   const unsigned dgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(nchunks, (uint64_t)ctx->num_sms * dper[W]));
   CUSCI_LAUNCH(ctx, PT_HASH, bucket_dedup_sort_kernel<W><<<dgrid, kBT, BDCfg<W>::SMEM, ctx->stream>>>(part, off, nb, B, chunk, tmp, surv, flags));
