@@ -334,9 +334,9 @@ def main():
     # algorithmic bytes per step for each kernel class
     alg = {
         "gen": sum(counts) * rec_bytes + n_par * 8 * W,                       # records written + parents read
-        "radix_downsweep": sum(dedup_passes(c) * c * 16 * W for c in counts),  # partition: read + write a key per pass
-        "radix_upsweep": sum(dedup_passes(c) * c * 8 * W for c in counts),     # per-pass histograms: read a key
-        "hash_filter": sum(c * 8 * W for c in counts),                         # bucket dedup: read every key once
+        "part_scatter": sum(dedup_passes(c) * c * 16 * W for c in counts),  # partition: read + write a key per pass
+        "part_hist": sum(dedup_passes(c) * c * 8 * W for c in counts),     # per-pass histograms: read a key
+        "bucket_unique": sum(c * 8 * W for c in counts),                         # bucket dedup: read every key once
     }
     kernels = {}
     for name, (kms, kl) in prof.items():

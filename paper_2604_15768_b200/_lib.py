@@ -17,7 +17,7 @@ EXPORTS = ["cusci_nccl_unique_id", "cusci_init", "cusci_finalize", "cusci_last_e
            "cusci_pool_copy", "cusci_pool_clear", "cusci_pool_destroy", "merge_space"]
 
 
-PROFILE_TAGS = ["prep", "validate", "gen", "hash_filter", "owner_scatter", "radix_upsweep", "radix_downsweep",
+PROFILE_TAGS = ["prep", "validate", "gen", "bucket_unique", "pack", "part_hist", "part_scatter",
                 "scan", "unique", "merge_split", "merge_tile", "sorted_check", "nccl_exchange", "memset"]
 
 

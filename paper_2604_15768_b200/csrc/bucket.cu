@@ -2,26 +2,26 @@
 // PAPER.md:380-382 local uniqueness filter, :454-460 local sort + unique).
 //
 // B200 design (reading r13): keys are ordered by the hash
-// order pi(j) = (hi, lo) -- a fixed bijection of the key space (hi =
-// owner mix, so owner(j) = floor(hi * P / 2^64) is monotone in it) -- instead
-// of the big-integer order.  Because pi is uniform, a 2-level MSD partition on
-// the top B bits of hi (B = log2(n / ~2k)) puts ~2k keys in every bucket:
-//   pass 1  histogram + scatter by the top hb (<= 9) bits (per-tile shared-
-//           memory ranks, one global atomic per (tile, digit) on an
-//           L2-resident cursor array -- no look-back chain, no stability
-//           requirement);
-//   pass 2  histogram + scatter by the full B bits, tiles binned locally on
-//           the <= 2 pass-1 digits a tile spans (far keys: direct atomics);
-// then ONE CTA per bucket: open-addressing hash table in shared memory
-// (64-bit atomicCAS / ATOMS.CAS.128) keeps the first copy of each key, and
-// the survivors are sorted inside the bucket by a counting sort on the next
-// bits of hi plus an insertion sort of the (rare) collisions.  Buckets are
-// then concatenated in bucket order: the result is sorted in the hash order
-// and unique -- a full sort in two partition passes.  A bucket with more
+// order pi(j) = (hi, lo) -- a fixed bijection of the key space (hi = owner
+// mix, so owner(j) = floor(hi * P / 2^64) is monotone in it) -- instead of the
+// big-integer order.  Because pi is uniform, an MSD partition on the top B
+// bits of hi (B = log2(n / ~1.5k)) puts ~1.5k keys in every bucket:
+//   passes  segmented MSD passes of <= 8 bits (per-tile histograms, one scan,
+//           staged coalesced scatter); the first pass maps keys to their
+//           pi-values, which the later passes and the dedup read directly;
+//   dedup   one CTA per bucket: the bucket streams into shared memory by TMA
+//           bulk copies (next bucket prefetched), an ORDER-PRESERVING open-
+//           addressing table (home = next bits of hi, linear probing, no
+//           wrap) keeps one copy of each pi-value, sorting each short cluster
+//           in place sorts the table, and the survivors are mapped back to
+//           keys (exact inverse mix);
+//   pack    buckets are concatenated in bucket order.
+// The result is unique and sorted in the hash order.  A bucket with more
 // distinct keys than its table holds is flagged; the host then finishes with
 // a full LSD sort over the hash digits + unique (exact, rare slow path).
 #include <algorithm>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "internal.cuh"
@@ -33,9 +33,16 @@ constexpr int kBT = 256;        // threads
 constexpr int kBI = 8;          // keys per thread per tile
 constexpr int kBTile = kBT * kBI;
 
+// digit source: the top bits of the pi-value's hi word (w0)
 template <int W>
-__device__ __forceinline__ uint32_t top_bits(const KeyT<W>& k, int bits) {
-  return bits ? (uint32_t)(hk_hi(k) >> (64 - bits)) : 0u;
+__device__ __forceinline__ uint32_t top_bits(const KeyT<W>& p, int bits) {
+  return bits ? (uint32_t)(p.w0 >> (64 - bits)) : 0u;
+}
+// key i of the pass input as a pi-value (RAW: the caller's keys, mixed here once)
+template <int W, bool RAW>
+__device__ __forceinline__ KeyT<W> load_pi(const uint64_t* in, uint64_t i) {
+  const KeyT<W> k = load_key<W>(in, i);
+  return RAW ? to_pi(k) : k;
 }
 
 // ---------------------------------------------------------------- partition passes
@@ -60,11 +67,11 @@ template <int W> struct SSCfg {
   static constexpr int SUB = kBT * ITEMS;        // 4096 / 2048 keys (32 KB staged)
 };
 
-template <int W>
+template <int W, bool RAW, int RB>
 __global__ void __launch_bounds__(kBT) tile_hist_kernel(const uint64_t* __restrict__ in,
                                                        const PTile* __restrict__ tiles, int bsel, uint32_t dmask,
                                                        uint32_t* __restrict__ mat) {
-  __shared__ uint32_t h[256];
+  __shared__ uint32_t h[1 << RB];
   const PTile t = tiles[blockIdx.x];
   for (uint32_t i = threadIdx.x; i <= dmask; i += kBT) h[i] = 0;
   __syncthreads();
@@ -73,7 +80,7 @@ __global__ void __launch_bounds__(kBT) tile_hist_kernel(const uint64_t* __restri
 #pragma unroll
     for (int u = 0; u < kBI; u++) {
       const uint32_t i = r0 + u * kBT + threadIdx.x;
-      if (i < t.len) k[u] = load_key<W>(in, t.start + i);
+      if (i < t.len) k[u] = load_pi<W, RAW>(in, t.start + i);
     }
 #pragma unroll
     for (int u = 0; u < kBI; u++) {
@@ -85,47 +92,127 @@ __global__ void __launch_bounds__(kBT) tile_hist_kernel(const uint64_t* __restri
   for (uint32_t d = threadIdx.x; d <= dmask; d += kBT) mat[t.mbase + (uint64_t)d * t.stride] = h[d];
 }
 
-constexpr int kST = 512;  // scatter threads (2 CTAs / SM at <= 64 registers)
+constexpr int kST = 512;  // scatter threads
+// dynamic shared memory: two TMA input buffers, the digit-ordered stage, digits, cursors
+template <int W, int RB> constexpr size_t scatter_smem() {
+  return 3 * ((size_t)SSCfg<W>::SUB + 2) * sizeof(KeyT<W>) + (size_t)SSCfg<W>::SUB * (RB > 8 ? 2 : 1) +
+         3 * sizeof(uint32_t) * (1u << RB);
+}
+
+// thread 0: bulk-copy keys [s, s + len) into buf so that key s + i lands at
+// buf[i + (s & 1)] (W = 1) / buf[i] (W = 2).  Only the 16-byte aligned core is
+// copied; keys outside it (an odd head or tail, W = 1) are read from global by
+// their consumer (scatter_key).  Returns the bytes the barrier expects (may be 0).
 template <int W>
-__global__ void __launch_bounds__(kST, 2) tile_scatter_kernel(const uint64_t* __restrict__ in,
+__device__ __forceinline__ uint32_t issue_core(const uint64_t* in, uint64_t s, uint32_t len, KeyT<W>* buf,
+                                               uint64_t* bar) {
+  if (W == 1) {
+    const uint64_t a0 = (s + 1) & ~1ull, a1 = (s + len) & ~1ull;
+    if (a1 <= a0) return 0;
+    const uint32_t bytes = (uint32_t)((a1 - a0) * 8);
+    tma_load_1d(buf + (a0 - s) + (s & 1), in + a0, bytes, bar);
+    return bytes;
+  } else {
+    if (!len) return 0;
+    tma_load_1d(buf, in + 2 * s, len * 16u, bar);
+    return len * 16u;
+  }
+}
+template <int W>
+__device__ __forceinline__ KeyT<W> scatter_key(const uint64_t* in, uint64_t s, uint32_t i, uint32_t len,
+                                               const KeyT<W>* buf, bool tma) {
+  if (!tma) return load_key<W>(in, s + i);
+  if (W == 1) {
+    const uint64_t g = s + i;
+    const bool core = g >= ((s + 1) & ~1ull) && g < ((s + len) & ~1ull);
+    return core ? buf[i + (s & 1)] : load_key<W>(in, g);
+  }
+  return buf[i];
+}
+
+// The tile streams through shared memory by 1-D TMA bulk copies, the next
+// sub-round's keys in flight while the current one is ranked and written.
+template <int W, bool RAW, int RB>
+__global__ void __launch_bounds__(kST, 2) tile_scatter_kernel(const uint64_t* __restrict__ in, int use_tma,
                                                              const PTile* __restrict__ tiles, int bsel, uint32_t dmask,
                                                              const uint32_t* __restrict__ offs, uint64_t* __restrict__ out) {
   constexpr int ITEMS = SSCfg<W>::SUB / kST;
   constexpr int SUB = SSCfg<W>::SUB;
-  __shared__ uint32_t cur[256], cnt[256], lst[256];
+  constexpr uint32_t RMAX = 1u << RB;
+  constexpr uint32_t DPT = RMAX > kST ? RMAX / kST : 1;  // digits per thread in the scan
+  using Dig = typename std::conditional<(RB > 8), uint16_t, uint8_t>::type;
+  extern __shared__ __align__(16) unsigned char ssm[];  // scatter_smem<W, RB>() bytes
+  KeyT<W>* inb = reinterpret_cast<KeyT<W>*>(ssm);        // [2][SUB + 2]
+  KeyT<W>* stage = inb + 2 * (SUB + 2);
+  uint32_t* cur = reinterpret_cast<uint32_t*>(stage + SUB + 2);
+  uint32_t* cnt = cur + RMAX;
+  uint32_t* lst = cnt + RMAX;
+  Dig* sdig = reinterpret_cast<Dig*>(lst + RMAX);
   __shared__ uint32_t red[33];
-  __shared__ KeyT<W> stage[SUB];
-  __shared__ uint8_t sdig[SUB];
+  __shared__ __align__(8) uint64_t bar[2];
   const PTile t = tiles[blockIdx.x];
   const uint32_t R = dmask + 1;
-  if (threadIdx.x < 256) {
-    const uint32_t d = threadIdx.x;
+  const bool tma = use_tma && ((reinterpret_cast<uintptr_t>(in) & 15u) == 0);
+  for (uint32_t d = threadIdx.x; d < RMAX; d += kST) {
     cur[d] = d < R ? offs[t.mbase + (uint64_t)d * t.stride] : 0u;
     cnt[d] = 0;
   }
+  const uint32_t nsub = (t.len + SUB - 1) / SUB;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_init_fence();
+  }
   __syncthreads();
-  for (uint32_t r0 = 0; r0 < t.len; r0 += SUB) {
+  if (tma && threadIdx.x == 0 && nsub) issue_core<W>(in, t.start, min((uint32_t)SUB, t.len), inb, &bar[0]);
+  uint32_t phase = 0;
+  for (uint32_t r = 0; r < nsub; r++) {
+    const uint32_t cb = r & 1, r0 = r * SUB;
     const uint32_t m = min((uint32_t)SUB, t.len - r0);
+    KeyT<W>* buf = inb + cb * (SUB + 2);
+    if (tma) {
+      if (threadIdx.x == 0 && r + 1 < nsub) {  // prefetch the next sub-round (its buffer was freed last round)
+        fence_proxy_async_smem();
+        issue_core<W>(in, t.start + r0 + SUB, min((uint32_t)SUB, t.len - r0 - SUB),
+                                       inb + (cb ^ 1) * (SUB + 2), &bar[cb ^ 1]);
+      }
+      // every thread knows whether a copy was issued (same arithmetic as issue_core)
+      const uint64_t s0 = t.start + r0;
+      const bool issued = W == 1 ? (((s0 + m) & ~1ull) > ((s0 + 1) & ~1ull)) : m > 0;
+      if (issued) {
+        mbar_wait(&bar[cb], (phase >> cb) & 1u);
+        phase ^= 1u << cb;
+      }
+    }
     KeyT<W> k[ITEMS];
     uint32_t dr[ITEMS];  // digit << 16 | rank within the sub-round
 #pragma unroll
     for (int u = 0; u < ITEMS; u++) {
       const uint32_t i = u * kST + threadIdx.x;
-      if (i < m) k[u] = load_key<W>(in, t.start + r0 + i);
-    }
-#pragma unroll
-    for (int u = 0; u < ITEMS; u++) {
-      const uint32_t i = u * kST + threadIdx.x;
       if (i < m) {
+        k[u] = scatter_key<W>(in, t.start + r0, i, m, buf, tma);
+        if (RAW) k[u] = to_pi(k[u]);
         const uint32_t d = top_bits<W>(k[u], bsel) & dmask;
         dr[u] = (d << 16) | atomicAdd(&cnt[d], 1u);
       }
     }
     __syncthreads();
+    // sub-round digit counts -> exclusive offsets (thread: DPT consecutive digits)
+    uint32_t c[DPT], loc = 0;
+#pragma unroll
+    for (uint32_t j = 0; j < DPT; j++) {
+      const uint32_t d = threadIdx.x * DPT + j;
+      c[j] = d < RMAX ? cnt[d] : 0u;
+      loc += c[j];
+    }
     uint32_t tot;
-    const uint32_t c = threadIdx.x < 256 ? cnt[threadIdx.x] : 0u;
-    const uint32_t ex = block_excl_scan_u32(c, red, tot);
-    if (threadIdx.x < 256) lst[threadIdx.x] = ex;
+    uint32_t ex = block_excl_scan_u32(loc, red, tot);
+#pragma unroll
+    for (uint32_t j = 0; j < DPT; j++) {
+      const uint32_t d = threadIdx.x * DPT + j;
+      if (d < RMAX) lst[d] = ex;
+      ex += c[j];
+    }
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < ITEMS; u++) {
@@ -134,7 +221,7 @@ __global__ void __launch_bounds__(kST, 2) tile_scatter_kernel(const uint64_t* __
         const uint32_t d = dr[u] >> 16;
         const uint32_t pos = lst[d] + (dr[u] & 0xffffu);
         stage[pos] = k[u];
-        sdig[pos] = (uint8_t)d;
+        sdig[pos] = (Dig)d;
       }
     }
     __syncthreads();
@@ -143,9 +230,13 @@ __global__ void __launch_bounds__(kST, 2) tile_scatter_kernel(const uint64_t* __
       store_key<W>(out, (uint64_t)cur[dj] + (j - lst[dj]), stage[j]);
     }
     __syncthreads();
-    if (threadIdx.x < 256) {
-      cur[threadIdx.x] += c;
-      cnt[threadIdx.x] = 0;
+#pragma unroll
+    for (uint32_t j = 0; j < DPT; j++) {
+      const uint32_t d = threadIdx.x * DPT + j;
+      if (d < RMAX) {
+        cur[d] += c[j];
+        cnt[d] = 0;
+      }
     }
     __syncthreads();
   }
@@ -167,18 +258,26 @@ __global__ void group_off_kernel(const uint32_t* __restrict__ offs, const uint4*
   off[id] = m.y ? offs[m.z + (uint64_t)d * m.y] : m.x;
 }
 
-// ---------------------------------------------------------------- per-bucket dedup + sort
-// survivor record: the key and its hash-order hi (computed once per key)
-template <int W> struct SvRec {
-  KeyT<W> key;
-  uint64_t hi;
-};
-template <int W> struct BDCfg {
-  static constexpr uint32_t TS = W == 1 ? 4096 : 2048;     // table slots (32 KB)
-  static constexpr uint32_t LIMIT = W == 1 ? 2560 : 1280;  // distinct keys per bucket
-  static constexpr uint32_t NBMAX = 2048;                  // counting-sort bins
-  static constexpr size_t SMEM = (size_t)TS * sizeof(KeyT<W>) + (size_t)LIMIT * sizeof(SvRec<W>);
-  static_assert(LIMIT * 2 + NBMAX * 4 <= TS * sizeof(KeyT<W>), "sort scratch must fit the table");
+// ---------------------------------------------------------------- per-bucket dedup (ordered table)
+// One CTA per bucket (static interleaved assignment: CTA c takes buckets c,
+// c + G, ...; G = resident CTAs).  A bucket is a contiguous run of pi-values
+// whose hi lies in [b, b+1) * 2^(64-B).  Its keys stream into shared memory by
+// 1-D TMA bulk copies (the NEXT bucket's first piece is in flight while this
+// one is processed) and are inserted into an ORDER-PRESERVING open-addressing
+// table: home slot = the next log2(ts) bits of hi below the bucket id, linear
+// probing forward with no wrap (an overflow tail of OV slots).  Since home is
+// monotone in hi, every cluster of occupied slots holds exactly the keys whose
+// homes fall inside it, so sorting each (short) cluster in place leaves the
+// whole table sorted in the hash order: no separate sort pass.  The
+// survivors are mapped back to keys (exact inverse mix) and written at the
+// bucket's input offset; a compaction kernel then packs the buckets.
+template <int W> struct BUCfg {
+  static constexpr uint32_t TS = W == 1 ? 4096 : 2048;   // max home slots
+  static constexpr uint32_t OV = W == 1 ? 256 : 128;     // overflow tail
+  static constexpr uint32_t BUFK = W == 1 ? 2048 : 1024; // keys per TMA piece (16 KB)
+  static constexpr uint32_t BUFE = BUFK + 2;             // + alignment slack (W = 1)
+  static constexpr uint32_t TARGET = W == 1 ? 1536 : 768;  // mean keys per bucket
+  static constexpr size_t SMEM = (size_t)(TS + OV) * sizeof(KeyT<W>) + 2 * (size_t)BUFE * sizeof(KeyT<W>);
 };
 
 __device__ __forceinline__ void cas_slot(KeyT<1>* slot, const KeyT<1>& k, KeyT<1>& old) {
@@ -202,191 +301,268 @@ __device__ __forceinline__ void cas_slot(KeyT<2>* slot, const KeyT<2>& k, KeyT<2
 __device__ __forceinline__ bool kzero(const KeyT<1>& k) { return k.w0 == 0; }
 __device__ __forceinline__ bool kzero(const KeyT<2>& k) { return (k.w0 | k.w1) == 0; }
 
-// returns true iff k was inserted (first copy); *full set when no slot found
-template <int W>
-__device__ __forceinline__ bool tab_insert(KeyT<W>* tab, uint32_t ts, const KeyT<W>& k, uint64_t hi, int* s_zero,
-                                           bool* full) {
-  if (kzero(k)) return atomicExch(s_zero, 1) == 0;
-  uint32_t h = (uint32_t)hi & (ts - 1);  // low bits of hi: uniform within a bucket
-  for (uint32_t probe = 0; probe < ts; probe++) {
-    const KeyT<W> cur = tab[h];
-    if (key_eq(cur, k)) return false;
-    if (kzero(cur)) {
-      KeyT<W> old;
-      cas_slot(&tab[h], k, old);
-      if (kzero(old)) return true;
-      if (key_eq(old, k)) return false;
+// insert pi-value p (nonzero) from its home slot, marking a newly claimed slot
+// in the occupancy bitmap; false when the span is exhausted.  W = 2 probes with
+// the 128-bit CAS itself (returns the slot's value atomically), so a probe
+// never sees a torn 16-byte entry.
+__device__ __forceinline__ bool otab_insert(KeyT<1>* tab, uint32_t* bm, uint32_t home, uint32_t span,
+                                            const KeyT<1>& p) {
+  for (uint32_t s = home; s < span; s++) {
+    const KeyT<1> cur = tab[s];
+    if (cur.w0 == p.w0) return true;
+    if (cur.w0 == 0) {
+      KeyT<1> old;
+      cas_slot(&tab[s], p, old);
+      if (old.w0 == 0) atomicOr(&bm[s >> 5], 1u << (s & 31));
+      if (old.w0 == 0 || old.w0 == p.w0) return true;
     }
-    h = (h + 1) & (ts - 1);
   }
-  *full = true;
+  return false;
+}
+__device__ __forceinline__ bool otab_insert(KeyT<2>* tab, uint32_t* bm, uint32_t home, uint32_t span,
+                                            const KeyT<2>& p) {
+  for (uint32_t s = home; s < span; s++) {
+    KeyT<2> old;
+    cas_slot(&tab[s], p, old);
+    if (kzero(old)) atomicOr(&bm[s >> 5], 1u << (s & 31));
+    if (kzero(old) || key_eq(old, p)) return true;
+  }
   return false;
 }
 
-// A CTA walks a chunk of consecutive buckets and processes them in RUNS:
-// as many consecutive buckets as fit RUN_CAP keys share one table clear, one
-// dedup and one sort (buckets hold ~1-2 Ki keys but often few distinct ones,
-// so per-bucket fixed costs would dominate).  The run's survivors (key + hi,
-// hi computed once per key) are counting-sorted by hi and written at the run's
-// first bucket offset; surv[] gets the run count there and 0 for the run's
-// other buckets, which is what the compaction expects.
+// thread 0: start the bulk copy of keys [s, s + len) of `part` into `buf`
 template <int W>
-__global__ void __launch_bounds__(kBT, 3) bucket_dedup_sort_kernel(const uint64_t* __restrict__ part,
-                                                                  const uint32_t* __restrict__ off, uint32_t nb, int B,
-                                                                  uint32_t chunk, uint64_t* __restrict__ tmp,
-                                                                  uint32_t* __restrict__ surv,
-                                                                  unsigned long long* __restrict__ flags) {
-  extern __shared__ __align__(16) unsigned char bsm[];
-  constexpr uint32_t TS = BDCfg<W>::TS, LIMIT = BDCfg<W>::LIMIT;
-  constexpr uint32_t RUN_CAP = TS / 2;
-  constexpr int PER_MAX = (LIMIT + kBT - 1) / kBT;
-  KeyT<W>* tab = reinterpret_cast<KeyT<W>*>(bsm);
-  SvRec<W>* sv = reinterpret_cast<SvRec<W>*>(tab + TS);
-  // after the dedup the table region is reused: sorted survivor indices + bin counters
-  uint16_t* so = reinterpret_cast<uint16_t*>(tab);
-  uint32_t* bins = reinterpret_cast<uint32_t*>(so + LIMIT);
-  __shared__ int s_zero;
-  __shared__ uint32_t s_ns, s_b1;
-  __shared__ int s_bad;
-  __shared__ uint32_t red[33];
-  __shared__ uint32_t soff[kBT + 1];  // the chunk's bucket offsets (one coalesced load)
-  const uint32_t nchunks = (nb + chunk - 1) / chunk;
-  for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-    const uint32_t cb0 = c * chunk, cb1 = min(nb, (c + 1) * chunk);
-    for (uint32_t x = threadIdx.x; x <= cb1 - cb0; x += kBT) soff[x] = off[cb0 + x];
-    __syncthreads();
-    uint32_t b0 = cb0;
-    while (b0 < cb1) {
-      if (threadIdx.x == 0) {
-        const uint32_t s0 = soff[b0 - cb0];
-        uint32_t b1 = b0 + 1;
-        while (b1 < cb1 && soff[b1 + 1 - cb0] - s0 <= RUN_CAP) b1++;
-        s_b1 = b1;
-        s_zero = 0;
-        s_ns = 0;
-        s_bad = 0;
-      }
-      __syncthreads();
-      const uint32_t b1 = s_b1;
-      const uint32_t start = soff[b0 - cb0], cnt = soff[b1 - cb0] - start;
-      if (cnt == 0) {
-        for (uint32_t x = b0 + threadIdx.x; x < b1; x += kBT) surv[x] = 0;
-        __syncthreads();
-        b0 = b1;
-        continue;
-      }
-      uint32_t ts = 64;
-      while (ts < 2 * cnt && ts < TS) ts <<= 1;
-      for (uint32_t i = threadIdx.x; i < ts; i += kBT) tab[i] = KeyT<W>{};
-      __syncthreads();
-      bool full = false;
-      for (uint32_t r0 = 0; r0 < cnt; r0 += kBTile) {
-        KeyT<W> kc[kBI];
-#pragma unroll
-        for (int u = 0; u < kBI; u++) {
-          const uint32_t i = r0 + u * kBT + threadIdx.x;
-          if (i < cnt) kc[u] = load_key<W>(part, (uint64_t)start + i);
-        }
-#pragma unroll
-        for (int u = 0; u < kBI; u++) {
-          const uint32_t i = r0 + u * kBT + threadIdx.x;
-          if (i < cnt) {
-            const uint64_t hi = hk_hi(kc[u]);
-            if (tab_insert<W>(tab, ts, kc[u], hi, &s_zero, &full)) {
-              const uint32_t j = atomicAdd(&s_ns, 1u);
-              if (j < LIMIT) sv[j] = SvRec<W>{kc[u], hi};
-            }
-          }
-        }
-      }
-      if (full) s_bad = 1;
-      __syncthreads();
-      const uint32_t ns = s_ns;
-      if (s_bad || ns > LIMIT) {
-        // overflow (one huge bucket): pass it through unfiltered, the host finishes
-        for (uint32_t i = threadIdx.x; i < cnt; i += kBT)
-          store_key<W>(tmp, (uint64_t)start + i, load_key<W>(part, (uint64_t)start + i));
-        for (uint32_t x = b0 + threadIdx.x; x < b1; x += kBT) surv[x] = x == b0 ? cnt : 0u;
-        if (threadIdx.x == 0) atomicAdd(&flags[0], 1ull);
-        __syncthreads();
-        b0 = b1;
-        continue;
-      }
-      // counting sort of the survivors on hi relative to the run's range
-      int sb = 8;
-      while ((1u << sb) < ns && sb < 11) sb++;
-      const uint32_t NB = 1u << sb;
-      int span = 64 - B;  // bits of hi below the bucket id
-      for (uint32_t w = b1 - b0 - 1; w; w >>= 1) span++;
-      const uint64_t base = B ? ((uint64_t)b0 << (64 - B)) : 0ull;
-      const int shift = span > sb ? span - sb : 0;
-      for (uint32_t i = threadIdx.x; i < NB; i += kBT) bins[i] = 0;
-      __syncthreads();
-      uint32_t myrank[PER_MAX];
-#pragma unroll
-      for (int u = 0; u < PER_MAX; u++) {
-        const uint32_t i = u * kBT + threadIdx.x;
-        if (i < ns) myrank[u] = atomicAdd(&bins[(uint32_t)((sv[i].hi - base) >> shift) & (NB - 1)], 1u);
-      }
-      __syncthreads();
-      const uint32_t per = NB / kBT;
-      uint32_t loc = 0;
-      uint32_t cnts[BDCfg<W>::NBMAX / kBT];
-      for (uint32_t j = 0; j < per; j++) {
-        cnts[j] = bins[threadIdx.x * per + j];
-        loc += cnts[j];
-      }
-      uint32_t tot;
-      uint32_t ex = block_excl_scan_u32(loc, red, tot);
-      for (uint32_t j = 0; j < per; j++) {
-        bins[threadIdx.x * per + j] = ex;  // bin start
-        ex += cnts[j];
-      }
-      __syncthreads();
-#pragma unroll
-      for (int u = 0; u < PER_MAX; u++) {
-        const uint32_t i = u * kBT + threadIdx.x;
-        if (i < ns) so[bins[(uint32_t)((sv[i].hi - base) >> shift) & (NB - 1)] + myrank[u]] = (uint16_t)i;
-      }
-      __syncthreads();
-      // order the (few) keys that share a bin: insertion sort in the hash order
-      for (uint32_t bi = threadIdx.x; bi < NB; bi += kBT) {
-        const uint32_t s0 = bins[bi];
-        const uint32_t s1 = (bi + 1 < NB) ? bins[bi + 1] : ns;
-        for (uint32_t i = s0 + 1; i < s1; i++) {
-          const uint16_t x = so[i];
-          const uint64_t hx = sv[x].hi;
-          uint32_t j = i;
-          while (j > s0) {
-            const uint16_t y = so[j - 1];
-            const uint64_t hy = sv[y].hi;
-            const bool lt = W == 1 ? hx < hy : (hx < hy || (hx == hy && hk_lo(sv[x].key) < hk_lo(sv[y].key)));
-            if (!lt) break;
-            so[j] = y;
-            j--;
-          }
-          so[j] = x;
-        }
-      }
-      __syncthreads();
-      for (uint32_t i = threadIdx.x; i < ns; i += kBT) store_key<W>(tmp, (uint64_t)start + i, sv[so[i]].key);
-      for (uint32_t x = b0 + threadIdx.x; x < b1; x += kBT) surv[x] = x == b0 ? ns : 0u;
-      __syncthreads();
-      b0 = b1;
-    }
+__device__ __forceinline__ void issue_piece(const uint64_t* part, uint64_t s, uint32_t len, KeyT<W>* buf, uint64_t* bar) {
+  if (W == 1) {
+    const uint64_t a0 = s & ~1ull, a1 = (s + len + 1) & ~1ull;
+    tma_load_1d(buf, part + a0, (uint32_t)((a1 - a0) * 8), bar);
+  } else {
+    tma_load_1d(buf, part + 2 * s, len * 16u, bar);
   }
 }
 
+template <int W>
+__global__ void __launch_bounds__(kBT, 3) bucket_unique_kernel(const uint64_t* __restrict__ part, int raw, int use_tma,
+                                                              const uint32_t* __restrict__ off, uint32_t nb, int B, uint32_t lf,
+                                                              uint64_t* __restrict__ tmp, uint32_t* __restrict__ surv,
+                                                              unsigned long long* __restrict__ flags) {
+  using K = KeyT<W>;
+  constexpr uint32_t TS = BUCfg<W>::TS, OV = BUCfg<W>::OV, BUFK = BUCfg<W>::BUFK, BUFE = BUCfg<W>::BUFE;
+  constexpr int NW = kBT / 32;
+  constexpr uint32_t WIN = kBT;  // buckets per staged offset window
+  extern __shared__ __align__(16) unsigned char bsm[];
+  K* tab = reinterpret_cast<K*>(bsm);
+  K* bufs = tab + TS + OV;
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ int s_zero, s_full;
+  __shared__ uint32_t wcnt[NW];
+  __shared__ uint32_t bm[(TS + OV) / 32];  // slot occupancy bitmap
+  __shared__ uint32_t soff[WIN + 2];       // off[w0 .. w0 + WIN + 1]
+  static_assert((TS + OV) / 32 <= kBT, "one bitmap word per thread");
+  static_assert(BUFE * sizeof(KeyT<W>) >= (TS + OV) * sizeof(uint16_t), "slot list must fit a buffer");
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5, t = threadIdx.x;
+  // TMA needs 16-byte aligned sources; raw (caller) input is read with plain loads
+  const bool tma = use_tma && !raw && ((reinterpret_cast<uintptr_t>(part) & 15u) == 0);
+  // this CTA's contiguous bucket range
+  const uint32_t bA = (uint32_t)((uint64_t)nb * blockIdx.x / gridDim.x);
+  const uint32_t bB = (uint32_t)((uint64_t)nb * (blockIdx.x + 1) / gridDim.x);
+  // the table is cleared once here and kept clean: the compaction zeroes every slot it reads
+  for (uint32_t i = t; i < TS + OV; i += kBT) tab[i] = K{};
+  for (uint32_t i = t; i < (TS + OV) / 32; i += kBT) bm[i] = 0;
+  if (t == 0) {
+    s_zero = 0;
+    s_full = 0;
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_init_fence();
+  }
+  uint32_t w0 = bA;
+  for (uint32_t i = t; i < WIN + 2 && w0 + i <= nb; i += kBT) soff[i] = off[w0 + i];
+  __syncthreads();
+  uint32_t phase = 0;  // bit i: parity of buffer i's next completion
+  int cb = 0;
+  if (tma && t == 0 && bA < bB) {
+    const uint32_t l0 = min(soff[1] - soff[0], BUFK);
+    if (l0) issue_piece<W>(part, soff[0], l0, bufs, &bar[0]);
+  }
+  for (uint32_t b = bA; b < bB; b++, cb ^= 1) {
+    if (b - w0 == WIN) {  // next offset window (one coalesced load)
+      w0 = b;
+      for (uint32_t i = t; i < WIN + 2 && w0 + i <= nb; i += kBT) soff[i] = off[w0 + i];
+      __syncthreads();
+    }
+    const uint32_t s = soff[b - w0], nk = soff[b - w0 + 1] - s;
+    K* buf = bufs + cb * BUFE;
+    // prefetch the next bucket's first piece into the other buffer (its last
+    // readers passed the previous bucket's final barrier)
+    if (tma && t == 0 && b + 1 < bB) {
+      const uint32_t sn = soff[b + 1 - w0], en = (b + 2 - w0 <= WIN + 1) ? soff[b + 2 - w0] : off[b + 2];
+      const uint32_t ln = min(en - sn, BUFK);
+      if (ln) {
+        fence_proxy_async_smem();
+        issue_piece<W>(part, sn, ln, bufs + (cb ^ 1) * BUFE, &bar[cb ^ 1]);
+      }
+    }
+    if (nk == 0) {
+      if (t == 0) surv[b] = 0;
+      continue;
+    }
+    // table size ~LF nk slots (load <= 1/LF even when every key is distinct:
+    // short clusters, cheap in-place sorts); home = floor(frac * ts), frac =
+    // the bits of hi below the bucket id
+    const uint32_t ts = min(TS, max(64u, (lf * nk + 31u) & ~31u));
+    const uint32_t span = ts + OV;
+    bool full = false;
+    for (uint32_t p0 = 0; p0 < nk; p0 += BUFK) {
+      const uint32_t len = min(BUFK, nk - p0);
+      uint32_t lead = 0;
+      if (tma) {
+        if (p0 > 0) {  // later pieces of a large bucket reuse the same buffer
+          __syncthreads();
+          if (t == 0) {
+            fence_proxy_async_smem();
+            issue_piece<W>(part, (uint64_t)s + p0, len, buf, &bar[cb]);
+          }
+        }
+        mbar_wait(&bar[cb], (phase >> cb) & 1u);
+        phase ^= 1u << cb;
+        lead = W == 1 ? (uint32_t)((s + p0) & 1u) : 0u;
+      }
+      for (uint32_t i = t; i < len; i += kBT) {
+        K p = tma ? buf[lead + i] : load_key<W>(part, (uint64_t)s + p0 + i);
+        if (raw) p = to_pi(p);
+        if (kzero(p)) {
+          s_zero = 1;
+          continue;
+        }
+        const uint32_t home = (uint32_t)__umul64hi(p.w0 << B, (uint64_t)ts);
+        full |= !otab_insert(tab, bm, home, span, p);
+      }
+    }
+    if (full) s_full = 1;
+    __syncthreads();  // (A) table complete; the input buffer is consumed
+    const uint32_t z = (uint32_t)s_zero;
+    if (s_full) {
+      // table overflow (pathological bucket): pass the keys through unfiltered
+      // (the host finishes with a full sort + unique); restore a clean table
+      for (uint32_t i = t; i < nk; i += kBT) {
+        const K p = load_key<W>(part, (uint64_t)s + i);
+        store_key<W>(tmp, (uint64_t)s + i, raw ? p : from_pi(p));
+      }
+      for (uint32_t i = t; i < span; i += kBT) tab[i] = K{};
+      for (uint32_t i = t; i < (span + 31) / 32; i += kBT) bm[i] = 0;
+      if (t == 0) {
+        surv[b] = nk;
+        atomicAdd(&flags[0], 1ull);
+      }
+      __syncthreads();
+      if (t == 0) {
+        s_full = 0;
+        s_zero = 0;
+      }
+      __syncthreads();
+      continue;
+    }
+    // pass 1 (thread t: bitmap word t = slots [32t, 32t + 32)): the thread
+    // owning a cluster's first slot insertion-sorts the cluster
+    const uint32_t nwd = (span + 31) / 32;
+    const uint32_t bits = t < nwd ? bm[t] : 0u;
+    if (bits) {
+      const uint32_t prev = t > 0 ? (bm[t - 1] >> 31) : 0u;
+      uint32_t starts = bits & ~((bits << 1) | prev);
+      while (starts) {
+        const uint32_t i = __ffs(starts) - 1;
+        starts &= starts - 1;
+        const uint32_t u = t * 32 + i;
+        // cluster end: the first clear bit at or after slot u
+        const uint32_t y = ~(bits >> i);
+        const uint32_t run = y ? __ffs(y) - 1 : 32u;  // ones from bit i up
+        uint32_t e = u + run;
+        if (run >= 32 - i) {  // the run reaches the word's end: continue in the next words
+          for (uint32_t w = t + 1; w < nwd; w++) {
+            const uint32_t x = bm[w];
+            e += x == ~0u ? 32u : (uint32_t)(__ffs(~x) - 1);
+            if (x != ~0u) break;
+          }
+        }
+        e = min(e, span);
+        for (uint32_t k = u + 1; k < e; k++) {
+          const K x = tab[k];
+          uint32_t j = k;
+          while (j > u && pi_lt(x, tab[j - 1])) {
+            tab[j] = tab[j - 1];
+            j--;
+          }
+          tab[j] = x;
+        }
+      }
+    }
+    // exclusive prefix of the per-word counts (warp scan + warp totals)
+    const uint32_t c = __popc(bits);
+    uint32_t inc = c;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, inc, o);
+      if ((int)lane >= o) inc += y;
+    }
+    if (lane == 31) wcnt[warp] = inc;
+    __syncthreads();  // (B) clusters sorted, per-warp counts
+    uint32_t pos = inc - c, tot = 0;
+    for (int w = 0; w < NW; w++) {
+      const uint32_t v = wcnt[w];
+      pos += w < (int)warp ? v : 0u;
+      tot += v;
+    }
+    // pass 2: the word owners list the occupied slots in order (in the consumed
+    // input buffer), then every thread writes survivors back as keys and
+    // clears their slots
+    uint16_t* sidx = reinterpret_cast<uint16_t*>(buf);
+    if (bits) {
+      uint32_t r = bits;
+      while (r) {
+        sidx[pos++] = (uint16_t)(t * 32 + __ffs(r) - 1);
+        r &= r - 1;
+      }
+      bm[t] = 0;
+    }
+    if (z && t == 0) store_key<W>(tmp, (uint64_t)s, from_pi(K{}));
+    __syncthreads();  // (C) slot list complete
+    for (uint32_t i = t; i < tot; i += kBT) {
+      const uint32_t u = sidx[i];
+      store_key<W>(tmp, (uint64_t)s + z + i, from_pi(tab[u]));
+      tab[u] = K{};
+    }
+    if (t == 0) {
+      surv[b] = tot + z;
+      s_zero = 0;
+    }
+    __syncthreads();  // (D) table clean for the next bucket
+  }
+}
+
+// pack the buckets' survivors: one warp per 32 consecutive buckets (metadata
+// loaded lane-parallel, then each bucket copied by the whole warp)
 template <int W>
 __global__ void __launch_bounds__(kBT) bucket_compact_kernel(const uint64_t* __restrict__ tmp,
                                                             const uint32_t* __restrict__ off,
                                                             const uint32_t* __restrict__ surv,
                                                             const uint64_t* __restrict__ soff, uint32_t nb,
                                                             uint64_t* __restrict__ out) {
-  for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {
-    const uint32_t start = off[b], ns = surv[b];
-    const uint64_t o = soff[b];
-    for (uint32_t i = threadIdx.x; i < ns; i += kBT) store_key<W>(out, o + i, load_key<W>(tmp, (uint64_t)start + i));
+  const uint32_t lane = lane_id();
+  const uint32_t gw = (blockIdx.x * kBT + threadIdx.x) >> 5, nw = (gridDim.x * kBT) >> 5;
+  for (uint32_t g = gw * 32; g < nb; g += nw * 32) {
+    const uint32_t b = g + lane;
+    uint32_t st = 0, ns = 0;
+    uint64_t o = 0;
+    if (b < nb) {
+      st = off[b];
+      ns = surv[b];
+      o = soff[b];
+    }
+    for (int l = 0; l < 32; l++) {
+      const uint32_t sl = __shfl_sync(kFull, st, l), nl = __shfl_sync(kFull, ns, l);
+      const uint64_t ol = __shfl_sync(kFull, o, l);
+      for (uint32_t i = lane; i < nl; i += 32) store_key<W>(out, ol + i, load_key<W>(tmp, (uint64_t)sl + i));
+    }
   }
 }
 
@@ -409,29 +585,48 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
   *n_out = 0;
   if (n == 0) return CUSCI_OK;
   Scratch s(ctx);
-  // B bits of hi: ~<= 2048 keys per bucket on average
+  // B bits of hi: ~TARGET keys per bucket on average
+  static const uint64_t target = [] {
+    const char* e = getenv("CUSCI_BUCKET_TARGET");  // tuning knob
+    return e ? (uint64_t)atoll(e) : (uint64_t)BUCfg<W>::TARGET;
+  }();
+  static const int max_pass_bits = [] {
+    const char* e = getenv("CUSCI_PASS_BITS");  // tuning knob (<= 11)
+    return e ? std::max(1, std::min(11, atoi(e))) : 8;
+  }();
+  static const int use_tma = getenv("CUSCI_NO_TMA") ? 0 : 1;  // A/B knob
+  static const uint32_t lf = [] {
+    const char* e = getenv("CUSCI_TABLE_LF");  // table slots per key (tuning knob)
+    return e ? (uint32_t)std::max(2, atoi(e)) : 4u;
+  }();
   int B = 0;
-  while ((n >> B) > 1792 && B < 22) B++;  // <= LIMIT distinct keys per bucket w.h.p.
+  while ((n >> B) > target && B < 22) B++;
   const uint32_t nb = 1u << B;
   uint64_t *a, *b2;
-  uint32_t *hist, *off, *cur, *surv;
+  uint32_t *off, *surv;
   uint64_t *surv64, *soff;
   unsigned long long* flags;
-  CUSCI_TRY(s.get_t(n * W, &a));
-  CUSCI_TRY(s.get_t(n * W, &b2));
-  CUSCI_TRY(s.get_t(nb + 1, &hist));
+  CUSCI_TRY(s.get_t((n + 2) * W, &a));   // + slack: TMA pieces round up to 16 bytes
+  CUSCI_TRY(s.get_t((n + 2) * W, &b2));
   CUSCI_TRY(s.get_t(nb + 1, &off));
-  CUSCI_TRY(s.get_t(nb + 1, &cur));
   CUSCI_TRY(s.get_t(nb + 1, &surv));
   CUSCI_TRY(s.get_t(nb + 1, &surv64));
   CUSCI_TRY(s.get_t(nb + 1, &soff));
   CUSCI_TRY(s.get_t(2, &flags));
   CUSCI_CUDA(ctx, cudaMemsetAsync(flags, 0, 2 * sizeof(unsigned long long), ctx->stream));
-  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + kBTile - 1) / kBTile, (uint64_t)ctx->num_sms * 8));
+  static bool sattr[3] = {false, false, false};
+  if (!sattr[W]) {
+    CUSCI_CUDA(ctx, cudaFuncSetAttribute(tile_scatter_kernel<W, true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scatter_smem<W, 8>()));
+    CUSCI_CUDA(ctx, cudaFuncSetAttribute(tile_scatter_kernel<W, false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scatter_smem<W, 8>()));
+    CUSCI_CUDA(ctx, cudaFuncSetAttribute(tile_scatter_kernel<W, true, 11>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scatter_smem<W, 11>()));
+    CUSCI_CUDA(ctx, cudaFuncSetAttribute(tile_scatter_kernel<W, false, 11>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scatter_smem<W, 11>()));
+    sattr[W] = true;
+  }
   const uint64_t* part = in;
   if (B > 0) {
-    // segmented MSD passes of <= 8 bits over the top B bits of hi
-    const int np = (B + 7) / 8;
+    // segmented MSD passes of <= 8 bits over the top B bits of hi; the first
+    // pass maps keys to pi-values, later passes and the dedup read pi-values
+    const int np = (B + max_pass_bits - 1) / max_pass_bits;
     int done = 0;
     std::vector<uint32_t> gstart{0u, (uint32_t)n};  // current groups (host)
     uint64_t* dst = a;
@@ -467,9 +662,21 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
       CUSCI_CUDA(ctx, cudaMemcpyAsync(dtl, tl.data(), nt * sizeof(PTile), cudaMemcpyHostToDevice, ctx->stream));
       CUSCI_CUDA(ctx, cudaMemcpyAsync(dgm, gm.data(), G * sizeof(uint4), cudaMemcpyHostToDevice, ctx->stream));
       const int sel = done + bits;
-      CUSCI_LAUNCH(ctx, PT_RADIX_UP, tile_hist_kernel<W><<<nt, kBT, 0, ctx->stream>>>(part, dtl, sel, R - 1, mat));
+      if (bits > 8) {
+        if (pi == 0) CUSCI_LAUNCH(ctx, PT_RADIX_UP, tile_hist_kernel<W, true, 11><<<nt, kBT, 0, ctx->stream>>>(part, dtl, sel, R - 1, mat));
+        else CUSCI_LAUNCH(ctx, PT_RADIX_UP, tile_hist_kernel<W, false, 11><<<nt, kBT, 0, ctx->stream>>>(part, dtl, sel, R - 1, mat));
+      } else {
+        if (pi == 0) CUSCI_LAUNCH(ctx, PT_RADIX_UP, tile_hist_kernel<W, true, 8><<<nt, kBT, 0, ctx->stream>>>(part, dtl, sel, R - 1, mat));
+        else CUSCI_LAUNCH(ctx, PT_RADIX_UP, tile_hist_kernel<W, false, 8><<<nt, kBT, 0, ctx->stream>>>(part, dtl, sel, R - 1, mat));
+      }
       CUSCI_TRY(scan_exclusive_u32(ctx, mat, offs, mb));
-      CUSCI_LAUNCH(ctx, PT_RADIX_DOWN, tile_scatter_kernel<W><<<nt, kST, 0, ctx->stream>>>(part, dtl, sel, R - 1, offs, dst));
+      if (bits > 8) {
+        if (pi == 0) CUSCI_LAUNCH(ctx, PT_RADIX_DOWN, tile_scatter_kernel<W, true, 11><<<nt, kST, scatter_smem<W, 11>(), ctx->stream>>>(part, use_tma, dtl, sel, R - 1, offs, dst));
+        else CUSCI_LAUNCH(ctx, PT_RADIX_DOWN, tile_scatter_kernel<W, false, 11><<<nt, kST, scatter_smem<W, 11>(), ctx->stream>>>(part, use_tma, dtl, sel, R - 1, offs, dst));
+      } else {
+        if (pi == 0) CUSCI_LAUNCH(ctx, PT_RADIX_DOWN, tile_scatter_kernel<W, true, 8><<<nt, kST, scatter_smem<W, 8>(), ctx->stream>>>(part, use_tma, dtl, sel, R - 1, offs, dst));
+        else CUSCI_LAUNCH(ctx, PT_RADIX_DOWN, tile_scatter_kernel<W, false, 8><<<nt, kST, scatter_smem<W, 8>(), ctx->stream>>>(part, use_tma, dtl, sel, R - 1, offs, dst));
+      }
       uint32_t* goff_final = (pi == np - 1) ? off : goff;
       CUSCI_LAUNCH(ctx, PT_SCATTER, group_off_kernel<<<(unsigned)(((uint64_t)G * R + 1 + 255) / 256), 256, 0, ctx->stream>>>(offs, dgm, G, bits, (uint32_t)n, goff_final));
       if (pi < np - 1) {
@@ -489,27 +696,22 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
     CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   }
   uint64_t* tmp = (part == a) ? b2 : a;
-  static bool attr[3] = {false, false, false};
-  if (!attr[W]) {
-    CUSCI_CUDA(ctx, cudaFuncSetAttribute(bucket_dedup_sort_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)BDCfg<W>::SMEM));
-    attr[W] = true;
-  }
   static int dper[3] = {0, 0, 0};
   if (!dper[W]) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&dper[W], bucket_dedup_sort_kernel<W>, kBT, BDCfg<W>::SMEM);
+    CUSCI_CUDA(ctx, cudaFuncSetAttribute(bucket_unique_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)BUCfg<W>::SMEM));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&dper[W], bucket_unique_kernel<W>, kBT, BUCfg<W>::SMEM);
     if (dper[W] < 1) dper[W] = 1;
   }
-  const uint32_t chunk = 128;  // consecutive buckets per CTA work item (<= kBT)
-  const uint32_t nchunks = (nb + chunk - 1) / chunk;
-  const unsigned dgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(nchunks, (uint64_t)ctx->num_sms * dper[W]));
-  CUSCI_LAUNCH(ctx, PT_HASH, bucket_dedup_sort_kernel<W><<<dgrid, kBT, BDCfg<W>::SMEM, ctx->stream>>>(part, off, nb, B, chunk, tmp, surv, flags));
-  // compact the buckets' survivors in bucket order
+  const unsigned dgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(nb, (uint64_t)ctx->num_sms * dper[W]));
+  CUSCI_LAUNCH(ctx, PT_HASH, bucket_unique_kernel<W><<<dgrid, kBT, BUCfg<W>::SMEM, ctx->stream>>>(part, part == in ? 1 : 0, use_tma, off, nb, B, lf, tmp, surv, flags));
+  // pack the buckets' survivors in bucket order
   CUSCI_CUDA(ctx, cudaMemsetAsync(surv64, 0, (nb + 1) * sizeof(uint64_t), ctx->stream));
   CUSCI_CUDA(ctx, cudaMemcpy2DAsync(surv64, sizeof(uint64_t), surv, sizeof(uint32_t), sizeof(uint32_t), nb,
                                     cudaMemcpyDeviceToDevice, ctx->stream));
   CUSCI_TRY(scan_exclusive_u64(ctx, surv64, soff, nb + 1, nullptr));
-  CUSCI_LAUNCH(ctx, PT_SCATTER, bucket_compact_kernel<W><<<dgrid, kBT, 0, ctx->stream>>>(tmp, off, surv, soff, nb, out));
+  const unsigned cgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nb + 255) / 256, (uint64_t)ctx->num_sms * 8));
+  CUSCI_LAUNCH(ctx, PT_SCATTER, bucket_compact_kernel<W><<<cgrid, kBT, 0, ctx->stream>>>(tmp, off, surv, soff, nb, out));
   uint64_t h[2];
   CUSCI_CUDA(ctx, cudaMemcpyAsync(ctx->host_pinned, soff + nb, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
   CUSCI_CUDA(ctx, cudaMemcpyAsync((char*)ctx->host_pinned + 8, flags, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));

@@ -256,6 +256,61 @@ template <int W> __device__ __forceinline__ bool hk_lt(const KeyT<W>& a, const K
 }
 template <int W> __device__ __forceinline__ bool hk_le(const KeyT<W>& a, const KeyT<W>& b) { return !hk_lt<W>(b, a); }
 
+// inverse of fmix64 (odd multipliers are invertible mod 2^64; x ^= x >> s is
+// undone by x ^= x >> s ^ x >> 2s ...)
+__device__ __forceinline__ uint64_t fmix64_inv(uint64_t x) {
+  x ^= (x >> 31) ^ (x >> 62);
+  x *= 0x319642B2D24D8EC3ull;  // (0x94D049BB133111EB)^-1 mod 2^64
+  x ^= (x >> 27) ^ (x >> 54);
+  x *= 0x96DE1B173F119089ull;  // (0xBF58476D1CE4E5B9)^-1 mod 2^64
+  x ^= (x >> 30) ^ (x >> 60);
+  return x;
+}
+// pi-values: the hash-order image of a key, stored in a KeyT slot.
+//   W = 1: w0 = hi;   W = 2: w0 = hi, w1 = lo   (compare w0 first)
+// Inside the dedup pipeline keys travel as pi-values (the mix is computed once,
+// on the first read) and are mapped back with the exact inverse on output.
+__device__ __forceinline__ KeyT<1> to_pi(const KeyT<1>& k) { return KeyT<1>{fmix64(k.w0)}; }
+__device__ __forceinline__ KeyT<2> to_pi(const KeyT<2>& k) {
+  const uint64_t lo = fmix64(k.w1 ^ 0x9E3779B97F4A7C15ull);
+  return KeyT<2>{fmix64(k.w0 ^ lo), lo};
+}
+__device__ __forceinline__ KeyT<1> from_pi(const KeyT<1>& p) { return KeyT<1>{fmix64_inv(p.w0)}; }
+__device__ __forceinline__ KeyT<2> from_pi(const KeyT<2>& p) {
+  return KeyT<2>{fmix64_inv(p.w0) ^ p.w1, fmix64_inv(p.w1) ^ 0x9E3779B97F4A7C15ull};
+}
+__device__ __forceinline__ bool pi_lt(const KeyT<1>& a, const KeyT<1>& b) { return a.w0 < b.w0; }
+__device__ __forceinline__ bool pi_lt(const KeyT<2>& a, const KeyT<2>& b) {
+  return a.w0 < b.w0 || (a.w0 == b.w0 && a.w1 < b.w1);
+}
+
+// ------------------------------------------------------------------ TMA bulk copies (1-D) + mbarriers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+// order earlier generic-proxy shared-memory accesses before later async-proxy (TMA) writes
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// one elected thread: arm `bar` for `bytes` and start global -> shared bulk copy
+// (src, dst 16-byte aligned, bytes a multiple of 16)
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
 // hash-table slot hash (independent of the owner mix)
 __device__ __forceinline__ uint64_t slot_hash(const KeyT<1>& k) { return fmix64(k.w0 ^ 0xD6E8FEB86659FD93ull); }
 __device__ __forceinline__ uint64_t slot_hash(const KeyT<2>& k) {
