@@ -5,21 +5,29 @@
 // order pi(j) = (hi, lo) -- a fixed bijection of the key space (hi = owner
 // mix, so owner(j) = floor(hi * P / 2^64) is monotone in it) -- instead of the
 // big-integer order.  Because pi is uniform, an MSD partition on the top B
-// bits of hi (B = log2(n / ~1.5k)) puts ~1.5k keys in every bucket:
-//   passes  segmented MSD passes of <= 8 bits (per-tile histograms, one scan,
-//           staged coalesced scatter); the first pass maps keys to their
-//           pi-values, which the later passes and the dedup read directly;
-//   dedup   one CTA per bucket: the bucket streams into shared memory by TMA
-//           bulk copies (next bucket prefetched), an ORDER-PRESERVING open-
-//           addressing table (home = next bits of hi, linear probing, no
-//           wrap) keeps one copy of each pi-value, sorting each short cluster
-//           in place sorts the table, and the survivors are mapped back to
-//           keys (exact inverse mix);
+// bits of hi puts the same number of DISTINCT keys (~2-3 Ki) in every bucket,
+// and each bucket is then de-duplicated and sorted inside shared memory:
+//   pass 1  per-tile histograms of the top (<= 8) bits + a HyperLogLog
+//           sketch of the distinct count D (2 Ki registers); one scan; a
+//           TMA-pipelined, shared-memory-staged scatter that also maps keys to
+//           their pi-values (read directly by every later step);
+//   plan    B = log2(D / DT) bits in total (the sketch decides how many
+//           partition passes a call needs: high redundancy -> fewer, larger
+//           buckets);
+//   pass k  (0-2 more) segmented passes of <= 9 bits;
+//   dedup   one CTA per run of buckets: each bucket streams through shared
+//           memory in TMA pieces (the next piece is always in flight) into an
+//           ORDER-PRESERVING open-addressing table (home = the bits of hi
+//           below the bucket id scaled to the table, linear probing, no wrap):
+//           every cluster holds exactly the keys whose homes fall inside it,
+//           so sorting each short cluster in place sorts the table; the
+//           survivors are mapped back to keys (exact inverse mix);
 //   pack    buckets are concatenated in bucket order.
 // The result is unique and sorted in the hash order.  A bucket with more
 // distinct keys than its table holds is flagged; the host then finishes with
 // a full LSD sort over the hash digits + unique (exact, rare slow path).
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <type_traits>
 #include <vector>
@@ -29,9 +37,11 @@
 namespace cusci {
 namespace {
 
-constexpr int kBT = 256;        // threads
-constexpr int kBI = 8;          // keys per thread per tile
+constexpr int kBT = 256;        // threads (hist, dedup, pack)
+constexpr int kBI = 8;          // keys per thread per hist round
 constexpr int kBTile = kBT * kBI;
+constexpr int kHllLog = 11;     // HyperLogLog: 2^11 registers (~2.3% standard error)
+constexpr uint32_t kHllM = 1u << kHllLog;
 
 // digit source: the top bits of the pi-value's hi word (w0)
 template <int W>
@@ -46,14 +56,13 @@ __device__ __forceinline__ KeyT<W> load_pi(const uint64_t* in, uint64_t i) {
 }
 
 // ---------------------------------------------------------------- partition passes
-// Segmented MSD passes of <= 8 bits of hi.  A pass = per-tile digit
-// histograms written to a matrix laid out group by group ([group][digit]
-// [tile]), ONE exclusive scan of that matrix (it then holds every (group,
-// digit, tile) output offset), and a scatter: each CTA loads its matrix
-// column as shared-memory cursors and, per 4 Ki-key sub-round, ranks its keys
-// with shared-memory atomics, stages them in digit order in shared memory and
-// writes them out as runs of consecutive addresses (~16 keys = 128 B per
-// digit), so HBM sees full sectors.  No global atomics, no look-back, no
+// Segmented MSD passes.  A pass = per-tile digit histograms written to a
+// matrix laid out group by group ([group][digit][tile]), ONE exclusive scan of
+// that matrix (it then holds every (group, digit, tile) output offset), and a
+// scatter: each CTA loads its matrix column as shared-memory cursors and, per
+// 4 Ki-key sub-round, ranks its keys with shared-memory atomics, stages them
+// in digit order in shared memory and writes them out as runs of consecutive
+// addresses, so HBM sees full sectors.  No global atomics, no look-back, no
 // stability requirement.  Tiles (<= 32 Ki keys) never straddle a group.
 struct PTile {
   uint64_t start;   // first key
@@ -63,33 +72,54 @@ struct PTile {
 };
 constexpr uint32_t kPTile = 32768;
 template <int W> struct SSCfg {
-  static constexpr int ITEMS = W == 1 ? 16 : 8;  // keys per thread per sub-round
-  static constexpr int SUB = kBT * ITEMS;        // 4096 / 2048 keys (32 KB staged)
+  static constexpr int SUB = W == 1 ? 4096 : 2048;  // keys per scatter sub-round (32 KB)
 };
 
+// histogram pass; the first (RAW) pass also feeds the HyperLogLog sketch
+// (register = low bits of hi, rank = leading zeros of hi + 1; a register is
+// only written when the rank grows, so almost every update is one load)
 template <int W, bool RAW, int RB>
 __global__ void __launch_bounds__(kBT) tile_hist_kernel(const uint64_t* __restrict__ in,
-                                                       const PTile* __restrict__ tiles, int bsel, uint32_t dmask,
-                                                       uint32_t* __restrict__ mat) {
+                                                       const PTile* __restrict__ tiles, uint32_t ntiles, int bsel,
+                                                       uint32_t dmask, uint32_t* __restrict__ mat,
+                                                       uint32_t* __restrict__ hll) {
   __shared__ uint32_t h[1 << RB];
-  const PTile t = tiles[blockIdx.x];
-  for (uint32_t i = threadIdx.x; i <= dmask; i += kBT) h[i] = 0;
-  __syncthreads();
-  for (uint32_t r0 = 0; r0 < t.len; r0 += kBTile) {
-    KeyT<W> k[kBI];
+  __shared__ uint32_t reg[RAW ? kHllM : 1];
+  if (RAW)
+    for (uint32_t i = threadIdx.x; i < kHllM; i += kBT) reg[i] = 0;
+  for (uint32_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+    const PTile t = tiles[ti];
+    for (uint32_t i = threadIdx.x; i <= dmask; i += kBT) h[i] = 0;
+    __syncthreads();
+    for (uint32_t r0 = 0; r0 < t.len; r0 += kBTile) {
+      KeyT<W> k[kBI];
 #pragma unroll
-    for (int u = 0; u < kBI; u++) {
-      const uint32_t i = r0 + u * kBT + threadIdx.x;
-      if (i < t.len) k[u] = load_pi<W, RAW>(in, t.start + i);
-    }
+      for (int u = 0; u < kBI; u++) {
+        const uint32_t i = r0 + u * kBT + threadIdx.x;
+        if (i < t.len) k[u] = load_pi<W, RAW>(in, t.start + i);
+      }
 #pragma unroll
-    for (int u = 0; u < kBI; u++) {
-      const uint32_t i = r0 + u * kBT + threadIdx.x;
-      if (i < t.len) atomicAdd(&h[top_bits<W>(k[u], bsel) & dmask], 1u);
+      for (int u = 0; u < kBI; u++) {
+        const uint32_t i = r0 + u * kBT + threadIdx.x;
+        if (i < t.len) {
+          atomicAdd(&h[top_bits<W>(k[u], bsel) & dmask], 1u);
+          if (RAW) {
+            const uint64_t hv = k[u].w0;  // hi: a 64-bit hash of the whole key
+            const uint32_t idx = (uint32_t)hv & (kHllM - 1);
+            const uint32_t rho = (uint32_t)min(__clzll(hv), 64 - kHllLog) + 1;
+            if (rho > reg[idx]) atomicMax(&reg[idx], rho);
+          }
+        }
+      }
     }
+    __syncthreads();
+    for (uint32_t d = threadIdx.x; d <= dmask; d += kBT) mat[t.mbase + (uint64_t)d * t.stride] = h[d];
   }
-  __syncthreads();
-  for (uint32_t d = threadIdx.x; d <= dmask; d += kBT) mat[t.mbase + (uint64_t)d * t.stride] = h[d];
+  if (RAW) {
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < kHllM; i += kBT)
+      if (reg[i]) atomicMax(&hll[i], reg[i]);
+  }
 }
 
 constexpr int kST = 512;  // scatter threads
@@ -136,7 +166,7 @@ template <int W, bool RAW, int RB>
 __global__ void __launch_bounds__(kST, 2) tile_scatter_kernel(const uint64_t* __restrict__ in, int use_tma,
                                                              const PTile* __restrict__ tiles, int bsel, uint32_t dmask,
                                                              const uint32_t* __restrict__ offs, uint64_t* __restrict__ out) {
-  constexpr int ITEMS = SSCfg<W>::SUB / kST;
+  constexpr int ITEMS = SSCfg<W>::SUB / kST;  // keys per thread per sub-round
   constexpr int SUB = SSCfg<W>::SUB;
   constexpr uint32_t RMAX = 1u << RB;
   constexpr uint32_t DPT = RMAX > kST ? RMAX / kST : 1;  // digits per thread in the scan
@@ -258,28 +288,6 @@ __global__ void group_off_kernel(const uint32_t* __restrict__ offs, const uint4*
   off[id] = m.y ? offs[m.z + (uint64_t)d * m.y] : m.x;
 }
 
-// ---------------------------------------------------------------- per-bucket dedup (ordered table)
-// One CTA per bucket (static interleaved assignment: CTA c takes buckets c,
-// c + G, ...; G = resident CTAs).  A bucket is a contiguous run of pi-values
-// whose hi lies in [b, b+1) * 2^(64-B).  Its keys stream into shared memory by
-// 1-D TMA bulk copies (the NEXT bucket's first piece is in flight while this
-// one is processed) and are inserted into an ORDER-PRESERVING open-addressing
-// table: home slot = the next log2(ts) bits of hi below the bucket id, linear
-// probing forward with no wrap (an overflow tail of OV slots).  Since home is
-// monotone in hi, every cluster of occupied slots holds exactly the keys whose
-// homes fall inside it, so sorting each (short) cluster in place leaves the
-// whole table sorted in the hash order: no separate sort pass.  The
-// survivors are mapped back to keys (exact inverse mix) and written at the
-// bucket's input offset; a compaction kernel then packs the buckets.
-template <int W> struct BUCfg {
-  static constexpr uint32_t TS = W == 1 ? 4096 : 2048;   // max home slots
-  static constexpr uint32_t OV = W == 1 ? 256 : 128;     // overflow tail
-  static constexpr uint32_t BUFK = W == 1 ? 2048 : 1024; // keys per TMA piece (16 KB)
-  static constexpr uint32_t BUFE = BUFK + 2;             // + alignment slack (W = 1)
-  static constexpr uint32_t TARGET = W == 1 ? 1536 : 768;  // mean keys per bucket
-  static constexpr size_t SMEM = (size_t)(TS + OV) * sizeof(KeyT<W>) + 2 * (size_t)BUFE * sizeof(KeyT<W>);
-};
-
 __device__ __forceinline__ void cas_slot(KeyT<1>* slot, const KeyT<1>& k, KeyT<1>& old) {
   old.w0 = atomicCAS(reinterpret_cast<unsigned long long*>(&slot->w0), 0ull, (unsigned long long)k.w0);
 }
@@ -330,45 +338,58 @@ __device__ __forceinline__ bool otab_insert(KeyT<2>* tab, uint32_t* bm, uint32_t
   return false;
 }
 
-// thread 0: start the bulk copy of keys [s, s + len) of `part` into `buf`
-template <int W>
-__device__ __forceinline__ void issue_piece(const uint64_t* part, uint64_t s, uint32_t len, KeyT<W>* buf, uint64_t* bar) {
-  if (W == 1) {
-    const uint64_t a0 = s & ~1ull, a1 = (s + len + 1) & ~1ull;
-    tma_load_1d(buf, part + a0, (uint32_t)((a1 - a0) * 8), bar);
-  } else {
-    tma_load_1d(buf, part + 2 * s, len * 16u, bar);
-  }
-}
+// ---------------------------------------------------------------- per-bucket dedup (ordered table)
+// CTA c owns a contiguous run of buckets.  The run's keys form one stream of
+// TMA pieces (<= BUFK keys, never straddling a bucket); piece k+1 is in flight
+// while piece k is inserted.  A bucket is a contiguous run of pi-values whose
+// hi lies in [b, b+1) * 2^(64-B).  Its keys go into an ORDER-PRESERVING
+// open-addressing table: home slot = floor(frac * ts), frac = the bits of hi
+// below the bucket id, linear probing forward with no wrap (an overflow tail
+// of OV slots), newly claimed slots marked in an occupancy bitmap.  Since home
+// is monotone in hi, every cluster of occupied slots holds exactly the keys
+// whose homes fall inside it, so sorting each (short) cluster in place sorts
+// the table.  The survivors are mapped back to keys (exact inverse mix) and
+// written at the bucket's input offset; the pack kernel then concatenates
+// the buckets.
+constexpr int kBU = 512;  // dedup threads (2 CTAs / SM share the shared-memory budget)
+constexpr int kILP = 4;   // keys per thread with first probes in flight together
+template <int W> struct BUCfg {
+  static constexpr uint32_t TS = W == 1 ? 8192 : 4096;   // max home slots (64 KB)
+  static constexpr uint32_t OV = W == 1 ? 512 : 256;     // overflow tail
+  static constexpr uint32_t BUFK = W == 1 ? 2304 : 1152; // keys per TMA piece (18 KB)
+  static constexpr uint32_t BUFE = BUFK + 2;             // + alignment slack (W = 1)
+  static constexpr uint32_t DT = W == 1 ? 3072 : 1536;   // target distinct keys per bucket
+  static constexpr uint32_t NWD = (TS + OV) / 32;        // bitmap words
+  static constexpr uint32_t WPT = (NWD + kBU - 1) / kBU; // bitmap words per thread
+  static constexpr size_t SMEM = (size_t)(TS + OV) * sizeof(KeyT<W>) + 2 * (size_t)BUFE * sizeof(KeyT<W>);
+  static_assert(BUFE * sizeof(KeyT<W>) >= (TS + OV) * sizeof(uint16_t), "the slot list must fit a buffer");
+};
 
 template <int W>
-__global__ void __launch_bounds__(kBT, 3) bucket_unique_kernel(const uint64_t* __restrict__ part, int raw, int use_tma,
-                                                              const uint32_t* __restrict__ off, uint32_t nb, int B, uint32_t lf,
-                                                              uint64_t* __restrict__ tmp, uint32_t* __restrict__ surv,
+__global__ void __launch_bounds__(kBU, 2) bucket_unique_kernel(const uint64_t* __restrict__ part, int raw, int use_tma,
+                                                              const uint32_t* __restrict__ off, uint32_t nb, int B,
+                                                              uint32_t lf, uint32_t dcap, uint64_t* __restrict__ tmp,
+                                                              uint32_t* __restrict__ surv,
                                                               unsigned long long* __restrict__ flags) {
   using K = KeyT<W>;
-  constexpr uint32_t TS = BUCfg<W>::TS, OV = BUCfg<W>::OV, BUFK = BUCfg<W>::BUFK, BUFE = BUCfg<W>::BUFE;
-  constexpr int NW = kBT / 32;
-  constexpr uint32_t WIN = kBT;  // buckets per staged offset window
+  using C = BUCfg<W>;
+  constexpr uint32_t TS = C::TS, OV = C::OV, BUFK = C::BUFK, BUFE = C::BUFE, WPT = C::WPT;
+  constexpr int NW = kBU / 32;
   extern __shared__ __align__(16) unsigned char bsm[];
   K* tab = reinterpret_cast<K*>(bsm);
   K* bufs = tab + TS + OV;
   __shared__ __align__(8) uint64_t bar[2];
   __shared__ int s_zero, s_full;
   __shared__ uint32_t wcnt[NW];
-  __shared__ uint32_t bm[(TS + OV) / 32];  // slot occupancy bitmap
-  __shared__ uint32_t soff[WIN + 2];       // off[w0 .. w0 + WIN + 1]
-  static_assert((TS + OV) / 32 <= kBT, "one bitmap word per thread");
-  static_assert(BUFE * sizeof(KeyT<W>) >= (TS + OV) * sizeof(uint16_t), "slot list must fit a buffer");
+  __shared__ uint32_t bm[C::NWD];  // slot occupancy bitmap (set on insert, cleared by pass 2)
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5, t = threadIdx.x;
   // TMA needs 16-byte aligned sources; raw (caller) input is read with plain loads
   const bool tma = use_tma && !raw && ((reinterpret_cast<uintptr_t>(part) & 15u) == 0);
-  // this CTA's contiguous bucket range
   const uint32_t bA = (uint32_t)((uint64_t)nb * blockIdx.x / gridDim.x);
   const uint32_t bB = (uint32_t)((uint64_t)nb * (blockIdx.x + 1) / gridDim.x);
   // the table is cleared once here and kept clean: the compaction zeroes every slot it reads
-  for (uint32_t i = t; i < TS + OV; i += kBT) tab[i] = K{};
-  for (uint32_t i = t; i < (TS + OV) / 32; i += kBT) bm[i] = 0;
+  for (uint32_t i = t; i < TS + OV; i += kBU) tab[i] = K{};
+  for (uint32_t i = t; i < C::NWD; i += kBU) bm[i] = 0;
   if (t == 0) {
     s_zero = 0;
     s_full = 0;
@@ -376,81 +397,96 @@ __global__ void __launch_bounds__(kBT, 3) bucket_unique_kernel(const uint64_t* _
     mbar_init(&bar[1], 1);
     mbar_init_fence();
   }
-  uint32_t w0 = bA;
-  for (uint32_t i = t; i < WIN + 2 && w0 + i <= nb; i += kBT) soff[i] = off[w0 + i];
   __syncthreads();
-  uint32_t phase = 0;  // bit i: parity of buffer i's next completion
-  int cb = 0;
-  if (tma && t == 0 && bA < bB) {
-    const uint32_t l0 = min(soff[1] - soff[0], BUFK);
-    if (l0) issue_piece<W>(part, soff[0], l0, bufs, &bar[0]);
-  }
-  for (uint32_t b = bA; b < bB; b++, cb ^= 1) {
-    if (b - w0 == WIN) {  // next offset window (one coalesced load)
-      w0 = b;
-      for (uint32_t i = t; i < WIN + 2 && w0 + i <= nb; i += kBT) soff[i] = off[w0 + i];
-      __syncthreads();
-    }
-    const uint32_t s = soff[b - w0], nk = soff[b - w0 + 1] - s;
-    K* buf = bufs + cb * BUFE;
-    // prefetch the next bucket's first piece into the other buffer (its last
-    // readers passed the previous bucket's final barrier)
-    if (tma && t == 0 && b + 1 < bB) {
-      const uint32_t sn = soff[b + 1 - w0], en = (b + 2 - w0 <= WIN + 1) ? soff[b + 2 - w0] : off[b + 2];
-      const uint32_t ln = min(en - sn, BUFK);
-      if (ln) {
+  // producer state (thread 0): the next piece to issue = (pb, pp)
+  uint32_t pb = bA, pp = 0, pk = 0;
+  auto issue_next = [&]() {
+    while (pb < bB) {
+      const uint32_t ps = off[pb], pn = off[pb + 1] - ps;
+      if (pp < pn) {
+        const uint32_t len = min(BUFK, pn - pp);
         fence_proxy_async_smem();
-        issue_piece<W>(part, sn, ln, bufs + (cb ^ 1) * BUFE, &bar[cb ^ 1]);
+        issue_core<W>(part, (uint64_t)ps + pp, len, bufs + (pk & 1) * BUFE, &bar[pk & 1]);
+        pp += BUFK;
+        pk++;
+        return;
       }
+      pb++;
+      pp = 0;
     }
+  };
+  if (tma && t == 0) issue_next();
+  uint32_t phase = 0, k = 0;  // consumer: piece counter, barrier parities
+  for (uint32_t b = bA; b < bB; b++) {
+    const uint32_t s = off[b], nk = off[b + 1] - s;
     if (nk == 0) {
       if (t == 0) surv[b] = 0;
       continue;
     }
-    // table size ~LF nk slots (load <= 1/LF even when every key is distinct:
-    // short clusters, cheap in-place sorts); home = floor(frac * ts), frac =
-    // the bits of hi below the bucket id
-    const uint32_t ts = min(TS, max(64u, (lf * nk + 31u) & ~31u));
+    // table size ~lf x (expected distinct keys) slots, capped
+    const uint32_t ts = min(TS, max(64u, (lf * min(nk, dcap) + 31u) & ~31u));
     const uint32_t span = ts + OV;
     bool full = false;
-    for (uint32_t p0 = 0; p0 < nk; p0 += BUFK) {
-      const uint32_t len = min(BUFK, nk - p0);
-      uint32_t lead = 0;
+    K* buf = bufs;
+    for (uint32_t p0 = 0; p0 < nk; p0 += BUFK, k++) {
+      const uint32_t len = min(BUFK, nk - p0), cb = k & 1;
+      buf = bufs + cb * BUFE;
       if (tma) {
-        if (p0 > 0) {  // later pieces of a large bucket reuse the same buffer
-          __syncthreads();
-          if (t == 0) {
-            fence_proxy_async_smem();
-            issue_piece<W>(part, (uint64_t)s + p0, len, buf, &bar[cb]);
+        if (t == 0) issue_next();  // piece k+1 -> the other buffer (freed by the last barrier)
+        const uint64_t g0 = (uint64_t)s + p0;
+        const bool issued = W == 1 ? (((g0 + len) & ~1ull) > ((g0 + 1) & ~1ull)) : true;
+        if (issued) {
+          mbar_wait(&bar[cb], (phase >> cb) & 1u);
+          phase ^= 1u << cb;
+        }
+      }
+      // kILP keys per thread: their first probes are issued together (most keys
+      // resolve on the first probe: already present, or an empty home slot)
+      const uint32_t c0 = (W == 1 && tma) ? (uint32_t)((s + p0) & 1u) : 0u;
+      const uint32_t c1 = (W == 1 && tma) ? len - (uint32_t)((s + p0 + len) & 1u) : len;
+      for (uint32_t i0 = t; i0 < len; i0 += kILP * kBU) {
+        K pv[kILP], cv[kILP];
+        uint32_t hm[kILP];
+        bool act[kILP];
+#pragma unroll
+        for (int u = 0; u < kILP; u++) {
+          const uint32_t i = i0 + u * kBU;
+          act[u] = i < len;
+          if (act[u]) {
+            if (!tma) pv[u] = load_key<W>(part, (uint64_t)s + p0 + i);
+            else if (W == 2 || (i >= c0 && i < c1)) pv[u] = buf[i + c0];  // TMA core (key s+p0+i at buf[i + lead])
+            else pv[u] = load_key<W>(part, (uint64_t)s + p0 + i);
+            if (raw) pv[u] = to_pi(pv[u]);
+            if (kzero(pv[u])) {
+              s_zero = 1;
+              act[u] = false;
+            }
           }
         }
-        mbar_wait(&bar[cb], (phase >> cb) & 1u);
-        phase ^= 1u << cb;
-        lead = W == 1 ? (uint32_t)((s + p0) & 1u) : 0u;
-      }
-      for (uint32_t i = t; i < len; i += kBT) {
-        K p = tma ? buf[lead + i] : load_key<W>(part, (uint64_t)s + p0 + i);
-        if (raw) p = to_pi(p);
-        if (kzero(p)) {
-          s_zero = 1;
-          continue;
+#pragma unroll
+        for (int u = 0; u < kILP; u++) {
+          if (act[u]) {
+            hm[u] = (uint32_t)__umul64hi(pv[u].w0 << B, (uint64_t)ts);
+            cv[u] = tab[hm[u]];
+          }
         }
-        const uint32_t home = (uint32_t)__umul64hi(p.w0 << B, (uint64_t)ts);
-        full |= !otab_insert(tab, bm, home, span, p);
+#pragma unroll
+        for (int u = 0; u < kILP; u++)
+          if (act[u] && !key_eq(cv[u], pv[u])) full |= !otab_insert(tab, bm, hm[u], span, pv[u]);
       }
+      if (full) s_full = 1;
+      __syncthreads();  // piece consumed (the last one: table complete)
     }
-    if (full) s_full = 1;
-    __syncthreads();  // (A) table complete; the input buffer is consumed
     const uint32_t z = (uint32_t)s_zero;
     if (s_full) {
       // table overflow (pathological bucket): pass the keys through unfiltered
       // (the host finishes with a full sort + unique); restore a clean table
-      for (uint32_t i = t; i < nk; i += kBT) {
+      for (uint32_t i = t; i < nk; i += kBU) {
         const K p = load_key<W>(part, (uint64_t)s + i);
         store_key<W>(tmp, (uint64_t)s + i, raw ? p : from_pi(p));
       }
-      for (uint32_t i = t; i < span; i += kBT) tab[i] = K{};
-      for (uint32_t i = t; i < (span + 31) / 32; i += kBT) bm[i] = 0;
+      for (uint32_t i = t; i < span; i += kBU) tab[i] = K{};
+      for (uint32_t i = t; i < C::NWD; i += kBU) bm[i] = 0;
       if (t == 0) {
         surv[b] = nk;
         atomicAdd(&flags[0], 1ull);
@@ -463,32 +499,36 @@ __global__ void __launch_bounds__(kBT, 3) bucket_unique_kernel(const uint64_t* _
       __syncthreads();
       continue;
     }
-    // pass 1 (thread t: bitmap word t = slots [32t, 32t + 32)): the thread
-    // owning a cluster's first slot insertion-sorts the cluster
     const uint32_t nwd = (span + 31) / 32;
-    const uint32_t bits = t < nwd ? bm[t] : 0u;
-    if (bits) {
-      const uint32_t prev = t > 0 ? (bm[t - 1] >> 31) : 0u;
+    // pass 1 (thread t: bitmap words [WPT t, WPT t + WPT)): the thread owning a
+    // cluster's first slot insertion-sorts the cluster
+    uint32_t c = 0;
+#pragma unroll
+    for (uint32_t q = 0; q < WPT; q++) {
+      const uint32_t w = t * WPT + q;
+      const uint32_t bits = w < nwd ? bm[w] : 0u;
+      c += __popc(bits);
+      if (!bits) continue;
+      const uint32_t prev = w > 0 ? (bm[w - 1] >> 31) : 0u;
       uint32_t starts = bits & ~((bits << 1) | prev);
       while (starts) {
         const uint32_t i = __ffs(starts) - 1;
         starts &= starts - 1;
-        const uint32_t u = t * 32 + i;
-        // cluster end: the first clear bit at or after slot u
+        const uint32_t u = w * 32 + i;
         const uint32_t y = ~(bits >> i);
         const uint32_t run = y ? __ffs(y) - 1 : 32u;  // ones from bit i up
         uint32_t e = u + run;
         if (run >= 32 - i) {  // the run reaches the word's end: continue in the next words
-          for (uint32_t w = t + 1; w < nwd; w++) {
-            const uint32_t x = bm[w];
-            e += x == ~0u ? 32u : (uint32_t)(__ffs(~x) - 1);
-            if (x != ~0u) break;
+          for (uint32_t x = w + 1; x < nwd; x++) {
+            const uint32_t v = bm[x];
+            e += v == ~0u ? 32u : (uint32_t)(__ffs(~v) - 1);
+            if (v != ~0u) break;
           }
         }
         e = min(e, span);
-        for (uint32_t k = u + 1; k < e; k++) {
-          const K x = tab[k];
-          uint32_t j = k;
+        for (uint32_t a = u + 1; a < e; a++) {
+          const K x = tab[a];
+          uint32_t j = a;
           while (j > u && pi_lt(x, tab[j - 1])) {
             tab[j] = tab[j - 1];
             j--;
@@ -497,36 +537,38 @@ __global__ void __launch_bounds__(kBT, 3) bucket_unique_kernel(const uint64_t* _
         }
       }
     }
-    // exclusive prefix of the per-word counts (warp scan + warp totals)
-    const uint32_t c = __popc(bits);
+    // exclusive prefix of the per-thread counts (warp scan + warp totals)
     uint32_t inc = c;
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(kFull, inc, o);
       if ((int)lane >= o) inc += y;
     }
     if (lane == 31) wcnt[warp] = inc;
-    __syncthreads();  // (B) clusters sorted, per-warp counts
+    __syncthreads();  // clusters sorted, per-warp counts
     uint32_t pos = inc - c, tot = 0;
     for (int w = 0; w < NW; w++) {
       const uint32_t v = wcnt[w];
       pos += w < (int)warp ? v : 0u;
       tot += v;
     }
-    // pass 2: the word owners list the occupied slots in order (in the consumed
-    // input buffer), then every thread writes survivors back as keys and
-    // clears their slots
+    // pass 2: the word owners list the occupied slots in order (in the last
+    // consumed input buffer), then every thread writes survivors back as keys
+    // and clears their slots
     uint16_t* sidx = reinterpret_cast<uint16_t*>(buf);
-    if (bits) {
-      uint32_t r = bits;
+#pragma unroll
+    for (uint32_t q = 0; q < WPT; q++) {
+      const uint32_t w = t * WPT + q;
+      if (w >= nwd) continue;
+      uint32_t r = bm[w];
       while (r) {
-        sidx[pos++] = (uint16_t)(t * 32 + __ffs(r) - 1);
+        sidx[pos++] = (uint16_t)(w * 32 + __ffs(r) - 1);
         r &= r - 1;
       }
-      bm[t] = 0;
+      bm[w] = 0;
     }
     if (z && t == 0) store_key<W>(tmp, (uint64_t)s, from_pi(K{}));
-    __syncthreads();  // (C) slot list complete
-    for (uint32_t i = t; i < tot; i += kBT) {
+    __syncthreads();  // slot list complete
+    for (uint32_t i = t; i < tot; i += kBU) {
       const uint32_t u = sidx[i];
       store_key<W>(tmp, (uint64_t)s + z + i, from_pi(tab[u]));
       tab[u] = K{};
@@ -535,7 +577,7 @@ __global__ void __launch_bounds__(kBT, 3) bucket_unique_kernel(const uint64_t* _
       surv[b] = tot + z;
       s_zero = 0;
     }
-    __syncthreads();  // (D) table clean for the next bucket
+    __syncthreads();  // table clean for the next bucket
   }
 }
 
@@ -580,58 +622,77 @@ __global__ void owner_bounds_kernel(const uint64_t* __restrict__ keys, uint64_t 
   bnd[r] = lo;
 }
 
+// HyperLogLog estimate of the distinct count from the 2^11 registers
+double hll_estimate(const uint32_t* reg) {
+  const double m = (double)kHllM;
+  double z = 0.0;
+  uint32_t zeros = 0;
+  for (uint32_t i = 0; i < kHllM; i++) {
+    z += std::ldexp(1.0, -(int)reg[i]);
+    zeros += reg[i] == 0;
+  }
+  double e = 0.7213 / (1.0 + 1.079 / m) * m * m / z;
+  if (e <= 2.5 * m && zeros) e = m * std::log(m / zeros);  // small-range (linear counting) correction
+  return e;
+}
+
 template <int W>
 int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* out, uint64_t* n_out) {
+  using C = BUCfg<W>;
   *n_out = 0;
   if (n == 0) return CUSCI_OK;
   Scratch s(ctx);
-  // B bits of hi: ~TARGET keys per bucket on average
-  static const uint64_t target = [] {
-    const char* e = getenv("CUSCI_BUCKET_TARGET");  // tuning knob
-    return e ? (uint64_t)atoll(e) : (uint64_t)BUCfg<W>::TARGET;
-  }();
-  static const int max_pass_bits = [] {
-    const char* e = getenv("CUSCI_PASS_BITS");  // tuning knob (<= 11)
-    return e ? std::max(1, std::min(11, atoi(e))) : 8;
-  }();
-  static const int use_tma = getenv("CUSCI_NO_TMA") ? 0 : 1;  // A/B knob
+  // tuning knobs (environment, read once)
+  static const int use_tma = getenv("CUSCI_NO_TMA") ? 0 : 1;
   static const uint32_t lf = [] {
-    const char* e = getenv("CUSCI_TABLE_LF");  // table slots per key (tuning knob)
+    const char* e = getenv("CUSCI_TABLE_LF");  // table slots per expected distinct key
     return e ? (uint32_t)std::max(2, atoi(e)) : 4u;
   }();
-  int B = 0;
-  while ((n >> B) > target && B < 22) B++;
-  const uint32_t nb = 1u << B;
+  static const uint64_t dt = [] {
+    const char* e = getenv("CUSCI_BUCKET_DISTINCT");  // target distinct keys per bucket
+    return e ? (uint64_t)std::max(64ll, atoll(e)) : (uint64_t)C::DT;
+  }();
+  static const int max_bits = [] {
+    const char* e = getenv("CUSCI_PASS_BITS");  // bits per later partition pass (<= 9)
+    return e ? std::max(1, std::min(9, atoi(e))) : 9;
+  }();
+  // upper bound on the bucket bits (every key distinct)
+  int Bmax = 0;
+  while ((n >> Bmax) > dt && Bmax < 22) Bmax++;
+  int B = Bmax;
+  uint32_t dcap = 0xffffffffu;  // cap on the distinct keys a bucket is expected to hold
+  const uint32_t nb_max = 1u << Bmax;
   uint64_t *a, *b2;
-  uint32_t *off, *surv;
+  uint32_t *off, *surv, *hll;
   uint64_t *surv64, *soff;
   unsigned long long* flags;
-  CUSCI_TRY(s.get_t((n + 2) * W, &a));   // + slack: TMA pieces round up to 16 bytes
+  CUSCI_TRY(s.get_t((n + 2) * W, &a));   // + slack: TMA pieces round to 16 bytes
   CUSCI_TRY(s.get_t((n + 2) * W, &b2));
-  CUSCI_TRY(s.get_t(nb + 1, &off));
-  CUSCI_TRY(s.get_t(nb + 1, &surv));
-  CUSCI_TRY(s.get_t(nb + 1, &surv64));
-  CUSCI_TRY(s.get_t(nb + 1, &soff));
+  CUSCI_TRY(s.get_t(nb_max + 1, &off));
+  CUSCI_TRY(s.get_t(nb_max + 1, &surv));
+  CUSCI_TRY(s.get_t(nb_max + 1, &surv64));
+  CUSCI_TRY(s.get_t(nb_max + 1, &soff));
+  CUSCI_TRY(s.get_t(kHllM, &hll));
   CUSCI_TRY(s.get_t(2, &flags));
   CUSCI_CUDA(ctx, cudaMemsetAsync(flags, 0, 2 * sizeof(unsigned long long), ctx->stream));
-  static bool sattr[3] = {false, false, false};
-  if (!sattr[W]) {
+  static bool attr[3] = {false, false, false};
+  static int dper[3] = {0, 0, 0};
+  if (!attr[W]) {
     CUSCI_CUDA(ctx, cudaFuncSetAttribute(tile_scatter_kernel<W, true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scatter_smem<W, 8>()));
     CUSCI_CUDA(ctx, cudaFuncSetAttribute(tile_scatter_kernel<W, false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scatter_smem<W, 8>()));
-    CUSCI_CUDA(ctx, cudaFuncSetAttribute(tile_scatter_kernel<W, true, 11>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scatter_smem<W, 11>()));
-    CUSCI_CUDA(ctx, cudaFuncSetAttribute(tile_scatter_kernel<W, false, 11>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scatter_smem<W, 11>()));
-    sattr[W] = true;
+    CUSCI_CUDA(ctx, cudaFuncSetAttribute(tile_scatter_kernel<W, false, 9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scatter_smem<W, 9>()));
+    CUSCI_CUDA(ctx, cudaFuncSetAttribute(bucket_unique_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&dper[W], bucket_unique_kernel<W>, kBU, C::SMEM);
+    if (dper[W] < 1) dper[W] = 1;
+    attr[W] = true;
   }
   const uint64_t* part = in;
-  if (B > 0) {
-    // segmented MSD passes of <= 8 bits over the top B bits of hi; the first
-    // pass maps keys to pi-values, later passes and the dedup read pi-values
-    const int np = (B + max_pass_bits - 1) / max_pass_bits;
-    int done = 0;
+  if (Bmax > 0) {
     std::vector<uint32_t> gstart{0u, (uint32_t)n};  // current groups (host)
     uint64_t* dst = a;
-    for (int pi = 0; pi < np; pi++) {
-      const int bits = (B - done + (np - pi) - 1) / (np - pi);  // even split
+    int done = 0;
+    // one segmented MSD pass of `bits` bits over the current groups
+    auto run_pass = [&](int bits, bool first, bool last) -> int {
       const uint32_t R = 1u << bits;
       const uint32_t G = (uint32_t)gstart.size() - 1;
       std::vector<PTile> tl;
@@ -662,24 +723,28 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
       CUSCI_CUDA(ctx, cudaMemcpyAsync(dtl, tl.data(), nt * sizeof(PTile), cudaMemcpyHostToDevice, ctx->stream));
       CUSCI_CUDA(ctx, cudaMemcpyAsync(dgm, gm.data(), G * sizeof(uint4), cudaMemcpyHostToDevice, ctx->stream));
       const int sel = done + bits;
-      if (bits > 8) {
-        if (pi == 0) CUSCI_LAUNCH(ctx, PT_RADIX_UP, tile_hist_kernel<W, true, 11><<<nt, kBT, 0, ctx->stream>>>(part, dtl, sel, R - 1, mat));
-        else CUSCI_LAUNCH(ctx, PT_RADIX_UP, tile_hist_kernel<W, false, 11><<<nt, kBT, 0, ctx->stream>>>(part, dtl, sel, R - 1, mat));
+      if (first) {
+        CUSCI_CUDA(ctx, cudaMemsetAsync(hll, 0, kHllM * sizeof(uint32_t), ctx->stream));
+        static const int hpm = [] {
+          const char* e = getenv("CUSCI_HIST_CTAS_PER_SM");  // tuning knob
+          return e ? std::max(1, atoi(e)) : 8;
+        }();
+        const unsigned hg = (unsigned)std::min<uint64_t>(nt, (uint64_t)ctx->num_sms * hpm);
+        CUSCI_LAUNCH(ctx, PT_RADIX_UP, tile_hist_kernel<W, true, 8><<<hg, kBT, 0, ctx->stream>>>(part, dtl, nt, sel, R - 1, mat, hll));
       } else {
-        if (pi == 0) CUSCI_LAUNCH(ctx, PT_RADIX_UP, tile_hist_kernel<W, true, 8><<<nt, kBT, 0, ctx->stream>>>(part, dtl, sel, R - 1, mat));
-        else CUSCI_LAUNCH(ctx, PT_RADIX_UP, tile_hist_kernel<W, false, 8><<<nt, kBT, 0, ctx->stream>>>(part, dtl, sel, R - 1, mat));
+        CUSCI_LAUNCH(ctx, PT_RADIX_UP, tile_hist_kernel<W, false, 9><<<nt, kBT, 0, ctx->stream>>>(part, dtl, nt, sel, R - 1, mat, hll));
       }
       CUSCI_TRY(scan_exclusive_u32(ctx, mat, offs, mb));
-      if (bits > 8) {
-        if (pi == 0) CUSCI_LAUNCH(ctx, PT_RADIX_DOWN, tile_scatter_kernel<W, true, 11><<<nt, kST, scatter_smem<W, 11>(), ctx->stream>>>(part, use_tma, dtl, sel, R - 1, offs, dst));
-        else CUSCI_LAUNCH(ctx, PT_RADIX_DOWN, tile_scatter_kernel<W, false, 11><<<nt, kST, scatter_smem<W, 11>(), ctx->stream>>>(part, use_tma, dtl, sel, R - 1, offs, dst));
+      if (first) {
+        CUSCI_LAUNCH(ctx, PT_RADIX_DOWN, tile_scatter_kernel<W, true, 8><<<nt, kST, scatter_smem<W, 8>(), ctx->stream>>>(part, use_tma, dtl, sel, R - 1, offs, dst));
+      } else if (bits <= 8) {
+        CUSCI_LAUNCH(ctx, PT_RADIX_DOWN, tile_scatter_kernel<W, false, 8><<<nt, kST, scatter_smem<W, 8>(), ctx->stream>>>(part, use_tma, dtl, sel, R - 1, offs, dst));
       } else {
-        if (pi == 0) CUSCI_LAUNCH(ctx, PT_RADIX_DOWN, tile_scatter_kernel<W, true, 8><<<nt, kST, scatter_smem<W, 8>(), ctx->stream>>>(part, use_tma, dtl, sel, R - 1, offs, dst));
-        else CUSCI_LAUNCH(ctx, PT_RADIX_DOWN, tile_scatter_kernel<W, false, 8><<<nt, kST, scatter_smem<W, 8>(), ctx->stream>>>(part, use_tma, dtl, sel, R - 1, offs, dst));
+        CUSCI_LAUNCH(ctx, PT_RADIX_DOWN, tile_scatter_kernel<W, false, 9><<<nt, kST, scatter_smem<W, 9>(), ctx->stream>>>(part, use_tma, dtl, sel, R - 1, offs, dst));
       }
-      uint32_t* goff_final = (pi == np - 1) ? off : goff;
+      uint32_t* goff_final = last ? off : goff;
       CUSCI_LAUNCH(ctx, PT_SCATTER, group_off_kernel<<<(unsigned)(((uint64_t)G * R + 1 + 255) / 256), 256, 0, ctx->stream>>>(offs, dgm, G, bits, (uint32_t)n, goff_final));
-      if (pi < np - 1) {
+      if (!last) {
         gstart.resize((size_t)G * R + 1);
         CUSCI_CUDA(ctx, cudaMemcpyAsync(gstart.data(), goff, gstart.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost,
                                         ctx->stream));
@@ -688,6 +753,30 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
       part = dst;
       dst = (dst == a) ? b2 : a;
       done += bits;
+      return CUSCI_OK;
+    };
+    const int bits1 = std::min(8, Bmax);
+    // the plan after pass 1 depends on the sketch, so pass 1 is "last" only if nothing can follow
+    CUSCI_TRY(run_pass(bits1, true, Bmax == bits1));
+    if (Bmax > bits1) {
+      std::vector<uint32_t> reg(kHllM);
+      CUSCI_CUDA(ctx, cudaMemcpy(reg.data(), hll, kHllM * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+      const double D = std::min<double>((double)n, std::max(1.0, hll_estimate(reg.data())));
+      int Bd = 0;
+      while (D / std::ldexp(1.0, Bd) > (double)dt && Bd < 22) Bd++;
+      B = std::max(bits1, std::min(Bmax, Bd));
+      const int rest = B - bits1;
+      const int np = (rest + max_bits - 1) / max_bits;
+      for (int pi = 0; pi < np; pi++) {
+        const int bits = (rest - (done - bits1) + (np - pi) - 1) / (np - pi);  // even split
+        CUSCI_TRY(run_pass(bits, false, pi == np - 1));
+      }
+      if (np == 0) {  // pass 1 already made the buckets: its groups are the bucket offsets
+        CUSCI_CUDA(ctx, cudaMemcpyAsync(off, gstart.data(), gstart.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                                        ctx->stream));
+        CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+      }
+      dcap = (uint32_t)std::min<double>(4e9, 2.0 * D / std::ldexp(1.0, B) + 64.0);
     }
   } else {
     const uint32_t o2[2] = {0u, (uint32_t)n};
@@ -695,16 +784,10 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
     CUSCI_CUDA(ctx, cudaMemcpyAsync(off, ctx->host_pinned, sizeof(o2), cudaMemcpyHostToDevice, ctx->stream));
     CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   }
+  const uint32_t nb = 1u << B;
   uint64_t* tmp = (part == a) ? b2 : a;
-  static int dper[3] = {0, 0, 0};
-  if (!dper[W]) {
-    CUSCI_CUDA(ctx, cudaFuncSetAttribute(bucket_unique_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)BUCfg<W>::SMEM));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&dper[W], bucket_unique_kernel<W>, kBT, BUCfg<W>::SMEM);
-    if (dper[W] < 1) dper[W] = 1;
-  }
   const unsigned dgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(nb, (uint64_t)ctx->num_sms * dper[W]));
-  CUSCI_LAUNCH(ctx, PT_HASH, bucket_unique_kernel<W><<<dgrid, kBT, BUCfg<W>::SMEM, ctx->stream>>>(part, part == in ? 1 : 0, use_tma, off, nb, B, lf, tmp, surv, flags));
+  CUSCI_LAUNCH(ctx, PT_HASH, bucket_unique_kernel<W><<<dgrid, kBU, C::SMEM, ctx->stream>>>(part, part == in ? 1 : 0, use_tma, off, nb, B, lf, dcap, tmp, surv, flags));
   // pack the buckets' survivors in bucket order
   CUSCI_CUDA(ctx, cudaMemsetAsync(surv64, 0, (nb + 1) * sizeof(uint64_t), ctx->stream));
   CUSCI_CUDA(ctx, cudaMemcpy2DAsync(surv64, sizeof(uint64_t), surv, sizeof(uint32_t), sizeof(uint32_t), nb,
