@@ -42,7 +42,7 @@ constexpr int kChunks = 4;  // 32-entry chunks (128-bit loads per lane) in fligh
 
 template <int W> struct GenCfg {
   static constexpr int STAGE = W == 1 ? 256 : 192;  // staged records per warp (4 CTAs/SM)
-  static constexpr size_t BYTES_PER_REC = (W == 1 ? 16 : 24) + 4 + 1;
+  static constexpr size_t BYTES_PER_REC = (W == 1 ? 16 : 24) + 1;
   static constexpr size_t SMEM = (size_t)kGenWarps * STAGE * BYTES_PER_REC;
 };
 
@@ -145,8 +145,10 @@ __global__ void validate_kernel(const uint64_t* __restrict__ parents, uint64_t n
   }
 }
 
-// per-warp staging buffer in shared memory: kh = (key, H) interleaved
-// (one 16-byte store per record at W=1), src, phase (only if requested)
+// per-warp staging buffer in shared memory: kh = (key, H) interleaved (one
+// 16-byte store per record at W=1), phase (only if requested).  The source
+// index is not staged per record: the records of one work unit are
+// contiguous in the stage, so a short list of runs (start, src) recovers it.
 template <int W> struct StRec;
 template <> struct __align__(16) StRec<1> {
   uint64_t k0;
@@ -156,12 +158,15 @@ template <> struct __align__(8) StRec<2> {
   uint64_t k0, k1;
   double h;
 };
+constexpr int kRuns = 8;  // source runs per stage
 template <int W>
 struct Stage {
   StRec<W>* kh;
-  uint32_t* src;
   int8_t* ph;
-  uint32_t n;  // warp-uniform fill
+  uint32_t* run;  // [2 kRuns]: run start, run src
+  uint32_t n;     // warp-uniform fill
+  uint32_t nrun;  // warp-uniform
+  uint32_t src;   // current unit's source index
 };
 __device__ __forceinline__ void st_put(StRec<1>& r, const KeyT<1>& k, double h) {
   *reinterpret_cast<ulonglong2*>(&r) = make_ulonglong2(k.w0, (unsigned long long)__double_as_longlong(h));
@@ -176,45 +181,62 @@ __device__ __forceinline__ KeyT<2> st_key(const StRec<2>& r) { return KeyT<2>{r.
 
 template <int W, int MODE>
 __device__ __forceinline__ void stage_flush(const GenArgs& a, Stage<W>& st) {
-  if (st.n == 0) return;
-  const unsigned lane = lane_id();
-  unsigned long long base = 0;
-  if (lane == 0) base = atomicAdd(&a.counter[0], (unsigned long long)st.n);
-  base = __shfl_sync(kFull, base, 0);
-  if (base + st.n <= a.capacity) {
-    if (a.src) {
-      for (uint32_t i = lane; i < st.n; i += 32) {
-        const StRec<W> r = st.kh[i];
-        store_key<W>(a.keys, base + i, st_key(r));
-        a.hij[base + i] = r.h;
-        a.src[base + i] = st.src[i];
-      }
-    } else {
+  __syncwarp();
+  if (st.n) {
+    const unsigned lane = lane_id();
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(&a.counter[0], (unsigned long long)st.n);
+    base = __shfl_sync(kFull, base, 0);
+    if (base + st.n <= a.capacity) {
       for (uint32_t i = lane; i < st.n; i += 32) {
         const StRec<W> r = st.kh[i];
         store_key<W>(a.keys, base + i, st_key(r));
         a.hij[base + i] = r.h;
       }
+      if (a.src) {
+        for (uint32_t i = lane; i < st.n; i += 32) {
+          uint32_t sv = st.run[kRuns];
+          for (uint32_t j = 1; j < st.nrun; j++)
+            if (st.run[j] <= i) sv = st.run[kRuns + j];
+          a.src[base + i] = sv;
+        }
+      }
+      if (MODE == 2)
+        for (uint32_t i = lane; i < st.n; i += 32) a.phase[base + i] = st.ph[i];
     }
-    if (MODE == 2)
-      for (uint32_t i = lane; i < st.n; i += 32) a.phase[base + i] = st.ph[i];
+    __syncwarp();
+  }
+  st.n = 0;
+  st.nrun = 1;  // the current unit continues as run 0
+  if (lane_id() == 0) {
+    st.run[0] = 0;
+    st.run[kRuns] = st.src;
   }
   __syncwarp();
-  st.n = 0;
+}
+
+// a new work unit (source index src) starts emitting
+template <int W, int MODE>
+__device__ __forceinline__ void stage_unit(const GenArgs& a, Stage<W>& st, uint32_t src) {
+  if (st.nrun == kRuns) stage_flush<W, MODE>(a, st);
+  st.src = src;
+  if (lane_id() == 0) {
+    st.run[st.nrun] = st.n;
+    st.run[kRuns + st.nrun] = src;
+  }
+  st.nrun++;
 }
 
 // append the lanes' survivors (ballot `bal`) to the stage
 template <int W, int MODE>
 __device__ __forceinline__ void stage_put(const GenArgs& a, Stage<W>& st, unsigned bal, bool keep, const KeyT<W>& key,
-                                          double H, uint32_t s, uint32_t par) {
+                                          double H, uint32_t par) {
   if (st.n + 32 > (uint32_t)GenCfg<W>::STAGE) stage_flush<W, MODE>(a, st);
   if (keep) {
     const uint32_t i = st.n + __popc(bal & lanemask_lt());
     st_put(st.kh[i], key, H);
-    st.src[i] = s;
     if (MODE == 2) st.ph[i] = par ? -1 : 1;
   }
-  __syncwarp();
   st.n += __popc(bal);
 }
 
@@ -283,7 +305,7 @@ __device__ __forceinline__ uint32_t do_singles(const GenArgs& a, const KeyT<W>& 
       const unsigned bal = __ballot_sync(kFull, keep);
       if (emit) {
         const KeyT<W> j = kxor(par, kxor(bitk<W>(pL), bitk<W>(t)));
-        stage_put<W, MODE>(a, st, bal, keep, j, H, s, ph);
+        stage_put<W, MODE>(a, st, bal, keep, j, H, ph);
       } else {
         total_kept += __popc(bal);
       }
@@ -292,89 +314,114 @@ __device__ __forceinline__ uint32_t do_singles(const GenArgs& a, const KeyT<W>& 
   return total_kept;
 }
 
-// pair rows [r0, r1) (1-based over the occupied pairs) of parent s.
-// Latency hiding: two 32-entry chunks (two 128-bit loads per lane) are in
-// flight per step, and the next row's CSR bounds are loaded while the current
-// row is processed.
-template <int W, int MODE>
-__device__ __forceinline__ void pair_chunk(const GenArgs& a, const ulonglong2& raw, bool valid, const KeyT<W>& par,
-                                           const KeyT<W>& base, const KeyT<W>& M, uint32_t rc, uint32_t s,
-                                           Stage<W>& st, uint32_t& total_kept) {
-  KeyT<W> abm{};
-  ent_mask(raw.x, abm);
-  const bool keep = valid && kdisjoint(par, abm);
-  const unsigned bal = __ballot_sync(kFull, keep);
-  if (MODE != 0) {
-    const uint32_t ph = rc ^ kparity_and(M, abm);
-    // H = +-v: flip the sign bit (exact)
-    const double H = __longlong_as_double((long long)(raw.y ^ ((unsigned long long)ph << 63)));
-    stage_put<W, MODE>(a, st, bal, keep, kxor(base, abm), H, s, ph);
-  } else {
-    total_kept += __popc(bal);
-  }
-}
+// Pair rows [r0, r1) (1-based over the occupied pairs x < y) of the parent,
+// processed in batches of <= kRowBatch rows.  Per batch the warp first sets up
+// one descriptor per row lane-parallel (table start, phase constant, target
+// base and phase mask of the row, start in the batch's entry stream), so the
+// serial row loop only reads one broadcast descriptor per row.
+constexpr int kRowBatch = 96;  // rows per descriptor batch (N2-like parents: one batch)
+template <int W> struct RowInfo;
+template <> struct __align__(8) RowInfo<1> {
+  uint32_t rs;  // first entry of the row in the flattened stream
+  uint32_t rb;  // table index of the row's first entry | phase constant << 31
+  uint64_t base, M;
+};
+template <> struct __align__(8) RowInfo<2> {
+  uint32_t rs, rb;
+  uint32_t pq;  // p | q << 8
+  uint32_t pad;
+};
 
 template <int W, int MODE>
 __device__ __forceinline__ uint32_t do_pairs(const GenArgs& a, const KeyT<W>& par, const KeyT<W>& PP,
-                                             const uint8_t* occ, const ulonglong2* bm, uint32_t s, uint32_t r0,
-                                             uint32_t r1, Stage<W>& st) {
+                                             const uint8_t* occ, RowInfo<W>* ri, uint32_t r0, uint32_t r1,
+                                             Stage<W>& st) {
   const unsigned lane = lane_id();
   const int n = a.n_elec;
   uint32_t total_kept = 0;
-  uint32_t k = r0 - 1;  // decode pair index -> (x, y), x < y
-  int x = 0;
-  while (k >= (uint32_t)(n - 1 - x)) {
-    k -= (uint32_t)(n - 1 - x);
-    x++;
-  }
-  int y = x + 1 + (int)k;
   const ulonglong2* ent = reinterpret_cast<const ulonglong2*>(a.ent);
-  int p = occ[x], q = occ[y];
-  uint32_t row = (uint32_t)q * (q - 1) / 2 + p;
-  uint32_t e0 = __ldg(a.rowptr + row), e1 = __ldg(a.rowptr + row + 1);
-  for (uint32_t r = r0; r < r1; r++) {
-    // next row's bounds, issued early
-    int nx = x, ny = y + 1;
-    if (ny == n) {
-      nx++;
-      ny = nx + 1;
-    }
-    uint32_t ne0 = 0, ne1 = 0;
-    int np_ = 0, nq = 0;
-    if (r + 1 < r1) {
-      np_ = occ[nx];
-      nq = occ[ny];
-      const uint32_t nrow = (uint32_t)nq * (nq - 1) / 2 + np_;
-      ne0 = __ldg(a.rowptr + nrow);
-      ne1 = __ldg(a.rowptr + nrow + 1);
-    }
-    KeyT<W> base, M;
-    if constexpr (W == 1) {  // per-occupied {2^p, PP ^ above(p)} precomputed once per unit
-      const ulonglong2 bx = bm[x], by = bm[y];
-      base = KeyT<W>{par.w0 ^ bx.x ^ by.x};
-      M = KeyT<W>{bx.y ^ by.y ^ PP.w0};  // (PP^above p)^(PP^above q)^PP = PP^above p^above q
-    } else {
-      base = kxor(par, kxor(bitk<W>(p), bitk<W>(q)));
-      M = kxor(PP, kxor(abovek<W>(p), abovek<W>(q)));
-    }
-    const uint32_t rc = (uint32_t)(x + y + 1) & 1u;
-    for (uint32_t e = e0; e < e1; e += 32 * kChunks) {
-      ulonglong2 raw[kChunks];
-#pragma unroll
-      for (int u = 0; u < kChunks; u++) {
-        const uint32_t i = e + 32 * u + lane;
-        raw[u] = i < e1 ? __ldg(ent + i) : make_ulonglong2(~0ull, 0ull);
+  for (uint32_t b0 = r0; b0 < r1; b0 += kRowBatch) {
+    const uint32_t nr = min((uint32_t)kRowBatch, r1 - b0);
+    // ---- row descriptors (lane-parallel) + exclusive scan of the row lengths
+    uint32_t carry = 0;
+    for (uint32_t j0 = 0; j0 < nr; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      uint32_t len = 0;
+      if (j < nr) {
+        uint32_t k = b0 + j - 1;  // pair index -> (x, y), x < y
+        int x = 0;
+        while (k >= (uint32_t)(n - 1 - x)) {
+          k -= (uint32_t)(n - 1 - x);
+          x++;
+        }
+        const int y = x + 1 + (int)k;
+        const int p = occ[x], q = occ[y];
+        const uint32_t row = (uint32_t)q * (q - 1) / 2 + p;
+        const uint32_t e0 = __ldg(a.rowptr + row);
+        len = __ldg(a.rowptr + row + 1) - e0;
+        RowInfo<W> r;
+        r.rb = e0 | ((uint32_t)((x + y + 1) & 1) << 31);
+        if constexpr (W == 1) {
+          r.base = par.w0 ^ (1ull << p) ^ (1ull << q);
+          r.M = PP.w0 ^ (p >= 63 ? 0ull : (~0ull << (p + 1))) ^ (q >= 63 ? 0ull : (~0ull << (q + 1)));
+        } else {
+          r.pq = (uint32_t)p | ((uint32_t)q << 8);
+          r.pad = 0;
+        }
+        const uint32_t incl = warp_incl_scan_u32(len);
+        r.rs = carry + incl - len;
+        ri[j] = r;
+        carry += __shfl_sync(kFull, incl, 31);
+      } else {
+        const uint32_t incl = warp_incl_scan_u32(0u);
+        carry += __shfl_sync(kFull, incl, 31);
       }
-#pragma unroll
-      for (int u = 0; u < kChunks; u++)
-        if (e + 32 * u < e1) pair_chunk<W, MODE>(a, raw[u], e + 32 * u + lane < e1, par, base, M, rc, s, st, total_kept);
     }
-    x = nx;
-    y = ny;
-    p = np_;
-    q = nq;
-    e0 = ne0;
-    e1 = ne1;
+    if (lane == 0) ri[nr].rs = carry;  // sentinel
+    __syncwarp();
+    const uint32_t T = carry;
+    // ---- rows: warp-uniform descriptor (one broadcast load), kChunks 32-entry
+    // chunks (128-bit loads) in flight per step
+    for (uint32_t j = 0; j < nr; j++) {
+      const RowInfo<W> R = ri[j];
+      const uint32_t len = ri[j + 1].rs - R.rs;
+      const ulonglong2* rowp = ent + (R.rb & 0x7fffffffu);
+      KeyT<W> base, M;
+      if constexpr (W == 1) {
+        base = KeyT<W>{R.base};
+        M = KeyT<W>{R.M};
+      } else {
+        const int p = (int)(R.pq & 0xff), q = (int)(R.pq >> 8);
+        base = kxor(par, kxor(bitk<W>(p), bitk<W>(q)));
+        M = kxor(PP, kxor(abovek<W>(p), abovek<W>(q)));
+      }
+      const uint32_t rc = R.rb >> 31;
+      for (uint32_t e = 0; e < len; e += 32 * kChunks) {
+        ulonglong2 raw[kChunks];
+#pragma unroll
+        for (int u = 0; u < kChunks; u++) {
+          const uint32_t i = e + 32 * u + lane;
+          raw[u] = i < len ? __ldg(rowp + i) : make_ulonglong2(~0ull, 0ull);
+        }
+#pragma unroll
+        for (int u = 0; u < kChunks; u++) {
+          if (e + 32 * u >= len) break;
+          KeyT<W> abm{};
+          ent_mask(raw[u].x, abm);
+          const bool keep = e + 32 * u + lane < len && kdisjoint(par, abm);
+          const unsigned bal = __ballot_sync(kFull, keep);
+          if (MODE != 0) {
+            const uint32_t ph = rc ^ kparity_and(M, abm);
+            // H = +-v: flip the sign bit (exact)
+            const double H = __longlong_as_double((long long)(raw[u].y ^ ((unsigned long long)ph << 63)));
+            stage_put<W, MODE>(a, st, bal, keep, kxor(base, abm), H, ph);
+          } else {
+            total_kept += __popc(bal);
+          }
+        }
+      }
+    }
+    __syncwarp();
   }
   return total_kept;
 }
@@ -383,7 +430,8 @@ template <int W, int MODE>
 __global__ void __launch_bounds__(kGenThreads, 4) gen_kernel(const GenArgs a) {
   extern __shared__ __align__(16) unsigned char gsm[];
   __shared__ uint8_t occ_s[kGenWarps][128];
-  __shared__ ulonglong2 bm_s[kGenWarps][W == 1 ? 64 : 1];  // {2^p, PP ^ above(p)} per occupied index
+  __shared__ RowInfo<W> ri_s[kGenWarps][kRowBatch + 1];   // pair-row descriptors of the current batch
+  __shared__ uint32_t run_s[kGenWarps][2 * kRuns];          // stage source runs
   __shared__ unsigned long long unit_s[kGenWarps];
   if (a.counter[2] != kNoError) return;  // invalid parent: write nothing
   const int w = threadIdx.x >> 5;
@@ -392,9 +440,11 @@ __global__ void __launch_bounds__(kGenThreads, 4) gen_kernel(const GenArgs a) {
   constexpr bool emit = MODE != 0;
   Stage<W> st;
   st.kh = reinterpret_cast<StRec<W>*>(gsm) + (size_t)w * S;
-  st.src = reinterpret_cast<uint32_t*>(gsm + (size_t)kGenWarps * S * sizeof(StRec<W>)) + (size_t)w * S;
-  st.ph = reinterpret_cast<int8_t*>(gsm + (size_t)kGenWarps * S * (sizeof(StRec<W>) + 4)) + (size_t)w * S;
+  st.ph = reinterpret_cast<int8_t*>(gsm + (size_t)kGenWarps * S * sizeof(StRec<W>)) + (size_t)w * S;
+  st.run = run_s[w];
   st.n = 0;
+  st.nrun = 0;
+  st.src = 0;
   uint8_t* occ = occ_s[w];
   for (;;) {
     if (lane == 0) unit_s[w] = atomicAdd(&a.counter[1], 1ull);
@@ -419,17 +469,12 @@ __global__ void __launch_bounds__(kGenThreads, 4) gen_kernel(const GenArgs a) {
       nocc += __popc(bal);
     }
     const KeyT<W> PP = prefix_parity(par);
-    if constexpr (W == 1) {
-      for (uint32_t x = lane; x < nocc; x += 32) {
-        const int t = occ[x];
-        bm_s[w][x] = make_ulonglong2(1ull << t, PP.w0 ^ (t >= 63 ? 0ull : (~0ull << (t + 1))));
-      }
-    }
     __syncwarp();
+    if (emit) stage_unit<W, MODE>(a, st, (uint32_t)s);
     uint32_t cnt = 0;
     if (r0 == 0 && r1 > 0) cnt += do_singles<W, MODE>(a, par, PP, occ, (uint32_t)s, st);
     const uint32_t pr0 = r0 == 0 ? 1 : r0;
-    if (r1 > pr0) cnt += do_pairs<W, MODE>(a, par, PP, occ, bm_s[w], (uint32_t)s, pr0, r1, st);
+    if (r1 > pr0) cnt += do_pairs<W, MODE>(a, par, PP, occ, ri_s[w], pr0, r1, st);
     if (!emit && lane == 0 && cnt) atomicAdd(&a.counter[0], (unsigned long long)cnt);
     __syncwarp();
   }
