@@ -70,7 +70,7 @@ struct PTile {
   uint32_t stride;  // matrix stride between digits (= tiles of this group)
   uint64_t mbase;   // matrix index of digit 0 of this tile
 };
-constexpr uint32_t kPTile = 32768;
+constexpr uint32_t kPTileDefault = 65536;  // keys per partition tile (one scatter CTA)
 template <int W> struct SSCfg {
   static constexpr int SUB = W == 1 ? 4096 : 2048;  // keys per scatter sub-round (32 KB)
 };
@@ -692,6 +692,10 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
     uint64_t* dst = a;
     int done = 0;
     // one segmented MSD pass of `bits` bits over the current groups
+    static const uint32_t kPTile = [] {
+      const char* e = getenv("CUSCI_PART_TILE");  // tuning knob
+      return e ? (uint32_t)std::max(4096ll, atoll(e)) : kPTileDefault;
+    }();
     auto run_pass = [&](int bits, bool first, bool last) -> int {
       const uint32_t R = 1u << bits;
       const uint32_t G = (uint32_t)gstart.size() - 1;

@@ -21,8 +21,12 @@ namespace {
 
 constexpr int kMergeThreads = 256;
 template <int W> struct MergeCfg {
-  static constexpr int ITEMS = W == 1 ? 8 : 4;  // keeps static smem < 48 KB
+  static constexpr int ITEMS = W == 1 ? 8 : 4;  // outputs per thread (<= 32: bit masks)
   static constexpr int TILE = kMergeThreads * ITEMS;
+  static constexpr int BUFE = TILE + 4;          // + parity slack of the two runs (W = 1)
+  // dynamic shared memory: two TMA input buffers, abh (hi; later the
+  // compacted output lists), mrg (merged order as buffer indices)
+  static constexpr size_t SMEM = 2 * (size_t)BUFE * sizeof(KeyT<W>) + (size_t)TILE * (8 + 2);
 };
 
 template <int W>
@@ -50,171 +54,311 @@ __global__ void check_sorted_kernel(const uint64_t* __restrict__ U, uint64_t n, 
 }
 
 // Single sweep: each CTA takes a tile ticket (predecessors are resident),
-// merges its S and U runs in shared memory, drops an element equal to its
-// predecessor, checks that its U run is strictly increasing in the hash order,
-// publishes its (kept, inserted) counts and resolves its output offsets by
-// decoupled look-back over its predecessors' published counts, then writes
-// S' and inserted with block-ordered compaction.
+// merges its S and U runs in shared memory (merge path), drops an element
+// equal to its predecessor (an element of U already in S), checks that its U
+// run is strictly increasing in the hash order, and counts its kept /
+// inserted outputs with ONE block scan.  Warp 0 publishes the tile counts
+// and resolves the tile's output offsets by a warp-parallel decoupled
+// look-back; the kept and inserted outputs are compacted into shared-memory
+// lists and written out with coalesced stores.
 constexpr uint64_t kMFlagA = 1ull << 62, kMFlagP = 2ull << 62, kMVal = (1ull << 62) - 1;
 
+// warp 0: decoupled look-back for tile t over status[2 q] (kept) and
+// status[2 q + 1] (inserted), published together; returns both exclusive
+// prefixes (all lanes).  A window covers 32 x kLB predecessors (kLB per lane,
+// one 16-byte load each), so the inclusive-prefix front advances kLB x 32
+// tiles per L2 round trip.
+constexpr int kLB = 1;
+__device__ __forceinline__ ulonglong2 ld_status2(volatile unsigned long long* p) {
+  ulonglong2 r;
+  asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(r.x), "=l"(r.y) : "l"((unsigned long long*)p));
+  return r;
+}
+__device__ __forceinline__ void lookback2(volatile unsigned long long* st, uint64_t t, uint64_t& ek, uint64_t& ei) {
+  const unsigned lane = lane_id();
+  ek = 0;
+  ei = 0;
+  bool dk = false, di = false;
+  int64_t q0 = (int64_t)t - 1;
+  while (q0 >= 0 && !(dk && di)) {
+    uint64_t vk[kLB], vi[kLB];
+#pragma unroll
+    for (int v = 0; v < kLB; v++) {
+      const int64_t q = q0 - (int64_t)(lane * kLB + v);  // (lane, v) -> distance lane kLB + v
+      vk[v] = kMFlagP;
+      vi[v] = kMFlagP;
+      if (q >= 0) {
+        const ulonglong2 x = ld_status2(st + 2 * q);
+        vk[v] = x.x;
+        vi[v] = x.y;
+      }
+    }
+    // wait until every status in the window has at least an aggregate
+    for (;;) {
+      bool miss = false;
+#pragma unroll
+      for (int v = 0; v < kLB; v++) miss |= (vk[v] >> 62) == 0 || (vi[v] >> 62) == 0;
+      if (!__any_sync(kFull, miss)) break;
+#pragma unroll
+      for (int v = 0; v < kLB; v++) {
+        const int64_t q = q0 - (int64_t)(lane * kLB + v);
+        if (q >= 0 && ((vk[v] >> 62) == 0 || (vi[v] >> 62) == 0)) {
+          const ulonglong2 x = ld_status2(st + 2 * q);
+          vk[v] = x.x;
+          vi[v] = x.y;
+        }
+      }
+    }
+    // per component: sum up to (and including) the nearest inclusive prefix
+    int fk = kLB, fi = kLB;  // first v with P in this lane
+#pragma unroll
+    for (int v = kLB - 1; v >= 0; v--) {
+      if ((vk[v] >> 62) == 2) fk = v;
+      if ((vi[v] >> 62) == 2) fi = v;
+    }
+    const unsigned bk = __ballot_sync(kFull, fk < kLB), bi = __ballot_sync(kFull, fi < kLB);
+    const int Lk = bk ? __ffs(bk) - 1 : 32, Li = bi ? __ffs(bi) - 1 : 32;
+    uint64_t sk = 0, si = 0;
+#pragma unroll
+    for (int v = 0; v < kLB; v++) {
+      if ((int)lane < Lk || ((int)lane == Lk && v <= fk)) sk += vk[v] & kMVal;
+      if ((int)lane < Li || ((int)lane == Li && v <= fi)) si += vi[v] & kMVal;
+    }
+    for (int o = 16; o; o >>= 1) {
+      sk += __shfl_xor_sync(kFull, sk, o);
+      si += __shfl_xor_sync(kFull, si, o);
+    }
+    if (!dk) ek += sk;
+    if (!di) ei += si;
+    dk = dk || bk;
+    di = di || bi;
+    q0 -= 32 * kLB;
+  }
+}
+
+// Tile geometry: S run [i0, i1), U run [j0, j1); in its shared-memory buffer
+// the S run starts at sl and the U run at ul, chosen so that a key's buffer
+// index has the parity of its global index (W = 1): then the 16-byte aligned
+// core of each run is one 1-D TMA bulk copy and only an odd head / tail key
+// is read with a plain load.
+struct MTile {
+  uint64_t i0, i1, j0, j1;
+  uint32_t na, nb, sl, ul;
+  bool inval;
+};
+template <int W>
+__device__ __forceinline__ MTile mtile(const uint64_t* split, uint64_t t, uint64_t nS, uint64_t nU) {
+  constexpr int kTile = MergeCfg<W>::TILE;
+  MTile g;
+  g.i0 = split[t];
+  g.i1 = split[t + 1];
+  const uint64_t d0 = t * kTile, d1 = std::min<uint64_t>(d0 + kTile, nS + nU);
+  g.j0 = d0 - g.i0;
+  g.j1 = d1 - g.i1;
+  // an unsorted U can make the merge-path splits inconsistent: process nothing
+  g.inval = g.i1 < g.i0 || g.j1 < g.j0 || (g.i1 - g.i0) + (g.j1 - g.j0) > (uint64_t)kTile || g.j1 > nU || g.i1 > nS;
+  g.na = g.inval ? 0u : (uint32_t)(g.i1 - g.i0);
+  g.nb = g.inval ? 0u : (uint32_t)(g.j1 - g.j0);
+  g.sl = W == 1 ? (uint32_t)(g.i0 & 1) : 0u;
+  g.ul = g.sl + g.na;
+  if (W == 1) g.ul += (uint32_t)((g.ul + g.j0) & 1);
+  return g;
+}
+// thread 0: TMA the aligned cores of both runs into buf (one barrier)
+template <int W>
+__device__ __forceinline__ void mtile_issue(const MTile& g, const uint64_t* S, const uint64_t* U, KeyT<W>* buf,
+                                            uint64_t* bar) {
+  uint32_t bytes = 0;
+  uint64_t sc0 = g.i0, sc1 = g.i0 + g.na, uc0 = g.j0, uc1 = g.j0 + g.nb;
+  if (W == 1) {
+    sc0 = (sc0 + 1) & ~1ull;
+    sc1 &= ~1ull;
+    uc0 = (uc0 + 1) & ~1ull;
+    uc1 &= ~1ull;
+  }
+  if (sc1 > sc0) bytes += (uint32_t)(sc1 - sc0) * 8u * W;
+  if (uc1 > uc0) bytes += (uint32_t)(uc1 - uc0) * 8u * W;
+  if (!bytes) return;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  if (sc1 > sc0)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(buf + g.sl + (sc0 - g.i0))),
+                 "l"(S + sc0 * W), "r"((uint32_t)(sc1 - sc0) * 8u * W), "r"(smem_u32(bar))
+                 : "memory");
+  if (uc1 > uc0)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(buf + g.ul + (uc0 - g.j0))),
+                 "l"(U + uc0 * W), "r"((uint32_t)(uc1 - uc0) * 8u * W), "r"(smem_u32(bar))
+                 : "memory");
+}
+template <int W>
+__device__ __forceinline__ bool mtile_issued(const MTile& g) {
+  if (W == 2) return g.na + g.nb > 0;
+  const uint64_t sc0 = (g.i0 + 1) & ~1ull, sc1 = (g.i0 + g.na) & ~1ull;
+  const uint64_t uc0 = (g.j0 + 1) & ~1ull, uc1 = (g.j0 + g.nb) & ~1ull;
+  return sc1 > sc0 || uc1 > uc0;
+}
+
+// Persistent merge: CTA c owns tiles c, c + G, ... (G = resident CTAs, so a
+// tile's predecessors are always being processed: the look-back cannot
+// deadlock).  While tile t is merged, the S and U runs of tile t + G stream
+// into the other buffer by TMA.  Per tile: merge path in shared memory (ties
+// S-first), drop an element equal to its predecessor (an element of U already
+// in S), check that the U run is strictly increasing in the hash order, count
+// kept / inserted outputs with one block scan, publish the counts and resolve
+// the output offsets by a warp-parallel decoupled look-back, compact the
+// outputs into shared-memory lists and write them with coalesced stores.
 template <int W>
 __global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(const uint64_t* __restrict__ S, uint64_t nS,
                                                                   const uint64_t* __restrict__ U, uint64_t nU,
-                                                                  const uint64_t* __restrict__ split,
+                                                                  const uint64_t* __restrict__ split, uint64_t ntiles,
                                                                   unsigned long long* __restrict__ status,
-                                                                  unsigned* __restrict__ tile_ctr,
                                                                   int* __restrict__ bad,
                                                                   uint64_t* __restrict__ out, uint64_t* __restrict__ ins) {
   constexpr int kMergeItems = MergeCfg<W>::ITEMS;
   constexpr int kTile = MergeCfg<W>::TILE;
-  __shared__ KeyT<W> ab[kTile];     // S run then U run
-  __shared__ uint64_t abh[kTile];   // their hash-order hi (computed once per element)
-  __shared__ uint16_t mrg[kTile];   // merged tile as indices into ab (>= na: from U)
-  __shared__ uint32_t wk[kMergeThreads / 32], wi[kMergeThreads / 32];
+  constexpr int BUFE = MergeCfg<W>::BUFE;
+  extern __shared__ __align__(16) unsigned char msm[];
+  KeyT<W>* bufs = reinterpret_cast<KeyT<W>*>(msm);                // [2][BUFE]
+  uint64_t* abh = reinterpret_cast<uint64_t*>(bufs + 2 * BUFE);   // hi by logical index (S run, then U run)
+  uint16_t* mrg = reinterpret_cast<uint16_t*>(abh + kTile);       // merged tile as buffer indices
+  uint16_t* lk = reinterpret_cast<uint16_t*>(abh);                // kept outputs (compacted; aliases abh)
+  uint16_t* li = lk + kTile;                                      // inserted outputs (compacted)
+  __shared__ uint32_t red[33], red2[33];
   __shared__ uint64_t run_k, run_i;
-  __shared__ unsigned s_tile;
-  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
-  __syncthreads();
-  const uint64_t t = s_tile;
-  const uint64_t i0 = split[t], i1 = split[t + 1];
-  const uint64_t d0 = t * kTile, d1 = std::min<uint64_t>(d0 + kTile, nS + nU);
-  const uint64_t j0 = d0 - i0, j1 = d1 - i1;
-  // an unsorted U can make the merge-path splits inconsistent: flag it and
-  // process nothing (the tile still publishes zero counts for its successors)
-  const bool inval = i1 < i0 || j1 < j0 || (i1 - i0) + (j1 - j0) > (uint64_t)kTile || j1 > nU || i1 > nS;
-  if (inval && threadIdx.x == 0) *bad = 1;
-  const int na = inval ? 0 : (int)(i1 - i0), nb = inval ? 0 : (int)(j1 - j0), len = na + nb;
-  for (int x = threadIdx.x; x < na; x += kMergeThreads) {
-    const KeyT<W> k = load_key<W>(S, i0 + x);
-    ab[x] = k;
-    abh[x] = hk_hi(k);
-  }
-  for (int x = threadIdx.x; x < nb; x += kMergeThreads) {
-    const KeyT<W> k = load_key<W>(U, j0 + x);
-    ab[na + x] = k;
-    abh[na + x] = hk_hi(k);
+  __shared__ __align__(8) uint64_t bar[2];
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_init_fence();
   }
   __syncthreads();
-  // hash-order comparisons on the staged elements: hi first, lo only on a tie (W = 2)
-  auto le = [&](int x, int y) -> bool {
-    const uint64_t hx = abh[x], hy = abh[y];
-    if (W == 1 || hx != hy) return hx <= hy;
-    return hk_lo(ab[x]) <= hk_lo(ab[y]);
-  };
-  // input check: U strictly increasing in the hash order (tile run + left boundary)
-  {
-    bool badu = false;
-    for (int x = threadIdx.x; x < nb; x += kMergeThreads) {
-      if (x > 0) badu |= le(na + x, na + x - 1);
-      else if (j0 > 0 && j0 <= nU) badu |= !hk_lt<W>(load_key<W>(U, j0 - 1), ab[na]);
+  const bool tma = ((reinterpret_cast<uintptr_t>(S) | reinterpret_cast<uintptr_t>(U)) & 15u) == 0;
+  uint32_t phase = 0;
+  int cb = 0;
+  if (tma && threadIdx.x == 0 && blockIdx.x < ntiles)
+    mtile_issue<W>(mtile<W>(split, blockIdx.x, nS, nU), S, U, bufs, &bar[0]);
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, cb ^= 1) {
+    const MTile g = mtile<W>(split, t, nS, nU);
+    KeyT<W>* buf = bufs + cb * BUFE;
+    if (tma && threadIdx.x == 0 && t + gridDim.x < ntiles) {  // prefetch the next tile into the other buffer
+      fence_proxy_async_smem();
+      mtile_issue<W>(mtile<W>(split, t + gridDim.x, nS, nU), S, U, bufs + (cb ^ 1) * BUFE, &bar[cb ^ 1]);
     }
-    if (badu) *bad = 1;
-  }
-  // each thread merges outputs [k0, k0 + ITEMS)
-  const int k0 = threadIdx.x * kMergeItems;
-  if (k0 < len) {
-    int lo = k0 > nb ? k0 - nb : 0, hi = std::min(k0, na);
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (le(mid, na + k0 - mid - 1)) lo = mid + 1;
-      else hi = mid;
+    if (g.inval && threadIdx.x == 0) *bad = 1;
+    const int na = (int)g.na, nb = (int)g.nb, len = na + nb;
+    if (tma && mtile_issued<W>(g)) {
+      mbar_wait(&bar[cb], (phase >> cb) & 1u);
+      phase ^= 1u << cb;
     }
-    int i = lo, j = k0 - lo;
-    for (int k = k0; k < std::min(k0 + kMergeItems, len); k++) {
-      const bool takeA = i < na && (j >= nb || le(i, na + j));
-      mrg[k] = (uint16_t)(takeA ? i++ : na + j++);
+    // keys outside the TMA cores (odd head / tail at W = 1, everything without
+    // TMA) come from plain loads; hi once per key
+    for (int x = threadIdx.x; x < len; x += kMergeThreads) {
+      const bool fromS = x < na;
+      const uint64_t gi = fromS ? g.i0 + x : g.j0 + (x - na);
+      const uint64_t gs = fromS ? g.i0 : g.j0, ge = fromS ? g.i0 + na : g.j0 + nb;
+      const uint32_t bi = fromS ? g.sl + x : g.ul + (x - na);
+      bool core = tma;
+      if (W == 1) core = core && gi >= ((gs + 1) & ~1ull) && gi < (ge & ~1ull);
+      KeyT<W> k;
+      if (core) {
+        k = buf[bi];
+      } else {
+        k = load_key<W>(fromS ? S : U, gi);
+        buf[bi] = k;
+      }
+      abh[x] = hk_hi(k);
     }
-  }
-  // predecessor of the tile's first output: the larger of S[i0-1], U[j0-1]
-  KeyT<W> prev0{};
-  bool has_prev0 = false;
-  if (!inval && i0 > 0) {
-    prev0 = load_key<W>(S, i0 - 1);
-    has_prev0 = true;
-  }
-  if (!inval && j0 > 0) {
-    const KeyT<W> u = load_key<W>(U, j0 - 1);
-    if (!has_prev0 || hk_lt<W>(prev0, u)) prev0 = u;
-    has_prev0 = true;
-  }
-  __syncthreads();
-  // tile counts
-  const int w = threadIdx.x >> 5;
-  uint32_t ck = 0, ci = 0;
-  for (int r = 0; r < kMergeItems; r++) {
-    const int k = r * kMergeThreads + threadIdx.x;
-    if (k < len) {
-      const bool dup = k > 0 ? key_eq(ab[mrg[k]], ab[mrg[k - 1]]) : (has_prev0 && key_eq(ab[mrg[0]], prev0));
-      ck += !dup;
-      ci += (!dup && mrg[k] >= na);
+    __syncthreads();
+    // hash-order comparisons by logical index: hi first, lo only on a tie (W = 2)
+    auto bidx = [&](int x) -> uint32_t { return x < na ? g.sl + x : g.ul + (x - na); };
+    auto le = [&](int x, int y) -> bool {
+      const uint64_t hx = abh[x], hy = abh[y];
+      if (W == 1 || hx != hy) return hx <= hy;
+      return hk_lo(buf[bidx(x)]) <= hk_lo(buf[bidx(y)]);
+    };
+    {  // input check: U strictly increasing in the hash order (tile run + left boundary)
+      bool badu = false;
+      for (int x = threadIdx.x; x < nb; x += kMergeThreads) {
+        if (x > 0) badu |= le(na + x, na + x - 1);
+        else if (g.j0 > 0 && g.j0 <= nU) badu |= !hk_lt<W>(load_key<W>(U, g.j0 - 1), buf[g.ul]);
+      }
+      if (badu) *bad = 1;
     }
-  }
-  for (int o = 16; o; o >>= 1) {
-    ck += __shfl_xor_sync(kFull, ck, o);
-    ci += __shfl_xor_sync(kFull, ci, o);
-  }
-  if (lane_id() == 0) {
-    wk[w] = ck;
-    wi[w] = ci;
-  }
-  __syncthreads();
-  // publish + look-back (thread 0: kept, thread 32: inserted)
-  volatile unsigned long long* st = status;
-  if (threadIdx.x == 0 || threadIdx.x == 32) {
-    const int which = threadIdx.x == 0 ? 0 : 1;
-    uint64_t mine = 0;
-    for (int x = 0; x < kMergeThreads / 32; x++) mine += which ? wi[x] : wk[x];
-    st[2 * t + which] = (t == 0 ? kMFlagP : kMFlagA) | mine;
-    uint64_t excl = 0;
-    if (t > 0) {
-      int64_t q = (int64_t)t - 1;
-      while (q >= 0) {
-        const uint64_t v = st[2 * q + which];
-        if ((v >> 62) == 0) {
-          __nanosleep(20);
-          continue;
+    // each thread merges outputs [k0, k0 + ITEMS)
+    const int k0 = threadIdx.x * kMergeItems;
+    if (k0 < len) {
+      int lo = k0 > nb ? k0 - nb : 0, hi = std::min(k0, na);
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (le(mid, na + k0 - mid - 1)) lo = mid + 1;
+        else hi = mid;
+      }
+      int i = lo, j = k0 - lo;
+      for (int k = k0; k < std::min(k0 + kMergeItems, len); k++) {
+        const bool takeA = i < na && (j >= nb || le(i, na + j));
+        mrg[k] = (uint16_t)(takeA ? g.sl + i++ : g.ul + j++);
+      }
+    }
+    // predecessor of the tile's first output: the larger of S[i0-1], U[j0-1]
+    KeyT<W> prev0{};
+    bool has_prev0 = false;
+    if (threadIdx.x == 0 && !g.inval) {
+      if (g.i0 > 0) {
+        prev0 = load_key<W>(S, g.i0 - 1);
+        has_prev0 = true;
+      }
+      if (g.j0 > 0) {
+        const KeyT<W> u = load_key<W>(U, g.j0 - 1);
+        if (!has_prev0 || hk_lt<W>(prev0, u)) prev0 = u;
+        has_prev0 = true;
+      }
+    }
+    __syncthreads();
+    // this thread's kept / inserted outputs (bit r = output k0 + r)
+    uint32_t km = 0, im = 0;
+    for (int r = 0; r < kMergeItems; r++) {
+      const int k = k0 + r;
+      if (k < len) {
+        const bool dup = k > 0 ? key_eq(buf[mrg[k]], buf[mrg[k - 1]]) : (has_prev0 && key_eq(buf[mrg[0]], prev0));
+        if (!dup) {
+          km |= 1u << r;
+          if (mrg[k] >= g.ul) im |= 1u << r;
         }
-        excl += v & kMVal;
-        if ((v >> 62) == 2) break;
-        q--;
       }
-      st[2 * t + which] = kMFlagP | (excl + mine);
     }
-    if (which == 0) run_k = excl;
-    else run_i = excl;
-  }
-  __syncthreads();
-  for (int r = 0; r < kMergeItems; r++) {
-    const int k = r * kMergeThreads + threadIdx.x;
-    bool keep = false, isins = false;
-    if (k < len) {
-      const bool dup = k > 0 ? key_eq(ab[mrg[k]], ab[mrg[k - 1]]) : (has_prev0 && key_eq(ab[mrg[0]], prev0));
-      keep = !dup;
-      isins = keep && mrg[k] >= na;
-    }
-    const unsigned bk = __ballot_sync(kFull, keep), bi = __ballot_sync(kFull, isins);
-    if (lane_id() == 0) {
-      wk[w] = __popc(bk);
-      wi[w] = __popc(bi);
-    }
-    __syncthreads();
-    uint32_t ok = 0, oi = 0, tk = 0, ti = 0;
-    for (int x = 0; x < kMergeThreads / 32; x++) {
-      if (x < w) {
-        ok += wk[x];
-        oi += wi[x];
+    uint32_t tk, ti;
+    uint32_t pk = block_excl_scan_u32(__popc(km), red, tk);
+    uint32_t pi = block_excl_scan_u32(__popc(im), red2, ti);
+    if (threadIdx.x < 32) {  // publish + warp-parallel look-back
+      volatile unsigned long long* st = status;
+      if (threadIdx.x == 0) {
+        st[2 * t] = (t == 0 ? kMFlagP : kMFlagA) | tk;
+        st[2 * t + 1] = (t == 0 ? kMFlagP : kMFlagA) | ti;
       }
-      tk += wk[x];
-      ti += wi[x];
+      uint64_t ek = 0, ei = 0;
+      if (t > 0) {
+        lookback2(st, t, ek, ei);
+        if (threadIdx.x == 0) {
+          st[2 * t] = kMFlagP | (ek + tk);
+          st[2 * t + 1] = kMFlagP | (ei + ti);
+        }
+      }
+      if (threadIdx.x == 0) {
+        run_k = ek;
+        run_i = ei;
+      }
     }
-    if (keep) store_key<W>(out, run_k + ok + __popc(bk & lanemask_lt()), ab[mrg[k]]);
-    if (isins && ins) store_key<W>(ins, run_i + oi + __popc(bi & lanemask_lt()), ab[mrg[k]]);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      run_k += tk;
-      run_i += ti;
+    for (int r = 0; r < kMergeItems; r++) {
+      if ((km >> r) & 1u) lk[pk++] = mrg[k0 + r];
+      if ((im >> r) & 1u) li[pi++] = mrg[k0 + r];
     }
     __syncthreads();
+    const uint64_t rk = run_k, rin = run_i;
+    for (uint32_t x = threadIdx.x; x < tk; x += kMergeThreads) store_key<W>(out, rk + x, buf[lk[x]]);
+    if (ins)
+      for (uint32_t x = threadIdx.x; x < ti; x += kMergeThreads) store_key<W>(ins, rin + x, buf[li[x]]);
+    __syncthreads();  // buffer, lists and run offsets free for the next tile
   }
 }
 
@@ -274,7 +418,15 @@ int merge_impl(cusci_ctx* ctx, cusci_pool* pool, const uint64_t* U, uint64_t nU,
     }
   }
   CUSCI_LAUNCH(ctx, PT_MERGE_SPLIT, merge_split_kernel<W><<<(unsigned)((ntiles + 1 + 255) / 256), 256, 0, ctx->stream>>>(S, nS, U, nU, ntiles, split));
-  CUSCI_LAUNCH(ctx, PT_MERGE_TILE, merge_tile_kernel<W><<<(unsigned)ntiles, kMergeThreads, 0, ctx->stream>>>(S, nS, U, nU, split, status, tctr, bad, dst, (uint64_t*)insp));
+  static int mper[3] = {0, 0, 0};
+  if (!mper[W]) {
+    CUSCI_CUDA(ctx, cudaFuncSetAttribute(merge_tile_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MergeCfg<W>::SMEM));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mper[W], merge_tile_kernel<W>, kMergeThreads, MergeCfg<W>::SMEM);
+    if (mper[W] < 1) mper[W] = 1;
+  }
+  // persistent grid: every CTA resident (the look-back relies on it)
+  const unsigned mgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * mper[W]));
+  CUSCI_LAUNCH(ctx, PT_MERGE_TILE, merge_tile_kernel<W><<<mgrid, kMergeThreads, MergeCfg<W>::SMEM, ctx->stream>>>(S, nS, U, nU, split, ntiles, status, bad, dst, (uint64_t*)insp));
   // totals = the last tile's inclusive counts; plus the input check flag
   uint64_t h[3];
   CUSCI_CUDA(ctx, cudaMemcpyAsync(ctx->host_pinned, status + 2 * (ntiles - 1), 2 * sizeof(uint64_t),
