@@ -242,6 +242,13 @@ def main():
     upool = ctx.pool(sp, 1 << 20)   # union of the unique coupled configurations C
     spool = ctx.pool(sp, 1 << 20)   # the space S (starts as the parent shard)
 
+    mstat = [0]  # merge algorithmic bytes (read |S| + |U|, write |S'|) accumulated by step()
+
+    def merge_acc(pool, n_new, fn):
+        before = len(pool)
+        fn()
+        mstat[0] += (before + n_new + len(pool)) * 8 * W
+
     def step(parents_dev, e2e=False):
         """one pass of the hot path; returns (records, unique, space_size)."""
         nrec = 0
@@ -251,10 +258,10 @@ def main():
             rec = ctx.gen_coupled(sp, parents_dev[a:b], di, args.eps, out=out)
             nrec += rec.count
             u = ctx.dedup_global(sp, rec.keys)
-            ctx.merge_space(upool, u)
+            merge_acc(upool, u.shape[0], lambda: ctx.merge_space(upool, u))
             del u
-        ctx.merge_space(spool, parents_dev)
-        ctx.merge_pool(spool, upool)
+        merge_acc(spool, parents_dev.shape[0], lambda: ctx.merge_space(spool, parents_dev))
+        merge_acc(spool, len(upool), lambda: ctx.merge_pool(spool, upool))
         return nrec, len(upool), len(spool)
 
     # warm-up
@@ -267,6 +274,8 @@ def main():
     clocks.start()
     ctx.profile(True)
     ctx.profile_read()
+    ctx.dedup_stats(reset=True)
+    mstat[0] = 0
     launches0 = ctx.kernel_launches
     barrier(pg)
     torch.cuda.synchronize()
@@ -283,6 +292,8 @@ def main():
     barrier(pg)
     ms_local = ev0.elapsed_time(ev1)
     prof = ctx.profile_read()
+    dstats = ctx.dedup_stats(reset=True)
+    merge_bytes = mstat[0] // args.steps
     ctx.profile(False)
     launches = ctx.kernel_launches - launches0
     clk = clocks.stop()
@@ -325,18 +336,15 @@ def main():
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
     rec_bytes = 8 * W + 8 + 4
 
-    def dedup_passes(n):  # bucket.cu: B = bits with <= 2048 keys/bucket (cap 22), <= 8-bit passes
-        B = 0
-        while (n >> B) > 1792 and B < 22:
-            B += 1
-        return (B + 7) // 8
-
-    # algorithmic bytes per step for each kernel class
+    # algorithmic bytes per step for each kernel class,
+    # from the library's own dedup plan (keys x partition passes)
+    ds = dstats
     alg = {
-        "gen": sum(counts) * rec_bytes + n_par * 8 * W,                       # records written + parents read
-        "part_scatter": sum(dedup_passes(c) * c * 16 * W for c in counts),  # partition: read + write a key per pass
-        "part_hist": sum(dedup_passes(c) * c * 8 * W for c in counts),     # per-pass histograms: read a key
-        "bucket_unique": sum(c * 8 * W for c in counts),                         # bucket dedup: read every key once
+        "gen": sum(counts) * rec_bytes + n_par * 8 * W,                  # records written + parents read
+        "part_scatter": ds["key_passes"] * 16 * W // args.steps,         # partition: read + write a key per pass
+        "part_hist": ds["key_passes"] * 8 * W // args.steps,             # per-pass histograms: read a key
+        "bucket_unique": (ds["keys_in"] + ds["keys_out"]) * 8 * W // args.steps,  # read every key, write survivors
+        "merge_tile": merge_bytes,                                       # read S and U, write S'
     }
     kernels = {}
     for name, (kms, kl) in prof.items():
@@ -345,11 +353,30 @@ def main():
             kernels[name] = {"ms_per_step": kms / args.steps, "achieved_GBs": ach, "frac": ach / hbm_peak}
     dname = max(prof.items(), key=lambda kv: kv[1][0])[0] if prof else None
     rname = dname if dname in kernels else (max(kernels, key=lambda k: kernels[k]["ms_per_step"]) if kernels else None)
+    # measured DRAM traffic per launch of each class: the committed ncu launch list
+    # of this command (profiles/*_traffic.json, newest round) -- null if absent
+    traffic, traffic_src = {}, None
+    try:
+        import glob
+        tj = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")))
+        if tj:
+            d = json.load(open(tj[-1]))
+            traffic = d.get("classes", {})
+            traffic_src = os.path.relpath(tj[-1], ROOT)
+    except (OSError, ValueError):
+        pass
     roof = None
     if rname:
+        launches_r = prof[rname][1] / args.steps
+        tr = traffic.get(rname, {}).get("dram_bytes_per_launch")
         roof = {"bound": "hbm", "kernel": rname, "achieved": kernels[rname]["achieved_GBs"], "peak": hbm_peak,
-                "unit": "GB/s", "frac": kernels[rname]["frac"], "traffic": None, "peak_source": peak_src,
-                "dominant_class": dname}
+                "unit": "GB/s", "frac": kernels[rname]["frac"],
+                "traffic": tr, "traffic_source": traffic_src,
+                "alg_bytes_per_launch": alg[rname] / launches_r if launches_r else None,
+                "peak_source": peak_src, "dominant_class": dname}
+        for k in kernels:
+            kernels[k]["dram_bytes_per_launch_ncu"] = traffic.get(k, {}).get("dram_bytes_per_launch")
+            kernels[k]["alg_bytes_per_launch"] = alg[k] / (prof[k][1] / args.steps)
     gen_roof = None
     if "gen" in kernels:
         gen_roof = {"achieved": kernels["gen"]["achieved_GBs"], "frac": kernels["gen"]["frac"],

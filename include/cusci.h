@@ -109,11 +109,19 @@ uint64_t cusci_kernel_launches(const cusci_ctx* ctx);
  * enabled, every library launch is bracketed by an event pair on the context
  * stream.  cusci_profile_read synchronises the stream, writes the summed
  * milliseconds and launch counts per class into ms[n_tags] / launches[n_tags]
- * (class ids: 0 prep, 1 validate, 2 gen, 3 hash filter, 4 owner scatter,
- * 5 radix upsweep, 6 radix downsweep, 7 scan, 8 unique, 9 merge split,
- * 10 merge tile, 11 sorted check, 12 NCCL exchange, 13 memset) and clears the log. */
+ * (class ids: 0 prep, 1 validate, 2 gen, 3 bucket dedup, 4 pack / owner
+ * bounds, 5 partition histogram, 6 partition scatter, 7 scan, 8 unique,
+ * 9 merge split, 10 merge tile, 11 sorted check, 12 NCCL exchange, 13 memset)
+ * and clears the log. */
 void cusci_profile_enable(cusci_ctx* ctx, int on);
 int cusci_profile_read(cusci_ctx* ctx, double* ms, uint64_t* launches, int n_tags);
+/* Local-dedup plan statistics accumulated since the last read (instrumentation
+ * for bench.py's algorithmic-byte accounting): stats[0] = dedup calls,
+ * stats[1] = keys in, stats[2] = key-passes of the partition (sum over calls
+ * of keys x passes), stats[3] = distinct keys out, stats[4] = buckets,
+ * stats[5] = calls that took the overflow slow path.  reset != 0 clears them.
+ * Returns CUSCI_OK (CUSCI_E_INVALID_ARG for NULL arguments). */
+int cusci_dedup_stats(cusci_ctx* ctx, uint64_t stats[6], int reset);
 
 /* ---- step 1: coupled generation ------------------------------------------ */
 

@@ -12,7 +12,7 @@ CUSCI_ERRORS = {0: "OK", 1: "E_INVALID_ARG", 2: "E_INVALID_PARENT", 3: "E_CAPACI
 
 # every symbol include/cusci.h declares
 EXPORTS = ["cusci_nccl_unique_id", "cusci_init", "cusci_finalize", "cusci_last_error", "cusci_invalidate_integrals",
-           "cusci_free", "cusci_kernel_launches", "cusci_profile_enable", "cusci_profile_read", "gen_coupled_bound", "gen_coupled", "gen_coupled_count",
+           "cusci_free", "cusci_kernel_launches", "cusci_profile_enable", "cusci_profile_read", "cusci_dedup_stats", "gen_coupled_bound", "gen_coupled", "gen_coupled_count",
            "dedup_global", "dedup_partition", "dedup_finalize", "cusci_pool_create", "cusci_pool_view",
            "cusci_pool_copy", "cusci_pool_clear", "cusci_pool_destroy", "merge_space"]
 
@@ -58,6 +58,8 @@ def lib():
     L.cusci_profile_enable.restype = None
     L.cusci_profile_read.argtypes = [vp, P(ctypes.c_double), P(u64), i32]
     L.cusci_profile_read.restype = i32
+    L.cusci_dedup_stats.argtypes = [vp, P(u64), i32]
+    L.cusci_dedup_stats.restype = i32
     L.gen_coupled_bound.argtypes = [vp, u64]
     L.gen_coupled_bound.restype = u64
     L.gen_coupled.argtypes = [vp, vp, vp, u64, vp, ctypes.c_double, vp]

@@ -247,6 +247,14 @@ void cusci_free(cusci_ctx* ctx, void* ptr) {
 
 uint64_t cusci_kernel_launches(const cusci_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+int cusci_dedup_stats(cusci_ctx* ctx, uint64_t stats[6], int reset) {
+  if (!ctx || !stats) return CUSCI_E_INVALID_ARG;
+  for (int i = 0; i < 6; i++) stats[i] = ctx->dstats[i];
+  if (reset)
+    for (int i = 0; i < 6; i++) ctx->dstats[i] = 0;
+  return CUSCI_OK;
+}
+
 void cusci_profile_enable(cusci_ctx* ctx, int on) {
   if (ctx) ctx->profiling = on != 0;
 }

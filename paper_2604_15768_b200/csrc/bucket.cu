@@ -757,6 +757,7 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
       part = dst;
       dst = (dst == a) ? b2 : a;
       done += bits;
+      ctx->dstats[2] += n;
       return CUSCI_OK;
     };
     const int bits1 = std::min(8, Bmax);
@@ -805,6 +806,10 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
   CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   memcpy(h, ctx->host_pinned, sizeof(h));
   *n_out = h[0];
+  ctx->dstats[0] += 1;
+  ctx->dstats[1] += n;
+  ctx->dstats[4] += nb;
+  ctx->dstats[5] += h[1] ? 1 : 0;
   if (h[1]) {
     // rare slow path: some bucket overflowed its table -> full LSD sort over the
     // hash digits (lo then hi for W = 2) + adjacent unique
@@ -824,6 +829,7 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
     CUSCI_TRY(unique_sorted_keys(ctx, W, a, m, out, cnt));
     CUSCI_TRY(read_u64(ctx, cnt, n_out, 1));
   }
+  ctx->dstats[3] += *n_out;
   return CUSCI_OK;
 }
 

@@ -417,29 +417,47 @@ int merge_impl(cusci_ctx* ctx, cusci_pool* pool, const uint64_t* U, uint64_t nU,
       return rc;
     }
   }
-  CUSCI_LAUNCH(ctx, PT_MERGE_SPLIT, merge_split_kernel<W><<<(unsigned)((ntiles + 1 + 255) / 256), 256, 0, ctx->stream>>>(S, nS, U, nU, ntiles, split));
-  static int mper[3] = {0, 0, 0};
-  if (!mper[W]) {
-    CUSCI_CUDA(ctx, cudaFuncSetAttribute(merge_tile_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MergeCfg<W>::SMEM));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mper[W], merge_tile_kernel<W>, kMergeThreads, MergeCfg<W>::SMEM);
-    if (mper[W] < 1) mper[W] = 1;
-  }
-  // persistent grid: every CTA resident (the look-back relies on it)
-  const unsigned mgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * mper[W]));
-  CUSCI_LAUNCH(ctx, PT_MERGE_TILE, merge_tile_kernel<W><<<mgrid, kMergeThreads, MergeCfg<W>::SMEM, ctx->stream>>>(S, nS, U, nU, split, ntiles, status, bad, dst, (uint64_t*)insp));
-  // totals = the last tile's inclusive counts; plus the input check flag
   uint64_t h[3];
-  CUSCI_CUDA(ctx, cudaMemcpyAsync(ctx->host_pinned, status + 2 * (ntiles - 1), 2 * sizeof(uint64_t),
-                                  cudaMemcpyDeviceToHost, ctx->stream));
-  CUSCI_CUDA(ctx, cudaMemcpyAsync((char*)ctx->host_pinned + 16, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-  CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-  memcpy(h, ctx->host_pinned, 2 * sizeof(uint64_t));
-  const int badflag = *(int*)((char*)ctx->host_pinned + 16);
-  if (badflag) {
-    for (int b = 0; b < 2; b++)
-      if (grown[b]) cudaFreeAsync(grown[b], ctx->stream);
-    if (insp) out_free(ctx, insp);
-    return set_error(ctx, CUSCI_E_INVALID_ARG, "merge_space: new_keys must be sorted in the pool (hash) order and unique");
+  if (nS == 0) {
+    // empty pool: S' = U (validated strictly increasing in the hash order), a copy
+    const unsigned cg = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nU + 255) / 256, (uint64_t)ctx->num_sms * 8));
+    CUSCI_LAUNCH(ctx, PT_CHECK, check_sorted_kernel<W><<<cg, 256, 0, ctx->stream>>>(U, nU, bad));
+    CUSCI_CUDA(ctx, cudaMemcpyAsync(dst, U, nU * W * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (insp) CUSCI_CUDA(ctx, cudaMemcpyAsync(insp, U, nU * W * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    CUSCI_CUDA(ctx, cudaMemcpyAsync((char*)ctx->host_pinned + 16, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    h[0] = nU;
+    h[1] = nU;
+    if (*(int*)((char*)ctx->host_pinned + 16)) {
+      for (int b = 0; b < 2; b++)
+        if (grown[b]) cudaFreeAsync(grown[b], ctx->stream);
+      if (insp) out_free(ctx, insp);
+      return set_error(ctx, CUSCI_E_INVALID_ARG, "merge_space: new_keys must be sorted in the pool (hash) order and unique");
+    }
+  } else {
+    CUSCI_LAUNCH(ctx, PT_MERGE_SPLIT, merge_split_kernel<W><<<(unsigned)((ntiles + 1 + 255) / 256), 256, 0, ctx->stream>>>(S, nS, U, nU, ntiles, split));
+    static int mper[3] = {0, 0, 0};
+    if (!mper[W]) {
+      CUSCI_CUDA(ctx, cudaFuncSetAttribute(merge_tile_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MergeCfg<W>::SMEM));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mper[W], merge_tile_kernel<W>, kMergeThreads, MergeCfg<W>::SMEM);
+      if (mper[W] < 1) mper[W] = 1;
+    }
+    // persistent grid: every CTA resident (the look-back relies on it)
+    const unsigned mgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * mper[W]));
+    CUSCI_LAUNCH(ctx, PT_MERGE_TILE, merge_tile_kernel<W><<<mgrid, kMergeThreads, MergeCfg<W>::SMEM, ctx->stream>>>(S, nS, U, nU, split, ntiles, status, bad, dst, (uint64_t*)insp));
+    // totals = the last tile's inclusive counts; plus the input check flag
+    CUSCI_CUDA(ctx, cudaMemcpyAsync(ctx->host_pinned, status + 2 * (ntiles - 1), 2 * sizeof(uint64_t),
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+    CUSCI_CUDA(ctx, cudaMemcpyAsync((char*)ctx->host_pinned + 16, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    memcpy(h, ctx->host_pinned, 2 * sizeof(uint64_t));
+    const int badflag = *(int*)((char*)ctx->host_pinned + 16);
+    if (badflag) {
+      for (int b = 0; b < 2; b++)
+        if (grown[b]) cudaFreeAsync(grown[b], ctx->stream);
+      if (insp) out_free(ctx, insp);
+      return set_error(ctx, CUSCI_E_INVALID_ARG, "merge_space: new_keys must be sorted in the pool (hash) order and unique");
+    }
   }
   const uint64_t n_new = h[0] & kMVal, n_ins = h[1] & kMVal;
   if (grown[0]) {

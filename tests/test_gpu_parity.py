@@ -308,6 +308,23 @@ def test_merge_parity(P, ctx, W):
     pool.close()
 
 
+@pytest.mark.parametrize("W", [1, 2])
+def test_merge_into_empty_pool(P, ctx, W):
+    """Empty pool: S' = U (copy path) -- still validated, inserted = U."""
+    rng = np.random.default_rng(40 + W)
+    sp = P.Space(64 * W, 1, 1)
+    U = synth.unique_keys(rng.integers(1, 1 << 40, size=(50_001, W), dtype=np.uint64))
+    pool = ctx.pool(sp, capacity=16)
+    ins = ctx.merge_space(pool, torch.from_numpy(hash_sort(U, W)).cuda(), want_inserted=True).cpu().numpy()
+    assert_hash_sorted_unique(pool.keys().cpu().numpy(), W)
+    assert np.array_equal(synth.sort_keys(pool.keys().cpu().numpy()), U) and np.array_equal(synth.sort_keys(ins), U)
+    pool.clear()
+    with pytest.raises(P.CusciError) as e:
+        ctx.merge_space(pool, torch.from_numpy(hash_sort(U, W)[::-1].copy()).cuda())
+    assert e.value.code == 1
+    pool.close()
+
+
 def test_pipeline_lih_merge_inserts_nothing(P, ctx):
     wl, ints, par = synth.workload_inputs("lih")
     sp = P.Space(12, 2, 2)

@@ -59,8 +59,42 @@ def full(rep):
         lines.append(f"| {i} | `{k}` | " + " | ".join(v.get(w, "") for w in want) + f" | {t[0]+t[1] if t else ''} |")
     return "\n".join(lines)
 
+CLASS = {"tile_scatter_kernel": "part_scatter", "tile_hist_kernel": "part_hist", "bucket_unique_kernel": "bucket_unique",
+         "bucket_compact_kernel": "pack", "group_off_kernel": "pack", "owner_bounds_kernel": "pack",
+         "gen_kernel": "gen", "merge_tile_kernel": "merge_tile", "merge_split_kernel": "merge_split"}
+
+
+def traffic_json(path, out_json):
+    """per profiler class: DRAM bytes per launch from the launch list (timed step)."""
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
+    hdr, data = rows[hi], rows[hi + 1:]
+    ki, mi, vi, ii = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value"), hdr.index("ID")
+    per = {}
+    for r in data:
+        if len(r) < len(hdr):
+            continue
+        per.setdefault(int(r[ii]), {"k": r[ki]})[r[mi]] = float(r[vi].replace(",", ""))
+    ids = sorted(per)
+    agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
+    for i in ids[len(ids) // 2:]:
+        d = per[i]
+        name = d["k"].split("(")[0].replace("void ", "").split("::")[-1].split("<")[0]
+        c = CLASS.get(name)
+        if c:
+            a = agg[c]
+            a[0] += 1
+            a[1] += d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0)
+            a[2] += d.get("gpu__time_duration.sum", 0)
+    out = {c: {"launches": a[0], "dram_bytes_per_launch": a[1] / a[0], "ncu_ms_per_launch": a[2] / a[0] / 1e6}
+           for c, a in agg.items() if a[0]}
+    json.dump({"source": path, "classes": out}, open(out_json, "w"), indent=1)
+    return out
+
+
 if __name__ == "__main__":
     tag = sys.argv[1]
+    print(json.dumps(traffic_json(f"gpurun_out/{tag}_launches.csv", f"profiles/{tag}_traffic.json"), indent=1))
     tbl, tot = launches(f"gpurun_out/{tag}_launches.csv", f"profiles/{tag}_launches.csv")
     print(tbl)
     print()
