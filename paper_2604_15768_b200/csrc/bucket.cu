@@ -42,6 +42,7 @@ constexpr int kBI = 8;          // keys per thread per hist round
 constexpr int kBTile = kBT * kBI;
 constexpr int kHllLog = 11;     // HyperLogLog: 2^11 registers (~2.3% standard error)
 constexpr uint32_t kHllM = 1u << kHllLog;
+constexpr uint32_t kHllSample = 16;  // the sketch sees a 1/16 hash sample of the keys
 
 // digit source: the top bits of the pi-value's hi word (w0)
 template <int W>
@@ -105,9 +106,13 @@ __global__ void __launch_bounds__(kBT) tile_hist_kernel(const uint64_t* __restri
           atomicAdd(&h[top_bits<W>(k[u], bsel) & dmask], 1u);
           if (RAW) {
             const uint64_t hv = k[u].w0;  // hi: a 64-bit hash of the whole key
-            const uint32_t idx = (uint32_t)hv & (kHllM - 1);
-            const uint32_t rho = (uint32_t)min(__clzll(hv), 64 - kHllLog) + 1;
-            if (rho > reg[idx]) atomicMax(&reg[idx], rho);
+            // hash-sampled sketch: only keys with bits [11, 15) of hi zero enter
+            // (a key is always or never sampled, so the sample's distinct count is D / 16)
+            if (((hv >> kHllLog) & (kHllSample - 1)) == 0) {
+              const uint32_t idx = (uint32_t)hv & (kHllM - 1);
+              const uint32_t rho = (uint32_t)min(__clzll(hv), 64 - kHllLog - 4) + 1;
+              if (rho > reg[idx]) atomicMax(&reg[idx], rho);
+            }
           }
         }
       }
@@ -123,10 +128,12 @@ __global__ void __launch_bounds__(kBT) tile_hist_kernel(const uint64_t* __restri
 }
 
 constexpr int kST = 512;  // scatter threads
-// dynamic shared memory: two TMA input buffers, the digit-ordered stage, digits, cursors
+constexpr int kSRing = 3;  // scatter input ring: one sub-round being ranked/staged, two in flight
+// dynamic shared memory: the TMA input ring (a slot doubles as the digit-ordered
+// stage of its own sub-round), digits, cursors
 template <int W, int RB> constexpr size_t scatter_smem() {
-  return 3 * ((size_t)SSCfg<W>::SUB + 2) * sizeof(KeyT<W>) + (size_t)SSCfg<W>::SUB * (RB > 8 ? 2 : 1) +
-         3 * sizeof(uint32_t) * (1u << RB);
+  return kSRing * ((size_t)SSCfg<W>::SUB + 2) * sizeof(KeyT<W>) + (size_t)SSCfg<W>::SUB * (RB > 8 ? 2 : 1) +
+         4 * sizeof(uint32_t) * (1u << RB);
 }
 
 // thread 0: bulk-copy keys [s, s + len) into buf so that key s + i lands at
@@ -160,8 +167,11 @@ __device__ __forceinline__ KeyT<W> scatter_key(const uint64_t* in, uint64_t s, u
   return buf[i];
 }
 
-// The tile streams through shared memory by 1-D TMA bulk copies, the next
-// sub-round's keys in flight while the current one is ranked and written.
+// The tile streams through shared memory by 1-D TMA bulk copies into a ring of
+// kSRing slots: two sub-rounds are in flight while the current one is ranked.
+// Its keys are held in registers after ranking, so the current slot itself is
+// reused as the digit-ordered stage (its next TMA is issued only after the
+// round's closing barrier).
 template <int W, bool RAW, int RB>
 __global__ void __launch_bounds__(kST, 2) tile_scatter_kernel(const uint64_t* __restrict__ in, int use_tma,
                                                              const PTile* __restrict__ tiles, int bsel, uint32_t dmask,
@@ -169,17 +179,15 @@ __global__ void __launch_bounds__(kST, 2) tile_scatter_kernel(const uint64_t* __
   constexpr int ITEMS = SSCfg<W>::SUB / kST;  // keys per thread per sub-round
   constexpr int SUB = SSCfg<W>::SUB;
   constexpr uint32_t RMAX = 1u << RB;
-  constexpr uint32_t DPT = RMAX > kST ? RMAX / kST : 1;  // digits per thread in the scan
   using Dig = typename std::conditional<(RB > 8), uint16_t, uint8_t>::type;
   extern __shared__ __align__(16) unsigned char ssm[];  // scatter_smem<W, RB>() bytes
-  KeyT<W>* inb = reinterpret_cast<KeyT<W>*>(ssm);        // [2][SUB + 2]
-  KeyT<W>* stage = inb + 2 * (SUB + 2);
-  uint32_t* cur = reinterpret_cast<uint32_t*>(stage + SUB + 2);
+  KeyT<W>* ring = reinterpret_cast<KeyT<W>*>(ssm);       // [kSRing][SUB + 2]
+  uint32_t* cur = reinterpret_cast<uint32_t*>(ring + kSRing * (SUB + 2));
   uint32_t* cnt = cur + RMAX;
   uint32_t* lst = cnt + RMAX;
-  Dig* sdig = reinterpret_cast<Dig*>(lst + RMAX);
-  __shared__ uint32_t red[33];
-  __shared__ __align__(8) uint64_t bar[2];
+  uint32_t* dl = lst + RMAX;
+  Dig* sdig = reinterpret_cast<Dig*>(dl + RMAX);
+  __shared__ __align__(8) uint64_t bar[kSRing];
   const PTile t = tiles[blockIdx.x];
   const uint32_t R = dmask + 1;
   const bool tma = use_tma && ((reinterpret_cast<uintptr_t>(in) & 15u) == 0);
@@ -189,29 +197,31 @@ __global__ void __launch_bounds__(kST, 2) tile_scatter_kernel(const uint64_t* __
   }
   const uint32_t nsub = (t.len + SUB - 1) / SUB;
   if (threadIdx.x == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    for (int i = 0; i < kSRing; i++) mbar_init(&bar[i], 1);
     mbar_init_fence();
   }
   __syncthreads();
-  if (tma && threadIdx.x == 0 && nsub) issue_core<W>(in, t.start, min((uint32_t)SUB, t.len), inb, &bar[0]);
+  auto issue = [&](uint32_t r) {  // thread 0: sub-round r -> slot r % kSRing
+    const uint32_t sl = r % kSRing;
+    fence_proxy_async_smem();
+    issue_core<W>(in, t.start + (uint64_t)r * SUB, min((uint32_t)SUB, t.len - r * SUB), ring + sl * (SUB + 2), &bar[sl]);
+  };
+  if (tma && threadIdx.x == 0)
+    for (uint32_t r = 0; r < min(nsub, (uint32_t)kSRing - 1); r++) issue(r);
   uint32_t phase = 0;
   for (uint32_t r = 0; r < nsub; r++) {
-    const uint32_t cb = r & 1, r0 = r * SUB;
+    const uint32_t sl = r % kSRing, r0 = r * SUB;
     const uint32_t m = min((uint32_t)SUB, t.len - r0);
-    KeyT<W>* buf = inb + cb * (SUB + 2);
+    KeyT<W>* buf = ring + sl * (SUB + 2);
     if (tma) {
-      if (threadIdx.x == 0 && r + 1 < nsub) {  // prefetch the next sub-round (its buffer was freed last round)
-        fence_proxy_async_smem();
-        issue_core<W>(in, t.start + r0 + SUB, min((uint32_t)SUB, t.len - r0 - SUB),
-                                       inb + (cb ^ 1) * (SUB + 2), &bar[cb ^ 1]);
-      }
-      // every thread knows whether a copy was issued (same arithmetic as issue_core)
-      const uint64_t s0 = t.start + r0;
+      // keep kSRing - 1 sub-rounds in flight: r + kSRing - 1 goes into the slot
+      // freed by the previous round's closing barrier
+      if (threadIdx.x == 0 && r + kSRing - 1 < nsub) issue(r + kSRing - 1);
+      const uint64_t s0 = t.start + r0;  // same arithmetic as issue_core: was a copy issued?
       const bool issued = W == 1 ? (((s0 + m) & ~1ull) > ((s0 + 1) & ~1ull)) : m > 0;
       if (issued) {
-        mbar_wait(&bar[cb], (phase >> cb) & 1u);
-        phase ^= 1u << cb;
+        mbar_wait(&bar[sl], (phase >> sl) & 1u);
+        phase ^= 1u << sl;
       }
     }
     KeyT<W> k[ITEMS];
@@ -226,24 +236,36 @@ __global__ void __launch_bounds__(kST, 2) tile_scatter_kernel(const uint64_t* __
         dr[u] = (d << 16) | atomicAdd(&cnt[d], 1u);
       }
     }
-    __syncthreads();
-    // sub-round digit counts -> exclusive offsets (thread: DPT consecutive digits)
-    uint32_t c[DPT], loc = 0;
+    __syncthreads();  // every key of the slot is in registers: the slot becomes the stage
+    // warp 0: exclusive scan of the sub-round digit counts (lane: RMAX/32
+    // consecutive digits); per digit the stage offset lst, the stage -> output
+    // offset dl, the advanced cursor, and the counter reset for the next round
+    if (threadIdx.x < 32) {
+      constexpr uint32_t DPL = RMAX / 32;
+      uint32_t c[DPL], loc = 0;
 #pragma unroll
-    for (uint32_t j = 0; j < DPT; j++) {
-      const uint32_t d = threadIdx.x * DPT + j;
-      c[j] = d < RMAX ? cnt[d] : 0u;
-      loc += c[j];
-    }
-    uint32_t tot;
-    uint32_t ex = block_excl_scan_u32(loc, red, tot);
+      for (uint32_t j = 0; j < DPL; j++) {
+        c[j] = cnt[threadIdx.x * DPL + j];
+        loc += c[j];
+      }
+      uint32_t inc = loc;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, inc, o);
+        if ((int)threadIdx.x >= o) inc += y;
+      }
+      uint32_t ex = inc - loc;
 #pragma unroll
-    for (uint32_t j = 0; j < DPT; j++) {
-      const uint32_t d = threadIdx.x * DPT + j;
-      if (d < RMAX) lst[d] = ex;
-      ex += c[j];
+      for (uint32_t j = 0; j < DPL; j++) {
+        const uint32_t d = threadIdx.x * DPL + j;
+        lst[d] = ex;
+        dl[d] = cur[d] - ex;
+        cur[d] += c[j];
+        cnt[d] = 0;
+        ex += c[j];
+      }
     }
     __syncthreads();
+    KeyT<W>* stage = buf;
 #pragma unroll
     for (int u = 0; u < ITEMS; u++) {
       const uint32_t i = u * kST + threadIdx.x;
@@ -255,20 +277,8 @@ __global__ void __launch_bounds__(kST, 2) tile_scatter_kernel(const uint64_t* __
       }
     }
     __syncthreads();
-    for (uint32_t j = threadIdx.x; j < m; j += kST) {
-      const uint32_t dj = sdig[j];
-      store_key<W>(out, (uint64_t)cur[dj] + (j - lst[dj]), stage[j]);
-    }
-    __syncthreads();
-#pragma unroll
-    for (uint32_t j = 0; j < DPT; j++) {
-      const uint32_t d = threadIdx.x * DPT + j;
-      if (d < RMAX) {
-        cur[d] += c[j];
-        cnt[d] = 0;
-      }
-    }
-    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < m; j += kST) store_key<W>(out, (uint64_t)(dl[sdig[j]] + j), stage[j]);
+    __syncthreads();  // the stage (this ring slot) is read out: its next TMA may be issued
   }
 }
 
@@ -766,9 +776,13 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
     if (Bmax > bits1) {
       std::vector<uint32_t> reg(kHllM);
       CUSCI_CUDA(ctx, cudaMemcpy(reg.data(), hll, kHllM * sizeof(uint32_t), cudaMemcpyDeviceToHost));
-      const double D = std::min<double>((double)n, std::max(1.0, hll_estimate(reg.data())));
+      const double D = std::min<double>((double)n, std::max(1.0, kHllSample * hll_estimate(reg.data())));
       int Bd = 0;
       while (D / std::ldexp(1.0, Bd) > (double)dt && Bd < 22) Bd++;
+      // one bit less when that saves a whole partition pass and the buckets stay
+      // within 1.6 x the target (table load <= ~0.6)
+      auto npass = [&](int b) { return (std::max(0, b - bits1) + max_bits - 1) / max_bits; };
+      if (Bd > bits1 && npass(Bd - 1) < npass(Bd) && D / std::ldexp(1.0, Bd - 1) <= 1.6 * (double)dt) Bd--;
       B = std::max(bits1, std::min(Bmax, Bd));
       const int rest = B - bits1;
       const int np = (rest + max_bits - 1) / max_bits;
