@@ -308,6 +308,8 @@ def main():
     if not args.no_e2e:
         barrier(pg)
         torch.cuda.synchronize()
+        eclocks = ClockSampler(local)
+        eclocks.start()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -320,11 +322,12 @@ def main():
             er += int(res[0])
         e1.record(stream)
         torch.cuda.synchronize()
+        eclk = eclocks.stop()
         barrier(pg)
         ems = allreduce_max(pg, e0.elapsed_time(e1))
         e2e = {"value": allreduce_sum(pg, er) / (ems / 1e3), "unit": "coupled configs/s",
                "h2d_bytes_per_step": int(shard_pinned.numel() * 8 + ints.h.nbytes * 0),
-               "d2h_bytes_per_step": 24}
+               "d2h_bytes_per_step": 24, "ms_per_step": ems / args.steps, "clocks": eclk}
 
     # ---------------- roofline of the dominant kernel class
     peaks = {}
