@@ -142,6 +142,15 @@ def allreduce_sum(pg, x: float) -> float:
     return float(t.item())
 
 
+def plan_batches(pg, n_par: int, batch: int):
+    """Parent batches of this rank's shard.  dedup_global is collective, so every
+    rank must make the same number of calls: the batch count is agreed (max
+    over ranks) and each shard is split evenly into that many batches."""
+    n_batches = int(allreduce_max(pg, float(max(1, -(-n_par // max(1, batch))))))
+    edges = [round(i * n_par / n_batches) for i in range(n_batches + 1)]
+    return [(edges[i], edges[i + 1]) for i in range(n_batches)]
+
+
 def barrier(pg):
     if pg is not None:
         pg.barrier()
@@ -227,8 +236,8 @@ def main():
     shard = ctx.dedup_global(sp, torch.from_numpy(mine).to(dev))   # parents owned by this rank (sorted)
     n_par = int(shard.shape[0])
     batch = args.batch or {"n2": 500_000, "c2h4": 20_000}.get(args.workload, max(1, n_par))
-    batch = max(1, min(batch, n_par))
-    batches = [(i, min(i + batch, n_par)) for i in range(0, n_par, batch)]
+    batches = plan_batches(pg, n_par, batch)
+    batch = max(b - a for a, b in batches) if batches else 0
     # plan: exact record counts per batch (buffer sizing; outside the timed region)
     counts = [ctx.gen_coupled_count(sp, shard[a:b], di, args.eps) for a, b in batches]
     cap = max(counts) if counts else 1

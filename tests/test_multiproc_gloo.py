@@ -36,6 +36,11 @@ def _worker(rank, world, port, q):
         # 2) timing reductions
         assert bench.allreduce_max(dist, float(rank + 1)) == float(world)
         assert bench.allreduce_sum(dist, 1.5) == 1.5 * world
+        # 2b) collective batch plan: unequal shards still give equal call counts
+        n_par = 500_300 if rank == 0 else 499_700
+        plan = bench.plan_batches(dist, n_par, 500_000)
+        assert len(plan) == 2 and plan[0][0] == 0 and plan[-1][1] == n_par
+        assert all(b > a for a, b in plan) and all(plan[i][1] == plan[i + 1][0] for i in range(len(plan) - 1))
         # 3) owner-sharded dedup protocol (logical; oracle arithmetic)
         for W in (1, 2):
             allk = synth.zipf_keys(60_000, W, 1.1, 1 << 12, seed=21)
