@@ -396,3 +396,45 @@ def test_dedup_bucket_overflow_slow_path(P, ctx):
     got = ctx.dedup_global(sp, torch.from_numpy(allk).cuda()).cpu().numpy()
     assert_hash_sorted_unique(got, 1)
     assert np.array_equal(synth.sort_keys(got), oracle.dedup(allk, 1))
+
+
+def _t_fmix64(x):
+    """splitmix64 finalizer on int64 torch tensors (logical shifts, wrapping multiplies)."""
+    def srl(v, s):
+        return (v >> s) & ((1 << (64 - s)) - 1)
+    c1 = 0xBF58476D1CE4E5B9 - (1 << 64)
+    c2 = 0x94D049BB133111EB - (1 << 64)
+    x = x ^ srl(x, 30)
+    x = x * c1
+    x = x ^ srl(x, 27)
+    x = x * c2
+    return x ^ srl(x, 31)
+
+
+def test_dedup_at_scale_three_passes(P, ctx):
+    """0.76e9 keys (0.66e9 distinct, 1e8 repeated), shuffled: exercises the
+    HyperLogLog plan with two further partition passes (B = 18 bucket bits).
+    Too large for the oracle: checked by the exact distinct count, strict hash
+    order and set equality with the generating set (torch sort on the GPU)."""
+    D, R = 660_000_000, 100_000_000
+    C = 0x9E3779B97F4A7C15 - (1 << 64)          # odd: i -> i * C is a bijection of Z/2^64
+    base = torch.arange(1, D + 1, dtype=torch.int64, device="cuda") * C
+    g = torch.Generator(device="cuda").manual_seed(7)
+    rep = base[torch.randint(0, D, (R,), device="cuda", generator=g)]
+    keys = torch.cat([base, rep])
+    del rep
+    keys = keys[torch.randperm(keys.numel(), device="cuda", generator=g)]
+    ctx.dedup_stats(reset=True)
+    u = ctx.dedup_global(P.Space(64, 1, 1), keys.view(torch.uint64).reshape(-1, 1))
+    st = ctx.dedup_stats(reset=True)
+    del keys
+    assert u.shape[0] == D
+    assert st["key_passes"] == 3 * (D + R) and st["slow_path_calls"] == 0, st
+    ui = u.view(torch.int64).reshape(-1)
+    flip = -(1 << 63)
+    hi = _t_fmix64(ui) ^ flip                      # signed order of hi ^ 2^63 = unsigned order of hi
+    assert bool((hi[1:] > hi[:-1]).all()), "not strictly in hash order"
+    del hi
+    a = torch.sort(ui ^ flip).values
+    b = torch.sort(base ^ flip).values
+    assert torch.equal(a, b)
