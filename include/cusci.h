@@ -199,6 +199,29 @@ void cusci_pool_destroy(cusci_pool* pool);
 int merge_space(cusci_ctx* ctx, cusci_pool* space, const uint64_t* new_keys, uint64_t n_new,
                 cusci_keys* inserted);
 
+/* ---- next row: Stage-3 contraction ----------------------- */
+
+/* Local-energy numerators of Eq. 5 over this rank's records, with
+ * the just-in-time reverse index of Stage 3 ("we construct
+ * the required reverse index just-in-time by searching against the full
+ * unique set"):
+ *     e[s] = sum over records r with src[r] = s of  H[r] * psi[idx(key[r])]
+ * idx(key) = position of key in `space_keys` ([n_space][words], device, sorted
+ * strictly in the pool hash order, e.g. a pool view or a dedup_global output);
+ * psi[n_space] (device, fp64) is aligned with it.  keys/hij/src are a
+ * gen_coupled output (device, n_rec records, src < n_parents); e[n_parents]
+ * (device, fp64) is overwritten.
+ * Deterministic reduction (reading r14): each product p = H*psi is
+ * the IEEE fp64 product, rounded half-to-even to the grid 2^-80 and summed
+ * EXACTLY in 128-bit integers (order independent), and e[s] is that sum
+ * rounded once to fp64.  Requires |p| < 2^20 (CUSCI_E_INVALID_ARG otherwise,
+ * e untouched).  A record whose key is not in the space contributes 0 and is
+ * counted in *n_missing (host).  Single rank: with world > 1 records and psi
+ * must first meet at the key's owner (CUSCI_E_INVALID_ARG for now). */
+int energy_contract(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* keys, const double* hij,
+                    const uint32_t* src, uint64_t n_rec, uint64_t n_parents, const uint64_t* space_keys,
+                    uint64_t n_space, const double* psi, double* e, uint64_t* n_missing);
+
 #ifdef __cplusplus
 }
 #endif

@@ -286,6 +286,30 @@ class Context:
             return self._take(k.keys, int(k.count), W)
         return None
 
+    def energy_contract(self, space: Space, rec: "Records", n_parents: int, space_keys: torch.Tensor,
+                        psi: torch.Tensor, e: torch.Tensor = None):
+        """Stage-3 contraction (Eq. 5): e[s] = sum_{r: src_r = s} H_r psi[idx(key_r)]
+        with the just-in-time reverse index into the hash-ordered unique set
+        `space_keys` (psi aligned with it).  Returns (e float64 [n_parents], n_missing)."""
+        W = space.words
+        n = int(rec.count)
+        keys = _as_u64_2d(rec.keys[:n], W)
+        if rec.src is None:
+            raise ValueError("energy_contract needs records with src")
+        sk = _as_u64_2d(space_keys, W)
+        psi = psi.contiguous()
+        if psi.dtype != torch.float64 or psi.numel() != sk.shape[0]:
+            raise ValueError("psi must be float64 and aligned with space_keys")
+        if e is None:
+            e = torch.empty(max(int(n_parents), 0), dtype=torch.float64, device=keys.device)
+        miss = ctypes.c_uint64()
+        rc = lib().energy_contract(self._ctx, ctypes.byref(space._c()), ctypes.c_void_p(keys.data_ptr()),
+                                   ctypes.c_void_p(rec.hij.data_ptr()), ctypes.c_void_p(rec.src.data_ptr()), n,
+                                   int(n_parents), ctypes.c_void_p(sk.data_ptr()), sk.shape[0],
+                                   ctypes.c_void_p(psi.data_ptr()), ctypes.c_void_p(e.data_ptr()), ctypes.byref(miss))
+        self._check(rc, "energy_contract")
+        return e, int(miss.value)
+
 
 class Pool:
     """GPU-resident sorted unique configuration shard (library owned)."""

@@ -14,11 +14,12 @@ CUSCI_ERRORS = {0: "OK", 1: "E_INVALID_ARG", 2: "E_INVALID_PARENT", 3: "E_CAPACI
 EXPORTS = ["cusci_nccl_unique_id", "cusci_init", "cusci_finalize", "cusci_last_error", "cusci_invalidate_integrals",
            "cusci_free", "cusci_kernel_launches", "cusci_profile_enable", "cusci_profile_read", "cusci_dedup_stats", "gen_coupled_bound", "gen_coupled", "gen_coupled_count",
            "dedup_global", "dedup_partition", "dedup_finalize", "cusci_pool_create", "cusci_pool_view",
-           "cusci_pool_copy", "cusci_pool_clear", "cusci_pool_destroy", "merge_space"]
+           "cusci_pool_copy", "cusci_pool_clear", "cusci_pool_destroy", "merge_space", "energy_contract"]
 
 
 PROFILE_TAGS = ["prep", "validate", "gen", "bucket_unique", "pack", "part_hist", "part_scatter",
-                "scan", "unique", "merge_split", "merge_tile", "sorted_check", "nccl_exchange", "memset"]
+                "scan", "unique", "merge_split", "merge_tile", "sorted_check", "nccl_exchange", "memset",
+                "energy"]
 
 
 class CusciError(RuntimeError):
@@ -84,5 +85,7 @@ def lib():
     L.cusci_pool_destroy.restype = None
     L.merge_space.argtypes = [vp, vp, vp, u64, vp]
     L.merge_space.restype = i32
+    L.energy_contract.argtypes = [vp, vp, vp, vp, vp, u64, u64, vp, u64, vp, vp, P(u64)]
+    L.energy_contract.restype = i32
     _lib = L
     return L

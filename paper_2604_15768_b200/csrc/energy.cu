@@ -1,0 +1,220 @@
+// energy_contract: Stage-3 contraction of the coupled records with amplitudes
+// (SURVEY 8(f) row f1; Eq. 5 :267-270, Stage 3 :398-403, :634).
+//
+//   e[s] = sum over records r with src[r] = s of H[r] * psi[idx(key[r])]
+//
+// B200 design (reading r14):
+//   reverse index  the unique set is sorted in the hash order pi (reading
+//                  r13) and pi is uniform, so a table T over the top k bits of
+//                  hi (k = log2(n_space / 4)) brackets every key in ~4 entries:
+//                  one table load + a 2-3 step binary search per record ("just
+//                  in time", nothing materialised per record);
+//   reduction      each product p = H * psi (IEEE fp64) is rounded half-to-even
+//                  to the grid 2^-80 and accumulated EXACTLY as a 128-bit
+//                  integer: a warp first sums the runs of equal src among its
+//                  lanes (gen_coupled writes a parent's records in runs), then
+//                  the run totals go into per-parent 4 x 32-bit limb
+//                  accumulators with 64-bit atomics.  Integer addition is
+//                  associative, so the result is independent of record order
+//                  and of the launch configuration; e[s] = the exact sum
+//                  rounded once to fp64.
+#include <algorithm>
+
+#include "internal.cuh"
+
+namespace cusci {
+namespace {
+
+constexpr int kET = 256;
+
+template <int W>
+__device__ __forceinline__ bool pi_less(const KeyT<W>& a, const KeyT<W>& b) { return pi_lt(a, b); }
+
+// T[b] = first index i with top_k(hi(space[i])) >= b, b in [0, 2^k]
+template <int W>
+__global__ void rindex_table_kernel(const uint64_t* __restrict__ space, uint64_t n, int k, uint32_t* __restrict__ T) {
+  const uint64_t nb = 1ull << k;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += stride) {
+    // buckets (prev, cur] start at i
+    const uint64_t cur = i < n ? (k ? (to_pi(load_key<W>(space, i)).w0 >> (64 - k)) : 0ull) : nb;
+    const int64_t prev = i > 0 ? (int64_t)(k ? (to_pi(load_key<W>(space, i - 1)).w0 >> (64 - k)) : 0ull) : -1;
+    for (int64_t b = prev + 1; b <= (int64_t)cur; b++) T[b] = (uint32_t)i;
+  }
+}
+
+// p -> round_half_even(p * 2^80) for |p| < 2^20 (exact integer arithmetic)
+__device__ __forceinline__ __int128 quantize80(double p) {
+  if (p == 0.0) return 0;
+  int E;
+  const double f = frexp(p, &E);                 // p = f 2^E, 0.5 <= |f| < 1
+  const long long m = (long long)ldexp(f, 53);   // exact: |m| < 2^53
+  const int sh = E - 53 + 80;
+  const bool neg = m < 0;
+  const unsigned long long am = neg ? (unsigned long long)(-m) : (unsigned long long)m;
+  unsigned __int128 q;
+  if (sh >= 0) {
+    q = (unsigned __int128)am << sh;
+  } else {
+    const int r = -sh;
+    if (r > 63) {
+      q = 0;  // |am| / 2^r < 2^53 / 2^64 < 1/2
+    } else {
+      const unsigned long long whole = am >> r, rem = am & ((1ull << r) - 1), half = 1ull << (r - 1);
+      q = whole + ((rem > half || (rem == half && (whole & 1ull))) ? 1u : 0u);
+    }
+  }
+  return neg ? -(__int128)q : (__int128)q;
+}
+
+// exact 128-bit integer -> nearest fp64 (ties to even)
+__device__ __forceinline__ double int128_to_double_rn(__int128 x) {
+  if (x == 0) return 0.0;
+  const bool neg = x < 0;
+  const unsigned __int128 u = neg ? (unsigned __int128)(-x) : (unsigned __int128)x;
+  const unsigned long long hi = (unsigned long long)(u >> 64), lo = (unsigned long long)u;
+  const int msb = hi ? 127 - __clzll((long long)hi) : 63 - __clzll((long long)lo);
+  double r;
+  if (msb < 53) {
+    r = (double)lo;
+  } else {
+    const int sh = msb - 52;
+    unsigned long long mant = (unsigned long long)(u >> sh);  // 53 bits
+    const unsigned __int128 rem = u & ((((unsigned __int128)1) << sh) - 1);
+    const unsigned __int128 half = ((unsigned __int128)1) << (sh - 1);
+    if (rem > half || (rem == half && (mant & 1ull))) mant++;
+    r = ldexp((double)mant, sh);  // mant may be 2^53: still exact in fp64
+  }
+  return neg ? -r : r;
+}
+
+template <int W>
+__global__ void __launch_bounds__(kET) contract_kernel(const uint64_t* __restrict__ keys, const double* __restrict__ hij,
+                                                      const uint32_t* __restrict__ src, uint64_t n_rec,
+                                                      const uint64_t* __restrict__ space, uint64_t n_space,
+                                                      const double* __restrict__ psi, const uint32_t* __restrict__ T,
+                                                      int k, unsigned long long* __restrict__ acc,
+                                                      unsigned long long* __restrict__ flags) {
+  const unsigned lane = lane_id();
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t missing = 0;
+  bool big = false;
+  // warp-uniform trip count so the warp-level reduction always has all lanes
+  const uint64_t base0 = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
+  for (uint64_t w0 = base0; w0 < n_rec; w0 += stride) {
+    const uint64_t r = w0 + lane;
+    const bool valid = r < n_rec;
+    uint32_t s = 0xffffffffu;
+    __int128 q = 0;
+    if (valid) {
+      s = src[r];
+      const KeyT<W> key = load_key<W>(keys, r);
+      const KeyT<W> p = to_pi(key);
+      const uint64_t b = k ? (p.w0 >> (64 - k)) : 0ull;
+      uint64_t lo = T[b], hi = T[b + 1];
+      while (lo < hi) {  // first index with pi >= p
+        const uint64_t mid = (lo + hi) >> 1;
+        if (pi_less<W>(to_pi(load_key<W>(space, mid)), p)) lo = mid + 1;
+        else hi = mid;
+      }
+      if (lo < n_space && key_eq(load_key<W>(space, lo), key)) {
+        const double prod = __dmul_rn(hij[r], psi[lo]);
+        if (!(fabs(prod) < 1048576.0)) big = true;
+        else q = quantize80(prod);
+      } else {
+        missing++;
+      }
+    }
+    // segmented inclusive sum over runs of equal src (lanes in record order)
+    const uint32_t sprev = __shfl_up_sync(kFull, s, 1);
+    const unsigned heads = __ballot_sync(kFull, lane == 0 || sprev != s);
+    const int start = 31 - __clz(heads & ((2u << lane) - 1u));  // head of this lane's run
+    __int128 acc128 = q;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long ql = __shfl_up_sync(kFull, (unsigned long long)acc128, o);
+      const unsigned long long qh = __shfl_up_sync(kFull, (unsigned long long)((unsigned __int128)acc128 >> 64), o);
+      if ((int)lane - o >= start) acc128 += (__int128)(((unsigned __int128)qh << 64) | ql);
+    }
+    // the last lane of each run adds the run total to the parent's limbs
+    const uint32_t snext = __shfl_down_sync(kFull, s, 1);
+    const bool tail = valid && (lane == 31 || snext != s || !(w0 + lane + 1 < n_rec));
+    if (tail && acc128 != 0) {
+      const unsigned __int128 u = (unsigned __int128)acc128;
+      const long long l0 = (long long)(uint32_t)(u), l1 = (long long)(uint32_t)(u >> 32),
+                      l2 = (long long)(uint32_t)(u >> 64), l3 = (long long)(int32_t)(uint32_t)(u >> 96);
+      unsigned long long* a4 = acc + 4ull * s;
+      atomicAdd(a4 + 0, (unsigned long long)l0);
+      atomicAdd(a4 + 1, (unsigned long long)l1);
+      atomicAdd(a4 + 2, (unsigned long long)l2);
+      atomicAdd(a4 + 3, (unsigned long long)l3);
+    }
+  }
+  for (int o = 16; o; o >>= 1) missing += __shfl_xor_sync(kFull, missing, o);
+  if (lane == 0 && missing) atomicAdd(&flags[0], (unsigned long long)missing);
+  if (__any_sync(kFull, big) && lane == 0) atomicOr(&flags[1], 1ull);
+}
+
+__global__ void contract_finalize_kernel(const unsigned long long* __restrict__ acc, uint64_t n, double* __restrict__ e) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += stride) {
+    const long long a0 = (long long)acc[4 * s], a1 = (long long)acc[4 * s + 1], a2 = (long long)acc[4 * s + 2],
+                    a3 = (long long)acc[4 * s + 3];
+    const __int128 v = (__int128)a0 + ((__int128)a1 << 32) + ((__int128)a2 << 64) + ((__int128)a3 << 96);
+    e[s] = ldexp(int128_to_double_rn(v), -80);
+  }
+}
+
+template <int W>
+int contract_impl(cusci_ctx* ctx, const uint64_t* keys, const double* hij, const uint32_t* src, uint64_t n_rec,
+                  uint64_t n_parents, const uint64_t* space, uint64_t n_space, const double* psi, double* e,
+                  uint64_t* n_missing) {
+  Scratch s(ctx);
+  int k = 0;
+  while ((n_space >> k) > 4 && k < 26) k++;
+  uint32_t* T;
+  unsigned long long *acc, *flags;
+  CUSCI_TRY(s.get_t(((size_t)1 << k) + 1, &T));
+  CUSCI_TRY(s.get_t(std::max<uint64_t>(4 * n_parents, 1), &acc));
+  CUSCI_TRY(s.get_t(2, &flags));
+  CUSCI_CUDA(ctx, cudaMemsetAsync(acc, 0, std::max<uint64_t>(4 * n_parents, 1) * 8, ctx->stream));
+  CUSCI_CUDA(ctx, cudaMemsetAsync(flags, 0, 16, ctx->stream));
+  const unsigned g1 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_space + kET) / kET, (uint64_t)ctx->num_sms * 8));
+  CUSCI_LAUNCH(ctx, PT_ENERGY, rindex_table_kernel<W><<<g1, kET, 0, ctx->stream>>>(space, n_space, k, T));
+  if (n_rec) {
+    const unsigned g2 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_rec + kET - 1) / kET, (uint64_t)ctx->num_sms * 16));
+    CUSCI_LAUNCH(ctx, PT_ENERGY, contract_kernel<W><<<g2, kET, 0, ctx->stream>>>(keys, hij, src, n_rec, space, n_space, psi, T, k, acc, flags));
+  }
+  uint64_t h[2];
+  CUSCI_TRY(read_u64(ctx, reinterpret_cast<const uint64_t*>(flags), h, 2));
+  if (h[1]) return set_error(ctx, CUSCI_E_INVALID_ARG, "energy_contract: |H psi| >= 2^20 (outside the exact-sum range)");
+  *n_missing = h[0];
+  if (n_parents) {
+    const unsigned g3 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_parents + kET - 1) / kET, (uint64_t)ctx->num_sms * 8));
+    CUSCI_LAUNCH(ctx, PT_ENERGY, contract_finalize_kernel<<<g3, kET, 0, ctx->stream>>>(acc, n_parents, e));
+  }
+  return CUSCI_OK;
+}
+
+}  // namespace
+}  // namespace cusci
+
+using namespace cusci;
+
+extern "C" int energy_contract(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* keys, const double* hij,
+                               const uint32_t* src, uint64_t n_rec, uint64_t n_parents, const uint64_t* space_keys,
+                               uint64_t n_space, const double* psi, double* e, uint64_t* n_missing) {
+  if (!ctx) return CUSCI_E_INVALID_ARG;
+  if (ctx->broken) return set_error(ctx, CUSCI_E_CUDA, "context is unusable after an earlier CUDA/NCCL error");
+  CUSCI_TRY(check_space(ctx, sp));
+  if (!n_missing) return set_error(ctx, CUSCI_E_INVALID_ARG, "n_missing is NULL");
+  if (ctx->world > 1)
+    return set_error(ctx, CUSCI_E_INVALID_ARG, "energy_contract: single rank only (records and psi must meet at the owner)");
+  if (n_rec && (!keys || !hij || !src)) return set_error(ctx, CUSCI_E_INVALID_ARG, "record arrays are NULL");
+  if (n_parents && !e) return set_error(ctx, CUSCI_E_INVALID_ARG, "e is NULL");
+  if (n_space && (!space_keys || !psi)) return set_error(ctx, CUSCI_E_INVALID_ARG, "space arrays are NULL");
+  if (n_space >= (1ull << 32)) return set_error(ctx, CUSCI_E_INVALID_ARG, "n_space must be < 2^32");
+  CUSCI_CUDA(ctx, cudaSetDevice(ctx->device));
+  *n_missing = 0;
+  return sp->words == 1 ? contract_impl<1>(ctx, keys, hij, src, n_rec, n_parents, space_keys, n_space, psi, e, n_missing)
+                        : contract_impl<2>(ctx, keys, hij, src, n_rec, n_parents, space_keys, n_space, psi, e, n_missing);
+}

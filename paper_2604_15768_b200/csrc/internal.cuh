@@ -74,7 +74,7 @@ struct Prep {
 // kernel classes for the optional per-launch event profiler (cusci_profile_*)
 enum ProfTag {
   PT_PREP = 0, PT_VALIDATE, PT_GEN, PT_HASH, PT_SCATTER, PT_RADIX_UP, PT_RADIX_DOWN, PT_SCAN, PT_UNIQUE,
-  PT_MERGE_SPLIT, PT_MERGE_TILE, PT_CHECK, PT_NCCL, PT_MEMSET, PT_COUNT
+  PT_MERGE_SPLIT, PT_MERGE_TILE, PT_CHECK, PT_NCCL, PT_MEMSET, PT_ENERGY, PT_COUNT
 };
 struct ProfRec {
   int tag;

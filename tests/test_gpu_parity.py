@@ -438,3 +438,46 @@ def test_dedup_at_scale_three_passes(P, ctx):
     a = torch.sort(ui ^ flip).values
     b = torch.sort(base ^ flip).values
     assert torch.equal(a, b)
+
+
+# ------------------------------------------------------------------ Stage-3 contraction
+def _contract_case(P, ctx, wl_key, n_par, W, seed, keep_every=1):
+    from oracle import energy
+    wl, ints, par = synth.workload_inputs(wl_key, n_parents=n_par)
+    sp = P.Space(wl.m, wl.n_alpha, wl.n_beta)
+    di = P.DeviceIntegrals(ints.h, ints.eri)
+    rec = ctx.gen_coupled(sp, torch.from_numpy(par).cuda(), di, 0.0, with_src=True)
+    uniq = ctx.dedup_global(sp, rec.keys)[::keep_every].contiguous()
+    rng = np.random.default_rng(seed)
+    psi = rng.uniform(-1.0, 1.0, size=uniq.shape[0])
+    e, miss = ctx.energy_contract(sp, rec, len(par), uniq, torch.from_numpy(psi).cuda())
+    keys = rec.keys[:rec.count].cpu().numpy().reshape(-1, W)
+    ref, rmiss = energy.contract(keys, rec.hij[:rec.count].cpu().numpy(), rec.src[:rec.count].cpu().numpy(),
+                                 len(par), uniq.cpu().numpy().reshape(-1, W), psi, W)
+    assert miss == rmiss
+    assert np.array_equal(e.cpu().numpy(), ref), "e not bit-identical to the oracle"
+    return miss
+
+
+def test_contract_lih(P, ctx):
+    assert _contract_case(P, ctx, "lih", None, 1, 1) == 0
+
+
+def test_contract_h2o_with_missing(P, ctx):
+    assert _contract_case(P, ctx, "h2o", 300, 1, 2) == 0
+    assert _contract_case(P, ctx, "h2o", 300, 1, 3, keep_every=2) > 0
+
+
+def test_contract_c2h4_w2(P, ctx):
+    assert _contract_case(P, ctx, "c2h4", 4, 2, 4, keep_every=3) > 0
+
+
+def test_contract_rejects_large_products(P, ctx):
+    wl, ints, par = synth.workload_inputs("lih")
+    sp = P.Space(wl.m, wl.n_alpha, wl.n_beta)
+    rec = ctx.gen_coupled(sp, torch.from_numpy(par).cuda(), P.DeviceIntegrals(ints.h, ints.eri), 0.0, with_src=True)
+    uniq = ctx.dedup_global(sp, rec.keys)
+    psi = torch.full((uniq.shape[0],), 2.0 ** 30, dtype=torch.float64, device="cuda")
+    with pytest.raises(P.CusciError) as e:
+        ctx.energy_contract(sp, rec, len(par), uniq, psi)
+    assert e.value.code == 1
