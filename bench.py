@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--batch", type=int, default=None, help="parents per gen_coupled call")
     ap.add_argument("--eps", type=float, default=0.0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-stage3", action="store_true", help="skip the Stage-3 contraction measurement (SURVEY 8(f) f1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=None, help="parents in the oracle's bounded sample")
     return ap.parse_args()
@@ -338,6 +339,35 @@ def main():
                "h2d_bytes_per_step": int(shard_pinned.numel() * 8 + ints.h.nbytes * 0),
                "d2h_bytes_per_step": 24, "ms_per_step": ems / args.steps, "clocks": eclk}
 
+    # ---------------- Stage-3 contraction (not part of the headline step):
+    # e[s] = sum_j H_sj psi_j over every batch's records, psi synthetic and
+    # aligned with the unique set C (the upool), reverse index just in time
+    stage3 = None
+    if not args.no_stage3 and world == 1:
+        ukeys = upool.keys()
+        g = torch.Generator(device=dev).manual_seed(11)
+        psi = torch.rand(ukeys.shape[0], dtype=torch.float64, device=dev, generator=g) * 2.0 - 1.0
+        e_all = torch.empty(n_par, dtype=torch.float64, device=dev)
+        s_ms, s_rec, s_miss = 0.0, 0, 0
+        for rep in range(2):  # first pass = warm-up
+            s_ms, s_rec, s_miss = 0.0, 0, 0
+            for (a, b) in batches:
+                rec = ctx.gen_coupled(sp, shard[a:b], di, args.eps, out=out)
+                c0 = torch.cuda.Event(enable_timing=True)
+                c1 = torch.cuda.Event(enable_timing=True)
+                c0.record(stream)
+                _, miss = ctx.energy_contract(sp, rec, b - a, ukeys, psi, e=e_all[a:b])
+                c1.record(stream)
+                torch.cuda.synchronize()
+                s_ms += c0.elapsed_time(c1)
+                s_rec += rec.count
+                s_miss += miss
+        s_bytes = s_rec * (8 * W + 8 + 4 + 8)   # record read + one psi gather per record
+        stage3 = {"records_per_s": s_rec / (s_ms / 1e3), "ms_per_step": s_ms, "records": s_rec, "missing": s_miss,
+                  "space": int(ukeys.shape[0]), "achieved_GBs": s_bytes / (s_ms / 1e3) / 1e9,
+                  "e_checksum": float(e_all.abs().sum().item())}
+        del ukeys, psi, e_all
+
     # ---------------- roofline of the dominant kernel class
     peaks = {}
     try:
@@ -404,6 +434,8 @@ def main():
                "sample": f"{n_sample} parents (first distinct sampler draws) of the workload through oracle gen -> std::set dedup -> "
                          f"set_union merge ({r} records, {u} unique, {dt:.1f} s)"}
 
+    if stage3:
+        stage3["frac"] = stage3["achieved_GBs"] / hbm_peak
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "coupled configs/s", "n_gpus": world, "steps": args.steps,
@@ -421,6 +453,7 @@ def main():
             "gen_kernel": gen_roof,
             "kernel_roofline": kernels,
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])},
+            "stage3_contract": stage3,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),

@@ -6,9 +6,10 @@
 // B200 design (reading r14):
 //   reverse index  the unique set is sorted in the hash order pi (reading
 //                  r13) and pi is uniform, so a table T over the top k bits of
-//                  hi (k = log2(n_space / 4)) brackets every key in ~4 entries:
-//                  one table load + a 2-3 step binary search per record ("just
-//                  in time", nothing materialised per record);
+//                  hi (2^k >= n_space) brackets every key in ~1 entry, stored
+//                  next to its amplitude: per record one table load and ~1
+//                  (key, psi) load ("just in time", nothing materialised per
+//                  record);
 //   reduction      each product p = H * psi (IEEE fp64) is rounded half-to-even
 //                  to the grid 2^-80 and accumulated EXACTLY as a 128-bit
 //                  integer: a warp first sums the runs of equal src among its
@@ -41,6 +42,36 @@ __global__ void rindex_table_kernel(const uint64_t* __restrict__ space, uint64_t
     const int64_t prev = i > 0 ? (int64_t)(k ? (to_pi(load_key<W>(space, i - 1)).w0 >> (64 - k)) : 0ull) : -1;
     for (int64_t b = prev + 1; b <= (int64_t)cur; b++) T[b] = (uint32_t)i;
   }
+}
+
+// (key, psi) side by side: one random sector serves the match and the amplitude
+template <int W> struct KPsi;
+template <> struct __align__(16) KPsi<1> {
+  uint64_t k0;
+  double psi;
+};
+template <> struct __align__(32) KPsi<2> {
+  uint64_t k0, k1;
+  double psi;
+  double pad;
+};
+template <int W>
+__global__ void kpsi_kernel(const uint64_t* __restrict__ space, const double* __restrict__ psi, uint64_t n,
+                            KPsi<W>* __restrict__ kp) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    KPsi<W> r{};
+    const KeyT<W> k = load_key<W>(space, i);
+    r.k0 = k.w0;
+    if constexpr (W == 2) r.k1 = k.w1;
+    r.psi = psi[i];
+    kp[i] = r;
+  }
+}
+template <int W> __device__ __forceinline__ bool kp_eq(const KPsi<W>& r, const KeyT<W>& k);
+template <> __device__ __forceinline__ bool kp_eq<1>(const KPsi<1>& r, const KeyT<1>& k) { return r.k0 == k.w0; }
+template <> __device__ __forceinline__ bool kp_eq<2>(const KPsi<2>& r, const KeyT<2>& k) {
+  return r.k0 == k.w0 && r.k1 == k.w1;
 }
 
 // p -> round_half_even(p * 2^80) for |p| < 2^20 (exact integer arithmetic)
@@ -91,62 +122,90 @@ __device__ __forceinline__ double int128_to_double_rn(__int128 x) {
 template <int W>
 __global__ void __launch_bounds__(kET) contract_kernel(const uint64_t* __restrict__ keys, const double* __restrict__ hij,
                                                       const uint32_t* __restrict__ src, uint64_t n_rec,
-                                                      const uint64_t* __restrict__ space, uint64_t n_space,
-                                                      const double* __restrict__ psi, const uint32_t* __restrict__ T,
+                                                      const KPsi<W>* __restrict__ kp, const uint32_t* __restrict__ T,
                                                       int k, unsigned long long* __restrict__ acc,
                                                       unsigned long long* __restrict__ flags) {
   const unsigned lane = lane_id();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   uint64_t missing = 0;
   bool big = false;
-  // warp-uniform trip count so the warp-level reduction always has all lanes
-  const uint64_t base0 = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
-  for (uint64_t w0 = base0; w0 < n_rec; w0 += stride) {
-    const uint64_t r = w0 + lane;
-    const bool valid = r < n_rec;
-    uint32_t s = 0xffffffffu;
-    __int128 q = 0;
-    if (valid) {
-      s = src[r];
-      const KeyT<W> key = load_key<W>(keys, r);
-      const KeyT<W> p = to_pi(key);
-      const uint64_t b = k ? (p.w0 >> (64 - k)) : 0ull;
-      uint64_t lo = T[b], hi = T[b + 1];
-      while (lo < hi) {  // first index with pi >= p
-        const uint64_t mid = (lo + hi) >> 1;
-        if (pi_less<W>(to_pi(load_key<W>(space, mid)), p)) lo = mid + 1;
-        else hi = mid;
-      }
-      if (lo < n_space && key_eq(load_key<W>(space, lo), key)) {
-        const double prod = __dmul_rn(hij[r], psi[lo]);
-        if (!(fabs(prod) < 1048576.0)) big = true;
-        else q = quantize80(prod);
-      } else {
-        missing++;
+  // warp-uniform trip count so the warp-level reduction always has all lanes;
+  // kU consecutive 32-record groups per step: their lookups are in flight together
+  constexpr int kU = 4;
+  const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = stride >> 5;
+  for (uint64_t w0 = wid * 32 * kU; w0 < n_rec; w0 += nw * 32 * kU) {
+    uint32_t sv[kU];
+    KeyT<W> kv[kU];
+    uint32_t lo[kU], hi[kU];
+    double hv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; u++) {
+      const uint64_t r = w0 + u * 32 + lane;
+      sv[u] = 0xffffffffu;
+      lo[u] = hi[u] = 0;
+      if (r < n_rec) {
+        sv[u] = src[r];
+        hv[u] = hij[r];
+        kv[u] = load_key<W>(keys, r);
+        // bucket of the key's hi; the table has ~1 key per bucket
+        const uint64_t b = k ? (to_pi(kv[u]).w0 >> (64 - k)) : 0ull;
+        lo[u] = T[b];
+        hi[u] = T[b + 1];
       }
     }
-    // segmented inclusive sum over runs of equal src (lanes in record order)
-    const uint32_t sprev = __shfl_up_sync(kFull, s, 1);
-    const unsigned heads = __ballot_sync(kFull, lane == 0 || sprev != s);
-    const int start = 31 - __clz(heads & ((2u << lane) - 1u));  // head of this lane's run
-    __int128 acc128 = q;
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long ql = __shfl_up_sync(kFull, (unsigned long long)acc128, o);
-      const unsigned long long qh = __shfl_up_sync(kFull, (unsigned long long)((unsigned __int128)acc128 >> 64), o);
-      if ((int)lane - o >= start) acc128 += (__int128)(((unsigned __int128)qh << 64) | ql);
+    __int128 qv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; u++) {
+      qv[u] = 0;
+      const uint64_t r = w0 + u * 32 + lane;
+      if (r < n_rec) {
+        bool found = false;
+        double ps = 0.0;
+        for (uint32_t i = lo[u]; i < hi[u]; i++) {
+          const KPsi<W> e = kp[i];
+          if (kp_eq<W>(e, kv[u])) {
+            found = true;
+            ps = e.psi;
+            break;
+          }
+        }
+        if (found) {
+          const double prod = __dmul_rn(hv[u], ps);
+          if (!(fabs(prod) < 1048576.0)) big = true;
+          else qv[u] = quantize80(prod);
+        } else {
+          missing++;
+        }
+      }
     }
-    // the last lane of each run adds the run total to the parent's limbs
-    const uint32_t snext = __shfl_down_sync(kFull, s, 1);
-    const bool tail = valid && (lane == 31 || snext != s || !(w0 + lane + 1 < n_rec));
-    if (tail && acc128 != 0) {
-      const unsigned __int128 u = (unsigned __int128)acc128;
-      const long long l0 = (long long)(uint32_t)(u), l1 = (long long)(uint32_t)(u >> 32),
-                      l2 = (long long)(uint32_t)(u >> 64), l3 = (long long)(int32_t)(uint32_t)(u >> 96);
-      unsigned long long* a4 = acc + 4ull * s;
-      atomicAdd(a4 + 0, (unsigned long long)l0);
-      atomicAdd(a4 + 1, (unsigned long long)l1);
-      atomicAdd(a4 + 2, (unsigned long long)l2);
-      atomicAdd(a4 + 3, (unsigned long long)l3);
+#pragma unroll
+    for (int u = 0; u < kU; u++) {
+      const uint32_t s = sv[u];
+      const bool valid = w0 + u * 32 + lane < n_rec;
+      // segmented inclusive sum over runs of equal src (lanes in record order)
+      const uint32_t sprev = __shfl_up_sync(kFull, s, 1);
+      const unsigned heads = __ballot_sync(kFull, lane == 0 || sprev != s);
+      const int start = 31 - __clz(heads & ((2u << lane) - 1u));  // head of this lane's run
+      __int128 acc128 = qv[u];
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long ql = __shfl_up_sync(kFull, (unsigned long long)acc128, o);
+        const unsigned long long qh = __shfl_up_sync(kFull, (unsigned long long)((unsigned __int128)acc128 >> 64), o);
+        if ((int)lane - o >= start) acc128 += (__int128)(((unsigned __int128)qh << 64) | ql);
+      }
+      // the last lane of each run adds the run total to the parent's limbs
+      const uint32_t snext = __shfl_down_sync(kFull, s, 1);
+      const bool tail = valid && (lane == 31 || snext != s);
+      if (tail && acc128 != 0) {
+        const unsigned __int128 uu = (unsigned __int128)acc128;
+        const long long l0 = (long long)(uint32_t)(uu), l1 = (long long)(uint32_t)(uu >> 32),
+                        l2 = (long long)(uint32_t)(uu >> 64), l3 = (long long)(int32_t)(uint32_t)(uu >> 96);
+        unsigned long long* a4 = acc + 4ull * s;
+        atomicAdd(a4 + 0, (unsigned long long)l0);
+        atomicAdd(a4 + 1, (unsigned long long)l1);
+        atomicAdd(a4 + 2, (unsigned long long)l2);
+        atomicAdd(a4 + 3, (unsigned long long)l3);
+      }
     }
   }
   for (int o = 16; o; o >>= 1) missing += __shfl_xor_sync(kFull, missing, o);
@@ -169,20 +228,24 @@ int contract_impl(cusci_ctx* ctx, const uint64_t* keys, const double* hij, const
                   uint64_t n_parents, const uint64_t* space, uint64_t n_space, const double* psi, double* e,
                   uint64_t* n_missing) {
   Scratch s(ctx);
+  // ~1 key per bucket of the reverse-index table (uniform hi)
   int k = 0;
-  while ((n_space >> k) > 4 && k < 26) k++;
+  while ((1ull << k) < n_space && k < 30) k++;
   uint32_t* T;
+  KPsi<W>* kp;
   unsigned long long *acc, *flags;
   CUSCI_TRY(s.get_t(((size_t)1 << k) + 1, &T));
+  CUSCI_TRY(s.get_t(std::max<uint64_t>(n_space, 1), &kp));
   CUSCI_TRY(s.get_t(std::max<uint64_t>(4 * n_parents, 1), &acc));
   CUSCI_TRY(s.get_t(2, &flags));
   CUSCI_CUDA(ctx, cudaMemsetAsync(acc, 0, std::max<uint64_t>(4 * n_parents, 1) * 8, ctx->stream));
   CUSCI_CUDA(ctx, cudaMemsetAsync(flags, 0, 16, ctx->stream));
   const unsigned g1 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_space + kET) / kET, (uint64_t)ctx->num_sms * 8));
   CUSCI_LAUNCH(ctx, PT_ENERGY, rindex_table_kernel<W><<<g1, kET, 0, ctx->stream>>>(space, n_space, k, T));
+  if (n_space) CUSCI_LAUNCH(ctx, PT_ENERGY, kpsi_kernel<W><<<g1, kET, 0, ctx->stream>>>(space, psi, n_space, kp));
   if (n_rec) {
     const unsigned g2 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_rec + kET - 1) / kET, (uint64_t)ctx->num_sms * 16));
-    CUSCI_LAUNCH(ctx, PT_ENERGY, contract_kernel<W><<<g2, kET, 0, ctx->stream>>>(keys, hij, src, n_rec, space, n_space, psi, T, k, acc, flags));
+    CUSCI_LAUNCH(ctx, PT_ENERGY, contract_kernel<W><<<g2, kET, 0, ctx->stream>>>(keys, hij, src, n_rec, kp, T, k, acc, flags));
   }
   uint64_t h[2];
   CUSCI_TRY(read_u64(ctx, reinterpret_cast<const uint64_t*>(flags), h, 2));
