@@ -427,7 +427,7 @@ __device__ __forceinline__ uint32_t do_pairs(const GenArgs& a, const KeyT<W>& pa
 }
 
 template <int W, int MODE>
-__global__ void __launch_bounds__(kGenThreads, 3) gen_kernel(const GenArgs a) {
+__global__ void __launch_bounds__(kGenThreads, 4) gen_kernel(const GenArgs a) {
   extern __shared__ __align__(16) unsigned char gsm[];
   __shared__ uint8_t occ_s[kGenWarps][128];
   __shared__ RowInfo<W> ri_s[kGenWarps][kRowBatch + 1];   // pair-row descriptors of the current batch
