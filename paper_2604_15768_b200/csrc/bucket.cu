@@ -361,14 +361,14 @@ __device__ __forceinline__ bool otab_insert(KeyT<2>* tab, uint32_t* bm, uint32_t
 // the table.  The survivors are mapped back to keys (exact inverse mix) and
 // written at the bucket's input offset; the pack kernel then concatenates
 // the buckets.
-constexpr int kBU = 512;  // dedup threads (2 CTAs / SM share the shared-memory budget)
+constexpr int kBU = 1024;  // dedup threads (one CTA per SM owns the shared-memory budget)
 constexpr int kILP = 4;   // keys per thread with first probes in flight together
 template <int W> struct BUCfg {
-  static constexpr uint32_t TS = W == 1 ? 8192 : 4096;   // max home slots (64 KB)
-  static constexpr uint32_t OV = W == 1 ? 512 : 256;     // overflow tail
-  static constexpr uint32_t BUFK = W == 1 ? 2304 : 1152; // keys per TMA piece (18 KB)
+  static constexpr uint32_t TS = W == 1 ? 16384 : 8192;  // max home slots (128 KB)
+  static constexpr uint32_t OV = W == 1 ? 1024 : 512;    // overflow tail
+  static constexpr uint32_t BUFK = W == 1 ? 4608 : 2304; // keys per TMA piece (36 KB)
   static constexpr uint32_t BUFE = BUFK + 2;             // + alignment slack (W = 1)
-  static constexpr uint32_t DT = W == 1 ? 3072 : 1536;   // target distinct keys per bucket
+  static constexpr uint32_t DT = W == 1 ? 6144 : 3072;   // target distinct keys per bucket
   static constexpr uint32_t NWD = (TS + OV) / 32;        // bitmap words
   static constexpr uint32_t WPT = (NWD + kBU - 1) / kBU; // bitmap words per thread
   static constexpr size_t SMEM = (size_t)(TS + OV) * sizeof(KeyT<W>) + 2 * (size_t)BUFE * sizeof(KeyT<W>);
@@ -376,7 +376,7 @@ template <int W> struct BUCfg {
 };
 
 template <int W>
-__global__ void __launch_bounds__(kBU, 2) bucket_unique_kernel(const uint64_t* __restrict__ part, int raw, int use_tma,
+__global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* __restrict__ part, int raw, int use_tma,
                                                               const uint32_t* __restrict__ off, uint32_t nb, int B,
                                                               uint32_t lf, uint32_t dcap, uint64_t* __restrict__ tmp,
                                                               uint32_t* __restrict__ surv,

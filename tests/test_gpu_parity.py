@@ -411,33 +411,53 @@ def _t_fmix64(x):
     return x ^ srl(x, 31)
 
 
-def test_dedup_at_scale_three_passes(P, ctx):
+_AT_SCALE = r"""
+import sys, torch
+sys.path.insert(0, %r)
+import paper_2604_15768_b200 as P
+from tests.test_gpu_parity import _t_fmix64
+ctx = P.Context(0)
+D, R = 660_000_000, 100_000_000
+C = 0x9E3779B97F4A7C15 - (1 << 64)          # odd: i -> i * C is a bijection of Z/2^64
+base = torch.arange(1, D + 1, dtype=torch.int64, device="cuda") * C
+g = torch.Generator(device="cuda").manual_seed(7)
+rep = base[torch.randint(0, D, (R,), device="cuda", generator=g)]
+keys = torch.cat([base, rep])
+del rep
+keys = keys[torch.randperm(keys.numel(), device="cuda", generator=g)]
+ctx.dedup_stats(reset=True)
+u = ctx.dedup_global(P.Space(64, 1, 1), keys.view(torch.uint64).reshape(-1, 1))
+st = ctx.dedup_stats(reset=True)
+del keys
+assert u.shape[0] == D
+assert st["key_passes"] == %d * (D + R) and st["slow_path_calls"] == 0, st
+ui = u.view(torch.int64).reshape(-1)
+flip = -(1 << 63)
+hi = _t_fmix64(ui) ^ flip                      # signed order of hi ^ 2^63 = unsigned order of hi
+assert bool((hi[1:] > hi[:-1]).all()), "not strictly in hash order"
+del hi
+assert torch.equal(torch.sort(ui ^ flip).values, torch.sort(base ^ flip).values)
+print("OK")
+"""
+
+
+@pytest.mark.parametrize("distinct_target,passes", [(None, 2), ("1536", 3)])
+def test_dedup_at_scale(distinct_target, passes):
     """0.76e9 keys (0.66e9 distinct, 1e8 repeated), shuffled: exercises the
-    HyperLogLog plan with two further partition passes (B = 18 bucket bits).
+    HyperLogLog plan with one further partition pass (default bucket target)
+    and with two (a smaller distinct-per-bucket target via the tuning knob).
     Too large for the oracle: checked by the exact distinct count, strict hash
     order and set equality with the generating set (torch sort on the GPU)."""
-    D, R = 660_000_000, 100_000_000
-    C = 0x9E3779B97F4A7C15 - (1 << 64)          # odd: i -> i * C is a bijection of Z/2^64
-    base = torch.arange(1, D + 1, dtype=torch.int64, device="cuda") * C
-    g = torch.Generator(device="cuda").manual_seed(7)
-    rep = base[torch.randint(0, D, (R,), device="cuda", generator=g)]
-    keys = torch.cat([base, rep])
-    del rep
-    keys = keys[torch.randperm(keys.numel(), device="cuda", generator=g)]
-    ctx.dedup_stats(reset=True)
-    u = ctx.dedup_global(P.Space(64, 1, 1), keys.view(torch.uint64).reshape(-1, 1))
-    st = ctx.dedup_stats(reset=True)
-    del keys
-    assert u.shape[0] == D
-    assert st["key_passes"] == 3 * (D + R) and st["slow_path_calls"] == 0, st
-    ui = u.view(torch.int64).reshape(-1)
-    flip = -(1 << 63)
-    hi = _t_fmix64(ui) ^ flip                      # signed order of hi ^ 2^63 = unsigned order of hi
-    assert bool((hi[1:] > hi[:-1]).all()), "not strictly in hash order"
-    del hi
-    a = torch.sort(ui ^ flip).values
-    b = torch.sort(base ^ flip).values
-    assert torch.equal(a, b)
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    if distinct_target:
+        env["CUSCI_BUCKET_DISTINCT"] = distinct_target
+    r = subprocess.run([sys.executable, "-c", _AT_SCALE % (root, passes)], env=env, capture_output=True, text=True,
+                       timeout=900, cwd=root)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
 
 
 # ------------------------------------------------------------------ Stage-3 contraction (SURVEY 8(f) f1)
