@@ -226,11 +226,15 @@ __global__ void __launch_bounds__(kST, 2) tile_scatter_kernel(const uint64_t* __
     }
     KeyT<W> k[ITEMS];
     uint32_t dr[ITEMS];  // digit << 16 | rank within the sub-round
+    // keys [c0, c1) of the sub-round are in the TMA core (W = 1: an odd head /
+    // tail key is read from global); key i sits at buf[i + c0]
+    const uint32_t c0 = (W == 1 && tma) ? (uint32_t)((t.start + r0) & 1u) : 0u;
+    const uint32_t c1 = !tma ? 0u : (W == 1 ? m - (uint32_t)((t.start + r0 + m) & 1u) : m);
 #pragma unroll
     for (int u = 0; u < ITEMS; u++) {
       const uint32_t i = u * kST + threadIdx.x;
       if (i < m) {
-        k[u] = scatter_key<W>(in, t.start + r0, i, m, buf, tma);
+        k[u] = (i >= c0 && i < c1) ? buf[i + c0] : load_key<W>(in, t.start + r0 + i);
         if (RAW) k[u] = to_pi(k[u]);
         const uint32_t d = top_bits<W>(k[u], bsel) & dmask;
         dr[u] = (d << 16) | atomicAdd(&cnt[d], 1u);
