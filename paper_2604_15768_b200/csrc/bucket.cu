@@ -782,7 +782,9 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
       CUSCI_CUDA(ctx, cudaMemcpy(reg.data(), hll, kHllM * sizeof(uint32_t), cudaMemcpyDeviceToHost));
       const double D = std::min<double>((double)n, std::max(1.0, kHllSample * hll_estimate(reg.data())));
       int Bd = 0;
-      while (D / std::ldexp(1.0, Bd) > (double)dt && Bd < 22) Bd++;
+      // up to 1.25 x the target per bucket before adding a bit (the sketch's
+      // noise must not flip a stream near the boundary into a wider pass)
+      while (D / std::ldexp(1.0, Bd) > 1.25 * (double)dt && Bd < 22) Bd++;
       // one bit less when that saves a whole partition pass and the buckets stay
       // within 1.6 x the target (table load <= ~0.6)
       auto npass = [&](int b) { return (std::max(0, b - bits1) + max_bits - 1) / max_bits; };

@@ -362,6 +362,79 @@ __global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(const uint64_
   }
 }
 
+// ---------------------------------------------------------------- sparse merge
+// |small| << |big| (e.g. S <- S u C with a few parents into a large unique set):
+// every small key finds its slot in the big run by binary search, the
+// non-duplicates are ranked by one scan, and the big run is copied with the
+// shift "non-duplicate small keys at or before me" (constant between insert
+// points) -- copy-speed traffic instead of a full merge.
+template <int W>
+__global__ void sparse_locate_kernel(const uint64_t* __restrict__ small, uint64_t ns, const uint64_t* __restrict__ big,
+                                     uint64_t nb, uint64_t* __restrict__ pos, uint32_t* __restrict__ keep) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += stride) {
+    const KeyT<W> x = load_key<W>(small, i);
+    uint64_t lo = 0, hi = nb;
+    while (lo < hi) {  // first big key >= x (hash order)
+      const uint64_t mid = (lo + hi) >> 1;
+      if (hk_lt<W>(load_key<W>(big, mid), x)) lo = mid + 1;
+      else hi = mid;
+    }
+    pos[i] = lo;
+    keep[i] = (lo < nb && key_eq(load_key<W>(big, lo), x)) ? 0u : 1u;
+  }
+}
+
+// big[j] -> out[j + shift(j)], shift(j) = rank[upper_bound(pos, j)]
+// (rank = exclusive scan of keep, rank[ns] = total inserts)
+template <int W>
+__global__ void sparse_copy_kernel(const uint64_t* __restrict__ big, uint64_t nb, const uint64_t* __restrict__ pos,
+                                   const uint64_t* __restrict__ rank, uint64_t ns, uint64_t* __restrict__ out) {
+  constexpr uint32_t CH = 4096;  // big keys per CTA chunk
+  __shared__ uint64_t s_u0, s_u1;
+  for (uint64_t j0 = (uint64_t)blockIdx.x * CH; j0 < nb; j0 += (uint64_t)gridDim.x * CH) {
+    const uint64_t j1 = min(nb, j0 + CH);
+    if (threadIdx.x < 2) {  // inserts with pos in (j0 - 1, j1 - 1]: indices [u0, u1)
+      const uint64_t v = threadIdx.x == 0 ? j0 : j1;  // upper_bound(pos, v - 1) = first pos >= v
+      uint64_t lo = 0, hi = ns;
+      while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (pos[mid] < v) lo = mid + 1;
+        else hi = mid;
+      }
+      if (threadIdx.x == 0) s_u0 = lo;
+      else s_u1 = lo;
+    }
+    __syncthreads();
+    // note: an insert with pos == j is placed before big[j], so big[j]'s shift
+    // counts inserts with pos <= j: rank at the first pos > j
+    const uint64_t u0 = s_u0, u1 = s_u1;
+    for (uint64_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+      uint64_t lo = u0, hi = u1;  // first index in [u0, u1) with pos > j (few candidates)
+      while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (pos[mid] <= j) lo = mid + 1;
+        else hi = mid;
+      }
+      store_key<W>(out, j + rank[lo], load_key<W>(big, j));
+    }
+    __syncthreads();
+  }
+}
+
+template <int W>
+__global__ void sparse_place_kernel(const uint64_t* __restrict__ small, uint64_t ns, const uint64_t* __restrict__ pos,
+                                    const uint32_t* __restrict__ keep, const uint64_t* __restrict__ rank,
+                                    uint64_t* __restrict__ out, uint64_t* __restrict__ ins) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += stride) {
+    if (!keep[i]) continue;
+    const KeyT<W> x = load_key<W>(small, i);
+    store_key<W>(out, pos[i] + rank[i], x);
+    if (ins) store_key<W>(ins, rank[i], x);
+  }
+}
+
 template <int W>
 int merge_impl(cusci_ctx* ctx, cusci_pool* pool, const uint64_t* U, uint64_t nU, cusci_keys* inserted) {
   const uint64_t nS = pool->count;
@@ -428,6 +501,44 @@ int merge_impl(cusci_ctx* ctx, cusci_pool* pool, const uint64_t* U, uint64_t nU,
     CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     h[0] = nU;
     h[1] = nU;
+    if (*(int*)((char*)ctx->host_pinned + 16)) {
+      for (int b = 0; b < 2; b++)
+        if (grown[b]) cudaFreeAsync(grown[b], ctx->stream);
+      if (insp) out_free(ctx, insp);
+      return set_error(ctx, CUSCI_E_INVALID_ARG, "merge_space: new_keys must be sorted in the pool (hash) order and unique");
+    }
+  } else if (nU * 64 <= nS || (nS * 64 <= nU && !inserted)) {
+    // sparse: the small run's keys are located in the big run and inserted while
+    // the big run is copied.  U small: inserted = the kept U keys, in order; S
+    // small (only without `inserted`): |inserted| = nU - (duplicates).
+    const bool u_small = nU * 64 <= nS;
+    const uint64_t* small = u_small ? U : S;
+    const uint64_t* big = u_small ? S : U;
+    const uint64_t nsm = u_small ? nU : nS, nbg = u_small ? nS : nU;
+    const unsigned cu = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nU + 255) / 256, (uint64_t)ctx->num_sms * 8));
+    CUSCI_LAUNCH(ctx, PT_CHECK, check_sorted_kernel<W><<<cu, 256, 0, ctx->stream>>>(U, nU, bad));
+    const unsigned cg = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nsm + 255) / 256, (uint64_t)ctx->num_sms * 8));
+    uint64_t *pos, *keep64, *rank;
+    uint32_t* keep;
+    CUSCI_TRY(s.get_t(nsm, &pos));
+    CUSCI_TRY(s.get_t(nsm, &keep));
+    CUSCI_TRY(s.get_t(nsm + 1, &keep64));
+    CUSCI_TRY(s.get_t(nsm + 1, &rank));
+    CUSCI_LAUNCH(ctx, PT_MERGE_SPLIT, sparse_locate_kernel<W><<<cg, 256, 0, ctx->stream>>>(small, nsm, big, nbg, pos, keep));
+    CUSCI_CUDA(ctx, cudaMemsetAsync(keep64, 0, (nsm + 1) * sizeof(uint64_t), ctx->stream));
+    CUSCI_CUDA(ctx, cudaMemcpy2DAsync(keep64, sizeof(uint64_t), keep, sizeof(uint32_t), sizeof(uint32_t), nsm,
+                                      cudaMemcpyDeviceToDevice, ctx->stream));
+    CUSCI_TRY(scan_exclusive_u64(ctx, keep64, rank, nsm + 1, nullptr));
+    const unsigned bg = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nbg + 4095) / 4096, (uint64_t)ctx->num_sms * 8));
+    CUSCI_LAUNCH(ctx, PT_MERGE_TILE, sparse_copy_kernel<W><<<bg, 256, 0, ctx->stream>>>(big, nbg, pos, rank, nsm, dst));
+    CUSCI_LAUNCH(ctx, PT_MERGE_TILE, sparse_place_kernel<W><<<cg, 256, 0, ctx->stream>>>(small, nsm, pos, keep, rank, dst, u_small ? (uint64_t*)insp : nullptr));
+    CUSCI_CUDA(ctx, cudaMemcpyAsync(ctx->host_pinned, rank + nsm, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CUSCI_CUDA(ctx, cudaMemcpyAsync((char*)ctx->host_pinned + 16, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    uint64_t nin;
+    memcpy(&nin, ctx->host_pinned, sizeof(uint64_t));
+    h[0] = nbg + nin;
+    h[1] = u_small ? nin : nU - (nS - nin);
     if (*(int*)((char*)ctx->host_pinned + 16)) {
       for (int b = 0; b < 2; b++)
         if (grown[b]) cudaFreeAsync(grown[b], ctx->stream);

@@ -325,6 +325,38 @@ def test_merge_into_empty_pool(P, ctx, W):
     pool.close()
 
 
+@pytest.mark.parametrize("W", [1, 2])
+def test_merge_sparse_paths(P, ctx, W):
+    """|U| << |S| (with inserted) and |S| << |U| (without): the sparse merge
+    (locate + shifted copy) must equal the set algebra."""
+    rng = np.random.default_rng(60 + W)
+    sp = P.Space(64 * W, 1, 1)
+    big = synth.unique_keys(rng.integers(1, 1 << 40, size=(400_000, W), dtype=np.uint64))
+    small = synth.unique_keys(np.concatenate([big[rng.choice(len(big), 2000, replace=False)],
+                                              rng.integers(1, 1 << 40, size=(3000, W), dtype=np.uint64)]))
+    # U small into a big pool, inserted requested
+    pool = ctx.pool(sp, 16)
+    ctx.merge_space(pool, torch.from_numpy(hash_sort(big, W)).cuda())
+    ins = ctx.merge_space(pool, torch.from_numpy(hash_sort(small, W)).cuda(), want_inserted=True).cpu().numpy()
+    ref_s, ref_ins = oracle.merge(big, small, W)
+    after = pool.keys().cpu().numpy()
+    assert_hash_sorted_unique(after, W)
+    assert np.array_equal(synth.sort_keys(after), ref_s) and np.array_equal(synth.sort_keys(ins), ref_ins)
+    assert_hash_sorted_unique(ins, W)
+    # S small, U big, no inserted
+    pool.clear()
+    ctx.merge_space(pool, torch.from_numpy(hash_sort(small, W)).cuda())
+    ctx.merge_space(pool, torch.from_numpy(hash_sort(big, W)).cuda())
+    after = pool.keys().cpu().numpy()
+    assert_hash_sorted_unique(after, W)
+    assert np.array_equal(synth.sort_keys(after), oracle.merge(small, big, W)[0])
+    # unsorted small U is rejected
+    with pytest.raises(P.CusciError) as e:
+        ctx.merge_space(pool, torch.from_numpy(hash_sort(small, W)[::-1].copy()).cuda())
+    assert e.value.code == 1
+    pool.close()
+
+
 def test_pipeline_lih_merge_inserts_nothing(P, ctx):
     wl, ints, par = synth.workload_inputs("lih")
     sp = P.Space(12, 2, 2)
