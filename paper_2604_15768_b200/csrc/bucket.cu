@@ -392,7 +392,8 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
   extern __shared__ __align__(16) unsigned char bsm[];
   K* tab = reinterpret_cast<K*>(bsm);
   K* bufs = tab + TS + OV;
-  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ __align__(8) uint64_t bar[2];   // buffer full (TMA transaction count)
+  __shared__ __align__(8) uint64_t ebar[2];  // buffer empty (one arrival per warp)
   __shared__ int s_zero, s_full;
   __shared__ uint32_t wcnt[NW];
   __shared__ uint32_t bm[C::NWD];  // slot occupancy bitmap (set on insert, cleared by pass 2)
@@ -409,16 +410,23 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
     s_full = 0;
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
+    mbar_init(&ebar[0], NW);
+    mbar_init(&ebar[1], NW);
     mbar_init_fence();
   }
   __syncthreads();
-  // producer state (thread 0): the next piece to issue = (pb, pp)
-  uint32_t pb = bA, pp = 0, pk = 0;
+  // producer state (thread 0): the next piece to issue = (pb, pp); a buffer is
+  // refilled once every warp has released the piece it held (no CTA barrier)
+  uint32_t pb = bA, pp = 0, pk = 0, epar = 0;
   auto issue_next = [&]() {
     while (pb < bB) {
       const uint32_t ps = off[pb], pn = off[pb + 1] - ps;
       if (pp < pn) {
         const uint32_t len = min(BUFK, pn - pp);
+        if (pk >= 2) {  // wait for the release of piece pk - 2 (same buffer)
+          mbar_wait(&ebar[pk & 1], (epar >> (pk & 1)) & 1u);
+          epar ^= 1u << (pk & 1);
+        }
         fence_proxy_async_smem();
         issue_core<W>(part, (uint64_t)ps + pp, len, bufs + (pk & 1) * BUFE, &bar[pk & 1]);
         pp += BUFK;
@@ -489,7 +497,9 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
           if (act[u] && !key_eq(cv[u], pv[u])) full |= !otab_insert(tab, bm, hm[u], span, pv[u]);
       }
       if (full) s_full = 1;
-      __syncthreads();  // piece consumed (the last one: table complete)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ebar[cb]);  // this warp is done with the buffer
+      if (p0 + BUFK >= nk) __syncthreads();   // last piece of the bucket: table complete
     }
     const uint32_t z = (uint32_t)s_zero;
     if (s_full) {
