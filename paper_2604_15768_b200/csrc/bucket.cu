@@ -381,7 +381,7 @@ template <int W> struct BUCfg {
 
 template <int W>
 __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* __restrict__ part, int raw, int use_tma,
-                                                              const uint32_t* __restrict__ off, uint32_t nb, int B,
+                                                              const uint32_t* __restrict__ off, uint32_t nb, int B, int V,
                                                               uint32_t lf, uint32_t dcap, uint64_t* __restrict__ tmp,
                                                               uint32_t* __restrict__ surv,
                                                               unsigned long long* __restrict__ flags) {
@@ -400,8 +400,12 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5, t = threadIdx.x;
   // TMA needs 16-byte aligned sources; raw (caller) input is read with plain loads
   const bool tma = use_tma && !raw && ((reinterpret_cast<uintptr_t>(part) & 15u) == 0);
-  const uint32_t bA = (uint32_t)((uint64_t)nb * blockIdx.x / gridDim.x);
-  const uint32_t bB = (uint32_t)((uint64_t)nb * (blockIdx.x + 1) / gridDim.x);
+  // work unit = sub-bucket sb: bucket sb >> V, keeping only the keys whose next
+  // V bits of hi equal sb's low V bits (V = 1 halves the table load; the second
+  // read of the bucket comes from L2)
+  const uint32_t nsb = nb << V;
+  const uint32_t bA = (uint32_t)((uint64_t)nsb * blockIdx.x / gridDim.x);
+  const uint32_t bB = (uint32_t)((uint64_t)nsb * (blockIdx.x + 1) / gridDim.x);
   // the table is cleared once here and kept clean: the compaction zeroes every slot it reads
   for (uint32_t i = t; i < TS + OV; i += kBU) tab[i] = K{};
   for (uint32_t i = t; i < C::NWD; i += kBU) bm[i] = 0;
@@ -420,7 +424,7 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
   uint32_t pb = bA, pp = 0, pk = 0, epar = 0;
   auto issue_next = [&]() {
     while (pb < bB) {
-      const uint32_t ps = off[pb], pn = off[pb + 1] - ps;
+      const uint32_t ps = off[pb >> V], pn = off[(pb >> V) + 1] - ps;
       if (pp < pn) {
         const uint32_t len = min(BUFK, pn - pp);
         if (pk >= 2) {  // wait for the release of piece pk - 2 (same buffer)
@@ -440,7 +444,8 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
   if (tma && t == 0) issue_next();
   uint32_t phase = 0, k = 0;  // consumer: piece counter, barrier parities
   for (uint32_t b = bA; b < bB; b++) {
-    const uint32_t s = off[b], nk = off[b + 1] - s;
+    const uint32_t s = off[b >> V], nk = off[(b >> V) + 1] - s;
+    const uint64_t vpart = (uint64_t)(b & ((1u << V) - 1u));
     if (nk == 0) {
       if (t == 0) surv[b] = 0;
       continue;
@@ -479,7 +484,8 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
             else if (W == 2 || (i >= c0 && i < c1)) pv[u] = buf[i + c0];  // TMA core (key s+p0+i at buf[i + lead])
             else pv[u] = load_key<W>(part, (uint64_t)s + p0 + i);
             if (raw) pv[u] = to_pi(pv[u]);
-            if (kzero(pv[u])) {
+            if (V && ((pv[u].w0 << B) >> (64 - V)) != vpart) act[u] = false;  // the other half
+            else if (kzero(pv[u])) {
               s_zero = 1;
               act[u] = false;
             }
@@ -488,7 +494,7 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
 #pragma unroll
         for (int u = 0; u < kILP; u++) {
           if (act[u]) {
-            hm[u] = (uint32_t)__umul64hi(pv[u].w0 << B, (uint64_t)ts);
+            hm[u] = (uint32_t)__umul64hi(pv[u].w0 << (B + V), (uint64_t)ts);
             cv[u] = tab[hm[u]];
           }
         }
@@ -503,16 +509,30 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
     }
     const uint32_t z = (uint32_t)s_zero;
     if (s_full) {
-      // table overflow (pathological bucket): pass the keys through unfiltered
-      // (the host finishes with a full sort + unique); restore a clean table
+      // table overflow (pathological bucket): pass this (sub-)bucket's keys
+      // through unfiltered (the host finishes with a full sort + unique);
+      // restore a clean table.  Part 0 fills its bucket region from the front,
+      // part 1 from the back.
+      auto mine = [&](const K& kk) { return !V || (((raw ? to_pi(kk) : kk).w0 << B) >> (64 - V)) == vpart; };
+      if (t == 0) wcnt[0] = 0;
+      __syncthreads();
+      uint32_t cnt = 0;
+      for (uint32_t i = t; i < nk; i += kBU) cnt += mine(load_key<W>(part, (uint64_t)s + i));
+      atomicAdd(&wcnt[0], cnt);
+      __syncthreads();
+      const uint32_t nh = wcnt[0];
+      __syncthreads();
+      if (t == 0) wcnt[0] = 0;
+      __syncthreads();
+      const uint64_t ob = vpart ? (uint64_t)s + nk - nh : (uint64_t)s;
       for (uint32_t i = t; i < nk; i += kBU) {
         const K p = load_key<W>(part, (uint64_t)s + i);
-        store_key<W>(tmp, (uint64_t)s + i, raw ? p : from_pi(p));
+        if (mine(p)) store_key<W>(tmp, ob + atomicAdd(&wcnt[0], 1u), raw ? p : from_pi(p));
       }
       for (uint32_t i = t; i < span; i += kBU) tab[i] = K{};
       for (uint32_t i = t; i < C::NWD; i += kBU) bm[i] = 0;
       if (t == 0) {
-        surv[b] = nk;
+        surv[b] = nh;
         atomicAdd(&flags[0], 1ull);
       }
       __syncthreads();
@@ -590,11 +610,13 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
       }
       bm[w] = 0;
     }
-    if (z && t == 0) store_key<W>(tmp, (uint64_t)s, from_pi(K{}));
+    // output region: part 0 from the bucket region's front, part 1 from its back
+    const uint64_t ob = vpart ? (uint64_t)s + nk - (tot + z) : (uint64_t)s;
+    if (z && t == 0) store_key<W>(tmp, ob, from_pi(K{}));
     __syncthreads();  // slot list complete
     for (uint32_t i = t; i < tot; i += kBU) {
       const uint32_t u = sidx[i];
-      store_key<W>(tmp, (uint64_t)s + z + i, from_pi(tab[u]));
+      store_key<W>(tmp, ob + z + i, from_pi(tab[u]));
       tab[u] = K{};
     }
     if (t == 0) {
@@ -611,7 +633,7 @@ template <int W>
 __global__ void __launch_bounds__(kBT) bucket_compact_kernel(const uint64_t* __restrict__ tmp,
                                                             const uint32_t* __restrict__ off,
                                                             const uint32_t* __restrict__ surv,
-                                                            const uint64_t* __restrict__ soff, uint32_t nb,
+                                                            const uint64_t* __restrict__ soff, uint32_t nb, int V,
                                                             uint64_t* __restrict__ out) {
   const uint32_t lane = lane_id();
   const uint32_t gw = (blockIdx.x * kBT + threadIdx.x) >> 5, nw = (gridDim.x * kBT) >> 5;
@@ -619,9 +641,9 @@ __global__ void __launch_bounds__(kBT) bucket_compact_kernel(const uint64_t* __r
     const uint32_t b = g + lane;
     uint32_t st = 0, ns = 0;
     uint64_t o = 0;
-    if (b < nb) {
-      st = off[b];
+    if (b < nb) {  // nb = sub-buckets; part 1 of a bucket sits at the back of its region
       ns = surv[b];
+      st = (V && (b & 1u)) ? off[(b >> V) + 1] - ns : off[b >> V];
       o = soff[b];
     }
     for (int l = 0; l < 32; l++) {
@@ -693,9 +715,9 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
   CUSCI_TRY(s.get_t((n + 2) * W, &a));   // + slack: TMA pieces round to 16 bytes
   CUSCI_TRY(s.get_t((n + 2) * W, &b2));
   CUSCI_TRY(s.get_t(nb_max + 1, &off));
-  CUSCI_TRY(s.get_t(nb_max + 1, &surv));
-  CUSCI_TRY(s.get_t(nb_max + 1, &surv64));
-  CUSCI_TRY(s.get_t(nb_max + 1, &soff));
+  CUSCI_TRY(s.get_t(2 * (size_t)nb_max + 1, &surv));   // x2: sub-buckets (V = 1)
+  CUSCI_TRY(s.get_t(2 * (size_t)nb_max + 1, &surv64));
+  CUSCI_TRY(s.get_t(2 * (size_t)nb_max + 1, &soff));
   CUSCI_TRY(s.get_t(kHllM, &hll));
   CUSCI_TRY(s.get_t(2, &flags));
   CUSCI_CUDA(ctx, cudaMemsetAsync(flags, 0, 2 * sizeof(unsigned long long), ctx->stream));
@@ -819,17 +841,28 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
     CUSCI_CUDA(ctx, cudaMemcpyAsync(off, ctx->host_pinned, sizeof(o2), cudaMemcpyHostToDevice, ctx->stream));
     CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   }
-  const uint32_t nb = 1u << B;
+  const uint32_t nbk = 1u << B;
+  // V = 1 (knob only): each bucket is processed as two halves (by the next bit
+  // of hi), each re-reading the bucket but filling its table half as much.
+  // Measured on the N2 batch: 26 ms vs 17.5 ms for V = 0 (the table load is not
+  // what bounds the kernel), so it is off by default.
+  static const int split_knob = [] {
+    const char* e = getenv("CUSCI_BUCKET_SPLIT");  // tuning knob
+    return e ? atoi(e) : 0;
+  }();
+  const int V = (split_knob == 1 && B < 63) ? 1 : 0;
+  const uint32_t vdcap = V ? (dcap == 0xffffffffu ? dcap : dcap / 2u + 64u) : dcap;
+  const uint32_t nb = nbk << V;  // work units (sub-buckets)
   uint64_t* tmp = (part == a) ? b2 : a;
   const unsigned dgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(nb, (uint64_t)ctx->num_sms * dper[W]));
-  CUSCI_LAUNCH(ctx, PT_HASH, bucket_unique_kernel<W><<<dgrid, kBU, C::SMEM, ctx->stream>>>(part, part == in ? 1 : 0, use_tma, off, nb, B, lf, dcap, tmp, surv, flags));
+  CUSCI_LAUNCH(ctx, PT_HASH, bucket_unique_kernel<W><<<dgrid, kBU, C::SMEM, ctx->stream>>>(part, part == in ? 1 : 0, use_tma, off, nbk, B, V, lf, vdcap, tmp, surv, flags));
   // pack the buckets' survivors in bucket order
   CUSCI_CUDA(ctx, cudaMemsetAsync(surv64, 0, (nb + 1) * sizeof(uint64_t), ctx->stream));
   CUSCI_CUDA(ctx, cudaMemcpy2DAsync(surv64, sizeof(uint64_t), surv, sizeof(uint32_t), sizeof(uint32_t), nb,
                                     cudaMemcpyDeviceToDevice, ctx->stream));
   CUSCI_TRY(scan_exclusive_u64(ctx, surv64, soff, nb + 1, nullptr));
   const unsigned cgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nb + 255) / 256, (uint64_t)ctx->num_sms * 8));
-  CUSCI_LAUNCH(ctx, PT_SCATTER, bucket_compact_kernel<W><<<cgrid, kBT, 0, ctx->stream>>>(tmp, off, surv, soff, nb, out));
+  CUSCI_LAUNCH(ctx, PT_SCATTER, bucket_compact_kernel<W><<<cgrid, kBT, 0, ctx->stream>>>(tmp, off, surv, soff, nb, V, out));
   uint64_t h[2];
   CUSCI_CUDA(ctx, cudaMemcpyAsync(ctx->host_pinned, soff + nb, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
   CUSCI_CUDA(ctx, cudaMemcpyAsync((char*)ctx->host_pinned + 8, flags, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));

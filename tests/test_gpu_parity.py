@@ -397,6 +397,27 @@ print("OK")
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
 
 
+def test_dedup_bucket_split_knob_subprocess():
+    """The half-bucket work split (CUSCI_BUCKET_SPLIT=1) gives the same sets."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import paper_2604_15768_b200 as P, oracle, synth
+ctx = P.Context(0)
+for W, n in [(1, 2_000_000), (2, 600_000)]:
+    keys = synth.zipf_keys(n, W, 1.05, 1 << 20, seed=3 + W)
+    got = ctx.dedup_global(P.Space(64 * W, 1, 1), torch.from_numpy(keys).cuda()).cpu().numpy().reshape(-1, W)
+    assert np.array_equal(synth.sort_keys(got), oracle.dedup(keys, W).reshape(-1, W)), W
+print("OK")
+''' % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CUSCI_BUCKET_SPLIT="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
+
+
 def _fmix64_inv(h):
     """inverse of the splitmix64 finalizer (to build keys with chosen hash)."""
     M = (1 << 64) - 1
