@@ -366,7 +366,7 @@ __device__ __forceinline__ bool otab_insert(KeyT<2>* tab, uint32_t* bm, uint32_t
 // written at the bucket's input offset; the pack kernel then concatenates
 // the buckets.
 constexpr int kBU = 1024;  // dedup threads (one CTA per SM owns the shared-memory budget)
-constexpr int kILP = 4;   // keys per thread with first probes in flight together
+constexpr int kILP = 8;   // keys per thread with first probes in flight together
 template <int W> struct BUCfg {
   static constexpr uint32_t TS = W == 1 ? 16384 : 8192;  // max home slots (128 KB)
   static constexpr uint32_t OV = W == 1 ? 1024 : 512;    // overflow tail
