@@ -286,6 +286,156 @@ __global__ void __launch_bounds__(kST, 2) tile_scatter_kernel(const uint64_t* __
   }
 }
 
+// ---------------------------------------------------------------- hist-free first pass
+// The first pass of a large call skips the histogram read: pi is uniform, so
+// each of the 256 top-byte groups gets a region of `cap` >= n/256 (+2% + 4 Ki)
+// keys and CTAs reserve their runs in it with one global atomic per (sub-round,
+// digit).  Persistent CTAs walk interleaved 4 Ki-key sub-rounds through the
+// same 3-slot TMA ring as tile_scatter_kernel, and keep the HyperLogLog sketch.
+// A region that would overflow (a pathologically skewed input) sets *ovf and
+// writes nothing past its end; the host then redoes the pass with histograms.
+// The next pass reads the groups from their regions and writes compactly.
+template <int W>
+__global__ void __launch_bounds__(kST, 2) scatter1_kernel(const uint64_t* __restrict__ in, uint64_t n, int use_tma,
+                                                         uint64_t cap, unsigned long long* __restrict__ gcur,
+                                                         uint64_t* __restrict__ out, uint32_t* __restrict__ hll,
+                                                         int* __restrict__ ovf) {
+  constexpr int ITEMS = SSCfg<W>::SUB / kST;
+  constexpr int SUB = SSCfg<W>::SUB;
+  constexpr uint32_t RMAX = 256;
+  extern __shared__ __align__(16) unsigned char ssm[];  // scatter1_smem<W>() bytes
+  KeyT<W>* ring = reinterpret_cast<KeyT<W>*>(ssm);       // [kSRing][SUB + 2]
+  unsigned long long* dl = reinterpret_cast<unsigned long long*>(ring + kSRing * (SUB + 2));  // [256]
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(dl + RMAX);
+  uint32_t* lst = cnt + RMAX;
+  uint8_t* reg = reinterpret_cast<uint8_t*>(lst + RMAX);   // [kHllM] HLL registers, one byte each
+  uint8_t* sdig = reg + kHllM;                             // [SUB]
+  __shared__ __align__(8) uint64_t bar[kSRing];
+  const bool tma = use_tma && ((reinterpret_cast<uintptr_t>(in) & 15u) == 0);
+  const uint64_t nsub = (n + SUB - 1) / SUB;
+  for (uint32_t d = threadIdx.x; d < RMAX; d += kST) cnt[d] = 0;
+  for (uint32_t i = threadIdx.x; i < kHllM / 4; i += kST) reinterpret_cast<uint32_t*>(reg)[i] = 0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kSRing; i++) mbar_init(&bar[i], 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
+  // this CTA's k-th sub-round is blockIdx.x + k * gridDim.x
+  auto sub_of = [&](uint64_t k) { return (uint64_t)blockIdx.x + k * gridDim.x; };
+  auto issue = [&](uint64_t k) {  // thread 0: local sub-round k -> slot k % kSRing
+    const uint64_t r = sub_of(k);
+    const uint32_t sl = (uint32_t)(k % kSRing);
+    fence_proxy_async_smem();
+    issue_core<W>(in, r * SUB, (uint32_t)min((uint64_t)SUB, n - r * SUB), ring + sl * (SUB + 2), &bar[sl]);
+  };
+  uint64_t nk = 0;  // local sub-rounds
+  if (blockIdx.x < nsub) nk = (nsub - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  if (tma && threadIdx.x == 0)
+    for (uint64_t k = 0; k < min(nk, (uint64_t)kSRing - 1); k++) issue(k);
+  uint32_t phase = 0;
+  for (uint64_t kk = 0; kk < nk; kk++) {
+    const uint64_t r = sub_of(kk), s0 = r * SUB;
+    const uint32_t sl = (uint32_t)(kk % kSRing);
+    const uint32_t m = (uint32_t)min((uint64_t)SUB, n - s0);
+    KeyT<W>* buf = ring + sl * (SUB + 2);
+    if (tma) {
+      if (threadIdx.x == 0 && kk + kSRing - 1 < nk) issue(kk + kSRing - 1);
+      const bool issued = W == 1 ? (((s0 + m) & ~1ull) > ((s0 + 1) & ~1ull)) : m > 0;
+      if (issued) {
+        mbar_wait(&bar[sl], (phase >> sl) & 1u);
+        phase ^= 1u << sl;
+      }
+    }
+    KeyT<W> k[ITEMS];
+    uint32_t dr[ITEMS];
+    const uint32_t c0 = (W == 1 && tma) ? (uint32_t)(s0 & 1u) : 0u;
+    const uint32_t c1 = !tma ? 0u : (W == 1 ? m - (uint32_t)((s0 + m) & 1u) : m);
+#pragma unroll
+    for (int u = 0; u < ITEMS; u++) {
+      const uint32_t i = u * kST + threadIdx.x;
+      if (i < m) {
+        k[u] = to_pi((i >= c0 && i < c1) ? buf[i + c0] : load_key<W>(in, s0 + i));
+        const uint32_t d = (uint32_t)(k[u].w0 >> 56);
+        dr[u] = (d << 16) | atomicAdd(&cnt[d], 1u);
+        const uint64_t hv = k[u].w0;  // hash-sampled HLL (see tile_hist_kernel)
+        if (((hv >> kHllLog) & (kHllSample - 1)) == 0) {
+          const uint32_t idx = (uint32_t)hv & (kHllM - 1);
+          const uint32_t rho = (uint32_t)min(__clzll(hv), 64 - kHllLog - 4) + 1;
+          if (rho > reg[idx]) {  // rare: byte max by a CAS on the containing word
+            uint32_t* wp = reinterpret_cast<uint32_t*>(reg) + (idx >> 2);
+            const uint32_t sh = (idx & 3u) * 8u;
+            uint32_t old = *wp;
+            while (((old >> sh) & 0xffu) < rho) {
+              const uint32_t nw = (old & ~(0xffu << sh)) | (rho << sh);
+              const uint32_t got = atomicCAS(wp, old, nw);
+              if (got == old) break;
+              old = got;
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();  // the slot's keys are in registers: it becomes the stage
+    if (threadIdx.x < 32) {  // warp 0: exclusive scan of the 256 digit counts
+      constexpr uint32_t DPL = RMAX / 32;
+      uint32_t c[DPL], loc = 0;
+#pragma unroll
+      for (uint32_t j = 0; j < DPL; j++) {
+        c[j] = cnt[threadIdx.x * DPL + j];
+        loc += c[j];
+      }
+      uint32_t inc = loc;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, inc, o);
+        if ((int)threadIdx.x >= o) inc += y;
+      }
+      uint32_t ex = inc - loc;
+#pragma unroll
+      for (uint32_t j = 0; j < DPL; j++) {
+        lst[threadIdx.x * DPL + j] = ex;
+        ex += c[j];
+      }
+    }
+    // every digit reserves its run in its group's region (one atomic each)
+    for (uint32_t d = threadIdx.x; d < RMAX; d += kST) {
+      const uint32_t cd = cnt[d];
+      unsigned long long v = ~0ull;  // no write
+      if (cd) {
+        const unsigned long long b = atomicAdd(&gcur[d], (unsigned long long)cd);
+        if (b + cd <= cap) v = (unsigned long long)d * cap + b;
+        else *ovf = 1;
+      }
+      dl[d] = v;
+    }
+    __syncthreads();
+    KeyT<W>* stage = buf;
+#pragma unroll
+    for (int u = 0; u < ITEMS; u++) {
+      const uint32_t i = u * kST + threadIdx.x;
+      if (i < m) {
+        const uint32_t d = dr[u] >> 16;
+        const uint32_t pos = lst[d] + (dr[u] & 0xffffu);
+        stage[pos] = k[u];
+        sdig[pos] = (uint8_t)d;
+      }
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < m; j += kST) {
+      const uint32_t d = sdig[j];
+      const unsigned long long b = dl[d];
+      if (b != ~0ull) store_key<W>(out, b + (j - lst[d]), stage[j]);
+    }
+    for (uint32_t d = threadIdx.x; d < RMAX; d += kST) cnt[d] = 0;
+    __syncthreads();  // stage read out, counters clear
+  }
+  for (uint32_t i = threadIdx.x; i < kHllM; i += kST)
+    if (reg[i]) atomicMax(&hll[i], reg[i]);
+}
+template <int W> constexpr size_t scatter1_smem() {
+  return kSRing * ((size_t)SSCfg<W>::SUB + 2) * sizeof(KeyT<W>) + 256 * 8 + 2 * 256 * 4 + kHllM +
+         (size_t)SSCfg<W>::SUB;
+}
+
 // group offsets after a pass: for old group g with meta {start, tiles, mbase},
 // new group g*R + d starts at offs[mbase + d * tiles] (or the old start if empty)
 __global__ void group_off_kernel(const uint32_t* __restrict__ offs, const uint4* __restrict__ gmeta, uint32_t G,
@@ -712,7 +862,14 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
   uint32_t *off, *surv, *hll;
   uint64_t *surv64, *soff;
   unsigned long long* flags;
-  CUSCI_TRY(s.get_t((n + 2) * W, &a));   // + slack: TMA pieces round to 16 bytes
+  // hist-free first pass (large calls): 256 group regions of `cap` keys in `a`
+  static const int hist_free_knob = [] {
+    const char* e = getenv("CUSCI_HIST_FREE_PASS1");  // tuning knob (0 disables)
+    return e ? atoi(e) : 1;
+  }();
+  const bool hist_free = hist_free_knob && n >= (1ull << 26) && Bmax > 8;
+  const uint64_t cap1 = (n + 255) / 256 + n / 256 / 50 + 4096;
+  CUSCI_TRY(s.get_t((std::max<uint64_t>(n, hist_free ? 256 * cap1 : 0) + 2) * W, &a));  // + slack: 16-byte TMA pieces
   CUSCI_TRY(s.get_t((n + 2) * W, &b2));
   CUSCI_TRY(s.get_t(nb_max + 1, &off));
   CUSCI_TRY(s.get_t(2 * (size_t)nb_max + 1, &surv));   // x2: sub-buckets (V = 1)
@@ -728,13 +885,15 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
     CUSCI_CUDA(ctx, cudaFuncSetAttribute(tile_scatter_kernel<W, false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scatter_smem<W, 8>()));
     CUSCI_CUDA(ctx, cudaFuncSetAttribute(tile_scatter_kernel<W, false, 9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scatter_smem<W, 9>()));
     CUSCI_CUDA(ctx, cudaFuncSetAttribute(bucket_unique_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    CUSCI_CUDA(ctx, cudaFuncSetAttribute(scatter1_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scatter1_smem<W>()));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&dper[W], bucket_unique_kernel<W>, kBU, C::SMEM);
     if (dper[W] < 1) dper[W] = 1;
     attr[W] = true;
   }
   const uint64_t* part = in;
   if (Bmax > 0) {
-    std::vector<uint32_t> gstart{0u, (uint32_t)n};  // current groups (host)
+    std::vector<uint32_t> gstart{0u, (uint32_t)n};  // current groups (host): compact prefix ...
+    std::vector<uint64_t> rstart, rend;                // ... or, after the hist-free pass, input regions
     uint64_t* dst = a;
     int done = 0;
     // one segmented MSD pass of `bits` bits over the current groups
@@ -750,9 +909,10 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
       tl.reserve(n / kPTile + G + 1);
       uint64_t mb = 0;
       for (uint32_t g = 0; g < G; g++) {
-        const uint64_t gs = gstart[g], ge = gstart[g + 1];
+        // input range of the group; gm.x = its compact output start
+        const uint64_t gs = rstart.empty() ? gstart[g] : rstart[g], ge = rstart.empty() ? gstart[g + 1] : rend[g];
         const uint32_t chunks = (uint32_t)((ge - gs + kPTile - 1) / kPTile);
-        gm[g] = make_uint4((uint32_t)gs, chunks, (uint32_t)mb, 0u);
+        gm[g] = make_uint4(gstart[g], chunks, (uint32_t)mb, 0u);
         for (uint32_t c = 0; c < chunks; c++) {
           const uint64_t st = gs + (uint64_t)c * kPTile;
           tl.push_back(PTile{st, (uint32_t)std::min<uint64_t>(kPTile, ge - st), chunks, mb + c});
@@ -804,11 +964,59 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
       dst = (dst == a) ? b2 : a;
       done += bits;
       ctx->dstats[2] += n;
+      rstart.clear();
+      rend.clear();
+      return CUSCI_OK;
+    };
+    // the hist-free first pass: scatter into group regions with atomic cursors
+    auto run_pass1_regions = [&]() -> int {
+      Scratch ps(ctx);
+      unsigned long long* gcur;
+      int* ovf;
+      CUSCI_TRY(ps.get_t(256, &gcur));
+      CUSCI_TRY(ps.get_t(1, &ovf));
+      CUSCI_CUDA(ctx, cudaMemsetAsync(gcur, 0, 256 * sizeof(unsigned long long), ctx->stream));
+      CUSCI_CUDA(ctx, cudaMemsetAsync(ovf, 0, sizeof(int), ctx->stream));
+      CUSCI_CUDA(ctx, cudaMemsetAsync(hll, 0, kHllM * sizeof(uint32_t), ctx->stream));
+      static int sper[3] = {0, 0, 0};
+      if (!sper[W]) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sper[W], scatter1_kernel<W>, kST, scatter1_smem<W>());
+        if (sper[W] < 1) sper[W] = 1;
+      }
+      const uint64_t nsub = (n + SSCfg<W>::SUB - 1) / SSCfg<W>::SUB;
+      const unsigned g1 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(nsub, (uint64_t)ctx->num_sms * sper[W]));
+      CUSCI_LAUNCH(ctx, PT_RADIX_DOWN, scatter1_kernel<W><<<g1, kST, scatter1_smem<W>(), ctx->stream>>>(in, n, use_tma, cap1, gcur, a, hll, ovf));
+      uint64_t hc[256];
+      int hv = 0;
+      CUSCI_TRY(read_u64(ctx, reinterpret_cast<const uint64_t*>(gcur), hc, 256));
+      CUSCI_CUDA(ctx, cudaMemcpy(&hv, ovf, sizeof(int), cudaMemcpyDeviceToHost));
+      if (hv) return -1;  // a region overflowed: redo the pass with histograms
+      gstart.assign(257, 0u);
+      rstart.resize(256);
+      rend.resize(256);
+      uint64_t acc = 0;
+      for (int g = 0; g < 256; g++) {
+        gstart[g] = (uint32_t)acc;
+        rstart[g] = (uint64_t)g * cap1;
+        rend[g] = rstart[g] + hc[g];
+        acc += hc[g];
+      }
+      gstart[256] = (uint32_t)acc;
+      part = a;
+      dst = b2;
+      done = 8;
+      ctx->dstats[2] += n;
       return CUSCI_OK;
     };
     const int bits1 = std::min(8, Bmax);
     // the plan after pass 1 depends on the sketch, so pass 1 is "last" only if nothing can follow
-    CUSCI_TRY(run_pass(bits1, true, Bmax == bits1));
+    bool regions = false;
+    if (hist_free) {
+      const int rc = run_pass1_regions();
+      if (rc == CUSCI_OK) regions = true;
+      else if (rc != -1) return rc;
+    }
+    if (!regions) CUSCI_TRY(run_pass(bits1, true, Bmax == bits1));
     if (Bmax > bits1) {
       std::vector<uint32_t> reg(kHllM);
       CUSCI_CUDA(ctx, cudaMemcpy(reg.data(), hll, kHllM * sizeof(uint32_t), cudaMemcpyDeviceToHost));
@@ -822,6 +1030,7 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
       auto npass = [&](int b) { return (std::max(0, b - bits1) + max_bits - 1) / max_bits; };
       if (Bd > bits1 && npass(Bd - 1) < npass(Bd) && D / std::ldexp(1.0, Bd - 1) <= 1.6 * (double)dt) Bd--;
       B = std::max(bits1, std::min(Bmax, Bd));
+      if (regions && B == bits1) B = bits1 + 1;  // the region layout needs one compacting pass
       const int rest = B - bits1;
       const int np = (rest + max_bits - 1) / max_bits;
       for (int pi = 0; pi < np; pi++) {

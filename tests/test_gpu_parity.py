@@ -464,6 +464,42 @@ def _t_fmix64(x):
     return x ^ srl(x, 31)
 
 
+def _t_fmix64_inv(x):
+    """inverse of the splitmix64 finalizer on int64 torch tensors."""
+    def srl(v, s):
+        return (v >> s) & ((1 << (64 - s)) - 1)
+    i2 = pow(0x94D049BB133111EB, -1, 1 << 64)
+    i1 = pow(0xBF58476D1CE4E5B9, -1, 1 << 64)
+    i2 = i2 - (1 << 64) if i2 >= 1 << 63 else i2
+    i1 = i1 - (1 << 64) if i1 >= 1 << 63 else i1
+    x = x ^ srl(x, 31) ^ srl(x, 62)
+    x = x * i2
+    x = x ^ srl(x, 27) ^ srl(x, 54)
+    x = x * i1
+    return x ^ srl(x, 30) ^ srl(x, 60)
+
+
+def test_dedup_hist_free_pass_overflow_falls_back(P, ctx):
+    """70M keys whose hash shares its top byte (one group): the hist-free first
+    pass overflows its region and the call redoes the pass with histograms --
+    the result must still be exact."""
+    g = torch.Generator(device="cuda").manual_seed(5)
+    D = 40_000_000
+    hi = torch.randint(0, 1 << 56, (D,), device="cuda", generator=g, dtype=torch.int64) | (0x5A << 56)
+    hi = torch.unique(hi)
+    base = _t_fmix64_inv(hi)
+    assert torch.equal(_t_fmix64(base), hi)
+    keys = torch.cat([base, base[: 30_000_000]])
+    keys = keys[torch.randperm(keys.numel(), device="cuda", generator=g)]
+    u = ctx.dedup_global(P.Space(64, 1, 1), keys.view(torch.uint64).reshape(-1, 1))
+    ui = u.view(torch.int64).reshape(-1)
+    flip = -(1 << 63)
+    assert u.shape[0] == base.numel()
+    h = _t_fmix64(ui) ^ flip
+    assert bool((h[1:] > h[:-1]).all())
+    assert torch.equal(torch.sort(ui ^ flip).values, torch.sort(base ^ flip).values)
+
+
 _AT_SCALE = r"""
 import sys, torch
 sys.path.insert(0, %r)
