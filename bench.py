@@ -384,7 +384,7 @@ def main():
     alg = {
         "gen": sum(counts) * rec_bytes + n_par * 8 * W,                  # records written + parents read
         "part_scatter": ds["key_passes"] * 16 * W // args.steps,         # partition: read + write a key per pass
-        "part_hist": ds["key_passes"] * 8 * W // args.steps,             # per-pass histograms: read a key
+        "part_hist": ds["hist_keys"] * 8 * W // args.steps,              # histogram passes: read a key
         "bucket_unique": (ds["keys_in"] + ds["keys_out"]) * 8 * W // args.steps,  # read every key, write survivors
         "merge_tile": merge_bytes,                                       # read S and U, write S'
     }

@@ -118,10 +118,12 @@ int cusci_profile_read(cusci_ctx* ctx, double* ms, uint64_t* launches, int n_tag
 /* Local-dedup plan statistics accumulated since the last read (instrumentation
  * for bench.py's algorithmic-byte accounting): stats[0] = dedup calls,
  * stats[1] = keys in, stats[2] = key-passes of the partition (sum over calls
- * of keys x passes), stats[3] = distinct keys out, stats[4] = buckets,
- * stats[5] = calls that took the overflow slow path.  reset != 0 clears them.
- * Returns CUSCI_OK (CUSCI_E_INVALID_ARG for NULL arguments). */
-int cusci_dedup_stats(cusci_ctx* ctx, uint64_t stats[6], int reset);
+ * of keys x scatter passes), stats[3] = distinct keys out, stats[4] = bucket
+ * work units, stats[5] = calls that took the overflow slow path, stats[6] =
+ * keys read by histogram passes, stats[7] = keys scattered by the hist-free
+ * first pass.  reset != 0 clears them.  Returns CUSCI_OK (CUSCI_E_INVALID_ARG
+ * for NULL arguments). */
+int cusci_dedup_stats(cusci_ctx* ctx, uint64_t stats[8], int reset);
 
 /* ---- step 1: coupled generation ------------------------------------------ */
 

@@ -171,9 +171,10 @@ class Context:
 
     def dedup_stats(self, reset: bool = True) -> dict:
         """Local-dedup plan statistics since the last reset (cusci_dedup_stats)."""
-        st = (ctypes.c_uint64 * 6)()
+        st = (ctypes.c_uint64 * 8)()
         self._check(lib().cusci_dedup_stats(self._ctx, st, 1 if reset else 0), "cusci_dedup_stats")
-        return dict(zip(("calls", "keys_in", "key_passes", "keys_out", "buckets", "slow_path_calls"), (int(x) for x in st)))
+        return dict(zip(("calls", "keys_in", "key_passes", "keys_out", "buckets", "slow_path_calls", "hist_keys",
+                         "hist_free_keys"), (int(x) for x in st)))
 
     def invalidate_integrals(self):
         lib().cusci_invalidate_integrals(self._ctx)

@@ -247,11 +247,11 @@ void cusci_free(cusci_ctx* ctx, void* ptr) {
 
 uint64_t cusci_kernel_launches(const cusci_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
-int cusci_dedup_stats(cusci_ctx* ctx, uint64_t stats[6], int reset) {
+int cusci_dedup_stats(cusci_ctx* ctx, uint64_t stats[8], int reset) {
   if (!ctx || !stats) return CUSCI_E_INVALID_ARG;
-  for (int i = 0; i < 6; i++) stats[i] = ctx->dstats[i];
+  for (int i = 0; i < 8; i++) stats[i] = ctx->dstats[i];
   if (reset)
-    for (int i = 0; i < 6; i++) ctx->dstats[i] = 0;
+    for (int i = 0; i < 8; i++) ctx->dstats[i] = 0;
   return CUSCI_OK;
 }
 

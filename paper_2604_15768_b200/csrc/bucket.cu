@@ -964,6 +964,7 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
       dst = (dst == a) ? b2 : a;
       done += bits;
       ctx->dstats[2] += n;
+      ctx->dstats[6] += n;
       rstart.clear();
       rend.clear();
       return CUSCI_OK;
@@ -1006,6 +1007,7 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
       dst = b2;
       done = 8;
       ctx->dstats[2] += n;
+      ctx->dstats[7] += n;
       return CUSCI_OK;
     };
     const int bits1 = std::min(8, Bmax);

@@ -101,7 +101,7 @@ struct cusci_ctx {
   uint64_t launches = 0;
   int num_sms = 148;
   bool profiling = false;
-  uint64_t dstats[6] = {0, 0, 0, 0, 0, 0};  // cusci_dedup_stats
+  uint64_t dstats[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // cusci_dedup_stats
   std::vector<cusci::ProfRec> prof;
   std::vector<cudaEvent_t> ev_free;
   std::string err;
