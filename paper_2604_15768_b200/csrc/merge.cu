@@ -389,7 +389,8 @@ __global__ void sparse_locate_kernel(const uint64_t* __restrict__ small, uint64_
 // (rank = exclusive scan of keep, rank[ns] = total inserts)
 template <int W>
 __global__ void sparse_copy_kernel(const uint64_t* __restrict__ big, uint64_t nb, const uint64_t* __restrict__ pos,
-                                   const uint64_t* __restrict__ rank, uint64_t ns, uint64_t* __restrict__ out) {
+                                   const uint64_t* __restrict__ rank, uint64_t ns, uint64_t* __restrict__ out,
+                                   int* __restrict__ bad /* non-null: also check big's strict hash order */) {
   constexpr uint32_t CH = 4096;  // big keys per CTA chunk
   __shared__ uint64_t s_u0, s_u1;
   for (uint64_t j0 = (uint64_t)blockIdx.x * CH; j0 < nb; j0 += (uint64_t)gridDim.x * CH) {
@@ -416,9 +417,24 @@ __global__ void sparse_copy_kernel(const uint64_t* __restrict__ big, uint64_t nb
         if (pos[mid] <= j) lo = mid + 1;
         else hi = mid;
       }
-      store_key<W>(out, j + rank[lo], load_key<W>(big, j));
+      const KeyT<W> x = load_key<W>(big, j);
+      store_key<W>(out, j + rank[lo], x);
+      if (bad && j > 0 && !hk_lt<W>(load_key<W>(big, j - 1), x)) *bad = 1;  // (j-1 is an L1 hit)
     }
     __syncthreads();
+  }
+}
+
+// empty pool: out = U (and ins = U) in one pass, checking U's strict hash order
+template <int W>
+__global__ void copy_check_kernel(const uint64_t* __restrict__ U, uint64_t n, uint64_t* __restrict__ out,
+                                  uint64_t* __restrict__ ins, int* __restrict__ bad) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const KeyT<W> x = load_key<W>(U, i);
+    store_key<W>(out, i, x);
+    if (ins) store_key<W>(ins, i, x);
+    if (i > 0 && !hk_lt<W>(load_key<W>(U, i - 1), x)) *bad = 1;
   }
 }
 
@@ -493,10 +509,8 @@ int merge_impl(cusci_ctx* ctx, cusci_pool* pool, const uint64_t* U, uint64_t nU,
   uint64_t h[3];
   if (nS == 0) {
     // empty pool: S' = U (validated strictly increasing in the hash order), a copy
-    const unsigned cg = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nU + 255) / 256, (uint64_t)ctx->num_sms * 8));
-    CUSCI_LAUNCH(ctx, PT_CHECK, check_sorted_kernel<W><<<cg, 256, 0, ctx->stream>>>(U, nU, bad));
-    CUSCI_CUDA(ctx, cudaMemcpyAsync(dst, U, nU * W * 8, cudaMemcpyDeviceToDevice, ctx->stream));
-    if (insp) CUSCI_CUDA(ctx, cudaMemcpyAsync(insp, U, nU * W * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    const unsigned cg = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nU + 255) / 256, (uint64_t)ctx->num_sms * 16));
+    CUSCI_LAUNCH(ctx, PT_CHECK, copy_check_kernel<W><<<cg, 256, 0, ctx->stream>>>(U, nU, dst, (uint64_t*)insp, bad));
     CUSCI_CUDA(ctx, cudaMemcpyAsync((char*)ctx->host_pinned + 16, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     h[0] = nU;
@@ -515,8 +529,10 @@ int merge_impl(cusci_ctx* ctx, cusci_pool* pool, const uint64_t* U, uint64_t nU,
     const uint64_t* small = u_small ? U : S;
     const uint64_t* big = u_small ? S : U;
     const uint64_t nsm = u_small ? nU : nS, nbg = u_small ? nS : nU;
-    const unsigned cu = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nU + 255) / 256, (uint64_t)ctx->num_sms * 8));
-    CUSCI_LAUNCH(ctx, PT_CHECK, check_sorted_kernel<W><<<cu, 256, 0, ctx->stream>>>(U, nU, bad));
+    if (u_small) {  // a large U is checked inside the copy
+      const unsigned cu = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nU + 255) / 256, (uint64_t)ctx->num_sms * 8));
+      CUSCI_LAUNCH(ctx, PT_CHECK, check_sorted_kernel<W><<<cu, 256, 0, ctx->stream>>>(U, nU, bad));
+    }
     const unsigned cg = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nsm + 255) / 256, (uint64_t)ctx->num_sms * 8));
     uint64_t *pos, *keep64, *rank;
     uint32_t* keep;
@@ -530,7 +546,7 @@ int merge_impl(cusci_ctx* ctx, cusci_pool* pool, const uint64_t* U, uint64_t nU,
                                       cudaMemcpyDeviceToDevice, ctx->stream));
     CUSCI_TRY(scan_exclusive_u64(ctx, keep64, rank, nsm + 1, nullptr));
     const unsigned bg = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nbg + 4095) / 4096, (uint64_t)ctx->num_sms * 8));
-    CUSCI_LAUNCH(ctx, PT_MERGE_TILE, sparse_copy_kernel<W><<<bg, 256, 0, ctx->stream>>>(big, nbg, pos, rank, nsm, dst));
+    CUSCI_LAUNCH(ctx, PT_MERGE_TILE, sparse_copy_kernel<W><<<bg, 256, 0, ctx->stream>>>(big, nbg, pos, rank, nsm, dst, u_small ? nullptr : bad));
     CUSCI_LAUNCH(ctx, PT_MERGE_TILE, sparse_place_kernel<W><<<cg, 256, 0, ctx->stream>>>(small, nsm, pos, keep, rank, dst, u_small ? (uint64_t*)insp : nullptr));
     CUSCI_CUDA(ctx, cudaMemcpyAsync(ctx->host_pinned, rank + nsm, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
     CUSCI_CUDA(ctx, cudaMemcpyAsync((char*)ctx->host_pinned + 16, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
