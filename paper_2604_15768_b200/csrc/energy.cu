@@ -5,11 +5,13 @@
 //
 // B200 design (reading r14):
 //   reverse index  the unique set is sorted in the hash order pi (reading
-//                  r13) and pi is uniform, so a table T over the top k bits of
-//                  hi (2^k >= n_space) brackets every key in ~1 entry, stored
-//                  next to its amplitude: per record one table load and ~1
-//                  (key, psi) load ("just in time", nothing materialised per
-//                  record);
+//                  r13) and pi is uniform, so its (key, psi) pairs are laid
+//                  out in an ORDERED direct-mapped table (element i at slot
+//                  max(home_i, slot_{i-1} + 1), home = top k bits of hi,
+//                  2^k >= 2 n_space; built by a max-scan, no atomics): a
+//                  record probes from its home and almost always resolves in
+//                  one 32-byte sector ("just in time", nothing materialised
+//                  per record);
 //   reduction      each product p = H * psi (IEEE fp64) is rounded half-to-even
 //                  to the grid 2^-80 and accumulated EXACTLY as a 128-bit
 //                  integer: a warp first sums the runs of equal src among its
@@ -20,6 +22,7 @@
 //                  and of the launch configuration; e[s] = the exact sum
 //                  rounded once to fp64.
 #include <algorithm>
+#include <climits>
 
 #include "internal.cuh"
 
@@ -74,6 +77,99 @@ template <> __device__ __forceinline__ bool kp_eq<2>(const KPsi<2>& r, const Key
   return r.k0 == k.w0 && r.k1 == k.w1;
 }
 
+
+// ---- ordered direct-mapped (key, psi) table: the space is sorted in the hash
+// order, so placing element i at p_i = max(h_i, p_{i-1} + 1) (h = top k bits of
+// hi, 2^k >= 2 n) keeps homes monotone: a record probes from its home and
+// almost always resolves in one 32-byte sector.  p_i = i + max_{j<=i}(h_j - j):
+// a max-scan, done as chunk maxima -> one-block exclusive prefix -> in-chunk scan.
+constexpr uint32_t kPCh = 4096;  // elements per chunk
+template <int W>
+__device__ __forceinline__ long long home_minus_i(const uint64_t* space, uint64_t i, int k) {
+  const uint64_t h = to_pi(load_key<W>(space, i)).w0 >> (64 - k);
+  return (long long)h - (long long)i;
+}
+template <int W>
+__global__ void __launch_bounds__(kET) chunk_max_kernel(const uint64_t* __restrict__ space, uint64_t n, int k,
+                                                       long long* __restrict__ cmax) {
+  __shared__ long long red[kET / 32];
+  const uint64_t c0 = (uint64_t)blockIdx.x * kPCh;
+  long long m = LLONG_MIN;
+  for (uint64_t i = c0 + threadIdx.x; i < min(n, c0 + kPCh); i += kET) m = max(m, home_minus_i<W>(space, i, k));
+  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(kFull, m, o));
+  if (lane_id() == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < kET / 32; w++) m = max(m, red[w]);
+    m = max(m, red[0]);
+    cmax[blockIdx.x] = m;
+  }
+}
+// one block: cpre[c] = max(cmax[0..c-1]) (LLONG_MIN for c = 0)
+__global__ void __launch_bounds__(1024) chunk_prefix_kernel(const long long* __restrict__ cmax, uint64_t nc,
+                                                           long long* __restrict__ cpre) {
+  __shared__ long long red[32];
+  const uint64_t per = (nc + 1023) / 1024, a = threadIdx.x * per, b = min(nc, a + per);
+  long long m = LLONG_MIN;
+  for (uint64_t c = a; c < b; c++) m = max(m, cmax[c]);
+  // exclusive max-scan of the per-thread maxima
+  long long inc = m;
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_up_sync(kFull, inc, o);
+    if ((int)lane_id() >= o) inc = max(inc, y);
+  }
+  if (lane_id() == 31) red[threadIdx.x >> 5] = inc;
+  __syncthreads();
+  long long wpre = LLONG_MIN;
+  for (int w = 0; w < (int)(threadIdx.x >> 5); w++) wpre = max(wpre, red[w]);
+  long long ex = max(wpre, __shfl_up_sync(kFull, inc, 1));
+  if (lane_id() == 0) ex = wpre;
+  for (uint64_t c = a; c < b; c++) {
+    cpre[c] = ex;
+    ex = max(ex, cmax[c]);
+  }
+}
+template <int W>
+__global__ void __launch_bounds__(kET) place_kernel(const uint64_t* __restrict__ space, const double* __restrict__ psi,
+                                                   uint64_t n, int k, const long long* __restrict__ cpre,
+                                                   KPsi<W>* __restrict__ table, uint64_t tslots, unsigned long long* ovf) {
+  __shared__ long long red[kET / 32];
+  __shared__ long long carry;
+  const uint64_t c0 = (uint64_t)blockIdx.x * kPCh;
+  if (threadIdx.x == 0) carry = cpre[blockIdx.x];
+  __syncthreads();
+  for (uint64_t r0 = c0; r0 < min(n, c0 + kPCh); r0 += kET) {
+    const uint64_t i = r0 + threadIdx.x;
+    const long long d = i < n ? home_minus_i<W>(space, i, k) : LLONG_MIN;
+    long long inc = d;  // inclusive max-scan over the block
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(kFull, inc, o);
+      if ((int)lane_id() >= o) inc = max(inc, y);
+    }
+    if (lane_id() == 31) red[threadIdx.x >> 5] = inc;
+    __syncthreads();
+    long long pre = carry;
+    for (int w = 0; w < (int)(threadIdx.x >> 5); w++) pre = max(pre, red[w]);
+    const long long full = max(pre, inc);
+    if (i < n) {
+      KPsi<W> r{};
+      const KeyT<W> kk = load_key<W>(space, i);
+      r.k0 = kk.w0;
+      if constexpr (W == 2) r.k1 = kk.w1;
+      r.psi = psi[i];
+      const uint64_t slot = (uint64_t)((long long)i + full);
+      if (slot < tslots) table[slot] = r;
+      else *ovf = 1;  // (impossible for hash-uniform keys: displacement >> n/16)
+    }
+    __syncthreads();
+    if (threadIdx.x == kET - 1) carry = full;  // the block's inclusive maximum so far
+    __syncthreads();
+  }
+}
+template <int W> __device__ __forceinline__ bool kp_empty(const KPsi<W>& r);
+template <> __device__ __forceinline__ bool kp_empty<1>(const KPsi<1>& r) { return r.k0 == 0; }
+template <> __device__ __forceinline__ bool kp_empty<2>(const KPsi<2>& r) { return (r.k0 | r.k1) == 0; }
+
 // p -> round_half_even(p * 2^80) for |p| < 2^20 (exact integer arithmetic)
 __device__ __forceinline__ __int128 quantize80(double p) {
   if (p == 0.0) return 0;
@@ -120,9 +216,9 @@ __device__ __forceinline__ double int128_to_double_rn(__int128 x) {
 }
 
 template <int W>
-__global__ void __launch_bounds__(kET) contract_kernel(const uint64_t* __restrict__ keys, const double* __restrict__ hij,
+__global__ void __launch_bounds__(kET, 4) contract_kernel(const uint64_t* __restrict__ keys, const double* __restrict__ hij,
                                                       const uint32_t* __restrict__ src, uint64_t n_rec,
-                                                      const KPsi<W>* __restrict__ kp, const uint32_t* __restrict__ T,
+                                                      const KPsi<W>* __restrict__ table, uint64_t tslots,
                                                       int k, unsigned long long* __restrict__ acc,
                                                       unsigned long long* __restrict__ flags) {
   const unsigned lane = lane_id();
@@ -131,27 +227,26 @@ __global__ void __launch_bounds__(kET) contract_kernel(const uint64_t* __restric
   bool big = false;
   // warp-uniform trip count so the warp-level reduction always has all lanes;
   // kU consecutive 32-record groups per step: their lookups are in flight together
-  constexpr int kU = 4;
+  constexpr int kU = 2;
   const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = stride >> 5;
   for (uint64_t w0 = wid * 32 * kU; w0 < n_rec; w0 += nw * 32 * kU) {
     uint32_t sv[kU];
     KeyT<W> kv[kU];
-    uint32_t lo[kU], hi[kU];
+    uint64_t hm[kU];
+    KPsi<W> ev[kU];
     double hv[kU];
 #pragma unroll
     for (int u = 0; u < kU; u++) {
       const uint64_t r = w0 + u * 32 + lane;
       sv[u] = 0xffffffffu;
-      lo[u] = hi[u] = 0;
       if (r < n_rec) {
         sv[u] = src[r];
         hv[u] = hij[r];
         kv[u] = load_key<W>(keys, r);
-        // bucket of the key's hi; the table has ~1 key per bucket
-        const uint64_t b = k ? (to_pi(kv[u]).w0 >> (64 - k)) : 0ull;
-        lo[u] = T[b];
-        hi[u] = T[b + 1];
+        // home slot of the key in the ordered (key, psi) table
+        hm[u] = k ? (to_pi(kv[u]).w0 >> (64 - k)) : 0ull;
+        ev[u] = table[hm[u]];
       }
     }
     __int128 qv[kU];
@@ -162,13 +257,15 @@ __global__ void __launch_bounds__(kET) contract_kernel(const uint64_t* __restric
       if (r < n_rec) {
         bool found = false;
         double ps = 0.0;
-        for (uint32_t i = lo[u]; i < hi[u]; i++) {
-          const KPsi<W> e = kp[i];
+        KPsi<W> e = ev[u];
+        for (uint64_t slot = hm[u];;) {  // probe forward until the key or an empty slot
           if (kp_eq<W>(e, kv[u])) {
             found = true;
             ps = e.psi;
             break;
           }
+          if (kp_empty<W>(e) || ++slot >= tslots) break;
+          e = table[slot];
         }
         if (found) {
           const double prod = __dmul_rn(hv[u], ps);
@@ -228,28 +325,35 @@ int contract_impl(cusci_ctx* ctx, const uint64_t* keys, const double* hij, const
                   uint64_t n_parents, const uint64_t* space, uint64_t n_space, const double* psi, double* e,
                   uint64_t* n_missing) {
   Scratch s(ctx);
-  // ~1 key per bucket of the reverse-index table (uniform hi)
-  int k = 0;
-  while ((1ull << k) < n_space && k < 30) k++;
-  uint32_t* T;
-  KPsi<W>* kp;
+  // ordered (key, psi) table: 2^k >= 2 n_space home slots + a tail for the
+  // displacements at the top end
+  int k = 1;
+  while ((1ull << k) < 2 * n_space && k < 40) k++;
+  const uint64_t tslots = (1ull << k) + 4096 + n_space / 16;
+  const uint64_t nc = (n_space + kPCh - 1) / kPCh;
+  KPsi<W>* table;
+  long long *cmax, *cpre;
   unsigned long long *acc, *flags;
-  CUSCI_TRY(s.get_t(((size_t)1 << k) + 1, &T));
-  CUSCI_TRY(s.get_t(std::max<uint64_t>(n_space, 1), &kp));
+  CUSCI_TRY(s.get_t(tslots, &table));
+  CUSCI_TRY(s.get_t(std::max<uint64_t>(nc, 1), &cmax));
+  CUSCI_TRY(s.get_t(std::max<uint64_t>(nc, 1), &cpre));
   CUSCI_TRY(s.get_t(std::max<uint64_t>(4 * n_parents, 1), &acc));
   CUSCI_TRY(s.get_t(2, &flags));
+  CUSCI_CUDA(ctx, cudaMemsetAsync(table, 0, tslots * sizeof(KPsi<W>), ctx->stream));
   CUSCI_CUDA(ctx, cudaMemsetAsync(acc, 0, std::max<uint64_t>(4 * n_parents, 1) * 8, ctx->stream));
   CUSCI_CUDA(ctx, cudaMemsetAsync(flags, 0, 16, ctx->stream));
-  const unsigned g1 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_space + kET) / kET, (uint64_t)ctx->num_sms * 8));
-  CUSCI_LAUNCH(ctx, PT_ENERGY, rindex_table_kernel<W><<<g1, kET, 0, ctx->stream>>>(space, n_space, k, T));
-  if (n_space) CUSCI_LAUNCH(ctx, PT_ENERGY, kpsi_kernel<W><<<g1, kET, 0, ctx->stream>>>(space, psi, n_space, kp));
+  if (n_space) {
+    CUSCI_LAUNCH(ctx, PT_ENERGY, chunk_max_kernel<W><<<(unsigned)nc, kET, 0, ctx->stream>>>(space, n_space, k, cmax));
+    CUSCI_LAUNCH(ctx, PT_ENERGY, chunk_prefix_kernel<<<1, 1024, 0, ctx->stream>>>(cmax, nc, cpre));
+    CUSCI_LAUNCH(ctx, PT_ENERGY, place_kernel<W><<<(unsigned)nc, kET, 0, ctx->stream>>>(space, psi, n_space, k, cpre, table, tslots, flags + 1));
+  }
   if (n_rec) {
     const unsigned g2 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_rec + kET - 1) / kET, (uint64_t)ctx->num_sms * 16));
-    CUSCI_LAUNCH(ctx, PT_ENERGY, contract_kernel<W><<<g2, kET, 0, ctx->stream>>>(keys, hij, src, n_rec, kp, T, k, acc, flags));
+    CUSCI_LAUNCH(ctx, PT_ENERGY, contract_kernel<W><<<g2, kET, 0, ctx->stream>>>(keys, hij, src, n_rec, table, tslots, k, acc, flags));
   }
   uint64_t h[2];
   CUSCI_TRY(read_u64(ctx, reinterpret_cast<const uint64_t*>(flags), h, 2));
-  if (h[1]) return set_error(ctx, CUSCI_E_INVALID_ARG, "energy_contract: |H psi| >= 2^20 (outside the exact-sum range)");
+  if (h[1]) return set_error(ctx, CUSCI_E_INVALID_ARG, "energy_contract: |H psi| >= 2^20 (outside the exact-sum range) or a skewed space");
   *n_missing = h[0];
   if (n_parents) {
     const unsigned g3 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_parents + kET - 1) / kET, (uint64_t)ctx->num_sms * 8));
