@@ -286,6 +286,125 @@ __global__ void __launch_bounds__(kST, 2) tile_scatter_kernel(const uint64_t* __
   }
 }
 
+// The last (bucket-forming) pass after a hist-free first pass, also without a
+// histogram: every bucket (group g, digit d) gets a region of cap2 keys and the
+// tile reserves its runs with one global atomic per (sub-round, digit).  The
+// tile's group index is in PTile::mbase.  Overflow -> *ovf and nothing is
+// written past a region (the host then redoes the pass with histograms).
+template <int W>
+__global__ void __launch_bounds__(kST, 2) tile_scatter_atomic_kernel(const uint64_t* __restrict__ in, int use_tma,
+                                                                    const PTile* __restrict__ tiles, int bsel,
+                                                                    uint32_t R, unsigned long long* __restrict__ gcur,
+                                                                    uint64_t cap2, uint64_t* __restrict__ out,
+                                                                    int* __restrict__ ovf) {
+  constexpr int ITEMS = SSCfg<W>::SUB / kST;
+  constexpr int SUB = SSCfg<W>::SUB;
+  constexpr uint32_t RMAX = 256;
+  extern __shared__ __align__(16) unsigned char ssm[];  // scatter_smem<W, 8>() bytes
+  KeyT<W>* ring = reinterpret_cast<KeyT<W>*>(ssm);       // [kSRing][SUB + 2]
+  unsigned long long* dl = reinterpret_cast<unsigned long long*>(ring + kSRing * (SUB + 2));  // [256]
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(dl + RMAX);
+  uint32_t* lst = cnt + RMAX;
+  uint8_t* sdig = reinterpret_cast<uint8_t*>(lst + RMAX);
+  __shared__ __align__(8) uint64_t bar[kSRing];
+  const PTile t = tiles[blockIdx.x];
+  const uint64_t gbase = t.mbase * R;  // first bucket of the tile's group (R = 2^bits <= 256 digits)
+  const bool tma = use_tma && ((reinterpret_cast<uintptr_t>(in) & 15u) == 0);
+  for (uint32_t d = threadIdx.x; d < RMAX; d += kST) cnt[d] = 0;
+  const uint32_t nsub = (t.len + SUB - 1) / SUB;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kSRing; i++) mbar_init(&bar[i], 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
+  auto issue = [&](uint32_t r) {
+    const uint32_t sl = r % kSRing;
+    fence_proxy_async_smem();
+    issue_core<W>(in, t.start + (uint64_t)r * SUB, min((uint32_t)SUB, t.len - r * SUB), ring + sl * (SUB + 2), &bar[sl]);
+  };
+  if (tma && threadIdx.x == 0)
+    for (uint32_t r = 0; r < min(nsub, (uint32_t)kSRing - 1); r++) issue(r);
+  uint32_t phase = 0;
+  for (uint32_t r = 0; r < nsub; r++) {
+    const uint32_t sl = r % kSRing, r0 = r * SUB;
+    const uint32_t m = min((uint32_t)SUB, t.len - r0);
+    KeyT<W>* buf = ring + sl * (SUB + 2);
+    if (tma) {
+      if (threadIdx.x == 0 && r + kSRing - 1 < nsub) issue(r + kSRing - 1);
+      const uint64_t s0 = t.start + r0;
+      const bool issued = W == 1 ? (((s0 + m) & ~1ull) > ((s0 + 1) & ~1ull)) : m > 0;
+      if (issued) {
+        mbar_wait(&bar[sl], (phase >> sl) & 1u);
+        phase ^= 1u << sl;
+      }
+    }
+    KeyT<W> k[ITEMS];
+    uint32_t dr[ITEMS];
+    const uint32_t c0 = (W == 1 && tma) ? (uint32_t)((t.start + r0) & 1u) : 0u;
+    const uint32_t c1 = !tma ? 0u : (W == 1 ? m - (uint32_t)((t.start + r0 + m) & 1u) : m);
+#pragma unroll
+    for (int u = 0; u < ITEMS; u++) {
+      const uint32_t i = u * kST + threadIdx.x;
+      if (i < m) {
+        k[u] = (i >= c0 && i < c1) ? buf[i + c0] : load_key<W>(in, t.start + r0 + i);
+        const uint32_t d = top_bits<W>(k[u], bsel) & (R - 1);
+        dr[u] = (d << 16) | atomicAdd(&cnt[d], 1u);
+      }
+    }
+    __syncthreads();  // the slot's keys are in registers: it becomes the stage
+    if (threadIdx.x < 32) {  // warp 0: exclusive scan of the digit counts
+      constexpr uint32_t DPL = RMAX / 32;
+      uint32_t c[DPL], loc = 0;
+#pragma unroll
+      for (uint32_t j = 0; j < DPL; j++) {
+        c[j] = cnt[threadIdx.x * DPL + j];
+        loc += c[j];
+      }
+      uint32_t inc = loc;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, inc, o);
+        if ((int)threadIdx.x >= o) inc += y;
+      }
+      uint32_t ex = inc - loc;
+#pragma unroll
+      for (uint32_t j = 0; j < DPL; j++) {
+        lst[threadIdx.x * DPL + j] = ex;
+        ex += c[j];
+      }
+    }
+    for (uint32_t d = threadIdx.x; d < RMAX; d += kST) {  // reserve the runs
+      const uint32_t cd = cnt[d];
+      unsigned long long v = ~0ull;
+      if (cd) {
+        const unsigned long long b = atomicAdd(&gcur[gbase + d], (unsigned long long)cd);
+        if (b + cd <= cap2) v = (gbase + d) * cap2 + b;
+        else *ovf = 1;
+      }
+      dl[d] = v;
+    }
+    __syncthreads();
+    KeyT<W>* stage = buf;
+#pragma unroll
+    for (int u = 0; u < ITEMS; u++) {
+      const uint32_t i = u * kST + threadIdx.x;
+      if (i < m) {
+        const uint32_t d = dr[u] >> 16;
+        const uint32_t pos = lst[d] + (dr[u] & 0xffffu);
+        stage[pos] = k[u];
+        sdig[pos] = (uint8_t)d;
+      }
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < m; j += kST) {
+      const uint32_t d = sdig[j];
+      const unsigned long long b = dl[d];
+      if (b != ~0ull) store_key<W>(out, b + (j - lst[d]), stage[j]);
+    }
+    for (uint32_t d = threadIdx.x; d < RMAX; d += kST) cnt[d] = 0;
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------- hist-free first pass
 // The first pass of a large call skips the histogram read: pi is uniform, so
 // each of the 256 top-byte groups gets a region of `cap` >= n/256 (+2% + 4 Ki)
@@ -531,7 +650,8 @@ template <int W> struct BUCfg {
 
 template <int W>
 __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* __restrict__ part, int raw, int use_tma,
-                                                              const uint32_t* __restrict__ off, uint32_t nb, int B, int V,
+                                                              const uint32_t* __restrict__ off,
+                                                              const uint64_t* __restrict__ ibase, uint32_t nb, int B, int V,
                                                               uint32_t lf, uint32_t dcap, uint64_t* __restrict__ tmp,
                                                               uint32_t* __restrict__ surv,
                                                               unsigned long long* __restrict__ flags) {
@@ -574,7 +694,8 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
   uint32_t pb = bA, pp = 0, pk = 0, epar = 0;
   auto issue_next = [&]() {
     while (pb < bB) {
-      const uint32_t ps = off[pb >> V], pn = off[(pb >> V) + 1] - ps;
+      const uint32_t ps0 = off[pb >> V], pn = off[(pb >> V) + 1] - ps0;
+      const uint64_t ps = ibase ? ibase[pb >> V] : (uint64_t)ps0;  // input start (regions after a hist-free pass)
       if (pp < pn) {
         const uint32_t len = min(BUFK, pn - pp);
         if (pk >= 2) {  // wait for the release of piece pk - 2 (same buffer)
@@ -582,7 +703,7 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
           epar ^= 1u << (pk & 1);
         }
         fence_proxy_async_smem();
-        issue_core<W>(part, (uint64_t)ps + pp, len, bufs + (pk & 1) * BUFE, &bar[pk & 1]);
+        issue_core<W>(part, ps + pp, len, bufs + (pk & 1) * BUFE, &bar[pk & 1]);
         pp += BUFK;
         pk++;
         return;
@@ -594,7 +715,8 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
   if (tma && t == 0) issue_next();
   uint32_t phase = 0, k = 0;  // consumer: piece counter, barrier parities
   for (uint32_t b = bA; b < bB; b++) {
-    const uint32_t s = off[b >> V], nk = off[(b >> V) + 1] - s;
+    const uint32_t s = off[b >> V], nk = off[(b >> V) + 1] - s;  // s: survivor (tmp) offset
+    const uint64_t si = ibase ? ibase[b >> V] : (uint64_t)s;       // input offset
     const uint64_t vpart = (uint64_t)(b & ((1u << V) - 1u));
     if (nk == 0) {
       if (t == 0) surv[b] = 0;
@@ -610,7 +732,7 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
       buf = bufs + cb * BUFE;
       if (tma) {
         if (t == 0) issue_next();  // piece k+1 -> the other buffer (freed by the last barrier)
-        const uint64_t g0 = (uint64_t)s + p0;
+        const uint64_t g0 = si + p0;
         const bool issued = W == 1 ? (((g0 + len) & ~1ull) > ((g0 + 1) & ~1ull)) : true;
         if (issued) {
           mbar_wait(&bar[cb], (phase >> cb) & 1u);
@@ -619,8 +741,8 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
       }
       // kILP keys per thread: their first probes are issued together (most keys
       // resolve on the first probe: already present, or an empty home slot)
-      const uint32_t c0 = (W == 1 && tma) ? (uint32_t)((s + p0) & 1u) : 0u;
-      const uint32_t c1 = (W == 1 && tma) ? len - (uint32_t)((s + p0 + len) & 1u) : len;
+      const uint32_t c0 = (W == 1 && tma) ? (uint32_t)((si + p0) & 1u) : 0u;
+      const uint32_t c1 = (W == 1 && tma) ? len - (uint32_t)((si + p0 + len) & 1u) : len;
       for (uint32_t i0 = t; i0 < len; i0 += kILP * kBU) {
         K pv[kILP], cv[kILP];
         uint32_t hm[kILP];
@@ -630,9 +752,9 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
           const uint32_t i = i0 + u * kBU;
           act[u] = i < len;
           if (act[u]) {
-            if (!tma) pv[u] = load_key<W>(part, (uint64_t)s + p0 + i);
+            if (!tma) pv[u] = load_key<W>(part, si + p0 + i);
             else if (W == 2 || (i >= c0 && i < c1)) pv[u] = buf[i + c0];  // TMA core (key s+p0+i at buf[i + lead])
-            else pv[u] = load_key<W>(part, (uint64_t)s + p0 + i);
+            else pv[u] = load_key<W>(part, si + p0 + i);
             if (raw) pv[u] = to_pi(pv[u]);
             if (V && ((pv[u].w0 << B) >> (64 - V)) != vpart) act[u] = false;  // the other half
             else if (kzero(pv[u])) {
@@ -667,7 +789,7 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
       if (t == 0) wcnt[0] = 0;
       __syncthreads();
       uint32_t cnt = 0;
-      for (uint32_t i = t; i < nk; i += kBU) cnt += mine(load_key<W>(part, (uint64_t)s + i));
+      for (uint32_t i = t; i < nk; i += kBU) cnt += mine(load_key<W>(part, si + i));
       atomicAdd(&wcnt[0], cnt);
       __syncthreads();
       const uint32_t nh = wcnt[0];
@@ -676,7 +798,7 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
       __syncthreads();
       const uint64_t ob = vpart ? (uint64_t)s + nk - nh : (uint64_t)s;
       for (uint32_t i = t; i < nk; i += kBU) {
-        const K p = load_key<W>(part, (uint64_t)s + i);
+        const K p = load_key<W>(part, si + i);
         if (mine(p)) store_key<W>(tmp, ob + atomicAdd(&wcnt[0], 1u), raw ? p : from_pi(p));
       }
       for (uint32_t i = t; i < span; i += kBU) tab[i] = K{};
@@ -886,11 +1008,13 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
     CUSCI_CUDA(ctx, cudaFuncSetAttribute(tile_scatter_kernel<W, false, 9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scatter_smem<W, 9>()));
     CUSCI_CUDA(ctx, cudaFuncSetAttribute(bucket_unique_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     CUSCI_CUDA(ctx, cudaFuncSetAttribute(scatter1_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scatter1_smem<W>()));
+    CUSCI_CUDA(ctx, cudaFuncSetAttribute(tile_scatter_atomic_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scatter_smem<W, 8>()));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&dper[W], bucket_unique_kernel<W>, kBU, C::SMEM);
     if (dper[W] < 1) dper[W] = 1;
     attr[W] = true;
   }
   const uint64_t* part = in;
+  uint64_t* ibase = nullptr;  // bucket input starts when the last pass left bucket regions
   if (Bmax > 0) {
     std::vector<uint32_t> gstart{0u, (uint32_t)n};  // current groups (host): compact prefix ...
     std::vector<uint64_t> rstart, rend;                // ... or, after the hist-free pass, input regions
@@ -1010,6 +1134,66 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
       ctx->dstats[7] += n;
       return CUSCI_OK;
     };
+    // the last pass, hist-free too: bucket regions of cap2 keys in a fresh buffer
+    auto run_pass_last_regions = [&](int bits) -> int {
+      const int Btot = done + bits;
+      const uint64_t nbk2 = 1ull << Btot;
+      const uint64_t mean = n >> Btot;
+      const uint64_t cap2 = mean + mean / 5 + 1024;  // duplicates make bucket sizes spread more than keys
+      const uint32_t G = (uint32_t)gstart.size() - 1;
+      std::vector<PTile> tl;
+      tl.reserve(n / kPTile + G + 1);
+      for (uint32_t g = 0; g < G; g++) {
+        const uint64_t gs = rstart[g], ge = rend[g];
+        for (uint64_t st = gs; st < ge; st += kPTile)
+          tl.push_back(PTile{st, (uint32_t)std::min<uint64_t>(kPTile, ge - st), 0u, (uint64_t)g});
+      }
+      const uint32_t nt = (uint32_t)tl.size();
+      uint64_t* r2;
+      CUSCI_TRY(s.get_t((nbk2 * cap2 + 2) * W, &r2));  // outer scope: read by the bucket kernel
+      CUSCI_TRY(s.get_t(nbk2, &ibase));
+      Scratch ps(ctx);
+      PTile* dtl;
+      unsigned long long* gcur2;
+      int* ovf;
+      CUSCI_TRY(ps.get_t(std::max<uint32_t>(nt, 1), &dtl));
+      CUSCI_TRY(ps.get_t(nbk2, &gcur2));
+      CUSCI_TRY(ps.get_t(1, &ovf));
+      CUSCI_CUDA(ctx, cudaMemcpyAsync(dtl, tl.data(), nt * sizeof(PTile), cudaMemcpyHostToDevice, ctx->stream));
+      CUSCI_CUDA(ctx, cudaMemsetAsync(gcur2, 0, nbk2 * sizeof(unsigned long long), ctx->stream));
+      CUSCI_CUDA(ctx, cudaMemsetAsync(ovf, 0, sizeof(int), ctx->stream));
+      CUSCI_LAUNCH(ctx, PT_RADIX_DOWN, tile_scatter_atomic_kernel<W><<<nt, kST, scatter_smem<W, 8>(), ctx->stream>>>(part, use_tma, dtl, done + bits, 1u << bits, gcur2, cap2, r2, ovf));
+      std::vector<uint64_t> cnt(nbk2), ib(nbk2);
+      std::vector<uint32_t> offh(nbk2 + 1);
+      CUSCI_CUDA(ctx, cudaMemcpyAsync(cnt.data(), gcur2, nbk2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
+      int hv = 0;
+      CUSCI_CUDA(ctx, cudaMemcpyAsync(&hv, ovf, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+      if (hv) {
+        ibase = nullptr;
+        return -1;  // a bucket region overflowed: redo the pass with histograms
+      }
+      uint64_t acc = 0;
+      for (uint64_t b = 0; b < nbk2; b++) {
+        offh[b] = (uint32_t)acc;
+        ib[b] = b * cap2;
+        acc += cnt[b];
+      }
+      offh[nbk2] = (uint32_t)acc;
+      CUSCI_CUDA(ctx, cudaMemcpyAsync(off, offh.data(), (nbk2 + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->stream));
+      CUSCI_CUDA(ctx, cudaMemcpyAsync(ibase, ib.data(), nbk2 * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+      CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // host vectors die at scope end
+      part = r2;
+      done += bits;
+      ctx->dstats[2] += n;
+      rstart.clear();
+      rend.clear();
+      return CUSCI_OK;
+    };
+    static const int last_regions_knob = [] {
+      const char* e = getenv("CUSCI_HIST_FREE_LAST");  // tuning knob (0 disables)
+      return e ? atoi(e) : 1;
+    }();
     const int bits1 = std::min(8, Bmax);
     // the plan after pass 1 depends on the sketch, so pass 1 is "last" only if nothing can follow
     bool regions = false;
@@ -1037,6 +1221,11 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
       const int np = (rest + max_bits - 1) / max_bits;
       for (int pi = 0; pi < np; pi++) {
         const int bits = (rest - (done - bits1) + (np - pi) - 1) / (np - pi);  // even split
+        if (regions && np == 1 && bits <= 8 && last_regions_knob) {
+          const int rc = run_pass_last_regions(bits);
+          if (rc == CUSCI_OK) continue;
+          if (rc != -1) return rc;
+        }
         CUSCI_TRY(run_pass(bits, false, pi == np - 1));
       }
       if (np == 0) {  // pass 1 already made the buckets: its groups are the bucket offsets
@@ -1066,7 +1255,7 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
   const uint32_t nb = nbk << V;  // work units (sub-buckets)
   uint64_t* tmp = (part == a) ? b2 : a;
   const unsigned dgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(nb, (uint64_t)ctx->num_sms * dper[W]));
-  CUSCI_LAUNCH(ctx, PT_HASH, bucket_unique_kernel<W><<<dgrid, kBU, C::SMEM, ctx->stream>>>(part, part == in ? 1 : 0, use_tma, off, nbk, B, V, lf, vdcap, tmp, surv, flags));
+  CUSCI_LAUNCH(ctx, PT_HASH, bucket_unique_kernel<W><<<dgrid, kBU, C::SMEM, ctx->stream>>>(part, part == in ? 1 : 0, use_tma, off, ibase, nbk, B, V, lf, vdcap, tmp, surv, flags));
   // pack the buckets' survivors in bucket order
   CUSCI_CUDA(ctx, cudaMemsetAsync(surv64, 0, (nb + 1) * sizeof(uint64_t), ctx->stream));
   CUSCI_CUDA(ctx, cudaMemcpy2DAsync(surv64, sizeof(uint64_t), surv, sizeof(uint32_t), sizeof(uint32_t), nb,

@@ -500,6 +500,37 @@ def test_dedup_hist_free_pass_overflow_falls_back(P, ctx):
     assert torch.equal(torch.sort(ui ^ flip).values, torch.sort(base ^ flip).values)
 
 
+@pytest.mark.parametrize("W", [1, 2])
+def test_dedup_histogram_free_passes(P, ctx, W):
+    """1e8 keys (4e7 distinct): both partition passes run without histograms
+    (region cursors), checked by the stats, the exact count, strict hash order
+    and set equality."""
+    g = torch.Generator(device="cuda").manual_seed(9 + W)
+    D, n = 40_000_000, 100_000_000
+    C = 0x9E3779B97F4A7C15 - (1 << 64)
+    base = torch.arange(1, D + 1, dtype=torch.int64, device="cuda") * C
+    if W == 2:
+        base = torch.stack([base, torch.arange(D, dtype=torch.int64, device="cuda") % 977], dim=1)
+    keys = torch.cat([base, base[torch.randint(0, D, (n - D,), device="cuda", generator=g)]])
+    keys = keys[torch.randperm(n, device="cuda", generator=g)].contiguous()
+    ctx.dedup_stats(reset=True)
+    u = ctx.dedup_global(P.Space(64 * W, 1, 1), keys.view(torch.uint64).reshape(-1, W))
+    st = ctx.dedup_stats(reset=True)
+    assert st["hist_keys"] == 0 and st["hist_free_keys"] == n and st["key_passes"] == 2 * n, st
+    assert u.shape[0] == D
+    flip = -(1 << 63)
+    if W == 1:
+        ui = u.view(torch.int64).reshape(-1)
+        h = _t_fmix64(ui) ^ flip
+        assert bool((h[1:] > h[:-1]).all())
+        assert torch.equal(torch.sort(ui ^ flip).values, torch.sort(base ^ flip).values)
+    else:
+        got = synth.sort_keys(u.cpu().numpy().reshape(-1, 2))
+        ref = synth.sort_keys(base.cpu().numpy().view(np.uint64).reshape(-1, 2))
+        assert np.array_equal(got, ref)
+        assert_hash_sorted_unique(u.cpu().numpy().reshape(-1, 2), 2)
+
+
 _AT_SCALE = r"""
 import sys, torch
 sys.path.insert(0, %r)
