@@ -387,55 +387,148 @@ __global__ void sparse_locate_kernel(const uint64_t* __restrict__ small, uint64_
 
 // big[j] -> out[j + shift(j)], shift(j) = rank[upper_bound(pos, j)]
 // (rank = exclusive scan of keep, rank[ns] = total inserts)
+// Copy kernels: one warp per span of SPAN = 32 R consecutive keys, R keys per
+// lane loaded before anything is stored (independent loads in flight, no
+// block barriers).  The order check compares each key's hash with its
+// predecessor's, taken from a neighbouring lane (one extra load per span).
+template <int W> struct CopyCfg {
+  static constexpr int R = W == 1 ? 16 : 8;
+  static constexpr uint32_t SPAN = 32 * R;
+};
+// strict order check of a span's keys x[] (predecessor of the span: pw/hw)
 template <int W>
-__global__ void sparse_copy_kernel(const uint64_t* __restrict__ big, uint64_t nb, const uint64_t* __restrict__ pos,
-                                   const uint64_t* __restrict__ rank, uint64_t ns, uint64_t* __restrict__ out,
-                                   int* __restrict__ bad /* non-null: also check big's strict hash order */) {
-  constexpr uint32_t CH = 4096;  // big keys per CTA chunk
-  __shared__ uint64_t s_u0, s_u1;
-  for (uint64_t j0 = (uint64_t)blockIdx.x * CH; j0 < nb; j0 += (uint64_t)gridDim.x * CH) {
-    const uint64_t j1 = min(nb, j0 + CH);
-    if (threadIdx.x < 2) {  // inserts with pos in (j0 - 1, j1 - 1]: indices [u0, u1)
-      const uint64_t v = threadIdx.x == 0 ? j0 : j1;  // upper_bound(pos, v - 1) = first pos >= v
-      uint64_t lo = 0, hi = ns;
-      while (lo < hi) {
-        const uint64_t mid = (lo + hi) >> 1;
-        if (pos[mid] < v) lo = mid + 1;
-        else hi = mid;
-      }
-      if (threadIdx.x == 0) s_u0 = lo;
-      else s_u1 = lo;
+__device__ __forceinline__ bool span_bad(const KeyT<W> (&x)[CopyCfg<W>::R], uint64_t j0, uint64_t j1,
+                                         const KeyT<W>& pw, uint64_t hw) {
+  constexpr int R = CopyCfg<W>::R;
+  const unsigned lane = lane_id();
+  bool bad = false;
+  uint64_t hl = hw;  // hash of the previous row's lane-31 key
+  KeyT<W> kl = pw;
+#pragma unroll
+  for (int r = 0; r < R; r++) {
+    const uint64_t j = j0 + (uint64_t)r * 32 + lane;
+    const uint64_t h = hk_hi(x[r]);
+    uint64_t hp = __shfl_up_sync(kFull, h, 1);
+    KeyT<W> kp;
+    kp.w0 = __shfl_up_sync(kFull, x[r].w0, 1);
+    if constexpr (W == 2) kp.w1 = __shfl_up_sync(kFull, x[r].w1, 1);
+    if (lane == 0) {
+      hp = hl;
+      kp = kl;
     }
-    __syncthreads();
-    // note: an insert with pos == j is placed before big[j], so big[j]'s shift
-    // counts inserts with pos <= j: rank at the first pos > j
-    const uint64_t u0 = s_u0, u1 = s_u1;
-    for (uint64_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
-      uint64_t lo = u0, hi = u1;  // first index in [u0, u1) with pos > j (few candidates)
-      while (lo < hi) {
-        const uint64_t mid = (lo + hi) >> 1;
-        if (pos[mid] <= j) lo = mid + 1;
-        else hi = mid;
-      }
-      const KeyT<W> x = load_key<W>(big, j);
-      store_key<W>(out, j + rank[lo], x);
-      if (bad && j > 0 && !hk_lt<W>(load_key<W>(big, j - 1), x)) *bad = 1;  // (j-1 is an L1 hit)
-    }
-    __syncthreads();
+    if (j < j1 && j > 0) bad |= hp > h || (hp == h && !hk_lt<W>(kp, x[r]));
+    hl = __shfl_sync(kFull, h, 31);
+    kl.w0 = __shfl_sync(kFull, x[r].w0, 31);
+    if constexpr (W == 2) kl.w1 = __shfl_sync(kFull, x[r].w1, 31);
   }
+  return bad;
+}
+
+// cb[s] = first i with pos[i] >= min(s SPAN, nb): the inserts before span s's keys
+template <int W>
+__global__ void sparse_bounds_kernel(const uint64_t* __restrict__ pos, uint64_t ns, uint64_t nb, uint64_t nsp,
+                                     uint64_t* __restrict__ cb) {
+  const uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > nsp) return;
+  const uint64_t v = std::min<uint64_t>(c * CopyCfg<W>::SPAN, nb);
+  uint64_t lo = 0, hi = ns;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (pos[mid] < v) lo = mid + 1;
+    else hi = mid;
+  }
+  cb[c] = lo;
+}
+
+// out[j + shift(j)] = big[j], shift(j) = rank at the first insert with pos > j
+// (an insert with pos == j is placed before big[j]).  A span with at most 31
+// inserts holds their positions / ranks in lanes; more fall back to a search.
+template <int W>
+__global__ void __launch_bounds__(256) sparse_copy_kernel(const uint64_t* __restrict__ big, uint64_t nb,
+                                                          const uint64_t* __restrict__ pos,
+                                                          const uint64_t* __restrict__ rank,
+                                                          const uint64_t* __restrict__ cb,
+                                                          uint64_t* __restrict__ out,
+                                                          int* __restrict__ bad /* non-null: also check big's strict hash order */) {
+  constexpr int R = CopyCfg<W>::R;
+  constexpr uint32_t SPAN = CopyCfg<W>::SPAN;
+  const unsigned lane = lane_id();
+  const uint64_t nsp = (nb + SPAN - 1) / SPAN;
+  const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x / 32);
+  bool badl = false;
+  for (uint64_t sp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; sp < nsp; sp += nw) {
+    const uint64_t j0 = sp * SPAN, j1 = std::min<uint64_t>(nb, j0 + SPAN);
+    KeyT<W> x[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      const uint64_t j = j0 + (uint64_t)r * 32 + lane;
+      if (j < j1) x[r] = load_key<W>(big, j);
+    }
+    KeyT<W> pw{};
+    if (bad && j0 > 0) pw = load_key<W>(big, j0 - 1);
+    const uint64_t u0 = cb[sp], u1 = cb[sp + 1];
+    const uint32_t m = (uint32_t)(u1 - u0);
+    uint64_t lp = ~0ull, lr = 0;  // lane i < m: insert u0 + i's position; lane i <= m: its rank
+    if (m < 32) {
+      if (lane < m) lp = pos[u0 + lane];
+      if (lane <= m) lr = rank[u0 + lane];
+    }
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      const uint64_t j = j0 + (uint64_t)r * 32 + lane;
+      uint64_t shift;
+      if (m < 32) {
+        uint32_t cnt = 0;
+        for (uint32_t i = 0; i < m; i++) cnt += __shfl_sync(kFull, lp, i) <= j;
+        shift = __shfl_sync(kFull, lr, cnt);
+      } else {
+        uint64_t lo = u0, hi = u1;
+        while (lo < hi) {
+          const uint64_t mid = (lo + hi) >> 1;
+          if (pos[mid] <= j) lo = mid + 1;
+          else hi = mid;
+        }
+        shift = rank[lo];
+      }
+      if (j < j1) store_key<W>(out, j + shift, x[r]);
+    }
+    if (bad) badl |= span_bad<W>(x, j0, j1, pw, hk_hi(pw));
+  }
+  if (badl) *bad = 1;
 }
 
 // empty pool: out = U (and ins = U) in one pass, checking U's strict hash order
 template <int W>
-__global__ void copy_check_kernel(const uint64_t* __restrict__ U, uint64_t n, uint64_t* __restrict__ out,
-                                  uint64_t* __restrict__ ins, int* __restrict__ bad) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const KeyT<W> x = load_key<W>(U, i);
-    store_key<W>(out, i, x);
-    if (ins) store_key<W>(ins, i, x);
-    if (i > 0 && !hk_lt<W>(load_key<W>(U, i - 1), x)) *bad = 1;
+__global__ void __launch_bounds__(256) copy_check_kernel(const uint64_t* __restrict__ U, uint64_t n,
+                                                         uint64_t* __restrict__ out, uint64_t* __restrict__ ins,
+                                                         int* __restrict__ bad) {
+  constexpr int R = CopyCfg<W>::R;
+  constexpr uint32_t SPAN = CopyCfg<W>::SPAN;
+  const unsigned lane = lane_id();
+  const uint64_t nsp = (n + SPAN - 1) / SPAN;
+  const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x / 32);
+  bool badl = false;
+  for (uint64_t sp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; sp < nsp; sp += nw) {
+    const uint64_t j0 = sp * SPAN, j1 = std::min<uint64_t>(n, j0 + SPAN);
+    KeyT<W> x[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      const uint64_t j = j0 + (uint64_t)r * 32 + lane;
+      if (j < j1) x[r] = load_key<W>(U, j);
+    }
+    KeyT<W> pw{};
+    if (j0 > 0) pw = load_key<W>(U, j0 - 1);
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      const uint64_t j = j0 + (uint64_t)r * 32 + lane;
+      if (j < j1) {
+        store_key<W>(out, j, x[r]);
+        if (ins) store_key<W>(ins, j, x[r]);
+      }
+    }
+    badl |= span_bad<W>(x, j0, j1, pw, hk_hi(pw));
   }
+  if (badl) *bad = 1;
 }
 
 template <int W>
@@ -509,7 +602,7 @@ int merge_impl(cusci_ctx* ctx, cusci_pool* pool, const uint64_t* U, uint64_t nU,
   uint64_t h[3];
   if (nS == 0) {
     // empty pool: S' = U (validated strictly increasing in the hash order), a copy
-    const unsigned cg = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nU + 255) / 256, (uint64_t)ctx->num_sms * 16));
+    const unsigned cg = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nU + 8 * CopyCfg<W>::SPAN - 1) / (8 * CopyCfg<W>::SPAN), (uint64_t)ctx->num_sms * 8));
     CUSCI_LAUNCH(ctx, PT_CHECK, copy_check_kernel<W><<<cg, 256, 0, ctx->stream>>>(U, nU, dst, (uint64_t*)insp, bad));
     CUSCI_CUDA(ctx, cudaMemcpyAsync((char*)ctx->host_pinned + 16, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
@@ -545,8 +638,12 @@ int merge_impl(cusci_ctx* ctx, cusci_pool* pool, const uint64_t* U, uint64_t nU,
     CUSCI_CUDA(ctx, cudaMemcpy2DAsync(keep64, sizeof(uint64_t), keep, sizeof(uint32_t), sizeof(uint32_t), nsm,
                                       cudaMemcpyDeviceToDevice, ctx->stream));
     CUSCI_TRY(scan_exclusive_u64(ctx, keep64, rank, nsm + 1, nullptr));
-    const unsigned bg = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nbg + 4095) / 4096, (uint64_t)ctx->num_sms * 8));
-    CUSCI_LAUNCH(ctx, PT_MERGE_TILE, sparse_copy_kernel<W><<<bg, 256, 0, ctx->stream>>>(big, nbg, pos, rank, nsm, dst, u_small ? nullptr : bad));
+    const uint64_t nsp = (nbg + CopyCfg<W>::SPAN - 1) / CopyCfg<W>::SPAN;
+    uint64_t* cb;
+    CUSCI_TRY(s.get_t(nsp + 1, &cb));
+    CUSCI_LAUNCH(ctx, PT_MERGE_SPLIT, sparse_bounds_kernel<W><<<(unsigned)((nsp + 1 + 255) / 256), 256, 0, ctx->stream>>>(pos, nsm, nbg, nsp, cb));
+    const unsigned bg = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nsp + 7) / 8, (uint64_t)ctx->num_sms * 8));
+    CUSCI_LAUNCH(ctx, PT_MERGE_TILE, sparse_copy_kernel<W><<<bg, 256, 0, ctx->stream>>>(big, nbg, pos, rank, cb, dst, u_small ? nullptr : bad));
     CUSCI_LAUNCH(ctx, PT_MERGE_TILE, sparse_place_kernel<W><<<cg, 256, 0, ctx->stream>>>(small, nsm, pos, keep, rank, dst, u_small ? (uint64_t*)insp : nullptr));
     CUSCI_CUDA(ctx, cudaMemcpyAsync(ctx->host_pinned, rank + nsm, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
     CUSCI_CUDA(ctx, cudaMemcpyAsync((char*)ctx->host_pinned + 16, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
