@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--eps", type=float, default=0.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-stage3", action="store_true", help="skip the Stage-3 contraction measurement (SURVEY 8(f) f1)")
+    ap.add_argument("--no-f2", action="store_true", help="skip the regular-sampling dedup measurement (SURVEY 8(f) f2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=None, help="parents in the oracle's bounded sample")
     return ap.parse_args()
@@ -375,6 +376,56 @@ def main():
                   "e_checksum": float(e_all.abs().sum().item())}
         del ukeys, psi, e_all
 
+    # ---------------- the paper's regular-sampling sorted dedup (not in the headline step):
+    # dedup_sorted on one batch's records against dedup_global on the same keys, and
+    # Table-1 balance (max/min, CV of the owned unique shard sizes) for P = 8 virtual
+    # ranks (the batch split by parent, as ranks would own it): regular-sampling
+    # splitters (S = 1024, PAPER.md :454) vs the hash owner (DESIGN.md r9)
+    f2 = None
+    if not args.no_f2 and world == 1 and batches:
+        a, b = batches[0]
+        rec = ctx.gen_coupled(sp, shard[a:b], di, args.eps, out=out)
+        kk = rec.keys
+        def timed(fn, reps=2):
+            fn()
+            torch.cuda.synchronize()
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t0.record(stream)
+            for _ in range(reps):
+                r = fn()
+                del r
+            t1.record(stream)
+            torch.cuda.synchronize()
+            return t0.elapsed_time(t1) / reps
+        ms_sorted = timed(lambda: ctx.dedup_sorted(sp, kk, 1024))
+        ms_hash = timed(lambda: ctx.dedup_global(sp, kk))
+        Pv, Sv = 8, 1024
+        ends = [a + (b - a) * i // Pv for i in range(Pv + 1)]
+        smp, spl_in = [], None
+        for i in range(Pv):   # Step 1 per virtual rank: sort + unique, regular samples
+            ri = ctx.gen_coupled(sp, shard[ends[i]:ends[i + 1]], di, args.eps, out=out, with_src=False)
+            d = ctx.sort_unique(sp, ri.keys)
+            smp.append(ctx.regular_samples(sp, d, Sv).clone())
+            del d
+        spl = ctx.select_splitters(sp, torch.cat(smp), Pv)
+        rec = ctx.gen_coupled(sp, shard[a:b], di, args.eps, out=out)
+        glob_sorted = ctx.sort_unique(sp, rec.keys)
+        bnd = ctx.split_bounds(sp, glob_sorted, spl, Pv)
+        n_uni = int(glob_sorted.shape[0])
+        del glob_sorted
+        _, hcounts = ctx.dedup_partition(sp, rec.keys, Pv)
+        def bal(c):
+            c = np.asarray(c, dtype=np.float64)
+            return {"sizes": [int(x) for x in c], "max_over_min": float(c.max() / max(c.min(), 1)),
+                    "cv": float(c.std() / c.mean())}
+        f2 = {"records": int(rec.count), "unique": n_uni,
+              "dedup_sorted_ms": ms_sorted, "dedup_sorted_keys_per_s": rec.count / (ms_sorted / 1e3),
+              "dedup_global_ms": ms_hash, "dedup_global_keys_per_s": rec.count / (ms_hash / 1e3),
+              "table1_P8": {"samples_per_rank": Sv,
+                            "regular_sampling": bal([bnd[r + 1] - bnd[r] for r in range(Pv)]),
+                            "hash_owner": bal(hcounts)}}
+
     # ---------------- roofline of the dominant kernel class
     peaks = {}
     try:
@@ -465,6 +516,7 @@ def main():
             "kernel_roofline": kernels,
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])},
             "stage3_contract": stage3,
+            "f2_regular_sampling": f2,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),

@@ -181,6 +181,44 @@ int dedup_partition(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* confi
 int dedup_finalize(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* keys, uint64_t n,
                    cusci_keys* unique_sorted);
 
+/* ---- the paper's sort-based regular-sampling dedup ------
+ * PAPER.md Sec 4.1.1 :448-462 ("Sort-Based Regular Sampling De-duplication",
+ * Steps 1-3).  Key order here is the big-integer order of the configuration
+ * bitstring (bit t of the key = orbital t; at words = 2 word 1 is the high
+ * word), NOT the pool's hash order.  All arrays [count][words] uint64.
+ *
+ * dedup_sorted (COLLECTIVE over ctx's ranks; world <= 256): Step 1 local LSD
+ *   radix sort + unique, n_samples (1..65536) regular samples at indices
+ *   floor(k |D| / n_samples) (all of D if |D| < n_samples); Step 2 all-gather
+ *   of the samples, sort, P-1 splitters sorted[floor(r M / P)], r = 1..P-1,
+ *   lower-bound partition of the local array; Step 3 NCCL all-to-all-v and
+ *   sort + unique of the received runs.  owned_sorted receives this rank's
+ *   shard (allocated through the ctx allocator, caller frees): the distinct
+ *   keys x of the union of all ranks' configs with spl_r <= x < spl_{r+1}
+ *   (spl_0 = -inf, spl_P = +inf), ascending.  splitters_host (HOST,
+ *   nullable, [(P-1)][words]) receives the splitters.  world = 1: the sorted
+ *   unique keys.  Errors: E_INVALID_ARG (bad arguments on any rank: every
+ *   rank returns it), E_OOM, E_CUDA / E_NCCL (context unusable).
+ *
+ * Building blocks (one GPU, no communication; the virtual-rank tests and the
+ * bench's balance metrics compose them):
+ *   sort_unique: out <- sorted unique keys of configs (DEVICE, n < 2^32).
+ *   regular_samples: samples (DEVICE, >= min(n_samples, n) keys) <- the
+ *     regular samples of a sorted unique array; *n_taken (HOST) their number.
+ *   select_splitters: splitters (DEVICE, [n_parts-1]) <- the splitters of
+ *     n_samples gathered samples (DEVICE, any order; not modified).
+ *   split_bounds: bounds (HOST, [n_parts+1]) <- 0, lower_bound(sorted,
+ *     spl_r) for r = 1..n_parts-1, n.  n_parts in 1..256. */
+int dedup_sorted(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* configs, uint64_t n, int n_samples,
+                 cusci_keys* owned_sorted, uint64_t* splitters_host);
+int sort_unique(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* configs, uint64_t n, cusci_keys* out);
+int regular_samples(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* sorted, uint64_t n, int n_samples,
+                    uint64_t* samples, uint64_t* n_taken);
+int select_splitters(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* samples, uint64_t n_samples, int n_parts,
+                     uint64_t* splitters);
+int split_bounds(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* sorted, uint64_t n, const uint64_t* splitters,
+                 int n_parts, uint64_t* bounds);
+
 /* ---- step 3: the GPU-resident configuration pool --------------------------- */
 
 /* Create an empty pool (capacity = initial key capacity; it grows). */

@@ -12,6 +12,7 @@ from __future__ import annotations
 import ctypes
 import os
 
+import numpy as np
 import torch
 
 from ._lib import CUSCI_ERRORS, CusciError, lib, LIB_PATH  # noqa: F401
@@ -250,6 +251,64 @@ class Context:
                                    n_owners, ctypes.byref(k), counts)
         self._check(rc, "dedup_partition")
         return self._take(k.keys, int(k.count), W), [int(c) for c in counts]
+
+    # ---- the paper's regular-sampling sorted dedup (PAPER.md :448-462)
+    def dedup_sorted(self, space: Space, configs: torch.Tensor, n_samples: int = 1024, want_splitters: bool = False):
+        """COLLECTIVE: this rank's shard of the distinct keys in the big-integer key order
+        (regular-sampling splitters); with want_splitters also the (P-1, W) host splitters."""
+        W = space.words
+        cfg = _as_u64_2d(configs, W)
+        k = _Keys()
+        sp = space._c()
+        nsp = max(self.world - 1, 1) * W
+        spl = (ctypes.c_uint64 * nsp)()
+        rc = lib().dedup_sorted(self._ctx, ctypes.byref(sp), ctypes.c_void_p(cfg.data_ptr()), cfg.shape[0], n_samples,
+                                ctypes.byref(k), spl)
+        self._check(rc, "dedup_sorted")
+        out = self._take(k.keys, int(k.count), W)
+        if want_splitters:
+            return out, np.array(spl[:(self.world - 1) * W], dtype=np.uint64).reshape(-1, W)
+        return out
+
+    def sort_unique(self, space: Space, configs: torch.Tensor) -> torch.Tensor:
+        """Sorted (big-integer order) unique keys of configs (Step 1 of the paper's dedup)."""
+        W = space.words
+        cfg = _as_u64_2d(configs, W)
+        k = _Keys()
+        sp = space._c()
+        self._check(lib().sort_unique(self._ctx, ctypes.byref(sp), ctypes.c_void_p(cfg.data_ptr()), cfg.shape[0],
+                                      ctypes.byref(k)), "sort_unique")
+        return self._take(k.keys, int(k.count), W)
+
+    def regular_samples(self, space: Space, sorted_keys: torch.Tensor, n_samples: int) -> torch.Tensor:
+        W = space.words
+        srt = _as_u64_2d(sorted_keys, W)
+        out = torch.empty((max(min(n_samples, srt.shape[0]), 1), W), dtype=torch.uint64, device=self.device)
+        taken = ctypes.c_uint64(0)
+        sp = space._c()
+        self._check(lib().regular_samples(self._ctx, ctypes.byref(sp), ctypes.c_void_p(srt.data_ptr()), srt.shape[0],
+                                          n_samples, ctypes.c_void_p(out.data_ptr()), ctypes.byref(taken)),
+                    "regular_samples")
+        return out[:taken.value]
+
+    def select_splitters(self, space: Space, samples: torch.Tensor, n_parts: int) -> torch.Tensor:
+        W = space.words
+        smp = _as_u64_2d(samples, W)
+        out = torch.zeros((max(n_parts - 1, 1), W), dtype=torch.uint64, device=self.device)
+        sp = space._c()
+        self._check(lib().select_splitters(self._ctx, ctypes.byref(sp), ctypes.c_void_p(smp.data_ptr()), smp.shape[0],
+                                           n_parts, ctypes.c_void_p(out.data_ptr())), "select_splitters")
+        return out[:n_parts - 1]
+
+    def split_bounds(self, space: Space, sorted_keys: torch.Tensor, splitters: torch.Tensor, n_parts: int):
+        W = space.words
+        srt = _as_u64_2d(sorted_keys, W)
+        spl = _as_u64_2d(splitters, W) if n_parts > 1 else srt
+        b = (ctypes.c_uint64 * (n_parts + 1))()
+        sp = space._c()
+        self._check(lib().split_bounds(self._ctx, ctypes.byref(sp), ctypes.c_void_p(srt.data_ptr()), srt.shape[0],
+                                       ctypes.c_void_p(spl.data_ptr()), n_parts, b), "split_bounds")
+        return [int(x) for x in b]
 
     def dedup_finalize(self, space: Space, keys: torch.Tensor) -> torch.Tensor:
         W = space.words

@@ -14,7 +14,8 @@ CUSCI_ERRORS = {0: "OK", 1: "E_INVALID_ARG", 2: "E_INVALID_PARENT", 3: "E_CAPACI
 EXPORTS = ["cusci_nccl_unique_id", "cusci_init", "cusci_finalize", "cusci_last_error", "cusci_invalidate_integrals",
            "cusci_free", "cusci_kernel_launches", "cusci_profile_enable", "cusci_profile_read", "cusci_dedup_stats", "gen_coupled_bound", "gen_coupled", "gen_coupled_count",
            "dedup_global", "dedup_partition", "dedup_finalize", "cusci_pool_create", "cusci_pool_view",
-           "cusci_pool_copy", "cusci_pool_clear", "cusci_pool_destroy", "merge_space", "energy_contract"]
+           "cusci_pool_copy", "cusci_pool_clear", "cusci_pool_destroy", "merge_space", "energy_contract",
+           "dedup_sorted", "sort_unique", "regular_samples", "select_splitters", "split_bounds"]
 
 
 PROFILE_TAGS = ["prep", "validate", "gen", "bucket_unique", "pack", "part_hist", "part_scatter",
@@ -73,6 +74,16 @@ def lib():
     L.dedup_partition.restype = i32
     L.dedup_finalize.argtypes = [vp, vp, vp, u64, vp]
     L.dedup_finalize.restype = i32
+    L.dedup_sorted.argtypes = [vp, vp, vp, u64, i32, vp, vp]
+    L.dedup_sorted.restype = i32
+    L.sort_unique.argtypes = [vp, vp, vp, u64, vp]
+    L.sort_unique.restype = i32
+    L.regular_samples.argtypes = [vp, vp, vp, u64, i32, vp, P(u64)]
+    L.regular_samples.restype = i32
+    L.select_splitters.argtypes = [vp, vp, vp, u64, i32, vp]
+    L.select_splitters.restype = i32
+    L.split_bounds.argtypes = [vp, vp, vp, u64, vp, i32, vp]
+    L.split_bounds.restype = i32
     L.cusci_pool_create.argtypes = [vp, vp, u64, P(vp)]
     L.cusci_pool_create.restype = i32
     L.cusci_pool_view.argtypes = [vp, P(vp), P(u64)]

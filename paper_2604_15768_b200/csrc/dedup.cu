@@ -48,6 +48,62 @@ int agree_status(cusci_ctx* ctx, int local) {
   return *(int*)ctx->host_pinned;
 }
 
+}  // namespace
+
+// a10: counts exchange, then payload all-to-all-v over NCCL grouped send/recv
+// (bins back to back by destination, send[r] keys for rank r); the received
+// runs land back to back by source rank in *rbuf (from s).
+int exchange_bins(cusci_ctx* ctx, int W, const uint64_t* bins, const uint64_t* send, Scratch& s, uint64_t** rbuf_out,
+                  uint64_t* nrecv_out) {
+  const int P = ctx->world;
+  uint64_t *dsend, *drecv, recv[512];
+  CUSCI_TRY(s.get_t(P, &dsend));
+  CUSCI_TRY(s.get_t(P, &drecv));
+  memcpy(ctx->host_pinned, send, P * sizeof(uint64_t));
+  CUSCI_CUDA(ctx, cudaMemcpyAsync(dsend, ctx->host_pinned, P * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+  CUSCI_TRY(nccl_check(ctx, ncclGroupStart(), "group start"));
+  for (int r = 0; r < P; r++) {
+    CUSCI_TRY(nccl_check(ctx, ncclSend(dsend + r, 1, ncclUint64, r, ctx->comm, ctx->stream), "count send"));
+    CUSCI_TRY(nccl_check(ctx, ncclRecv(drecv + r, 1, ncclUint64, r, ctx->comm, ctx->stream), "count recv"));
+  }
+  CUSCI_TRY(nccl_check(ctx, ncclGroupEnd(), "group end"));
+  CUSCI_TRY(read_u64(ctx, drecv, recv, P));
+  uint64_t nrecv = 0, soff[512], roff[512];
+  {
+    uint64_t a = 0;
+    for (int r = 0; r < P; r++) {
+      soff[r] = a;
+      a += send[r];
+      roff[r] = nrecv;
+      nrecv += recv[r];
+    }
+  }
+  uint64_t* rbuf;
+  CUSCI_TRY(s.get_t(std::max<uint64_t>(nrecv, 1) * W, &rbuf));
+  Prof pf_x(ctx, PT_NCCL);
+  CUSCI_TRY(nccl_check(ctx, ncclGroupStart(), "group start"));
+  for (int r = 0; r < P; r++) {
+    if (r == ctx->rank) continue;
+    if (send[r])
+      CUSCI_TRY(nccl_check(ctx, ncclSend(bins + soff[r] * W, send[r] * W, ncclUint64, r, ctx->comm, ctx->stream), "send"));
+    if (recv[r])
+      CUSCI_TRY(nccl_check(ctx, ncclRecv(rbuf + roff[r] * W, recv[r] * W, ncclUint64, r, ctx->comm, ctx->stream), "recv"));
+  }
+  CUSCI_TRY(nccl_check(ctx, ncclGroupEnd(), "group end"));
+  if (send[ctx->rank])
+    CUSCI_CUDA(ctx, cudaMemcpyAsync(rbuf + roff[ctx->rank] * W, bins + soff[ctx->rank] * W, send[ctx->rank] * W * 8,
+                                    cudaMemcpyDeviceToDevice, ctx->stream));
+  *rbuf_out = rbuf;
+  *nrecv_out = nrecv;
+  return CUSCI_OK;
+}
+
+// collective status agreement (max over ranks)
+int agree_status_all(cusci_ctx* ctx, int local) { return agree_status(ctx, local); }
+int nccl_ok(cusci_ctx* ctx, ncclResult_t r, const char* what) { return nccl_check(ctx, r, what); }
+
+namespace {
+
 // local unique filter (a8) + owner partition (a9): the local dedup returns the
 // distinct keys in the hash order, which is owner-major, so the owner bins are
 // contiguous ranges (found by P binary searches).  bins_out holds >= n keys.
@@ -149,43 +205,8 @@ extern "C" int dedup_global(cusci_ctx* ctx, const cusci_space* sp, const uint64_
   uint64_t total = 0;
   CUSCI_TRY(W == 1 ? partition_impl<1>(ctx, configs, n, P, bins, send, &total)
                    : partition_impl<2>(ctx, configs, n, P, bins, send, &total));
-  // ---- a10: counts exchange, then payload all-to-all-v over NCCL
-  uint64_t *dsend, *drecv;
-  CUSCI_TRY(s.get_t(P, &dsend));
-  CUSCI_TRY(s.get_t(P, &drecv));
-  memcpy(ctx->host_pinned, send, P * sizeof(uint64_t));
-  CUSCI_CUDA(ctx, cudaMemcpyAsync(dsend, ctx->host_pinned, P * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
-  CUSCI_TRY(nccl_check(ctx, ncclGroupStart(), "group start"));
-  for (int r = 0; r < P; r++) {
-    CUSCI_TRY(nccl_check(ctx, ncclSend(dsend + r, 1, ncclUint64, r, ctx->comm, ctx->stream), "count send"));
-    CUSCI_TRY(nccl_check(ctx, ncclRecv(drecv + r, 1, ncclUint64, r, ctx->comm, ctx->stream), "count recv"));
-  }
-  CUSCI_TRY(nccl_check(ctx, ncclGroupEnd(), "group end"));
-  CUSCI_TRY(read_u64(ctx, drecv, recv, P));
-  uint64_t nrecv = 0, soff[512], roff[512];
-  {
-    uint64_t a = 0;
-    for (int r = 0; r < P; r++) {
-      soff[r] = a;
-      a += send[r];
-      roff[r] = nrecv;
-      nrecv += recv[r];
-    }
-  }
   uint64_t* rbuf;
-  CUSCI_TRY(s.get_t(std::max<uint64_t>(nrecv, 1) * W, &rbuf));
-  Prof pf_x(ctx, PT_NCCL);
-  CUSCI_TRY(nccl_check(ctx, ncclGroupStart(), "group start"));
-  for (int r = 0; r < P; r++) {
-    if (r == ctx->rank) continue;
-    if (send[r])
-      CUSCI_TRY(nccl_check(ctx, ncclSend(bins + soff[r] * W, send[r] * W, ncclUint64, r, ctx->comm, ctx->stream), "send"));
-    if (recv[r])
-      CUSCI_TRY(nccl_check(ctx, ncclRecv(rbuf + roff[r] * W, recv[r] * W, ncclUint64, r, ctx->comm, ctx->stream), "recv"));
-  }
-  CUSCI_TRY(nccl_check(ctx, ncclGroupEnd(), "group end"));
-  if (send[ctx->rank])
-    CUSCI_CUDA(ctx, cudaMemcpyAsync(rbuf + roff[ctx->rank] * W, bins + soff[ctx->rank] * W, send[ctx->rank] * W * 8,
-                                    cudaMemcpyDeviceToDevice, ctx->stream));
+  uint64_t nrecv;
+  CUSCI_TRY(exchange_bins(ctx, W, bins, send, s, &rbuf, &nrecv));
   return finalize_impl(ctx, sp, rbuf, nrecv, owned_unique);
 }

@@ -395,6 +395,12 @@ int owner_counts(cusci_ctx* ctx, int W, const uint64_t* keys, uint64_t n, int P,
 // unique compaction of sorted keys into out; count written to device *n_out_dev
 int unique_sorted_keys(cusci_ctx* ctx, int W, const uint64_t* in, uint64_t n, uint64_t* out,
                        uint64_t* n_out_dev);
+// dedup.cu: payload all-to-all-v of bins (send[r] keys to rank r, back to back)
+// into a scratch buffer *rbuf (received runs back to back by source rank)
+int exchange_bins(cusci_ctx* ctx, int W, const uint64_t* bins, const uint64_t* send, Scratch& s, uint64_t** rbuf,
+                  uint64_t* nrecv);
+int agree_status_all(cusci_ctx* ctx, int local);
+int nccl_ok(cusci_ctx* ctx, ncclResult_t r, const char* what);
 // sync the stream and read a device u64
 int read_u64(cusci_ctx* ctx, const uint64_t* dev, uint64_t* host, int count = 1);
 

@@ -621,3 +621,74 @@ def test_contract_rejects_large_products(P, ctx):
     with pytest.raises(P.CusciError) as e:
         ctx.energy_contract(sp, rec, len(par), uniq, psi)
     assert e.value.code == 1
+
+
+# ---- the paper's regular-sampling sorted dedup (oracle/sampling.py)
+def _f2_keys(W, n, seed):
+    return synth.zipf_keys(max(n, 1), W, 1.1, 1 << 16, seed=seed)[:n]
+
+
+@pytest.mark.parametrize("W,n", [(1, 0), (1, 1), (1, 4097), (1, 300_001), (2, 150_001)])
+def test_f2_sort_unique(P, ctx, W, n):
+    from oracle import sampling as S
+    sp = P.Space(64 * W, 1, 1)
+    keys = _f2_keys(W, n, 31 + W)
+    got = ctx.sort_unique(sp, torch.from_numpy(keys).cuda()).cpu().numpy().reshape(-1, W)
+    ref = S.from_ints(S.sort_unique(S.to_ints(keys, W)), W)
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("W", [1, 2])
+def test_f2_blocks_virtual_ranks(P, ctx, W):
+    """Steps 1-3 composed from the exported blocks over 5 virtual ranks on one GPU
+    (the NCCL transport is dedup_global's) against the oracle protocol."""
+    from oracle import sampling as S
+    sp = P.Space(64 * W, 1, 1)
+    keys = _f2_keys(W, 90_000, 41 + W)
+    Pn, Ssz = 5, 37
+    parts = [keys[i::Pn] for i in range(Pn)]
+    parts[3] = parts[3][:0]                                   # an empty rank
+    local = [S.to_ints(x, W) for x in parts]
+    D_ref = [S.sort_unique(x) for x in local]
+    D = [ctx.sort_unique(sp, torch.from_numpy(x).cuda()) if len(x) else torch.empty((0, W), dtype=torch.uint64, device="cuda")
+         for x in parts]
+    smp = []
+    for d, dr in zip(D, D_ref):
+        assert np.array_equal(d.cpu().numpy().reshape(-1, W), S.from_ints(dr, W))
+        s = ctx.regular_samples(sp, d, Ssz)
+        assert np.array_equal(s.cpu().numpy().reshape(-1, W), S.from_ints(S.regular_samples(dr, Ssz), W))
+        smp.append(s)
+    gathered = torch.cat(smp[::-1])                           # any order
+    spl = ctx.select_splitters(sp, gathered, Pn)
+    spl_ref = S.select_splitters([x for dr in D_ref for x in S.regular_samples(dr, Ssz)], Pn)
+    assert np.array_equal(spl.cpu().numpy().reshape(-1, W), S.from_ints(spl_ref, W))
+    recv = [[] for _ in range(Pn)]
+    for d, dr in zip(D, D_ref):
+        b = ctx.split_bounds(sp, d, spl, Pn)
+        assert b == S.split_bounds(dr, spl_ref)
+        for r in range(Pn):
+            recv[r].append(d[b[r]:b[r + 1]])
+    shards_ref, _ = S.dedup_sorted(local, Ssz)
+    for r in range(Pn):
+        got = ctx.sort_unique(sp, torch.cat(recv[r])).cpu().numpy().reshape(-1, W) if sum(len(x) for x in recv[r]) else np.zeros((0, W), np.uint64)
+        assert np.array_equal(got, S.from_ints(shards_ref[r], W)), r
+
+
+@pytest.mark.parametrize("W", [1, 2])
+def test_f2_dedup_sorted_world1(P, ctx, W):
+    from oracle import sampling as S
+    sp = P.Space(64 * W, 1, 1)
+    keys = _f2_keys(W, 200_003, 51 + W)
+    got = ctx.dedup_sorted(sp, torch.from_numpy(keys).cuda(), 64).cpu().numpy().reshape(-1, W)
+    assert np.array_equal(got, S.from_ints(S.sort_unique(S.to_ints(keys, W)), W))
+
+
+def test_f2_n2_records_sorted_dedup(P, ctx):
+    """Sorted dedup of a generated N2 stream equals the hash-order dedup's set, re-sorted."""
+    wl, ints, par = synth.workload_inputs("n2", n_parents=300)
+    sp = P.Space(wl.m, wl.n_alpha, wl.n_beta)
+    di = P.DeviceIntegrals(ints.h, ints.eri)
+    rec = ctx.gen_coupled(sp, torch.from_numpy(par).cuda(), di, 0.0, with_src=False)
+    got = ctx.dedup_sorted(sp, rec.keys, 256).cpu().numpy().reshape(-1)
+    ref = np.unique(oracle.dedup(rec.keys.cpu().numpy(), 1).reshape(-1))
+    assert np.array_equal(got, ref)

@@ -58,6 +58,23 @@ def _worker(rank, world, port, q):
             assert np.array_equal(shard, ref), (rank, W)
             tot = bench.allreduce_sum(dist, float(len(shard)))
             assert tot == len(oracle.dedup(allk, W))
+        # 4) the paper's regular-sampling protocol (oracle arithmetic)
+        from oracle import sampling as S
+        for W in (1, 2):
+            allk = synth.zipf_keys(40_000, W, 1.1, 1 << 12, seed=23)
+            local = [S.to_ints(x, W) for x in np.array_split(allk, world)]
+            D = S.sort_unique(local[rank])
+            gathered = [None] * world
+            dist.all_gather_object(gathered, S.regular_samples(D, 64))
+            spl = S.select_splitters([x for g in gathered for x in g], world)
+            b = S.split_bounds(D, spl)
+            outgoing = [D[b[r]:b[r + 1]] for r in range(world)]
+            # all-to-all-v of the runs (object transport)
+            got = [None] * world
+            dist.all_gather_object(got, outgoing)
+            shard = sorted(set(x for i in range(world) for x in got[i][rank]))
+            ref_shards, ref_spl = S.dedup_sorted(local, 64)
+            assert spl == ref_spl and shard == ref_shards[rank], (rank, W)
         q.put((rank, "ok"))
     except Exception as e:  # surface failures to the parent
         q.put((rank, repr(e)))
