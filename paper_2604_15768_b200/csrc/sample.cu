@@ -2,8 +2,9 @@
 // (Sec 4.1.1 :448-462, Steps 1-3, Fig. "unique").
 //
 //   Step 1  each rank sorts its keys (LSD radix sort over the m significant
-//           bits = the big-integer key order) and removes adjacent duplicates
-//           (reading r15: local unique before sampling), then takes
+//           bits = the big-integer key order) and removes duplicates (reading
+//           r15: local unique before sampling; the hash dedup runs
+//           first so only the survivors are sorted), then takes
 //           S regular samples at indices floor(k |D_i| / S), k = 0..S-1
 //           (all of D_i when |D_i| < S).
 //   Step 2  the samples are all-gathered (every rank computes what the
@@ -91,22 +92,27 @@ int args_ok(cusci_ctx* ctx, const cusci_space* sp) {
   return check_space(ctx, sp);
 }
 
-// Step 1: out (device, >= n keys) <- sorted unique keys; *u (host) their number
+// Step 1: out (device, >= n keys) <- sorted unique keys; *u (host) their number.
+// The hash dedup runs first (SURVEY 8(a) a11 variant: only the survivors are
+// sorted), then an LSD radix sort over the m significant bits -- the same set
+// and order as sort + adjacent unique of the raw buffer, with ~1/redundancy of
+// the sort traffic.
 int sort_unique_impl(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* configs, uint64_t n, uint64_t* out,
                      uint64_t* u) {
   const int W = sp->words;
   *u = 0;
   if (n == 0) return CUSCI_OK;
   Scratch s(ctx);
-  uint64_t *a, *b, *cnt;
+  uint64_t* a;
   CUSCI_TRY(s.get_t(n * W, &a));
-  CUSCI_TRY(s.get_t(n * W, &b));
-  CUSCI_TRY(s.get_t(1, &cnt));
-  CUSCI_CUDA(ctx, cudaMemcpyAsync(a, configs, n * W * 8, cudaMemcpyDeviceToDevice, ctx->stream));
-  uint64_t* srt;
-  CUSCI_TRY(radix_sort_keys(ctx, W, a, b, n, sp->m, &srt));
-  CUSCI_TRY(unique_sorted_keys(ctx, W, srt, n, out, cnt));
-  return read_u64(ctx, cnt, u);
+  uint64_t nu = 0;
+  CUSCI_TRY(local_dedup(ctx, W, configs, n, a, &nu));
+  uint64_t* srt = a;
+  if (nu) CUSCI_TRY(radix_sort_keys(ctx, W, a, out, nu, sp->m, &srt));
+  if (srt != out && nu) CUSCI_CUDA(ctx, cudaMemcpyAsync(out, srt, nu * W * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  *u = nu;
+  return CUSCI_OK;
 }
 
 int samples_impl(cusci_ctx* ctx, int W, const uint64_t* srt, uint64_t n, uint32_t S, uint64_t* out, uint64_t* taken) {
