@@ -286,6 +286,10 @@ __global__ void __launch_bounds__(kST, 2) tile_scatter_kernel(const uint64_t* __
   }
 }
 
+template <int W> constexpr size_t scatter_atomic_smem() {
+  return kSRing * ((size_t)SSCfg<W>::SUB + 2) * sizeof(KeyT<W>) + 2 * 256 * 8 + 3 * 256 * 4;
+}
+
 // The last (bucket-forming) pass after a hist-free first pass, also without a
 // histogram: every bucket (group g, digit d) gets a region of cap2 keys and the
 // tile reserves its runs with one global atomic per (sub-round, digit).  The
@@ -300,12 +304,11 @@ __global__ void __launch_bounds__(kST, 2) tile_scatter_atomic_kernel(const uint6
   constexpr int ITEMS = SSCfg<W>::SUB / kST;
   constexpr int SUB = SSCfg<W>::SUB;
   constexpr uint32_t RMAX = 256;
-  extern __shared__ __align__(16) unsigned char ssm[];  // scatter_smem<W, 8>() bytes
+  extern __shared__ __align__(16) unsigned char ssm[];  // scatter_atomic_smem<W>() bytes
   KeyT<W>* ring = reinterpret_cast<KeyT<W>*>(ssm);       // [kSRing][SUB + 2]
-  unsigned long long* dl = reinterpret_cast<unsigned long long*>(ring + kSRing * (SUB + 2));  // [256]
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(dl + RMAX);
-  uint32_t* lst = cnt + RMAX;
-  uint8_t* sdig = reinterpret_cast<uint8_t*>(lst + RMAX);
+  unsigned long long* dl = reinterpret_cast<unsigned long long*>(ring + kSRing * (SUB + 2));  // [2][256]
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(dl + 2 * RMAX);
+  uint32_t* lst = cnt + RMAX;  // [2][256]
   __shared__ __align__(8) uint64_t bar[kSRing];
   const PTile t = tiles[blockIdx.x];
   const uint64_t gbase = t.mbase * R;  // first bucket of the tile's group (R = 2^bits <= 256 digits)
@@ -317,20 +320,40 @@ __global__ void __launch_bounds__(kST, 2) tile_scatter_atomic_kernel(const uint6
     mbar_init_fence();
   }
   __syncthreads();
+  auto sub_len = [&](uint32_t r) { return min((uint32_t)SUB, t.len - r * SUB); };
   auto issue = [&](uint32_t r) {
     const uint32_t sl = r % kSRing;
     fence_proxy_async_smem();
-    issue_core<W>(in, t.start + (uint64_t)r * SUB, min((uint32_t)SUB, t.len - r * SUB), ring + sl * (SUB + 2), &bar[sl]);
+    issue_core<W>(in, t.start + (uint64_t)r * SUB, sub_len(r), ring + sl * (SUB + 2), &bar[sl]);
+  };
+  auto resolve = [&](uint32_t d, uint32_t cd, unsigned long long b) -> unsigned long long {
+    if (!cd) return ~0ull;
+    if (b + cd <= cap2) return (gbase + d) * cap2 + b;
+    *ovf = 1;
+    return ~0ull;
+  };
+  auto store_round = [&](uint32_t r) {
+    const uint32_t q = r & 1, m = sub_len(r);
+    const KeyT<W>* stage = ring + (r % kSRing) * (SUB + 2);
+    for (uint32_t j = threadIdx.x; j < m; j += kST) {
+      const KeyT<W> x = stage[j];
+      const uint32_t d = top_bits<W>(x, bsel) & (R - 1);
+      const unsigned long long bd = dl[q * RMAX + d];
+      if (bd != ~0ull) store_key<W>(out, bd + (j - lst[q * RMAX + d]), x);
+    }
   };
   if (tma && threadIdx.x == 0)
     for (uint32_t r = 0; r < min(nsub, (uint32_t)kSRing - 1); r++) issue(r);
   uint32_t phase = 0;
+  // pipelined reservation, as in scatter1_kernel: round r's atomics are
+  // consumed in round r + 1, round r - 1 is stored while round r is staged
+  unsigned long long bres = 0;
+  uint32_t pcd = 0;
   for (uint32_t r = 0; r < nsub; r++) {
-    const uint32_t sl = r % kSRing, r0 = r * SUB;
-    const uint32_t m = min((uint32_t)SUB, t.len - r0);
+    const uint32_t sl = r % kSRing, r0 = r * SUB, q = r & 1;
+    const uint32_t m = sub_len(r);
     KeyT<W>* buf = ring + sl * (SUB + 2);
     if (tma) {
-      if (threadIdx.x == 0 && r + kSRing - 1 < nsub) issue(r + kSRing - 1);
       const uint64_t s0 = t.start + r0;
       const bool issued = W == 1 ? (((s0 + m) & ~1ull) > ((s0 + 1) & ~1ull)) : m > 0;
       if (issued) {
@@ -351,7 +374,7 @@ __global__ void __launch_bounds__(kST, 2) tile_scatter_atomic_kernel(const uint6
         dr[u] = (d << 16) | atomicAdd(&cnt[d], 1u);
       }
     }
-    __syncthreads();  // the slot's keys are in registers: it becomes the stage
+    __syncthreads();  // counts final; the slot's keys are in registers: it becomes the stage
     if (threadIdx.x < 32) {  // warp 0: exclusive scan of the digit counts
       constexpr uint32_t DPL = RMAX / 32;
       uint32_t c[DPL], loc = 0;
@@ -368,40 +391,32 @@ __global__ void __launch_bounds__(kST, 2) tile_scatter_atomic_kernel(const uint6
       uint32_t ex = inc - loc;
 #pragma unroll
       for (uint32_t j = 0; j < DPL; j++) {
-        lst[threadIdx.x * DPL + j] = ex;
+        lst[q * RMAX + threadIdx.x * DPL + j] = ex;
         ex += c[j];
       }
     }
-    for (uint32_t d = threadIdx.x; d < RMAX; d += kST) {  // reserve the runs
-      const uint32_t cd = cnt[d];
-      unsigned long long v = ~0ull;
-      if (cd) {
-        const unsigned long long b = atomicAdd(&gcur[gbase + d], (unsigned long long)cd);
-        if (b + cd <= cap2) v = (gbase + d) * cap2 + b;
-        else *ovf = 1;
-      }
-      dl[d] = v;
+    if (threadIdx.x < RMAX) {  // publish the previous round's runs, reserve this round's
+      const uint32_t d = threadIdx.x;
+      if (r > 0) dl[(q ^ 1) * RMAX + d] = resolve(d, pcd, bres);
+      pcd = cnt[d];
+      bres = pcd ? atomicAdd(&gcur[gbase + d], (unsigned long long)pcd) : 0ull;
     }
     __syncthreads();
     KeyT<W>* stage = buf;
 #pragma unroll
     for (int u = 0; u < ITEMS; u++) {
       const uint32_t i = u * kST + threadIdx.x;
-      if (i < m) {
-        const uint32_t d = dr[u] >> 16;
-        const uint32_t pos = lst[d] + (dr[u] & 0xffffu);
-        stage[pos] = k[u];
-        sdig[pos] = (uint8_t)d;
-      }
+      if (i < m) stage[lst[q * RMAX + (dr[u] >> 16)] + (dr[u] & 0xffffu)] = k[u];
     }
-    __syncthreads();
-    for (uint32_t j = threadIdx.x; j < m; j += kST) {
-      const uint32_t d = sdig[j];
-      const unsigned long long b = dl[d];
-      if (b != ~0ull) store_key<W>(out, b + (j - lst[d]), stage[j]);
-    }
+    if (r > 0) store_round(r - 1);
     for (uint32_t d = threadIdx.x; d < RMAX; d += kST) cnt[d] = 0;
     __syncthreads();
+    if (tma && threadIdx.x == 0 && r + kSRing - 1 < nsub) issue(r + kSRing - 1);  // into round r-1's slot
+  }
+  if (nsub > 0) {
+    if (threadIdx.x < RMAX) dl[((nsub - 1) & 1) * RMAX + threadIdx.x] = resolve(threadIdx.x, pcd, bres);
+    __syncthreads();
+    store_round(nsub - 1);
   }
 }
 
@@ -424,11 +439,10 @@ __global__ void __launch_bounds__(kST, 2) scatter1_kernel(const uint64_t* __rest
   constexpr uint32_t RMAX = 256;
   extern __shared__ __align__(16) unsigned char ssm[];  // scatter1_smem<W>() bytes
   KeyT<W>* ring = reinterpret_cast<KeyT<W>*>(ssm);       // [kSRing][SUB + 2]
-  unsigned long long* dl = reinterpret_cast<unsigned long long*>(ring + kSRing * (SUB + 2));  // [256]
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(dl + RMAX);
-  uint32_t* lst = cnt + RMAX;
-  uint8_t* reg = reinterpret_cast<uint8_t*>(lst + RMAX);   // [kHllM] HLL registers, one byte each
-  uint8_t* sdig = reg + kHllM;                             // [SUB]
+  unsigned long long* dl = reinterpret_cast<unsigned long long*>(ring + kSRing * (SUB + 2));  // [2][256]
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(dl + 2 * RMAX);
+  uint32_t* lst = cnt + RMAX;                              // [2][256]
+  uint8_t* reg = reinterpret_cast<uint8_t*>(lst + 2 * RMAX);  // [kHllM] HLL registers, one byte each
   __shared__ __align__(8) uint64_t bar[kSRing];
   const bool tma = use_tma && ((reinterpret_cast<uintptr_t>(in) & 15u) == 0);
   const uint64_t nsub = (n + SUB - 1) / SUB;
@@ -441,24 +455,48 @@ __global__ void __launch_bounds__(kST, 2) scatter1_kernel(const uint64_t* __rest
   __syncthreads();
   // this CTA's k-th sub-round is blockIdx.x + k * gridDim.x
   auto sub_of = [&](uint64_t k) { return (uint64_t)blockIdx.x + k * gridDim.x; };
+  auto sub_len = [&](uint64_t k) { return (uint32_t)min((uint64_t)SUB, n - sub_of(k) * SUB); };
   auto issue = [&](uint64_t k) {  // thread 0: local sub-round k -> slot k % kSRing
-    const uint64_t r = sub_of(k);
     const uint32_t sl = (uint32_t)(k % kSRing);
     fence_proxy_async_smem();
-    issue_core<W>(in, r * SUB, (uint32_t)min((uint64_t)SUB, n - r * SUB), ring + sl * (SUB + 2), &bar[sl]);
+    issue_core<W>(in, sub_of(k) * SUB, sub_len(k), ring + sl * (SUB + 2), &bar[sl]);
+  };
+  // the run reservation of digit d (thread d) for the round whose atomic returned b
+  auto resolve = [&](uint32_t d, uint32_t cd, unsigned long long b) -> unsigned long long {
+    if (!cd) return ~0ull;  // no write
+    if (b + cd <= cap) return (unsigned long long)d * cap + b;
+    *ovf = 1;
+    return ~0ull;
+  };
+  // stores of local round k (staged, digit-ordered, in its slot)
+  auto store_round = [&](uint64_t k) {
+    const uint32_t q = (uint32_t)(k & 1);
+    const uint32_t m = sub_len(k);
+    const KeyT<W>* stage = ring + (uint32_t)(k % kSRing) * (SUB + 2);
+    for (uint32_t j = threadIdx.x; j < m; j += kST) {
+      const KeyT<W> x = stage[j];
+      const uint32_t d = (uint32_t)(x.w0 >> 56);
+      const unsigned long long bd = dl[q * RMAX + d];
+      if (bd != ~0ull) store_key<W>(out, bd + (j - lst[q * RMAX + d]), x);
+    }
   };
   uint64_t nk = 0;  // local sub-rounds
   if (blockIdx.x < nsub) nk = (nsub - blockIdx.x + gridDim.x - 1) / gridDim.x;
   if (tma && threadIdx.x == 0)
     for (uint64_t k = 0; k < min(nk, (uint64_t)kSRing - 1); k++) issue(k);
   uint32_t phase = 0;
+  // Pipelined reservation: round kk's global atomics are issued after its
+  // ranking and consumed one round later, so their L2 latency overlaps the
+  // next round's TMA wait + ranking; round kk-1 is stored from its slot while
+  // round kk is staged into its own.
+  unsigned long long bres = 0;  // thread d < 256: the previous round's atomic result
+  uint32_t pcd = 0;             // ... and its count
   for (uint64_t kk = 0; kk < nk; kk++) {
-    const uint64_t r = sub_of(kk), s0 = r * SUB;
-    const uint32_t sl = (uint32_t)(kk % kSRing);
-    const uint32_t m = (uint32_t)min((uint64_t)SUB, n - s0);
+    const uint64_t s0 = sub_of(kk) * SUB;
+    const uint32_t sl = (uint32_t)(kk % kSRing), q = (uint32_t)(kk & 1);
+    const uint32_t m = sub_len(kk);
     KeyT<W>* buf = ring + sl * (SUB + 2);
     if (tma) {
-      if (threadIdx.x == 0 && kk + kSRing - 1 < nk) issue(kk + kSRing - 1);
       const bool issued = W == 1 ? (((s0 + m) & ~1ull) > ((s0 + 1) & ~1ull)) : m > 0;
       if (issued) {
         mbar_wait(&bar[sl], (phase >> sl) & 1u);
@@ -494,7 +532,7 @@ __global__ void __launch_bounds__(kST, 2) scatter1_kernel(const uint64_t* __rest
         }
       }
     }
-    __syncthreads();  // the slot's keys are in registers: it becomes the stage
+    __syncthreads();  // counts final; the slot's keys are in registers: it becomes the stage
     if (threadIdx.x < 32) {  // warp 0: exclusive scan of the 256 digit counts
       constexpr uint32_t DPL = RMAX / 32;
       uint32_t c[DPL], loc = 0;
@@ -511,48 +549,38 @@ __global__ void __launch_bounds__(kST, 2) scatter1_kernel(const uint64_t* __rest
       uint32_t ex = inc - loc;
 #pragma unroll
       for (uint32_t j = 0; j < DPL; j++) {
-        lst[threadIdx.x * DPL + j] = ex;
+        lst[q * RMAX + threadIdx.x * DPL + j] = ex;
         ex += c[j];
       }
     }
-    // every digit reserves its run in its group's region (one atomic each)
-    for (uint32_t d = threadIdx.x; d < RMAX; d += kST) {
-      const uint32_t cd = cnt[d];
-      unsigned long long v = ~0ull;  // no write
-      if (cd) {
-        const unsigned long long b = atomicAdd(&gcur[d], (unsigned long long)cd);
-        if (b + cd <= cap) v = (unsigned long long)d * cap + b;
-        else *ovf = 1;
-      }
-      dl[d] = v;
+    if (threadIdx.x < RMAX) {  // publish the previous round's runs, reserve this round's
+      const uint32_t d = threadIdx.x;
+      if (kk > 0) dl[(q ^ 1) * RMAX + d] = resolve(d, pcd, bres);
+      pcd = cnt[d];
+      bres = pcd ? atomicAdd(&gcur[d], (unsigned long long)pcd) : 0ull;
     }
-    __syncthreads();
+    __syncthreads();  // lst[q], dl[q ^ 1] ready; cnt read out
     KeyT<W>* stage = buf;
 #pragma unroll
     for (int u = 0; u < ITEMS; u++) {
       const uint32_t i = u * kST + threadIdx.x;
-      if (i < m) {
-        const uint32_t d = dr[u] >> 16;
-        const uint32_t pos = lst[d] + (dr[u] & 0xffffu);
-        stage[pos] = k[u];
-        sdig[pos] = (uint8_t)d;
-      }
+      if (i < m) stage[lst[q * RMAX + (dr[u] >> 16)] + (dr[u] & 0xffffu)] = k[u];
     }
-    __syncthreads();
-    for (uint32_t j = threadIdx.x; j < m; j += kST) {
-      const uint32_t d = sdig[j];
-      const unsigned long long b = dl[d];
-      if (b != ~0ull) store_key<W>(out, b + (j - lst[d]), stage[j]);
-    }
+    if (kk > 0) store_round(kk - 1);
     for (uint32_t d = threadIdx.x; d < RMAX; d += kST) cnt[d] = 0;
-    __syncthreads();  // stage read out, counters clear
+    __syncthreads();  // round kk-1's slot read out, round kk staged, counters clear
+    if (tma && threadIdx.x == 0 && kk + kSRing - 1 < nk) issue(kk + kSRing - 1);  // into round kk-1's slot
+  }
+  if (nk > 0) {
+    if (threadIdx.x < RMAX) dl[((nk - 1) & 1) * RMAX + threadIdx.x] = resolve(threadIdx.x, pcd, bres);
+    __syncthreads();
+    store_round(nk - 1);
   }
   for (uint32_t i = threadIdx.x; i < kHllM; i += kST)
     if (reg[i]) atomicMax(&hll[i], reg[i]);
 }
 template <int W> constexpr size_t scatter1_smem() {
-  return kSRing * ((size_t)SSCfg<W>::SUB + 2) * sizeof(KeyT<W>) + 256 * 8 + 2 * 256 * 4 + kHllM +
-         (size_t)SSCfg<W>::SUB;
+  return kSRing * ((size_t)SSCfg<W>::SUB + 2) * sizeof(KeyT<W>) + 2 * 256 * 8 + 3 * 256 * 4 + kHllM;
 }
 
 // group offsets after a pass: for old group g with meta {start, tiles, mbase},
@@ -1008,7 +1036,7 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
     CUSCI_CUDA(ctx, cudaFuncSetAttribute(tile_scatter_kernel<W, false, 9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scatter_smem<W, 9>()));
     CUSCI_CUDA(ctx, cudaFuncSetAttribute(bucket_unique_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     CUSCI_CUDA(ctx, cudaFuncSetAttribute(scatter1_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scatter1_smem<W>()));
-    CUSCI_CUDA(ctx, cudaFuncSetAttribute(tile_scatter_atomic_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scatter_smem<W, 8>()));
+    CUSCI_CUDA(ctx, cudaFuncSetAttribute(tile_scatter_atomic_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scatter_atomic_smem<W>()));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&dper[W], bucket_unique_kernel<W>, kBU, C::SMEM);
     if (dper[W] < 1) dper[W] = 1;
     attr[W] = true;
@@ -1162,7 +1190,7 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
       CUSCI_CUDA(ctx, cudaMemcpyAsync(dtl, tl.data(), nt * sizeof(PTile), cudaMemcpyHostToDevice, ctx->stream));
       CUSCI_CUDA(ctx, cudaMemsetAsync(gcur2, 0, nbk2 * sizeof(unsigned long long), ctx->stream));
       CUSCI_CUDA(ctx, cudaMemsetAsync(ovf, 0, sizeof(int), ctx->stream));
-      CUSCI_LAUNCH(ctx, PT_RADIX_DOWN, tile_scatter_atomic_kernel<W><<<nt, kST, scatter_smem<W, 8>(), ctx->stream>>>(part, use_tma, dtl, done + bits, 1u << bits, gcur2, cap2, r2, ovf));
+      CUSCI_LAUNCH(ctx, PT_RADIX_DOWN, tile_scatter_atomic_kernel<W><<<nt, kST, scatter_atomic_smem<W>(), ctx->stream>>>(part, use_tma, dtl, done + bits, 1u << bits, gcur2, cap2, r2, ovf));
       std::vector<uint64_t> cnt(nbk2), ib(nbk2);
       std::vector<uint32_t> offh(nbk2 + 1);
       CUSCI_CUDA(ctx, cudaMemcpyAsync(cnt.data(), gcur2, nbk2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
