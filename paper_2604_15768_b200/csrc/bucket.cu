@@ -844,42 +844,38 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
       continue;
     }
     const uint32_t nwd = (span + 31) / 32;
-    // pass 1 (thread t: bitmap words [WPT t, WPT t + WPT)): the thread owning a
-    // cluster's first slot insertion-sorts the cluster
-    uint32_t c = 0;
-#pragma unroll
-    for (uint32_t q = 0; q < WPT; q++) {
-      const uint32_t w = t * WPT + q;
-      const uint32_t bits = w < nwd ? bm[w] : 0u;
-      c += __popc(bits);
+    // pass 1 (thread t: the 16-slot half-words t, t + kBU, ...): the thread
+    // owning a cluster's first slot insertion-sorts the cluster
+    for (uint32_t h = t; h < 2 * nwd; h += kBU) {
+      const uint32_t w = h >> 1, sh = (h & 1u) * 16u;
+      const uint32_t word = bm[w];
+      const uint32_t bits = (word >> sh) & 0xffffu;
       if (!bits) continue;
-      const uint32_t prev = w > 0 ? (bm[w - 1] >> 31) : 0u;
-      uint32_t starts = bits & ~((bits << 1) | prev);
+      const uint32_t prev = sh ? ((word >> (sh - 1)) & 1u) : (w > 0 ? (bm[w - 1] >> 31) : 0u);
+      uint32_t starts = bits & ~((bits << 1) | prev) & 0xffffu;
       while (starts) {
         const uint32_t i = __ffs(starts) - 1;
         starts &= starts - 1;
-        const uint32_t u = w * 32 + i;
-        const uint32_t y = ~(bits >> i);
-        const uint32_t run = y ? __ffs(y) - 1 : 32u;  // ones from bit i up
-        uint32_t e = u + run;
-        if (run >= 32 - i) {  // the run reaches the word's end: continue in the next words
-          for (uint32_t x = w + 1; x < nwd; x++) {
-            const uint32_t v = bm[x];
-            e += v == ~0u ? 32u : (uint32_t)(__ffs(~v) - 1);
-            if (v != ~0u) break;
-          }
-        }
-        e = min(e, span);
+        const uint32_t u = w * 32 + sh + i;
+        uint32_t x = w, z = ~word & (~0u << (sh + i));  // first empty slot at or after u
+        while (!z && ++x < nwd) z = ~bm[x];
+        const uint32_t e = min(z ? x * 32 + __ffs(z) - 1 : nwd * 32, span);
         for (uint32_t a = u + 1; a < e; a++) {
-          const K x = tab[a];
+          const K xk = tab[a];
           uint32_t j = a;
-          while (j > u && pi_lt(x, tab[j - 1])) {
+          while (j > u && pi_lt(xk, tab[j - 1])) {
             tab[j] = tab[j - 1];
             j--;
           }
-          tab[j] = x;
+          tab[j] = xk;
         }
       }
+    }
+    uint32_t c = 0;  // occupied slots in this thread's pass-2 words
+#pragma unroll
+    for (uint32_t q = 0; q < WPT; q++) {
+      const uint32_t w = t * WPT + q;
+      if (w < nwd) c += __popc(bm[w]);
     }
     // exclusive prefix of the per-thread counts (warp scan + warp totals)
     uint32_t inc = c;
