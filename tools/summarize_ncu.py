@@ -61,7 +61,11 @@ def full(rep):
 
 CLASS = {"tile_scatter_kernel": "part_scatter", "tile_hist_kernel": "part_hist", "bucket_unique_kernel": "bucket_unique",
          "bucket_compact_kernel": "pack", "group_off_kernel": "pack", "owner_bounds_kernel": "pack",
-         "gen_kernel": "gen", "merge_tile_kernel": "merge_tile", "merge_split_kernel": "merge_split"}
+         "gen_kernel": "gen", "merge_tile_kernel": "merge_tile", "merge_split_kernel": "merge_split",
+         "scatter1_kernel": "part_scatter", "tile_scatter_atomic_kernel": "part_scatter",
+         "sparse_copy_kernel": "merge_tile", "sparse_place_kernel": "merge_tile",
+         "sparse_locate_kernel": "merge_split", "sparse_bounds_kernel": "merge_split",
+         "copy_check_kernel": "sorted_check", "check_sorted_kernel": "sorted_check"}
 
 
 def traffic_json(path, out_json):
