@@ -357,6 +357,63 @@ def test_merge_sparse_paths(P, ctx, W):
     pool.close()
 
 
+@pytest.mark.parametrize("W", [1, 2])
+def test_merge_sparse_clustered_inserts(P, ctx, W):
+    """Inserts clustered in the hash order: > 31 inserts land in one warp span of
+    the big run (the copy kernel's search fallback) next to spans with none."""
+    rng = np.random.default_rng(70 + W)
+    sp = P.Space(64 * W, 1, 1)
+    big = hash_sort(synth.unique_keys(rng.integers(1, 1 << 40, size=(300_007, W), dtype=np.uint64)), W)
+    extra = hash_sort(synth.unique_keys(rng.integers(1 << 41, 1 << 42, size=(200_000, W), dtype=np.uint64)), W)
+    hb, _ = hash_hi_lo(big, W)
+    he, _ = hash_hi_lo(extra, W)
+    lo, hi = hb[100_000], hb[100_400]                 # a 400-key window of the big run (< 2 warp spans)
+    clustered = extra[(he > lo) & (he < hi)][:3000]
+    small = np.concatenate([clustered, big[rng.choice(len(big), 1000, replace=False)]])
+    small = hash_sort(synth.unique_keys(small), W)
+    assert len(clustered) > 64
+    pool = ctx.pool(sp, 16)
+    ctx.merge_space(pool, torch.from_numpy(big).cuda())
+    ins = ctx.merge_space(pool, torch.from_numpy(small).cuda(), want_inserted=True).cpu().numpy()
+    ref_s, ref_ins = oracle.merge(big, small, W)
+    after = pool.keys().cpu().numpy()
+    assert_hash_sorted_unique(after, W)
+    assert np.array_equal(synth.sort_keys(after), ref_s) and np.array_equal(synth.sort_keys(ins), ref_ins)
+    # and the other direction (big U into a small pool, no inserted)
+    pool.clear()
+    ctx.merge_space(pool, torch.from_numpy(small).cuda())
+    ctx.merge_space(pool, torch.from_numpy(big).cuda())
+    after = pool.keys().cpu().numpy()
+    assert_hash_sorted_unique(after, W)
+    assert np.array_equal(synth.sort_keys(after), oracle.merge(small, big, W)[0])
+    pool.close()
+
+
+@pytest.mark.parametrize("W", [1, 2])
+@pytest.mark.parametrize("where", ["span_start", "lane0", "mid", "last"])
+def test_merge_copy_paths_reject_one_swap(P, ctx, W, where):
+    """One adjacent swap anywhere in a large U must be caught by the copy kernels'
+    order check (empty pool, and |S| << |U| sparse), wherever it falls relative
+    to the warp spans (R x 32 keys) and lanes."""
+    rng = np.random.default_rng(80 + W)
+    sp = P.Space(64 * W, 1, 1)
+    U = hash_sort(synth.unique_keys(rng.integers(1, 1 << 40, size=(100_003, W), dtype=np.uint64)), W)
+    span = 32 * (16 if W == 1 else 8)
+    i = {"span_start": 7 * span, "lane0": 7 * span + 32 * 3, "mid": 7 * span + 32 * 3 + 17, "last": len(U) - 1}[where]
+    bad = U.copy()
+    bad[[i - 1, i]] = bad[[i, i - 1]]
+    pool = ctx.pool(sp, 16)
+    with pytest.raises(P.CusciError) as e:
+        ctx.merge_space(pool, torch.from_numpy(bad).cuda())
+    assert e.value.code == 1
+    pool.clear()
+    ctx.merge_space(pool, torch.from_numpy(U[::997].copy()).cuda())   # a small S: the sparse path copies U
+    with pytest.raises(P.CusciError) as e:
+        ctx.merge_space(pool, torch.from_numpy(bad).cuda())
+    assert e.value.code == 1
+    pool.close()
+
+
 def test_pipeline_lih_merge_inserts_nothing(P, ctx):
     wl, ints, par = synth.workload_inputs("lih")
     sp = P.Space(12, 2, 2)
