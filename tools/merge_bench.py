@@ -30,6 +30,8 @@ n_in = u1.shape[0] * 2 + u2.shape[0]; n_out = u1.shape[0] + len(pool)
 gb = (n_in + n_out) * 8 / 1e9
 ms = e0.elapsed_time(e1) / reps
 print(f"merge |U1|={u1.shape[0]} |U2|={u2.shape[0]} -> {len(pool)}: {ms:.2f} ms/pair ({gb/ms*1e3:.0f} GB/s algorithmic)  " + " ".join(f"{k}={v[0]/reps:.2f}" for k, v in sorted(p.items(), key=lambda kv: -kv[1][0])))
+if len(sys.argv) > 3 and sys.argv[3] == "nosparse":
+    sys.exit(0)
 # sparse: a pool of the parents (1 / |U| ~ 1/400) merged with the union (S <- S u C)
 spool = ctx.pool(sp, 1 << 20)
 pd = ctx.dedup_global(sp, torch.from_numpy(par).cuda())
