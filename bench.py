@@ -445,10 +445,16 @@ def main():
         "part_scatter": ds["key_passes"] * 16 * W // args.steps,         # partition: read + write a key per pass
         "part_hist": ds["hist_keys"] * 8 * W // args.steps,              # histogram passes: read a key
         "bucket_unique": (ds["keys_in"] + ds["keys_out"]) * 8 * W // args.steps,  # read every key, write survivors
-        "merge_tile": merge_bytes,                                       # read S and U, write S'
+        "merge": merge_bytes,                                            # read S and U, write S'
     }
+    # merge_space runs as merge_split + merge_tile (general / sparse) or a validated
+    # copy (sorted_check, empty pool): its bytes are timed against all of them
+    mparts = [prof[c] for c in ("merge_split", "merge_tile", "sorted_check") if c in prof]
+    timing = dict(prof)
+    if mparts:
+        timing["merge"] = (sum(x[0] for x in mparts), sum(x[1] for x in mparts))
     kernels = {}
-    for name, (kms, kl) in prof.items():
+    for name, (kms, kl) in timing.items():
         if name in alg and kl:
             ach = alg[name] * args.steps / (kms / 1e3) / 1e9
             # frac: vs the measured copy bandwidth (a read-only stream can exceed it);
@@ -471,7 +477,7 @@ def main():
         pass
     roof = None
     if rname:
-        launches_r = prof[rname][1] / args.steps
+        launches_r = timing[rname][1] / args.steps
         tr = traffic.get(rname, {}).get("dram_bytes_per_launch")
         roof = {"bound": "hbm", "kernel": rname, "achieved": kernels[rname]["achieved_GBs"], "peak": hbm_peak,
                 "unit": "GB/s", "frac": kernels[rname]["frac"],
@@ -481,7 +487,7 @@ def main():
                 "peak_source": peak_src, "dominant_class": dname}
         for k in kernels:
             kernels[k]["dram_bytes_per_launch_ncu"] = traffic.get(k, {}).get("dram_bytes_per_launch")
-            kernels[k]["alg_bytes_per_launch"] = alg[k] / (prof[k][1] / args.steps)
+            kernels[k]["alg_bytes_per_launch"] = alg[k] / (timing[k][1] / args.steps)
     gen_roof = None
     if "gen" in kernels:
         gen_roof = {"achieved": kernels["gen"]["achieved_GBs"], "frac": kernels["gen"]["frac"],
