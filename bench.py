@@ -173,6 +173,29 @@ def oracle_sample(wl, ints, par, n_sample: int):
     return len(rec["src"]), len(u), dt
 
 
+def oracle_sample_mt(wl, ints, par, n_sample: int, threads: int):
+    """oracle-MT: the same unmodified oracle calls with the parents
+    sharded over host threads (ctypes releases the GIL inside the C++ oracle):
+    per-shard gen + std::set dedup in parallel, then one std::set dedup of the
+    shards' unique keys and the set_union merge."""
+    import oracle
+    from concurrent.futures import ThreadPoolExecutor
+    sample = par[:n_sample]
+    shards = [x for x in np.array_split(sample, threads) if len(x)]
+    t0 = time.perf_counter()
+
+    def work(sh):
+        rec = oracle.gen_coupled(wl.m, wl.n_alpha, wl.n_beta, sh, ints, 0.0)
+        return len(rec["src"]), oracle.dedup(rec["keys"], wl.words)
+
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        parts = list(ex.map(work, shards))
+    nrec = sum(p[0] for p in parts)
+    u = oracle.dedup(np.concatenate([p[1] for p in parts]), wl.words)
+    oracle.merge(sample, u, wl.words)
+    return nrec, len(u), time.perf_counter() - t0
+
+
 def default_cpu_sample(wl) -> int:
     return {"lih": 225, "h2o": 4000, "h2o_dense": 1000, "n2": 1000, "c2h4": 40, "m120": 4}.get(wl, 100)
 
@@ -494,7 +517,7 @@ def main():
                     "records_per_s_kernel": tot_rec / (prof["gen"][0] / 1e3)}
 
     # ---------------- cpu baseline (oracle, rank 0, N=1 only)
-    cpu = None
+    cpu = cpu_mt = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         n_sample = args.cpu_sample or default_cpu_sample(args.workload)
         _, _, par_s = synth.workload_inputs(args.workload, n_parents=n_sample)
@@ -502,6 +525,13 @@ def main():
         cpu = {"value": r / dt, "unit": "coupled configs/s", "cores": 1, "kind": "oracle",
                "sample": f"{n_sample} parents (first distinct sampler draws) of the workload through oracle gen -> std::set dedup -> "
                          f"set_union merge ({r} records, {u} unique, {dt:.1f} s)"}
+        # oracle-MT: the same oracle sharded over every host core
+        nth = max(1, len(os.sched_getaffinity(0)))
+        n_mt = n_sample * nth
+        _, _, par_m = synth.workload_inputs(args.workload, n_parents=n_mt)
+        rm, um, dtm = oracle_sample_mt(wl, ints, par_m, n_mt, nth)
+        cpu_mt = {"value": rm / dtm, "unit": "coupled configs/s", "cores": nth, "kind": "oracle-MT",
+                  "sample": f"{n_mt} parents sharded over {nth} threads ({rm} records, {um} unique, {dtm:.1f} s)"}
 
     if stage3:
         stage3["frac"] = stage3["achieved_GBs"] / hbm_peak
@@ -525,6 +555,7 @@ def main():
             "stage3_contract": stage3,
             "f2_regular_sampling": f2,
             "cpu_baseline": cpu,
+            "cpu_baseline_mt": cpu_mt,
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clk,
