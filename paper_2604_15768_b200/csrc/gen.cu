@@ -193,12 +193,10 @@ __device__ __forceinline__ void stage_flush(const GenArgs& a, Stage<W>& st) {
         store_key<W>(a.keys, base + i, st_key(r));
         a.hij[base + i] = r.h;
       }
-      if (a.src) {
-        for (uint32_t i = lane; i < st.n; i += 32) {
-          uint32_t sv = st.run[kRuns];
-          for (uint32_t j = 1; j < st.nrun; j++)
-            if (st.run[j] <= i) sv = st.run[kRuns + j];
-          a.src[base + i] = sv;
+      if (a.src) {  // each source run is a contiguous range of the stage
+        for (uint32_t j = 0; j < st.nrun; j++) {
+          const uint32_t r0 = st.run[j], r1 = j + 1 < st.nrun ? st.run[j + 1] : st.n, sv = st.run[kRuns + j];
+          for (uint32_t i = r0 + lane; i < r1; i += 32) a.src[base + i] = sv;
         }
       }
       if (MODE == 2)
