@@ -667,7 +667,7 @@ constexpr int kILP = 8;   // keys per thread with first probes in flight togethe
 template <int W> struct BUCfg {
   static constexpr uint32_t TS = W == 1 ? 16384 : 8192;  // max home slots (128 KB)
   static constexpr uint32_t OV = W == 1 ? 1024 : 512;    // overflow tail
-  static constexpr uint32_t BUFK = W == 1 ? 5120 : 2304; // keys per TMA piece (40 KB): 5 per thread
+  static constexpr uint32_t BUFK = W == 1 ? 5120 : 2048; // keys per TMA piece (40 / 32 KB): 5 / 2 per thread
   static constexpr uint32_t BUFE = BUFK + 2;             // + alignment slack (W = 1)
   static constexpr uint32_t DT = W == 1 ? 6144 : 3072;   // target distinct keys per bucket
   static constexpr uint32_t NWD = (TS + OV) / 32;        // bitmap words
