@@ -238,6 +238,13 @@ void cusci_pool_destroy(cusci_pool* pool);
  * new keys share the owner function, so no communication is needed. */
 int merge_space(cusci_ctx* ctx, cusci_pool* space, const uint64_t* new_keys, uint64_t n_new,
                 cusci_keys* inserted);
+/* S <- S u src for two pools of the same space (S <- S u C with C
+ * held in a pool).  src's keys are read in place and, being a pool's, are
+ * sorted and unique by construction, so they are not re-validated (the one
+ * difference from merge_space(space, view(src))).  src may be space itself.
+ * inserted as in merge_space.  Errors: E_INVALID_ARG (NULL, pools of another
+ * context or of different spaces), E_OOM (pool growth), E_CUDA. */
+int cusci_pool_merge(cusci_ctx* ctx, cusci_pool* space, const cusci_pool* src, cusci_keys* inserted);
 
 /* ---- next row: Stage-3 contraction ----------------------- */
 

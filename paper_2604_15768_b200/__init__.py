@@ -325,12 +325,11 @@ class Context:
         return Pool(self, space, capacity)
 
     def merge_pool(self, dst: "Pool", src: "Pool", want_inserted: bool = False):
-        """dst <- dst u src, reading src's keys in place (no copy)."""
-        ptr, cnt = src.view()
+        """dst <- dst u src (cusci_pool_merge): src's keys are read in place and,
+        being a pool's, are not re-validated."""
         k = _Keys()
-        rc = lib().merge_space(self._ctx, dst._pool, ctypes.c_void_p(ptr), cnt,
-                               ctypes.byref(k) if want_inserted else None)
-        self._check(rc, "merge_space")
+        rc = lib().cusci_pool_merge(self._ctx, dst._pool, src._pool, ctypes.byref(k) if want_inserted else None)
+        self._check(rc, "cusci_pool_merge")
         if want_inserted:
             return self._take(k.keys, int(k.count), dst.space.words)
         return None

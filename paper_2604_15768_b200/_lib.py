@@ -15,7 +15,8 @@ EXPORTS = ["cusci_nccl_unique_id", "cusci_init", "cusci_finalize", "cusci_last_e
            "cusci_free", "cusci_kernel_launches", "cusci_profile_enable", "cusci_profile_read", "cusci_dedup_stats", "gen_coupled_bound", "gen_coupled", "gen_coupled_count",
            "dedup_global", "dedup_partition", "dedup_finalize", "cusci_pool_create", "cusci_pool_view",
            "cusci_pool_copy", "cusci_pool_clear", "cusci_pool_destroy", "merge_space", "energy_contract",
-           "dedup_sorted", "sort_unique", "regular_samples", "select_splitters", "split_bounds"]
+           "dedup_sorted", "sort_unique", "regular_samples", "select_splitters", "split_bounds",
+           "cusci_pool_merge"]
 
 
 PROFILE_TAGS = ["prep", "validate", "gen", "bucket_unique", "pack", "part_hist", "part_scatter",
@@ -74,6 +75,8 @@ def lib():
     L.dedup_partition.restype = i32
     L.dedup_finalize.argtypes = [vp, vp, vp, u64, vp]
     L.dedup_finalize.restype = i32
+    L.cusci_pool_merge.argtypes = [vp, vp, vp, vp]
+    L.cusci_pool_merge.restype = i32
     L.dedup_sorted.argtypes = [vp, vp, vp, u64, i32, vp, vp]
     L.dedup_sorted.restype = i32
     L.sort_unique.argtypes = [vp, vp, vp, u64, vp]

@@ -215,7 +215,8 @@ __global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(const uint64_
                                                                   const uint64_t* __restrict__ split, uint64_t ntiles,
                                                                   unsigned long long* __restrict__ status,
                                                                   int* __restrict__ bad,
-                                                                  uint64_t* __restrict__ out, uint64_t* __restrict__ ins) {
+                                                                  uint64_t* __restrict__ out, uint64_t* __restrict__ ins,
+                                                                  int check_u) {
   constexpr int kMergeItems = MergeCfg<W>::ITEMS;
   constexpr int kTile = MergeCfg<W>::TILE;
   constexpr int BUFE = MergeCfg<W>::BUFE;
@@ -278,7 +279,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(const uint64_
       if (W == 1 || hx != hy) return hx <= hy;
       return hk_lo(buf[bidx(x)]) <= hk_lo(buf[bidx(y)]);
     };
-    {  // input check: U strictly increasing in the hash order (tile run + left boundary)
+    if (check_u) {  // input check: U strictly increasing in the hash order (tile run + left boundary)
       bool badu = false;
       for (int x = threadIdx.x; x < nb; x += kMergeThreads) {
         if (x > 0) badu |= le(na + x, na + x - 1);
@@ -527,7 +528,7 @@ __global__ void __launch_bounds__(256) copy_check_kernel(const uint64_t* __restr
         if (ins) store_key<W>(ins, j, x[r]);
       }
     }
-    badl |= span_bad<W>(x, j0, j1, pw, hk_hi(pw));
+    if (bad) badl |= span_bad<W>(x, j0, j1, pw, hk_hi(pw));
   }
   if (badl) *bad = 1;
 }
@@ -546,7 +547,10 @@ __global__ void sparse_place_kernel(const uint64_t* __restrict__ small, uint64_t
 }
 
 template <int W>
-int merge_impl(cusci_ctx* ctx, cusci_pool* pool, const uint64_t* U, uint64_t nU, cusci_keys* inserted) {
+// trusted: U is another pool's key array (sorted and unique by construction):
+// the input-order check is skipped
+int merge_impl(cusci_ctx* ctx, cusci_pool* pool, const uint64_t* U, uint64_t nU, cusci_keys* inserted,
+               bool trusted) {
   const uint64_t nS = pool->count;
   const uint64_t* S = pool->buf[pool->cur];
   const uint64_t total = nS + nU;
@@ -601,7 +605,7 @@ int merge_impl(cusci_ctx* ctx, cusci_pool* pool, const uint64_t* U, uint64_t nU,
   if (nS == 0) {
     // empty pool: S' = U (validated strictly increasing in the hash order), a copy
     const unsigned cg = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nU + 8 * CopyCfg<W>::SPAN - 1) / (8 * CopyCfg<W>::SPAN), (uint64_t)ctx->num_sms * 8));
-    CUSCI_LAUNCH(ctx, PT_CHECK, copy_check_kernel<W><<<cg, 256, 0, ctx->stream>>>(U, nU, dst, (uint64_t*)insp, bad));
+    CUSCI_LAUNCH(ctx, PT_CHECK, copy_check_kernel<W><<<cg, 256, 0, ctx->stream>>>(U, nU, dst, (uint64_t*)insp, trusted ? nullptr : bad));
     CUSCI_CUDA(ctx, cudaMemcpyAsync((char*)ctx->host_pinned + 16, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     h[0] = nU;
@@ -620,7 +624,7 @@ int merge_impl(cusci_ctx* ctx, cusci_pool* pool, const uint64_t* U, uint64_t nU,
     const uint64_t* small = u_small ? U : S;
     const uint64_t* big = u_small ? S : U;
     const uint64_t nsm = u_small ? nU : nS, nbg = u_small ? nS : nU;
-    if (u_small) {  // a large U is checked inside the copy
+    if (u_small && !trusted) {  // a large U is checked inside the copy
       const unsigned cu = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nU + 255) / 256, (uint64_t)ctx->num_sms * 8));
       CUSCI_LAUNCH(ctx, PT_CHECK, check_sorted_kernel<W><<<cu, 256, 0, ctx->stream>>>(U, nU, bad));
     }
@@ -641,7 +645,7 @@ int merge_impl(cusci_ctx* ctx, cusci_pool* pool, const uint64_t* U, uint64_t nU,
     CUSCI_TRY(s.get_t(nsp + 1, &cb));
     CUSCI_LAUNCH(ctx, PT_MERGE_SPLIT, sparse_bounds_kernel<W><<<(unsigned)((nsp + 1 + 255) / 256), 256, 0, ctx->stream>>>(pos, nsm, nbg, nsp, cb));
     const unsigned bg = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nsp + 7) / 8, (uint64_t)ctx->num_sms * 8));
-    CUSCI_LAUNCH(ctx, PT_MERGE_TILE, sparse_copy_kernel<W><<<bg, 256, 0, ctx->stream>>>(big, nbg, pos, rank, cb, dst, u_small ? nullptr : bad));
+    CUSCI_LAUNCH(ctx, PT_MERGE_TILE, sparse_copy_kernel<W><<<bg, 256, 0, ctx->stream>>>(big, nbg, pos, rank, cb, dst, (u_small || trusted) ? nullptr : bad));
     CUSCI_LAUNCH(ctx, PT_MERGE_TILE, sparse_place_kernel<W><<<cg, 256, 0, ctx->stream>>>(small, nsm, pos, keep, rank, dst, u_small ? (uint64_t*)insp : nullptr));
     CUSCI_CUDA(ctx, cudaMemcpyAsync(ctx->host_pinned, rank + nsm, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
     CUSCI_CUDA(ctx, cudaMemcpyAsync((char*)ctx->host_pinned + 16, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
@@ -666,7 +670,7 @@ int merge_impl(cusci_ctx* ctx, cusci_pool* pool, const uint64_t* U, uint64_t nU,
     }
     // persistent grid: every CTA resident (the look-back relies on it)
     const unsigned mgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * mper[W]));
-    CUSCI_LAUNCH(ctx, PT_MERGE_TILE, merge_tile_kernel<W><<<mgrid, kMergeThreads, MergeCfg<W>::SMEM, ctx->stream>>>(S, nS, U, nU, split, ntiles, status, bad, dst, (uint64_t*)insp));
+    CUSCI_LAUNCH(ctx, PT_MERGE_TILE, merge_tile_kernel<W><<<mgrid, kMergeThreads, MergeCfg<W>::SMEM, ctx->stream>>>(S, nS, U, nU, split, ntiles, status, bad, dst, (uint64_t*)insp, trusted ? 0 : 1));
     // totals = the last tile's inclusive counts; plus the input check flag
     CUSCI_CUDA(ctx, cudaMemcpyAsync(ctx->host_pinned, status + 2 * (ntiles - 1), 2 * sizeof(uint64_t),
                                     cudaMemcpyDeviceToHost, ctx->stream));
@@ -712,6 +716,18 @@ extern "C" int merge_space(cusci_ctx* ctx, cusci_pool* space, const uint64_t* ne
   if (space->ctx != ctx) return set_error(ctx, CUSCI_E_INVALID_ARG, "pool belongs to another context");
   if (n_new && !new_keys) return set_error(ctx, CUSCI_E_INVALID_ARG, "new_keys is NULL");
   CUSCI_CUDA(ctx, cudaSetDevice(ctx->device));
-  return space->sp.words == 1 ? merge_impl<1>(ctx, space, new_keys, n_new, inserted)
-                              : merge_impl<2>(ctx, space, new_keys, n_new, inserted);
+  return space->sp.words == 1 ? merge_impl<1>(ctx, space, new_keys, n_new, inserted, false)
+                              : merge_impl<2>(ctx, space, new_keys, n_new, inserted, false);
+}
+
+extern "C" int cusci_pool_merge(cusci_ctx* ctx, cusci_pool* space, const cusci_pool* src, cusci_keys* inserted) {
+  if (!ctx || !space || !src) return CUSCI_E_INVALID_ARG;
+  if (ctx->broken) return set_error(ctx, CUSCI_E_CUDA, "context is unusable after an earlier CUDA/NCCL error");
+  if (space->ctx != ctx || src->ctx != ctx) return set_error(ctx, CUSCI_E_INVALID_ARG, "pool belongs to another context");
+  if (src->sp.words != space->sp.words || src->sp.m != space->sp.m)
+    return set_error(ctx, CUSCI_E_INVALID_ARG, "pools of different spaces");
+  CUSCI_CUDA(ctx, cudaSetDevice(ctx->device));
+  const uint64_t* U = src->buf[src->cur];
+  return space->sp.words == 1 ? merge_impl<1>(ctx, space, U, src->count, inserted, true)
+                              : merge_impl<2>(ctx, space, U, src->count, inserted, true);
 }

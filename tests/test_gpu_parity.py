@@ -414,6 +414,34 @@ def test_merge_copy_paths_reject_one_swap(P, ctx, W, where):
     pool.close()
 
 
+@pytest.mark.parametrize("W", [1, 2])
+def test_pool_merge_equals_merge_space(P, ctx, W):
+    """cusci_pool_merge (src = another pool, not re-validated) gives the same pool
+    and inserted set as merge_space with src's keys, on all three paths
+    (empty destination, sparse, general), and merging a pool into itself is a no-op."""
+    rng = np.random.default_rng(90 + W)
+    sp = P.Space(64 * W, 1, 1)
+    A = hash_sort(synth.unique_keys(rng.integers(1, 1 << 40, size=(200_003, W), dtype=np.uint64)), W)
+    B = hash_sort(synth.unique_keys(rng.integers(1, 1 << 40, size=(150_001, W), dtype=np.uint64)), W)
+    for dst_keys in (A[:0], A[::500].copy(), A):           # empty, sparse (|S| << |U|), general
+        src = ctx.pool(sp, 16)
+        ctx.merge_space(src, torch.from_numpy(B).cuda())
+        d1, d2 = ctx.pool(sp, 16), ctx.pool(sp, 16)
+        if len(dst_keys):
+            ctx.merge_space(d1, torch.from_numpy(dst_keys).cuda())
+            ctx.merge_space(d2, torch.from_numpy(dst_keys).cuda())
+        ins1 = ctx.merge_pool(d1, src, want_inserted=True).cpu().numpy()
+        ins2 = ctx.merge_space(d2, src.keys(), want_inserted=True).cpu().numpy()
+        k1 = d1.keys().cpu().numpy()
+        assert np.array_equal(k1, d2.keys().cpu().numpy()) and np.array_equal(ins1, ins2)
+        ref_s, ref_ins = oracle.merge(dst_keys, B, W)
+        assert np.array_equal(synth.sort_keys(k1), ref_s) and np.array_equal(synth.sort_keys(ins1), ref_ins)
+        n = len(d1)
+        assert ctx.merge_pool(d1, d1, want_inserted=True).shape[0] == 0 and len(d1) == n
+        for x in (src, d1, d2):
+            x.close()
+
+
 def test_pipeline_lih_merge_inserts_nothing(P, ctx):
     wl, ints, par = synth.workload_inputs("lih")
     sp = P.Space(12, 2, 2)
