@@ -10,8 +10,18 @@
  *     words, words = 1 if m <= 64 else 2 (m <= 128).  Spin orbital t lives in
  *     word t/64 at bit t%64.  Spin orbitals are interleaved:
  *     t = 2P + sigma, sigma 0 = alpha, 1 = beta; P = t/2 is the spatial index.
- *   - Key arrays are row-major [n][words]; keys are ordered as one big
- *     unsigned integer with word (words-1) most significant.
+ *   - Key arrays are row-major [n][words].  Two key orders are used:
+ *       big-integer order: the key as one unsigned integer, word (words-1)
+ *         most significant -- the order of the f2 calls (dedup_sorted,
+ *         sort_unique, ...);
+ *       pool hash order pi (reading r13): pi(j) = (hi, lo) compared
+ *         lexicographically, with fmix = the splitmix64 finalizer and
+ *           words = 1: hi = fmix(w0), lo = 0;
+ *           words = 2: lo = fmix(w1 ^ 0x9E3779B97F4A7C15), hi = fmix(w0 ^ lo);
+ *         pi is a bijection, and owner(j) = floor(hi * world / 2^64), so
+ *         every rank's shard is a contiguous pi range.  dedup_global's
+ *         output, the pool and merge_space's inputs/outputs are strictly
+ *         increasing in pi.
  *   - Integrals are real fp64: h[K*K] (symmetric, row-major) and the
  *     two-electron integrals (PQ|RS) in chemist notation, 8-fold packed:
  *       ij = max(P,Q)(max(P,Q)+1)/2 + min(P,Q);  idx = max(ij,kl)(max(ij,kl)+1)/2 + min(ij,kl).
@@ -47,6 +57,8 @@ extern "C" {
 #define CUSCI_E_CUDA 4           /* CUDA runtime error */
 #define CUSCI_E_NCCL 5           /* NCCL error (communicator aborted; all ranks report it) */
 #define CUSCI_E_OOM 6            /* device scratch allocation failed */
+
+#define CUSCI_MAX_WORLD 512      /* ranks per communicator */
 
 typedef struct cusci_ctx cusci_ctx;    /* device, stream, NCCL comm, allocator, workspace, cached Hamiltonian prep */
 typedef struct cusci_pool cusci_pool;  /* GPU-resident owned shard of the configuration space S (sorted, unique) */
@@ -89,9 +101,11 @@ typedef void (*cusci_free_fn)(void* ptr, void* user);
  * 0, then broadcast it to all ranks, e.g. with torch.distributed). */
 int cusci_nccl_unique_id(void* out128);
 
-/* Create a context on `device` for rank `rank` of `world` (world >= 1).
- * nccl_unique_id: host pointer to the 128-byte id (required iff world > 1;
- * collective over all ranks when world > 1).  cuda_stream: the cudaStream_t on
+/* Create a context on `device` for rank `rank` of `world` (1 <= world <=
+ * CUSCI_MAX_WORLD, else CUSCI_E_INVALID_ARG).
+ * nccl_unique_id: host pointer to the 128-byte id (required when world > 1;
+ * collective over all ranks).  With world = 1 it is optional: when given, a
+ * 1-rank NCCL communicator is created, which CUSCI_OPT_FORCE_COLLECTIVE uses.  cuda_stream: the cudaStream_t on
  * `device` every call is ordered on (NULL = the legacy default stream; pass the
  * stream the caller's producers and consumers of these buffers use).  alloc/free: output
  * allocator (both NULL = cudaMallocAsync / cudaFreeAsync on the stream). */
@@ -99,7 +113,18 @@ int cusci_init(cusci_ctx** ctx, int device, int rank, int world, const void* ncc
                void* cuda_stream, cusci_alloc_fn alloc, cusci_free_fn free_fn, void* alloc_user);
 void cusci_finalize(cusci_ctx* ctx);
 const char* cusci_last_error(const cusci_ctx* ctx);
-/* Drop the cached Hamiltonian prep (call after mutating integrals in place). */
+/* Context options.  CUSCI_OPT_FORCE_COLLECTIVE (value 0/1): run the
+ * collective protocol of dedup_global / dedup_sorted / energy_contract --
+ * status-carrying count exchange, NCCL payload exchange (the own bin too,
+ * through ncclSend/ncclRecv to self), owner-side finalize -- even at
+ * world = 1 (needs a communicator: pass an NCCL id to cusci_init).  This is
+ * how the exchange step is exercised on one GPU; results are
+ * identical to the world = 1 shortcut.  Errors: E_INVALID_ARG (unknown
+ * option, or no communicator). */
+#define CUSCI_OPT_FORCE_COLLECTIVE 1
+int cusci_set_option(cusci_ctx* ctx, int option, int64_t value);
+/* Drop the cached Hamiltonian prep (call after mutating or freeing the
+ * integrals the cache was built from). */
 void cusci_invalidate_integrals(cusci_ctx* ctx);
 /* Free a library-allocated output when the context has no free callback. */
 void cusci_free(cusci_ctx* ctx, void* ptr);
@@ -149,7 +174,11 @@ uint64_t gen_coupled_bound(const cusci_space* sp, uint64_t n_parents);
  * If the total exceeds out->capacity, nothing beyond capacity is written,
  * out->count = true total and CUSCI_E_CAPACITY is returned.
  * The Hamiltonian prep (pair tables) is built on first use and cached per
- * (h, eri, K, threshold). */
+ * (h pointer, eri pointer, K, threshold) without re-reading the integrals:
+ * after mutating the integrals in place, or freeing them while the context
+ * lives (a new buffer can reuse the address), call cusci_invalidate_integrals
+ * (the Python binding keeps the integrals of the cached prep alive and
+ * invalidates when another integrals object is passed). */
 int gen_coupled(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* parents, uint64_t n_parents,
                 const cusci_integrals* ints, double threshold, cusci_records* out);
 
@@ -160,13 +189,17 @@ int gen_coupled_count(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* par
 /* ---- step 2: global de-duplication (COLLECTIVE when world > 1) ------------ */
 
 /* Global de-duplication of the union over all ranks of `configs` (device,
- * [n][words]) (Sec 2.2; Sec 4.1.1): local unique filter
- * (P:380-382), hash-owner partition owner(j) = floor(mix(j) * world / 2^64)
- * (DESIGN.md r9), one all-to-all exchange over NCCL, local radix sort
- * + unique.  On return owned_unique holds, sorted ascending, exactly the
- * distinct keys j of the global union with owner(j) == rank.  Every rank must
- * call it with the same cusci_space; argument errors are agreed across ranks
- * before any data moves. */
+ * [n][words], n < 2^32) (Sec 2.2; Sec 4.1.1): local
+ * unique filter, hash-owner partition owner(j) = floor(hi(j) *
+ * world / 2^64) (DESIGN.md r9), one all-to-all exchange over NCCL,
+ * owner-side unique of the received runs.  On return owned_unique holds,
+ * strictly increasing in the pool hash order pi, exactly the distinct keys j
+ * of the global union with owner(j) == rank.  Every rank must call it with
+ * the same cusci_space.  Errors are agreed across ranks: a rank whose
+ * arguments or local step failed still takes part in the count exchange
+ * (sending a failure marker), and every rank then returns an error (its own
+ * code, or that code of a peer's failure) -- no rank is left blocked in the
+ * exchange. */
 int dedup_global(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* configs, uint64_t n,
                  cusci_keys* owned_unique);
 
@@ -175,7 +208,8 @@ int dedup_global(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* configs,
  *   dedup_partition: local unique filter + owner partition into n_owners bins;
  *     bins->keys holds the bins back to back (bin r first at offset
  *     sum_{r'<r} counts[r']); counts (HOST, [n_owners]) receives the sizes.
- *   dedup_finalize: sort + unique of a received buffer (device, [n][words]). */
+ *   dedup_finalize: unique of a received buffer (device, [n][words]) into
+ *     the pool hash order pi. */
 int dedup_partition(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* configs, uint64_t n,
                     int n_owners, cusci_keys* bins, uint64_t* counts);
 int dedup_finalize(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* keys, uint64_t n,
@@ -223,7 +257,8 @@ int split_bounds(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* sorted, 
 
 /* Create an empty pool (capacity = initial key capacity; it grows). */
 int cusci_pool_create(cusci_ctx* ctx, const cusci_space* sp, uint64_t capacity, cusci_pool** out);
-/* Read-only view of the pool's sorted unique keys; valid until the next merge_space. */
+/* Read-only view of the pool's keys (strictly increasing in pi); valid until
+ * the next merge_space or cusci_pool_merge into this pool. */
 int cusci_pool_view(const cusci_pool* pool, const uint64_t** keys, uint64_t* count);
 /* Empty the pool (keeps its buffers, so a reused pool never reallocates). */
 int cusci_pool_clear(cusci_pool* pool);
@@ -232,9 +267,10 @@ int cusci_pool_copy(const cusci_pool* pool, uint64_t* dst, uint64_t capacity_key
 void cusci_pool_destroy(cusci_pool* pool);
 
 /* S <- S u new (Sec 2.2).  new_keys (device,
- * [n_new][words]) must be sorted ascending and unique (as returned by
- * dedup_global on this rank; CUSCI_E_INVALID_ARG otherwise).  If `inserted`
- * is non-NULL it receives new \ S_old, sorted.  Local: the pool shard and the
+ * [n_new][words]) must be strictly increasing in the pool hash order pi (as
+ * returned by dedup_global on this rank; CUSCI_E_INVALID_ARG otherwise -- a
+ * big-integer-sorted array such as dedup_sorted's output is rejected).  If
+ * `inserted` is non-NULL it receives new \ S_old, in pi order.  Local: the pool shard and the
  * new keys share the owner function, so no communication is needed. */
 int merge_space(cusci_ctx* ctx, cusci_pool* space, const uint64_t* new_keys, uint64_t n_new,
                 cusci_keys* inserted);

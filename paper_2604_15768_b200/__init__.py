@@ -118,9 +118,11 @@ class Context:
         self._alloc_cb = _ALLOC_FN(_alloc)
         self._free_cb = _FREE_FN(_free)
         idbuf = None
-        if world > 1:
-            if nccl_id is None or len(nccl_id) != 128:
-                raise ValueError("world > 1 needs the 128-byte NCCL unique id")
+        if world > 1 and nccl_id is None:
+            raise ValueError("world > 1 needs the 128-byte NCCL unique id")
+        if nccl_id is not None:   # world = 1 with an id: a 1-rank communicator (force_collective)
+            if len(nccl_id) != 128:
+                raise ValueError("the NCCL unique id is 128 bytes")
             idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
         ctx = ctypes.c_void_p()
         rc = lib().cusci_init(ctypes.byref(ctx), device, rank, world, idbuf, ctypes.c_void_p(self.stream.cuda_stream),
@@ -129,6 +131,7 @@ class Context:
             raise CusciError(rc, "cusci_init failed")
         self._ctx = ctx
         self.rank, self.world = rank, world
+        self._ints = None   # the integrals of the library's cached Hamiltonian prep (kept alive)
 
     # ------------------------------------------------------------------ plumbing
     def close(self):
@@ -179,6 +182,20 @@ class Context:
 
     def invalidate_integrals(self):
         lib().cusci_invalidate_integrals(self._ctx)
+        self._ints = None
+
+    def _use_integrals(self, ints: "DeviceIntegrals"):
+        # the library caches its prep by pointer: keep these integrals alive while
+        # cached, and drop the cache when another integrals object comes in
+        if ints is not self._ints:
+            lib().cusci_invalidate_integrals(self._ctx)
+            self._ints = ints
+
+    def force_collective(self, on: bool = True):
+        """Run the collective protocol (status-carrying count exchange, NCCL
+        payload exchange) even at world = 1 (needs Context(..., nccl_id=...))."""
+        from ._lib import CUSCI_OPT_FORCE_COLLECTIVE
+        self._check(lib().cusci_set_option(self._ctx, CUSCI_OPT_FORCE_COLLECTIVE, 1 if on else 0), "cusci_set_option")
 
     @staticmethod
     def nccl_unique_id() -> bytes:
@@ -208,6 +225,7 @@ class Context:
         else:
             keys, hij, src, phase = out.keys, out.hij, out.src, out.phase
             cap = int(keys.shape[0])
+        self._use_integrals(ints)
         rec = _Records(keys.data_ptr(), hij.data_ptr(), src.data_ptr() if src is not None else None,
                        phase.data_ptr() if phase is not None else None, cap, 0)
         sp, ci = space._c(), ints._c()
@@ -221,6 +239,7 @@ class Context:
     def gen_coupled_count(self, space: Space, parents: torch.Tensor, ints: DeviceIntegrals,
                           threshold: float = 0.0) -> int:
         par = _as_u64_2d(parents, space.words)
+        self._use_integrals(ints)
         cnt = ctypes.c_uint64(0)
         sp, ci = space._c(), ints._c()
         rc = lib().gen_coupled_count(self._ctx, ctypes.byref(sp), ctypes.c_void_p(par.data_ptr()), par.shape[0],
@@ -361,6 +380,8 @@ class Context:
             raise ValueError("psi must be float64 and aligned with space_keys")
         if e is None:
             e = torch.empty(max(int(n_parents), 0), dtype=torch.float64, device=keys.device)
+        elif e.dtype != torch.float64 or e.numel() < int(n_parents) or not e.is_contiguous() or not e.is_cuda:
+            raise ValueError("e must be a contiguous CUDA float64 tensor with >= n_parents elements")
         miss = ctypes.c_uint64()
         rc = lib().energy_contract(self._ctx, ctypes.byref(space._c()), ctypes.c_void_p(keys.data_ptr()),
                                    ctypes.c_void_p(rec.hij.data_ptr()), ctypes.c_void_p(rec.src.data_ptr()), n,

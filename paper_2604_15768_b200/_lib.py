@@ -16,7 +16,9 @@ EXPORTS = ["cusci_nccl_unique_id", "cusci_init", "cusci_finalize", "cusci_last_e
            "dedup_global", "dedup_partition", "dedup_finalize", "cusci_pool_create", "cusci_pool_view",
            "cusci_pool_copy", "cusci_pool_clear", "cusci_pool_destroy", "merge_space", "energy_contract",
            "dedup_sorted", "sort_unique", "regular_samples", "select_splitters", "split_bounds",
-           "cusci_pool_merge"]
+           "cusci_pool_merge", "cusci_set_option"]
+
+CUSCI_OPT_FORCE_COLLECTIVE = 1
 
 
 PROFILE_TAGS = ["prep", "validate", "gen", "bucket_unique", "pack", "part_hist", "part_scatter",
@@ -49,6 +51,8 @@ def lib():
     L.cusci_init.restype = i32
     L.cusci_finalize.argtypes = [vp]
     L.cusci_finalize.restype = None
+    L.cusci_set_option.argtypes = [vp, i32, ctypes.c_int64]
+    L.cusci_set_option.restype = i32
     L.cusci_last_error.argtypes = [vp]
     L.cusci_last_error.restype = ctypes.c_char_p
     L.cusci_invalidate_integrals.argtypes = [vp]

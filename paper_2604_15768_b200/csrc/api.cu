@@ -116,9 +116,25 @@ int check_space(cusci_ctx* ctx, const cusci_space* sp) {
   return CUSCI_OK;
 }
 
+int kernel_setup(cusci_ctx* ctx, const void* fn, int threads, size_t smem, int* per_sm) {
+  for (const KSetup& k : ctx->ksetup)
+    if (k.fn == fn && k.smem == smem && k.threads == threads) {
+      *per_sm = k.per_sm;
+      return CUSCI_OK;
+    }
+  if (smem > 48 * 1024) CUSCI_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  CUSCI_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem));
+  if (occ < 1) occ = 1;
+  ctx->ksetup.push_back(KSetup{fn, smem, threads, occ});
+  *per_sm = occ;
+  return CUSCI_OK;
+}
+
 int read_u64(cusci_ctx* ctx, const uint64_t* dev, uint64_t* host, int count) {
   uint64_t* pinned = (uint64_t*)ctx->host_pinned;
-  if (count > 512) return set_error(ctx, CUSCI_E_INVALID_ARG, "read_u64 count too large");
+  if (count < 0 || (size_t)count * sizeof(uint64_t) > kHostPinnedBytes)
+    return set_error(ctx, CUSCI_E_INVALID_ARG, "read_u64 count too large");
   CUSCI_CUDA(ctx, cudaMemcpyAsync(pinned, dev, sizeof(uint64_t) * count, cudaMemcpyDeviceToHost, ctx->stream));
   CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   memcpy(host, pinned, sizeof(uint64_t) * count);
@@ -168,7 +184,7 @@ int cusci_init(cusci_ctx** out, int device, int rank, int world, const void* ncc
                cusci_alloc_fn alloc, cusci_free_fn free_fn, void* alloc_user) {
   if (!out) return CUSCI_E_INVALID_ARG;
   *out = nullptr;
-  if (world < 1 || rank < 0 || rank >= world) return CUSCI_E_INVALID_ARG;
+  if (world < 1 || world > CUSCI_MAX_WORLD || rank < 0 || rank >= world) return CUSCI_E_INVALID_ARG;
   if (world > 1 && !nccl_unique_id) return CUSCI_E_INVALID_ARG;
   if ((alloc == nullptr) != (free_fn == nullptr)) return CUSCI_E_INVALID_ARG;
   cusci_ctx* ctx = new cusci_ctx;
@@ -194,14 +210,17 @@ int cusci_init(cusci_ctx** out, int device, int rank, int world, const void* ncc
   if (cudaMemPoolCreate(&ctx->pool, &props) != cudaSuccess) return fail(CUSCI_E_CUDA);
   uint64_t thresh = UINT64_MAX;
   cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &thresh);
-  if (cudaMallocHost(&ctx->host_pinned, 4096) != cudaSuccess) return fail(CUSCI_E_CUDA);
-  if (world > 1) {
+  if (cudaMallocHost(&ctx->host_pinned, kHostPinnedBytes) != cudaSuccess) return fail(CUSCI_E_CUDA);
+  if (nccl_unique_id) {  // world = 1 with an id: a 1-rank communicator (CUSCI_OPT_FORCE_COLLECTIVE)
     ncclUniqueId id;
     memcpy(&id, nccl_unique_id, sizeof(id));
     if (ncclCommInitRank(&ctx->comm, world, id, rank) != ncclSuccess) {
       ctx->comm = nullptr;
       return fail(CUSCI_E_NCCL);
     }
+    // persistent device words of the collective protocol (counts, status), so
+    // the exchange never needs a scratch allocation that could fail on one rank
+    if (cudaMalloc((void**)&ctx->dcomm, kCommWords * sizeof(uint64_t)) != cudaSuccess) return fail(CUSCI_E_CUDA);
   }
   *out = ctx;
   return CUSCI_OK;
@@ -227,6 +246,7 @@ void cusci_finalize(cusci_ctx* ctx) {
     cudaEventDestroy(r.b);
   }
   for (auto e : ctx->ev_free) cudaEventDestroy(e);
+  if (ctx->dcomm) cudaFree(ctx->dcomm);
   if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
   if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -234,6 +254,19 @@ void cusci_finalize(cusci_ctx* ctx) {
 }
 
 const char* cusci_last_error(const cusci_ctx* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+
+int cusci_set_option(cusci_ctx* ctx, int option, int64_t value) {
+  if (!ctx) return CUSCI_E_INVALID_ARG;
+  switch (option) {
+    case CUSCI_OPT_FORCE_COLLECTIVE:
+      if (value && !ctx->comm)
+        return set_error(ctx, CUSCI_E_INVALID_ARG, "CUSCI_OPT_FORCE_COLLECTIVE needs a communicator (pass an NCCL id to cusci_init)");
+      ctx->force_collective = value ? 1 : 0;
+      return CUSCI_OK;
+    default:
+      return set_error(ctx, CUSCI_E_INVALID_ARG, "unknown option %d", option);
+  }
+}
 
 void cusci_invalidate_integrals(cusci_ctx* ctx) {
   if (!ctx) return;

@@ -1024,19 +1024,12 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
   CUSCI_TRY(s.get_t(kHllM, &hll));
   CUSCI_TRY(s.get_t(2, &flags));
   CUSCI_CUDA(ctx, cudaMemsetAsync(flags, 0, 2 * sizeof(unsigned long long), ctx->stream));
-  static bool attr[3] = {false, false, false};
-  static int dper[3] = {0, 0, 0};
-  if (!attr[W]) {
-    CUSCI_CUDA(ctx, cudaFuncSetAttribute(tile_scatter_kernel<W, true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scatter_smem<W, 8>()));
-    CUSCI_CUDA(ctx, cudaFuncSetAttribute(tile_scatter_kernel<W, false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scatter_smem<W, 8>()));
-    CUSCI_CUDA(ctx, cudaFuncSetAttribute(tile_scatter_kernel<W, false, 9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scatter_smem<W, 9>()));
-    CUSCI_CUDA(ctx, cudaFuncSetAttribute(bucket_unique_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-    CUSCI_CUDA(ctx, cudaFuncSetAttribute(scatter1_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scatter1_smem<W>()));
-    CUSCI_CUDA(ctx, cudaFuncSetAttribute(tile_scatter_atomic_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scatter_atomic_smem<W>()));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&dper[W], bucket_unique_kernel<W>, kBU, C::SMEM);
-    if (dper[W] < 1) dper[W] = 1;
-    attr[W] = true;
-  }
+  int dper = 1, unused = 0;
+  CUSCI_TRY(kernel_setup(ctx, (const void*)tile_scatter_kernel<W, true, 8>, kST, scatter_smem<W, 8>(), &unused));
+  CUSCI_TRY(kernel_setup(ctx, (const void*)tile_scatter_kernel<W, false, 8>, kST, scatter_smem<W, 8>(), &unused));
+  CUSCI_TRY(kernel_setup(ctx, (const void*)tile_scatter_kernel<W, false, 9>, kST, scatter_smem<W, 9>(), &unused));
+  CUSCI_TRY(kernel_setup(ctx, (const void*)tile_scatter_atomic_kernel<W>, kST, scatter_atomic_smem<W>(), &unused));
+  CUSCI_TRY(kernel_setup(ctx, (const void*)bucket_unique_kernel<W>, kBU, C::SMEM, &dper));
   const uint64_t* part = in;
   uint64_t* ibase = nullptr;  // bucket input starts when the last pass left bucket regions
   if (Bmax > 0) {
@@ -1127,13 +1120,10 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
       CUSCI_CUDA(ctx, cudaMemsetAsync(gcur, 0, 256 * sizeof(unsigned long long), ctx->stream));
       CUSCI_CUDA(ctx, cudaMemsetAsync(ovf, 0, sizeof(int), ctx->stream));
       CUSCI_CUDA(ctx, cudaMemsetAsync(hll, 0, kHllM * sizeof(uint32_t), ctx->stream));
-      static int sper[3] = {0, 0, 0};
-      if (!sper[W]) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sper[W], scatter1_kernel<W>, kST, scatter1_smem<W>());
-        if (sper[W] < 1) sper[W] = 1;
-      }
+      int sper = 1;
+      CUSCI_TRY(kernel_setup(ctx, (const void*)scatter1_kernel<W>, kST, scatter1_smem<W>(), &sper));
       const uint64_t nsub = (n + SSCfg<W>::SUB - 1) / SSCfg<W>::SUB;
-      const unsigned g1 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(nsub, (uint64_t)ctx->num_sms * sper[W]));
+      const unsigned g1 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(nsub, (uint64_t)ctx->num_sms * sper));
       CUSCI_LAUNCH(ctx, PT_RADIX_DOWN, scatter1_kernel<W><<<g1, kST, scatter1_smem<W>(), ctx->stream>>>(in, n, use_tma, cap1, gcur, a, hll, ovf));
       uint64_t hc[256];
       int hv = 0;
@@ -1278,7 +1268,7 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
   const uint32_t vdcap = V ? (dcap == 0xffffffffu ? dcap : dcap / 2u + 64u) : dcap;
   const uint32_t nb = nbk << V;  // work units (sub-buckets)
   uint64_t* tmp = (part == a) ? b2 : a;
-  const unsigned dgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(nb, (uint64_t)ctx->num_sms * dper[W]));
+  const unsigned dgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(nb, (uint64_t)ctx->num_sms * dper));
   CUSCI_LAUNCH(ctx, PT_HASH, bucket_unique_kernel<W><<<dgrid, kBU, C::SMEM, ctx->stream>>>(part, part == in ? 1 : 0, use_tma, off, ibase, nbk, B, V, lf, vdcap, tmp, surv, flags));
   // pack the buckets' survivors in bucket order
   CUSCI_CUDA(ctx, cudaMemsetAsync(surv64, 0, (nb + 1) * sizeof(uint64_t), ctx->stream));

@@ -219,12 +219,12 @@ template <int W>
 __global__ void __launch_bounds__(kET, 4) contract_kernel(const uint64_t* __restrict__ keys, const double* __restrict__ hij,
                                                       const uint32_t* __restrict__ src, uint64_t n_rec,
                                                       const KPsi<W>* __restrict__ table, uint64_t tslots,
-                                                      int k, unsigned long long* __restrict__ acc,
+                                                      int k, uint64_t n_parents, unsigned long long* __restrict__ acc,
                                                       unsigned long long* __restrict__ flags) {
   const unsigned lane = lane_id();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   uint64_t missing = 0;
-  bool big = false;
+  bool big = false, badsrc = false;
   // warp-uniform trip count so the warp-level reduction always has all lanes;
   // kU consecutive 32-record groups per step: their lookups are in flight together
   constexpr int kU = 2;
@@ -242,6 +242,10 @@ __global__ void __launch_bounds__(kET, 4) contract_kernel(const uint64_t* __rest
       sv[u] = 0xffffffffu;
       if (r < n_rec) {
         sv[u] = src[r];
+        if (sv[u] >= n_parents) {  // out-of-range parent index: flagged, never accumulated
+          badsrc = true;
+          sv[u] = 0xffffffffu;
+        }
         hv[u] = hij[r];
         kv[u] = load_key<W>(keys, r);
         // home slot of the key in the ordered (key, psi) table
@@ -292,7 +296,7 @@ __global__ void __launch_bounds__(kET, 4) contract_kernel(const uint64_t* __rest
       }
       // the last lane of each run adds the run total to the parent's limbs
       const uint32_t snext = __shfl_down_sync(kFull, s, 1);
-      const bool tail = valid && (lane == 31 || snext != s);
+      const bool tail = valid && s != 0xffffffffu && (lane == 31 || snext != s);
       if (tail && acc128 != 0) {
         const unsigned __int128 uu = (unsigned __int128)acc128;
         const long long l0 = (long long)(uint32_t)(uu), l1 = (long long)(uint32_t)(uu >> 32),
@@ -308,6 +312,7 @@ __global__ void __launch_bounds__(kET, 4) contract_kernel(const uint64_t* __rest
   for (int o = 16; o; o >>= 1) missing += __shfl_xor_sync(kFull, missing, o);
   if (lane == 0 && missing) atomicAdd(&flags[0], (unsigned long long)missing);
   if (__any_sync(kFull, big) && lane == 0) atomicOr(&flags[1], 1ull);
+  if (__any_sync(kFull, badsrc) && lane == 0) atomicOr(&flags[1], 2ull);
 }
 
 __global__ void contract_finalize_kernel(const unsigned long long* __restrict__ acc, uint64_t n, double* __restrict__ e) {
@@ -349,10 +354,11 @@ int contract_impl(cusci_ctx* ctx, const uint64_t* keys, const double* hij, const
   }
   if (n_rec) {
     const unsigned g2 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_rec + kET - 1) / kET, (uint64_t)ctx->num_sms * 16));
-    CUSCI_LAUNCH(ctx, PT_ENERGY, contract_kernel<W><<<g2, kET, 0, ctx->stream>>>(keys, hij, src, n_rec, table, tslots, k, acc, flags));
+    CUSCI_LAUNCH(ctx, PT_ENERGY, contract_kernel<W><<<g2, kET, 0, ctx->stream>>>(keys, hij, src, n_rec, table, tslots, k, n_parents, acc, flags));
   }
   uint64_t h[2];
   CUSCI_TRY(read_u64(ctx, reinterpret_cast<const uint64_t*>(flags), h, 2));
+  if (h[1] & 2) return set_error(ctx, CUSCI_E_INVALID_ARG, "energy_contract: a record's src >= n_parents");
   if (h[1]) return set_error(ctx, CUSCI_E_INVALID_ARG, "energy_contract: |H psi| >= 2^20 (outside the exact-sum range) or a skewed space");
   *n_missing = h[0];
   if (n_parents) {

@@ -550,13 +550,9 @@ int gen_impl(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* parents, uin
   void (*kern)(const GenArgs) = nullptr;
   if (W == 1) kern = mode == 0 ? gen_kernel<1, 0> : (mode == 1 ? gen_kernel<1, 1> : gen_kernel<1, 2>);
   else kern = mode == 0 ? gen_kernel<2, 0> : (mode == 1 ? gen_kernel<2, 1> : gen_kernel<2, 2>);
-  static int per_sm[3][3] = {{0}};
-  if (!per_sm[W][mode]) {
-    CUSCI_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[W][mode], kern, kGenThreads, smem);
-    if (per_sm[W][mode] < 1) per_sm[W][mode] = 1;
-  }
-  const unsigned blocks = (unsigned)(ctx->num_sms * per_sm[W][mode]);
+  int per_sm = 1;
+  CUSCI_TRY(kernel_setup(ctx, (const void*)kern, kGenThreads, smem, &per_sm));
+  const unsigned blocks = (unsigned)(ctx->num_sms * per_sm);
   CUSCI_LAUNCH(ctx, PT_GEN, kern<<<blocks, kGenThreads, smem, ctx->stream>>>(a));
   unsigned long long res[4];
   CUSCI_CUDA(ctx, cudaMemcpyAsync(ctx->host_pinned, counter, sizeof(res), cudaMemcpyDeviceToHost, ctx->stream));

@@ -14,6 +14,8 @@
 namespace cusci {
 
 constexpr int kWarp = 32;
+constexpr size_t kHostPinnedBytes = 3 * CUSCI_MAX_WORLD * sizeof(uint64_t) + 4096;
+constexpr size_t kCommWords = 2 * CUSCI_MAX_WORLD + 8;  // send counts, recv counts, status words
 constexpr unsigned kFull = 0xffffffffu;
 
 // ------------------------------------------------------------------ status
@@ -54,7 +56,6 @@ struct Prep {
   const double* eri = nullptr;
   int K = 0;
   double eps = -1.0;
-  uint64_t fingerprint = 0;
   bool valid = false;
   // pair rows over spin-orbital pairs p<q, row id = q(q-1)/2 + p
   uint32_t* rowptr = nullptr;   // [npq + 1]
@@ -80,6 +81,15 @@ struct ProfRec {
   int tag;
   cudaEvent_t a, b;
 };
+// per-context launch setup of one kernel (the large-shared-memory opt-in is a
+// property of the device context, so it is cached per library context, never
+// in process-wide statics)
+struct KSetup {
+  const void* fn;
+  size_t smem;
+  int threads;
+  int per_sm;
+};
 
 }  // namespace cusci
 
@@ -97,13 +107,16 @@ struct cusci_ctx {
   cudaMemPool_t pool = nullptr;
   cusci::Arena arena;
   cusci::Prep prep;
-  void* host_pinned = nullptr;  // small pinned staging (counts, flags)
+  void* host_pinned = nullptr;  // small pinned staging (counts, flags), kHostPinnedBytes
+  uint64_t* dcomm = nullptr;    // device [kCommWords]: collective counts / status (with a communicator)
   uint64_t launches = 0;
   int num_sms = 148;
   bool profiling = false;
   uint64_t dstats[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // cusci_dedup_stats
   std::vector<cusci::ProfRec> prof;
   std::vector<cudaEvent_t> ev_free;
+  std::vector<cusci::KSetup> ksetup;  // kernel_setup cache (this context's device)
+  int force_collective = 0;           // CUSCI_OPT_FORCE_COLLECTIVE
   std::string err;
 };
 
@@ -176,6 +189,13 @@ int out_alloc(cusci_ctx* ctx, size_t bytes, void** p);
 void out_free(cusci_ctx* ctx, void* p);
 
 int check_space(cusci_ctx* ctx, const cusci_space* sp);
+// opt a kernel into `smem` bytes of dynamic shared memory on this context's
+// device (once per context) and return its resident CTAs per SM
+int kernel_setup(cusci_ctx* ctx, const void* fn, int threads, size_t smem, int* per_sm);
+// collective calls run their NCCL protocol (status + count exchange, payload
+// exchange) when the context spans several ranks, or when a 1-rank
+// communicator exists and CUSCI_OPT_FORCE_COLLECTIVE is set (tests)
+inline bool collective(const cusci_ctx* ctx) { return ctx->world > 1 || (ctx->force_collective && ctx->comm); }
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 // ------------------------------------------------------------------ keys
@@ -397,8 +417,11 @@ int unique_sorted_keys(cusci_ctx* ctx, int W, const uint64_t* in, uint64_t n, ui
                        uint64_t* n_out_dev);
 // dedup.cu: payload all-to-all-v of bins (send[r] keys to rank r, back to back)
 // into a scratch buffer *rbuf (received runs back to back by source rank)
+// The counts exchange carries each rank's local status: a rank that failed
+// sends ~0 to every peer and every rank returns the agreed error (no peer is
+// left waiting in a send/recv).  local_rc is this rank's status so far.
 int exchange_bins(cusci_ctx* ctx, int W, const uint64_t* bins, const uint64_t* send, Scratch& s, uint64_t** rbuf,
-                  uint64_t* nrecv);
+                  uint64_t* nrecv, int local_rc = CUSCI_OK, uint64_t* recv_counts = nullptr);
 int agree_status_all(cusci_ctx* ctx, int local);
 int nccl_ok(cusci_ctx* ctx, ncclResult_t r, const char* what);
 // sync the stream and read a device u64

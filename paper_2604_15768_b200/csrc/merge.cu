@@ -662,15 +662,40 @@ int merge_impl(cusci_ctx* ctx, cusci_pool* pool, const uint64_t* U, uint64_t nU,
     }
   } else {
     CUSCI_LAUNCH(ctx, PT_MERGE_SPLIT, merge_split_kernel<W><<<(unsigned)((ntiles + 1 + 255) / 256), 256, 0, ctx->stream>>>(S, nS, U, nU, ntiles, split));
-    static int mper[3] = {0, 0, 0};
-    if (!mper[W]) {
-      CUSCI_CUDA(ctx, cudaFuncSetAttribute(merge_tile_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MergeCfg<W>::SMEM));
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mper[W], merge_tile_kernel<W>, kMergeThreads, MergeCfg<W>::SMEM);
-      if (mper[W] < 1) mper[W] = 1;
+    int mper = 1;
+    CUSCI_TRY(kernel_setup(ctx, (const void*)merge_tile_kernel<W>, kMergeThreads, MergeCfg<W>::SMEM, &mper));
+    // persistent grid whose CTAs must all be resident (the static tile order's
+    // decoupled look-back waits on predecessors): a COOPERATIVE launch, which
+    // the runtime refuses rather than under-schedules; when fewer SMs are
+    // available (MPS limits, green contexts) the grid is halved until it fits
+    unsigned mgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * mper));
+    const int chk = trusted ? 0 : 1;
+    for (;;) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(mgrid);
+      cfg.blockDim = dim3(kMergeThreads);
+      cfg.dynamicSmemBytes = MergeCfg<W>::SMEM;
+      cfg.stream = ctx->stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeCooperative;
+      at[0].val.cooperative = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      cudaError_t e;
+      {
+        Prof pf_(ctx, PT_MERGE_TILE);
+        e = cudaLaunchKernelEx(&cfg, merge_tile_kernel<W>, S, nS, U, nU, (const uint64_t*)split, ntiles, status, bad, dst,
+                               (uint64_t*)insp, chk);
+      }
+      if (e == cudaErrorCooperativeLaunchTooLarge && mgrid > 1) {
+        cudaGetLastError();
+        mgrid = (mgrid + 1) / 2;
+        continue;
+      }
+      CUSCI_CUDA(ctx, e);
+      CUSCI_LAUNCH_CHECK(ctx);
+      break;
     }
-    // persistent grid: every CTA resident (the look-back relies on it)
-    const unsigned mgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * mper[W]));
-    CUSCI_LAUNCH(ctx, PT_MERGE_TILE, merge_tile_kernel<W><<<mgrid, kMergeThreads, MergeCfg<W>::SMEM, ctx->stream>>>(S, nS, U, nU, split, ntiles, status, bad, dst, (uint64_t*)insp, trusted ? 0 : 1));
     // totals = the last tile's inclusive counts; plus the input check flag
     CUSCI_CUDA(ctx, cudaMemcpyAsync(ctx->host_pinned, status + 2 * (ntiles - 1), 2 * sizeof(uint64_t),
                                     cudaMemcpyDeviceToHost, ctx->stream));

@@ -157,37 +157,12 @@ __global__ void singles_rows_kernel(const uint8_t* __restrict__ nonzero, int K, 
   srowptr[m] = n;
 }
 
-// order-independent 64-bit fingerprint of the integral bits (cache validation:
-// a freed-and-reallocated buffer can reuse the same device address)
-__global__ void fingerprint_kernel(const double* __restrict__ h, uint64_t nh, const double* __restrict__ eri,
-                                   uint64_t ne, unsigned long long* __restrict__ out) {
-  uint64_t acc = 0;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nh + ne; i += stride) {
-    const double x = i < nh ? h[i] : eri[i - nh];
-    acc ^= fmix64((uint64_t)__double_as_longlong(x) + (i + 1) * 0x9E3779B97F4A7C15ull);
-  }
-  for (int o = 16; o; o >>= 1) acc ^= __shfl_xor_sync(kFull, acc, o);
-  if (lane_id() == 0 && acc) atomicXor(out, (unsigned long long)acc);
-}
-
 }  // namespace
 
 int prep_build(cusci_ctx* ctx, const cusci_space* sp, const cusci_integrals* ints, double eps) {
   Prep& pr = ctx->prep;
   const int K = ints->n_spatial, m = sp->m;
-  uint64_t fp = 0;
-  {
-    Scratch fs(ctx);
-    unsigned long long* dfp;
-    CUSCI_TRY(fs.get_t(1, &dfp));
-    CUSCI_CUDA(ctx, cudaMemsetAsync(dfp, 0, 8, ctx->stream));
-    const uint64_t npair = (uint64_t)K * (K + 1) / 2, ne = npair * (npair + 1) / 2, nh = (uint64_t)K * K;
-    const unsigned blocks = (unsigned)std::min<uint64_t>((nh + ne + 255) / 256, (uint64_t)ctx->num_sms * 4);
-    CUSCI_LAUNCH(ctx, PT_PREP, fingerprint_kernel<<<blocks, 256, 0, ctx->stream>>>(ints->h, nh, ints->eri, ne, dfp));
-    CUSCI_TRY(read_u64(ctx, (const uint64_t*)dfp, &fp, 1));
-  }
-  if (pr.valid && pr.h == ints->h && pr.eri == ints->eri && pr.K == K && pr.eps == eps && pr.fingerprint == fp)
+  if (pr.valid && pr.h == ints->h && pr.eri == ints->eri && pr.K == K && pr.eps == eps)
     return CUSCI_OK;
   if (pr.block) {
     CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
@@ -256,7 +231,6 @@ int prep_build(cusci_ctx* ctx, const cusci_space* sp, const cusci_integrals* int
   pr.eri = ints->eri;
   pr.K = K;
   pr.eps = eps;
-  pr.fingerprint = fp;
   pr.valid = true;
   return CUSCI_OK;
 }

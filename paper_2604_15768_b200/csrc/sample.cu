@@ -44,18 +44,6 @@ __global__ void regular_sample_kernel(const uint64_t* __restrict__ srt, uint64_t
   store_key<W>(out, k, load_key<W>(srt, i));
 }
 
-// gathered [P][S] with counts[P] -> the valid samples back to back
-template <int W>
-__global__ void compact_samples_kernel(const uint64_t* __restrict__ g, const uint64_t* __restrict__ cnt, int P,
-                                       uint32_t S, uint64_t* __restrict__ out) {
-  uint64_t off = 0;
-  for (int r = 0; r < P; r++) {
-    const uint64_t c = cnt[r];
-    for (uint64_t k = threadIdx.x; k < c; k += blockDim.x) store_key<W>(out, off + k, load_key<W>(g, (uint64_t)r * S + k));
-    off += c;
-  }
-}
-
 // spl[r-1] = sorted samples[floor(r M / P)], r = 1..P-1 (zero keys if M = 0)
 template <int W>
 __global__ void pick_splitters_kernel(const uint64_t* __restrict__ s, uint64_t M, int P, uint64_t* __restrict__ spl) {
@@ -215,20 +203,19 @@ extern "C" int split_bounds(cusci_ctx* ctx, const cusci_space* sp, const uint64_
 extern "C" int dedup_sorted(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* configs, uint64_t n,
                             int n_samples, cusci_keys* owned_sorted, uint64_t* splitters_host) {
   if (!ctx) return CUSCI_E_INVALID_ARG;
+  if (ctx->broken) return set_error(ctx, CUSCI_E_CUDA, "context is unusable after an earlier CUDA/NCCL error");
   int rc = args_ok(ctx, sp);
   if (rc == CUSCI_OK && (!owned_sorted || (n && !configs) || n >= (1ull << 32) || n_samples < 1 || n_samples > (1 << 16) || ctx->world > 256))
     rc = set_error(ctx, CUSCI_E_INVALID_ARG, "dedup_sorted: bad arguments");
-  if (ctx->broken) return rc;
   CUSCI_CUDA(ctx, cudaSetDevice(ctx->device));
-  rc = agree_status_all(ctx, rc);  // collective: failing ranks still take part
-  if (rc != CUSCI_OK) {
-    if (ctx->err.empty()) set_error(ctx, rc, "dedup_sorted: a peer rank rejected its arguments");
-    return rc;
+  if (owned_sorted) {
+    owned_sorted->keys = nullptr;
+    owned_sorted->count = 0;
   }
-  const int W = sp->words, P = ctx->world;
-  owned_sorted->keys = nullptr;
-  owned_sorted->count = 0;
-  if (P == 1) {  // Steps 2-3 are the identity: the sorted unique keys
+  const int P = ctx->world;
+  if (!collective(ctx)) {  // one rank: Steps 2-3 are the identity, the sorted unique keys
+    if (rc != CUSCI_OK) return rc;
+    const int W = sp->words;
     void* o;
     CUSCI_TRY(out_alloc(ctx, std::max<uint64_t>(n, 1) * W * 8, &o));
     uint64_t u;
@@ -241,35 +228,60 @@ extern "C" int dedup_sorted(cusci_ctx* ctx, const cusci_space* sp, const uint64_
     owned_sorted->count = u;
     return CUSCI_OK;
   }
+  // collective protocol; a rank that fails before data moves still takes part
+  // in the status-carrying count all-gather (and the status all-reduce after
+  // the gather buffer is reserved), so no peer is left blocked
+  const int W = rc == CUSCI_OK ? sp->words : 1;
+  const uint32_t S = rc == CUSCI_OK ? (uint32_t)n_samples : 1u;
   Scratch s(ctx);
   // Step 1: local sort + unique, regular samples
-  uint64_t* D;
-  uint64_t nd;
-  CUSCI_TRY(s.get_t(std::max<uint64_t>(n, 1) * W, &D));
-  CUSCI_TRY(sort_unique_impl(ctx, sp, configs, n, D, &nd));
-  const uint32_t S = (uint32_t)n_samples;
-  uint64_t *gath, *cnt, *smp, *spl;
-  CUSCI_TRY(s.get_t((uint64_t)P * S * W, &gath));
-  CUSCI_TRY(s.get_t(P, &cnt));
-  CUSCI_TRY(s.get_t((uint64_t)P * S * W, &smp));
-  CUSCI_TRY(s.get_t((uint64_t)(P - 1) * W, &spl));
-  uint64_t taken;
-  CUSCI_TRY(samples_impl(ctx, W, D, nd, S, gath + (uint64_t)ctx->rank * S * W, &taken));
-  memcpy(ctx->host_pinned, &taken, sizeof(uint64_t));
-  CUSCI_CUDA(ctx, cudaMemcpyAsync(cnt + ctx->rank, ctx->host_pinned, sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
-  // Step 2: gather the samples (in place), splitters, bounds
-  CUSCI_TRY(nccl_ok(ctx, ncclGroupStart(), "group start"));
-  CUSCI_TRY(nccl_ok(ctx, ncclAllGather(gath + (uint64_t)ctx->rank * S * W, gath, (size_t)S * W, ncclUint64, ctx->comm, ctx->stream),
-                    "sample allgather"));
+  uint64_t* D = nullptr;
+  uint64_t nd = 0, taken = 0;
+  uint64_t* smp_local = nullptr;
+  if (rc == CUSCI_OK) rc = s.get_t(std::max<uint64_t>(n, 1) * W, &D);
+  if (rc == CUSCI_OK) rc = sort_unique_impl(ctx, sp, configs, n, D, &nd);
+  if (rc == CUSCI_OK) rc = s.get_t((uint64_t)S * W, &smp_local);
+  if (rc == CUSCI_OK) rc = samples_impl(ctx, W, D, nd, S, smp_local, &taken);
+  if (ctx->broken) return rc;
+  // Step 2a: all-gather of the sample counts, each carrying its rank's status
+  constexpr uint64_t kFail = 0xFA11000000000000ull;
+  uint64_t* cnt = ctx->dcomm;  // [P] (persistent: cannot fail)
+  uint64_t* hp = reinterpret_cast<uint64_t*>(ctx->host_pinned);
+  hp[0] = rc == CUSCI_OK ? taken : (kFail | (uint64_t)rc);
+  CUSCI_CUDA(ctx, cudaMemcpyAsync(cnt + ctx->rank, hp, sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
   CUSCI_TRY(nccl_ok(ctx, ncclAllGather(cnt + ctx->rank, cnt, 1, ncclUint64, ctx->comm, ctx->stream), "count allgather"));
-  CUSCI_TRY(nccl_ok(ctx, ncclGroupEnd(), "group end"));
-  uint64_t hc[512], M = 0;
+  uint64_t hc[CUSCI_MAX_WORLD], M = 0;
   CUSCI_TRY(read_u64(ctx, cnt, hc, P));
+  int agreed = rc;
+  for (int r = 0; r < P; r++)
+    if ((hc[r] & 0xFFFF000000000000ull) == kFail) agreed = std::max(agreed, (int)(hc[r] & 0xffff));
+  if (agreed != CUSCI_OK) {
+    if (rc == CUSCI_OK) set_error(ctx, agreed, "dedup_sorted failed on a peer rank (code %d)", agreed);
+    return agreed;
+  }
   for (int r = 0; r < P; r++) M += hc[r];
-  if (W == 1) CUSCI_LAUNCH(ctx, PT_PREP, compact_samples_kernel<1><<<1, 256, 0, ctx->stream>>>(gath, cnt, P, S, smp));
-  else CUSCI_LAUNCH(ctx, PT_PREP, compact_samples_kernel<2><<<1, 256, 0, ctx->stream>>>(gath, cnt, P, S, smp));
+  // Step 2b: gather the samples back to back (grouped sends/recvs of each
+  // rank's taken samples), splitters, bounds
+  uint64_t *smp = nullptr, *spl = nullptr;
+  int arc = s.get_t(std::max<uint64_t>(M, 1) * W, &smp);
+  if (arc == CUSCI_OK) arc = s.get_t((uint64_t)std::max(P - 1, 1) * W, &spl);
+  const int rc2 = agree_status_all(ctx, arc);
+  if (rc2 != CUSCI_OK) {
+    if (arc == CUSCI_OK) set_error(ctx, rc2, "dedup_sorted failed on a peer rank (code %d)", rc2);
+    return rc2;
+  }
+  CUSCI_TRY(nccl_ok(ctx, ncclGroupStart(), "group start"));
+  {
+    uint64_t off = 0;
+    for (int r = 0; r < P; r++) {
+      if (taken) CUSCI_TRY(nccl_ok(ctx, ncclSend(smp_local, taken * W, ncclUint64, r, ctx->comm, ctx->stream), "sample send"));
+      if (hc[r]) CUSCI_TRY(nccl_ok(ctx, ncclRecv(smp + off * W, hc[r] * W, ncclUint64, r, ctx->comm, ctx->stream), "sample recv"));
+      off += hc[r];
+    }
+  }
+  CUSCI_TRY(nccl_ok(ctx, ncclGroupEnd(), "group end"));
   CUSCI_TRY(splitters_impl(ctx, sp, smp, M, P, spl));
-  uint64_t bounds[513], send[512];
+  uint64_t bounds[CUSCI_MAX_WORLD + 1], send[CUSCI_MAX_WORLD];
   CUSCI_TRY(bounds_impl(ctx, W, D, nd, spl, P, bounds));
   for (int r = 0; r < P; r++) send[r] = bounds[r + 1] - bounds[r];
   // Step 3: exchange, then sort + unique of the received runs
@@ -277,10 +289,11 @@ extern "C" int dedup_sorted(cusci_ctx* ctx, const cusci_space* sp, const uint64_
   uint64_t nrecv;
   CUSCI_TRY(exchange_bins(ctx, W, D, send, s, &rbuf, &nrecv));
   void* o;
-  CUSCI_TRY(out_alloc(ctx, std::max<uint64_t>(nrecv, 1) * W * 8, &o));
+  rc = out_alloc(ctx, std::max<uint64_t>(nrecv, 1) * W * 8, &o);
+  if (rc != CUSCI_OK) return rc;
   uint64_t u;
   rc = sort_unique_impl(ctx, sp, rbuf, nrecv, (uint64_t*)o, &u);
-  if (rc == CUSCI_OK && splitters_host) {
+  if (rc == CUSCI_OK && splitters_host && P > 1) {
     CUSCI_CUDA(ctx, cudaMemcpyAsync(ctx->host_pinned, spl, (size_t)(P - 1) * W * 8, cudaMemcpyDeviceToHost, ctx->stream));
     CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     memcpy(splitters_host, ctx->host_pinned, (size_t)(P - 1) * W * 8);

@@ -183,9 +183,14 @@ def parse(text: str) -> np.ndarray:
 
 
 def full_space(K: int, n_alpha: int, n_beta: int) -> np.ndarray:
-    """All determinants with n_alpha / n_beta electrons, sorted (e.g. LiH: 225)."""
+    """All determinants with n_alpha / n_beta electrons, sorted (e.g. LiH: 225;
+    H2O-like K = 13, 5/5: 1,656,369)."""
     from itertools import combinations
     m = 2 * K
+    if m <= 64:   # vectorised: every alpha string OR every beta string
+        a = np.array([sum(1 << (2 * P) for P in c) for c in combinations(range(K), n_alpha)], dtype=np.uint64)
+        b = np.array([sum(1 << (2 * P + 1) for P in c) for c in combinations(range(K), n_beta)], dtype=np.uint64)
+        return np.sort((a[:, None] | b[None, :]).reshape(-1)).reshape(-1, 1)
     rows = []
     for ca in combinations(range(K), n_alpha):
         for cb in combinations(range(K), n_beta):
