@@ -122,7 +122,9 @@ int kernel_setup(cusci_ctx* ctx, const void* fn, int threads, size_t smem, int* 
       *per_sm = k.per_sm;
       return CUSCI_OK;
     }
-  if (smem > 48 * 1024) CUSCI_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // always opt in: static + dynamic shared memory above 48 KB needs it even
+  // when the dynamic part alone is smaller
+  if (smem) CUSCI_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
   CUSCI_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem));
   if (occ < 1) occ = 1;

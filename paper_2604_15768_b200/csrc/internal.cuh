@@ -149,10 +149,12 @@ int set_error(cusci_ctx* ctx, int code, const char* fmt, ...);
     if (rc_ != CUSCI_OK) return rc_; \
   } while (0)
 
+// cudaGetLastError (not Peek): a failed launch's error is consumed here, so it
+// cannot be reported again by a later, unrelated launch check
 #define CUSCI_LAUNCH_CHECK(ctx)                  \
   do {                                           \
     (ctx)->launches++;                           \
-    CUSCI_CUDA((ctx), cudaPeekAtLastError());    \
+    CUSCI_CUDA((ctx), cudaGetLastError());       \
   } while (0)
 
 // launch a kernel under the profiler scope of class `tag`
