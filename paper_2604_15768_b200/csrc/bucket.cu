@@ -286,8 +286,8 @@ __global__ void __launch_bounds__(kST, 2) tile_scatter_kernel(const uint64_t* __
   }
 }
 
-template <int W> constexpr size_t scatter_atomic_smem() {
-  return kSRing * ((size_t)SSCfg<W>::SUB + 2) * sizeof(KeyT<W>) + 2 * 256 * 8 + 3 * 256 * 4;
+template <int W, int RB> constexpr size_t scatter_atomic_smem() {
+  return kSRing * ((size_t)SSCfg<W>::SUB + 2) * sizeof(KeyT<W>) + 2 * (1u << RB) * 8 + 3 * (1u << RB) * 4;
 }
 
 // The last (bucket-forming) pass after a hist-free first pass, also without a
@@ -295,7 +295,8 @@ template <int W> constexpr size_t scatter_atomic_smem() {
 // tile reserves its runs with one global atomic per (sub-round, digit).  The
 // tile's group index is in PTile::mbase.  Overflow -> *ovf and nothing is
 // written past a region (the host then redoes the pass with histograms).
-template <int W>
+// RB = 8 or 9 digit bits (2^RB <= kST: one thread per digit).
+template <int W, int RB>
 __global__ void __launch_bounds__(kST, 2) tile_scatter_atomic_kernel(const uint64_t* __restrict__ in, int use_tma,
                                                                     const PTile* __restrict__ tiles, int bsel,
                                                                     uint32_t R, unsigned long long* __restrict__ gcur,
@@ -303,15 +304,16 @@ __global__ void __launch_bounds__(kST, 2) tile_scatter_atomic_kernel(const uint6
                                                                     int* __restrict__ ovf) {
   constexpr int ITEMS = SSCfg<W>::SUB / kST;
   constexpr int SUB = SSCfg<W>::SUB;
-  constexpr uint32_t RMAX = 256;
-  extern __shared__ __align__(16) unsigned char ssm[];  // scatter_atomic_smem<W>() bytes
+  constexpr uint32_t RMAX = 1u << RB;
+  static_assert(RMAX <= (uint32_t)kST, "one thread per digit");
+  extern __shared__ __align__(16) unsigned char ssm[];  // scatter_atomic_smem<W, RB>() bytes
   KeyT<W>* ring = reinterpret_cast<KeyT<W>*>(ssm);       // [kSRing][SUB + 2]
   unsigned long long* dl = reinterpret_cast<unsigned long long*>(ring + kSRing * (SUB + 2));  // [2][256]
   uint32_t* cnt = reinterpret_cast<uint32_t*>(dl + 2 * RMAX);
   uint32_t* lst = cnt + RMAX;  // [2][256]
   __shared__ __align__(8) uint64_t bar[kSRing];
   const PTile t = tiles[blockIdx.x];
-  const uint64_t gbase = t.mbase * R;  // first bucket of the tile's group (R = 2^bits <= 256 digits)
+  const uint64_t gbase = t.mbase * R;  // first bucket of the tile's group (R = 2^bits <= RMAX digits)
   const bool tma = use_tma && ((reinterpret_cast<uintptr_t>(in) & 15u) == 0);
   for (uint32_t d = threadIdx.x; d < RMAX; d += kST) cnt[d] = 0;
   const uint32_t nsub = (t.len + SUB - 1) / SUB;
@@ -617,131 +619,105 @@ __device__ __forceinline__ void cas_slot(KeyT<2>* slot, const KeyT<2>& k, KeyT<2
   old.w0 = o0;
   old.w1 = o1;
 }
-__device__ __forceinline__ bool kzero(const KeyT<1>& k) { return k.w0 == 0; }
-__device__ __forceinline__ bool kzero(const KeyT<2>& k) { return (k.w0 | k.w1) == 0; }
-
-// insert pi-value p (nonzero) from its home slot, marking a newly claimed slot
-// in the occupancy bitmap; false when the span is exhausted.  W = 2 probes with
-// the 128-bit CAS itself (returns the slot's value atomically), so a probe
-// never sees a torn 16-byte entry.
-__device__ __forceinline__ bool otab_insert(KeyT<1>* tab, uint32_t* bm, uint32_t home, uint32_t span,
-                                            const KeyT<1>& p) {
-  for (uint32_t s = home; s < span; s++) {
-    const KeyT<1> cur = tab[s];
-    if (cur.w0 == p.w0) return true;
-    if (cur.w0 == 0) {
-      KeyT<1> old;
-      cas_slot(&tab[s], p, old);
-      if (old.w0 == 0) atomicOr(&bm[s >> 5], 1u << (s & 31));
-      if (old.w0 == 0 || old.w0 == p.w0) return true;
-    }
-  }
-  return false;
-}
-__device__ __forceinline__ bool otab_insert(KeyT<2>* tab, uint32_t* bm, uint32_t home, uint32_t span,
-                                            const KeyT<2>& p) {
-  for (uint32_t s = home; s < span; s++) {
-    KeyT<2> old;
-    cas_slot(&tab[s], p, old);
-    if (kzero(old)) atomicOr(&bm[s >> 5], 1u << (s & 31));
-    if (kzero(old) || key_eq(old, p)) return true;
-  }
-  return false;
-}
 
 // ---------------------------------------------------------------- per-bucket dedup (ordered table)
-// CTA c owns a contiguous run of buckets.  The run's keys form one stream of
-// TMA pieces (<= BUFK keys, never straddling a bucket); piece k+1 is in flight
-// while piece k is inserted.  A bucket is a contiguous run of pi-values whose
-// hi lies in [b, b+1) * 2^(64-B).  Its keys go into an ORDER-PRESERVING
-// open-addressing table: home slot = floor(frac * ts), frac = the bits of hi
-// below the bucket id, linear probing forward with no wrap (an overflow tail
-// of OV slots), newly claimed slots marked in an occupancy bitmap.  Since home
-// is monotone in hi, every cluster of occupied slots holds exactly the keys
-// whose homes fall inside it, so sorting each (short) cluster in place sorts
-// the table.  The survivors are mapped back to keys (exact inverse mix) and
-// written at the bucket's input offset; the pack kernel then concatenates
-// the buckets.
-constexpr int kBU = 1024;  // dedup threads (one CTA per SM owns the shared-memory budget)
-constexpr int kILP = 8;   // keys per thread with first probes in flight together
+// One CTA per SM (the table takes the shared memory) owns a contiguous run of
+// (sub-)buckets.  A (sub-)bucket is a contiguous run of pi-values whose top
+// S = B + V bits of hi are fixed, so a table slot stores the remaining bits
+// exactly as T = (hi << S) | 1 (never 0: 0 marks an empty slot, and a zero
+// pi-value needs no special case), next to lo at W = 2.  The keys go into an
+// ORDER-PRESERVING open-addressing table of 2^logts home slots: home = the
+// top logts bits of T, linear probing forward with no wrap (an overflow tail
+// of OV slots).  Since home is monotone in T, every cluster of occupied slots
+// holds exactly the keys whose homes fall inside it, and clusters are ordered
+// among themselves.
+//
+// Insertion: each round a thread loads ILP keys straight from global memory
+// (coalesced, all in flight together) and takes them through the FAST path:
+// one shared load of the home slot -- equal: duplicate; empty: one CAS (W = 2
+// probes with the 128-bit CAS itself).  Keys that miss (home held by another
+// key, a lost CAS) are appended BY VALUE to a per-warp queue (ballot
+// compaction); whenever 32 are queued the warp drains them with every lane
+// probing, so the divergent probe loop runs on full warps.
+// Output: occupancy words by warp ballots over 32-slot windows, one block scan
+// of the window counts, the list of occupied slots (in the queue's space),
+// then -- 32 consecutive survivors per warp step, every lane busy -- each
+// survivor's rank = (occupied slots before its cluster) + (keys of its
+// cluster with a smaller T): the table is never sorted in place (no serial
+// insertion sort on the critical path); survivors are written as keys (exact
+// inverse mix) at the bucket offset + rank.
+constexpr int kBU = 1024;  // dedup threads; one CTA per SM
 template <int W> struct BUCfg {
-  static constexpr uint32_t TS = W == 1 ? 16384 : 8192;  // max home slots (128 KB)
-  static constexpr uint32_t OV = W == 1 ? 1024 : 512;    // overflow tail
-  static constexpr uint32_t BUFK = W == 1 ? 5120 : 2048; // keys per TMA piece (40 / 32 KB): 5 / 2 per thread
-  static constexpr uint32_t BUFE = BUFK + 2;             // + alignment slack (W = 1)
-  static constexpr uint32_t DT = W == 1 ? 6144 : 3072;   // target distinct keys per bucket
-  static constexpr uint32_t NWD = (TS + OV) / 32;        // bitmap words
-  static constexpr uint32_t WPT = (NWD + kBU - 1) / kBU; // bitmap words per thread
-  static constexpr size_t SMEM = (size_t)(TS + OV) * sizeof(KeyT<W>) + 2 * (size_t)BUFE * sizeof(KeyT<W>);
-  static_assert(BUFE * sizeof(KeyT<W>) >= (TS + OV) * sizeof(uint16_t), "the slot list must fit a buffer");
+  static constexpr int ILP = W == 1 ? 4 : 2;              // keys per thread per round
+  static constexpr int LOGTS = W == 1 ? 14 : 13;          // max home slots 2^LOGTS
+  static constexpr uint32_t TS = 1u << LOGTS;
+  static constexpr uint32_t OV = W == 1 ? 1024 : 512;     // overflow tail
+  static constexpr uint32_t NWIN = (TS + OV) / 32;        // 32-slot windows
+  static constexpr uint32_t QCAP = 32u * ILP + 32u;       // per-warp slow-path queue (keys)
+  static constexpr uint32_t DT = W == 1 ? 6144 : 3072;    // plan: target distinct keys per bucket
+  static constexpr size_t QBYTES = (size_t)(kBU / 32) * QCAP * sizeof(KeyT<W>);
+  static constexpr size_t SMEM = (size_t)(TS + OV) * sizeof(KeyT<W>) + QBYTES + 2 * (size_t)NWIN * sizeof(uint32_t);
+  static_assert(NWIN <= kBU, "one window count per thread in the block scan");
+  static_assert(QBYTES >= (TS + OV) * sizeof(uint16_t), "the occupied-slot list reuses the queue space");
+  static_assert(SMEM <= 227 * 1024 - 1024, "shared memory budget");
 };
 
+// table entry: T = (hi << S) | 1 (w0), lo (w1, W = 2)
+__device__ __forceinline__ KeyT<1> tenc(const KeyT<1>& p, int S) { return KeyT<1>{(p.w0 << S) | 1ull}; }
+__device__ __forceinline__ KeyT<2> tenc(const KeyT<2>& p, int S) { return KeyT<2>{(p.w0 << S) | 1ull, p.w1}; }
+__device__ __forceinline__ KeyT<1> tdec(const KeyT<1>& t, int S, uint64_t top) { return KeyT<1>{(t.w0 >> S) | top}; }
+__device__ __forceinline__ KeyT<2> tdec(const KeyT<2>& t, int S, uint64_t top) { return KeyT<2>{(t.w0 >> S) | top, t.w1}; }
+__device__ __forceinline__ bool tzero(const KeyT<1>& t) { return t.w0 == 0; }
+__device__ __forceinline__ bool tzero(const KeyT<2>& t) { return t.w0 == 0; }
+__device__ __forceinline__ bool tlt(const KeyT<1>& a, const KeyT<1>& b) { return a.w0 < b.w0; }
+__device__ __forceinline__ bool tlt(const KeyT<2>& a, const KeyT<2>& b) {
+  return a.w0 < b.w0 || (a.w0 == b.w0 && a.w1 < b.w1);
+}
+__device__ __forceinline__ uint32_t thome(const KeyT<1>& t, int logts) { return (uint32_t)(t.w0 >> (64 - logts)); }
+__device__ __forceinline__ uint32_t thome(const KeyT<2>& t, int logts) { return (uint32_t)(t.w0 >> (64 - logts)); }
+
+// one probe step at slot s: true when p is now in the table (found or inserted)
 template <int W>
-__global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* __restrict__ part, int raw, int use_tma,
+__device__ __forceinline__ bool tprobe(KeyT<W>* tab, uint32_t s, const KeyT<W>& p) {
+  KeyT<W> old;
+  if (W == 1) {
+    const KeyT<W> c = tab[s];
+    if (key_eq(c, p)) return true;
+    if (!tzero(c)) return false;
+  }
+  cas_slot(&tab[s], p, old);  // W = 2: the 128-bit CAS is the probe (never a torn read)
+  return tzero(old) || key_eq(old, p);
+}
+
+// GEN: raw (caller) input or split buckets (V = 1); the common case compiles without them
+template <int W, bool GEN>
+__global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* __restrict__ part, int raw,
                                                               const uint32_t* __restrict__ off,
-                                                              const uint64_t* __restrict__ ibase, uint32_t nb, int B, int V,
-                                                              uint32_t lf, uint32_t dcap, uint64_t* __restrict__ tmp,
-                                                              uint32_t* __restrict__ surv,
+                                                              const uint64_t* __restrict__ ibase, uint32_t nb, int B,
+                                                              int V, uint32_t lf, uint32_t dmean,
+                                                              uint64_t* __restrict__ tmp, uint32_t* __restrict__ surv,
                                                               unsigned long long* __restrict__ flags) {
   using K = KeyT<W>;
   using C = BUCfg<W>;
-  constexpr uint32_t TS = C::TS, OV = C::OV, BUFK = C::BUFK, BUFE = C::BUFE, WPT = C::WPT;
-  constexpr int NW = kBU / 32;
+  constexpr uint32_t TS = C::TS, OV = C::OV, QCAP = C::QCAP, NWIN = C::NWIN;
+  constexpr int ILP = C::ILP, NW = kBU / 32;
   extern __shared__ __align__(16) unsigned char bsm[];
   K* tab = reinterpret_cast<K*>(bsm);
-  K* bufs = tab + TS + OV;
-  __shared__ __align__(8) uint64_t bar[2];   // buffer full (TMA transaction count)
-  __shared__ __align__(8) uint64_t ebar[2];  // buffer empty (one arrival per warp)
-  __shared__ int s_zero, s_full;
-  __shared__ uint32_t wcnt[NW];
-  __shared__ uint32_t bm[C::NWD];  // slot occupancy bitmap (set on insert, cleared by pass 2)
+  K* qall = tab + TS + OV;                                        // [NW][QCAP]
+  uint32_t* bm = reinterpret_cast<uint32_t*>(qall + NW * QCAP);   // [NWIN] occupancy words
+  uint32_t* wbase = bm + NWIN;                                    // [NWIN] occupied slots before the window
+  __shared__ int s_full;
+  __shared__ uint32_t red[33];
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5, t = threadIdx.x;
-  // TMA needs 16-byte aligned sources; raw (caller) input is read with plain loads
-  const bool tma = use_tma && !raw && ((reinterpret_cast<uintptr_t>(part) & 15u) == 0);
-  // work unit = sub-bucket sb: bucket sb >> V, keeping only the keys whose next
-  // V bits of hi equal sb's low V bits (V = 1 halves the table load; the second
-  // read of the bucket comes from L2)
+  K* q = qall + warp * QCAP;
+  const int S = B + V;
   const uint32_t nsb = nb << V;
   const uint32_t bA = (uint32_t)((uint64_t)nsb * blockIdx.x / gridDim.x);
   const uint32_t bB = (uint32_t)((uint64_t)nsb * (blockIdx.x + 1) / gridDim.x);
-  // the table is cleared once here and kept clean: the compaction zeroes every slot it reads
+  // the table is cleared once here and after every bucket's output
   for (uint32_t i = t; i < TS + OV; i += kBU) tab[i] = K{};
-  for (uint32_t i = t; i < C::NWD; i += kBU) bm[i] = 0;
-  if (t == 0) {
-    s_zero = 0;
-    s_full = 0;
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    mbar_init(&ebar[0], NW);
-    mbar_init(&ebar[1], NW);
-    mbar_init_fence();
-  }
+  if (t == 0) s_full = 0;
   __syncthreads();
-  // producer state (thread 0): the next piece to issue = (pb, pp); a buffer is
-  // refilled once every warp has released the piece it held (no CTA barrier)
-  uint32_t pb = bA, pp = 0, pk = 0, epar = 0;
-  auto issue_next = [&]() {
-    while (pb < bB) {
-      const uint32_t ps0 = off[pb >> V], pn = off[(pb >> V) + 1] - ps0;
-      const uint64_t ps = ibase ? ibase[pb >> V] : (uint64_t)ps0;  // input start (regions after a hist-free pass)
-      if (pp < pn) {
-        const uint32_t len = min(BUFK, pn - pp);
-        if (pk >= 2) {  // wait for the release of piece pk - 2 (same buffer)
-          mbar_wait(&ebar[pk & 1], (epar >> (pk & 1)) & 1u);
-          epar ^= 1u << (pk & 1);
-        }
-        fence_proxy_async_smem();
-        issue_core<W>(part, ps + pp, len, bufs + (pk & 1) * BUFE, &bar[pk & 1]);
-        pp += BUFK;
-        pk++;
-        return;
-      }
-      pb++;
-      pp = 0;
-    }
-  };
-  if (tma && t == 0) issue_next();
-  uint32_t phase = 0, k = 0;  // consumer: piece counter, barrier parities
   for (uint32_t b = bA; b < bB; b++) {
     const uint32_t s = off[b >> V], nk = off[(b >> V) + 1] - s;  // s: survivor (tmp) offset
     const uint64_t si = ibase ? ibase[b >> V] : (uint64_t)s;       // input offset
@@ -750,175 +726,147 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
       if (t == 0) surv[b] = 0;
       continue;
     }
-    // table size ~lf x (expected distinct keys) slots, capped
-    const uint32_t ts = min(TS, max(64u, (lf * min(nk, dcap) + 31u) & ~31u));
-    const uint32_t span = ts + OV;
+    // 2^logts home slots ~ lf x the expected distinct keys (<= nk), capped
+    const uint32_t want = lf * min(nk, dmean);
+    int logts = 5;
+    while (logts < C::LOGTS && (1u << logts) < want) logts++;
+    const uint32_t span = (1u << logts) + OV;
     bool full = false;
-    K* buf = bufs;
-    for (uint32_t p0 = 0; p0 < nk; p0 += BUFK, k++) {
-      const uint32_t len = min(BUFK, nk - p0), cb = k & 1;
-      buf = bufs + cb * BUFE;
-      if (tma) {
-        if (t == 0) issue_next();  // piece k+1 -> the other buffer (freed by the last barrier)
-        const uint64_t g0 = si + p0;
-        const bool issued = W == 1 ? (((g0 + len) & ~1ull) > ((g0 + 1) & ~1ull)) : true;
-        if (issued) {
-          mbar_wait(&bar[cb], (phase >> cb) & 1u);
-          phase ^= 1u << cb;
+    uint32_t qn = 0;  // warp-uniform queue fill
+    // drain queue entries [qn - 32, qn) (or all, at the end) with every lane probing
+    auto drain = [&](uint32_t cnt) {
+      const uint32_t q0 = qn - cnt;
+      if (lane < cnt) {
+        const K p = q[q0 + lane];
+        uint32_t sidx = thome(p, logts) + 1;  // the home slot holds another key
+        for (;;) {
+          if (sidx >= span) {
+            full = true;
+            break;
+          }
+          if (tprobe<W>(tab, sidx, p)) break;
+          sidx++;
         }
       }
-      // kILP keys per thread: their first probes are issued together (most keys
-      // resolve on the first probe: already present, or an empty home slot)
-      const uint32_t c0 = (W == 1 && tma) ? (uint32_t)((si + p0) & 1u) : 0u;
-      const uint32_t c1 = (W == 1 && tma) ? len - (uint32_t)((si + p0 + len) & 1u) : len;
-      for (uint32_t i0 = t; i0 < len; i0 += kILP * kBU) {
-        K pv[kILP], cv[kILP];
-        uint32_t hm[kILP];
-        bool act[kILP];
-#pragma unroll
-        for (int u = 0; u < kILP; u++) {
-          const uint32_t i = i0 + u * kBU;
-          act[u] = i < len;
-          if (act[u]) {
-            if (!tma) pv[u] = load_key<W>(part, si + p0 + i);
-            else if (W == 2 || (i >= c0 && i < c1)) pv[u] = buf[i + c0];  // TMA core (key s+p0+i at buf[i + lead])
-            else pv[u] = load_key<W>(part, si + p0 + i);
-            if (raw) pv[u] = to_pi(pv[u]);
-            if (V && ((pv[u].w0 << B) >> (64 - V)) != vpart) act[u] = false;  // the other half
-            else if (kzero(pv[u])) {
-              s_zero = 1;
-              act[u] = false;
-            }
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < kILP; u++) {
-          if (act[u]) {
-            hm[u] = (uint32_t)__umul64hi(pv[u].w0 << (B + V), (uint64_t)ts);
-            cv[u] = tab[hm[u]];
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < kILP; u++)
-          if (act[u] && !key_eq(cv[u], pv[u])) full |= !otab_insert(tab, bm, hm[u], span, pv[u]);
-      }
-      if (full) s_full = 1;
+      qn = q0;
       __syncwarp();
-      if (lane == 0) mbar_arrive(&ebar[cb]);  // this warp is done with the buffer
-      if (p0 + BUFK >= nk) __syncthreads();   // last piece of the bucket: table complete
+    };
+    for (uint32_t r0 = 0; r0 < nk; r0 += ILP * kBU) {
+      K pv[ILP];
+      bool act[ILP];
+#pragma unroll
+      for (int u = 0; u < ILP; u++) {
+        const uint32_t i = r0 + u * kBU + t;
+        act[u] = i < nk;
+        if (act[u]) pv[u] = load_key<W>(part, si + i);
+      }
+#pragma unroll
+      for (int u = 0; u < ILP; u++) {
+        bool slow = false;
+        if (act[u]) {
+          K p = pv[u];
+          if (GEN && raw) p = to_pi(p);
+          if (!GEN || !V || ((p.w0 << B) >> (64 - V)) == vpart) {  // (V: the other sub-bucket is skipped)
+            p = tenc(p, S);
+            pv[u] = p;
+            slow = !tprobe<W>(tab, thome(p, logts), p);
+          }
+        }
+        const unsigned sb = __ballot_sync(kFull, slow);
+        if (slow) q[qn + __popc(sb & lanemask_lt())] = pv[u];
+        qn += __popc(sb);
+      }
+      __syncwarp();
+      while (qn >= 32) drain(32);
     }
-    const uint32_t z = (uint32_t)s_zero;
+    if (qn) drain(qn);
+    if (full) s_full = 1;
+    __syncthreads();  // table complete
+    const uint64_t top = (uint64_t)b << (64 - S);  // the sub-bucket's fixed top S bits of hi
     if (s_full) {
       // table overflow (pathological bucket): pass this (sub-)bucket's keys
-      // through unfiltered (the host finishes with a full sort + unique);
+      // through unfiltered (the host finishes with a full sort + unique) and
       // restore a clean table.  Part 0 fills its bucket region from the front,
       // part 1 from the back.
       auto mine = [&](const K& kk) { return !V || (((raw ? to_pi(kk) : kk).w0 << B) >> (64 - V)) == vpart; };
-      if (t == 0) wcnt[0] = 0;
+      if (t == 0) red[0] = 0;
       __syncthreads();
       uint32_t cnt = 0;
       for (uint32_t i = t; i < nk; i += kBU) cnt += mine(load_key<W>(part, si + i));
-      atomicAdd(&wcnt[0], cnt);
+      atomicAdd(&red[0], cnt);
       __syncthreads();
-      const uint32_t nh = wcnt[0];
+      const uint32_t nh = red[0];
       __syncthreads();
-      if (t == 0) wcnt[0] = 0;
+      if (t == 0) red[0] = 0;
       __syncthreads();
       const uint64_t ob = vpart ? (uint64_t)s + nk - nh : (uint64_t)s;
       for (uint32_t i = t; i < nk; i += kBU) {
         const K p = load_key<W>(part, si + i);
-        if (mine(p)) store_key<W>(tmp, ob + atomicAdd(&wcnt[0], 1u), raw ? p : from_pi(p));
+        if (mine(p)) store_key<W>(tmp, ob + atomicAdd(&red[0], 1u), raw ? p : from_pi(p));
       }
       for (uint32_t i = t; i < span; i += kBU) tab[i] = K{};
-      for (uint32_t i = t; i < C::NWD; i += kBU) bm[i] = 0;
       if (t == 0) {
         surv[b] = nh;
         atomicAdd(&flags[0], 1ull);
-      }
-      __syncthreads();
-      if (t == 0) {
         s_full = 0;
-        s_zero = 0;
       }
       __syncthreads();
       continue;
     }
-    const uint32_t nwd = (span + 31) / 32;
-    // pass 1 (thread t: the 16-slot half-words t, t + kBU, ...): the thread
-    // owning a cluster's first slot insertion-sorts the cluster
-    for (uint32_t h = t; h < 2 * nwd; h += kBU) {
-      const uint32_t w = h >> 1, sh = (h & 1u) * 16u;
-      const uint32_t word = bm[w];
-      const uint32_t bits = (word >> sh) & 0xffffu;
-      if (!bits) continue;
-      const uint32_t prev = sh ? ((word >> (sh - 1)) & 1u) : (w > 0 ? (bm[w - 1] >> 31) : 0u);
-      uint32_t starts = bits & ~((bits << 1) | prev) & 0xffffu;
-      while (starts) {
-        const uint32_t i = __ffs(starts) - 1;
-        starts &= starts - 1;
-        const uint32_t u = w * 32 + sh + i;
-        uint32_t x = w, z = ~word & (~0u << (sh + i));  // first empty slot at or after u
-        while (!z && ++x < nwd) z = ~bm[x];
-        const uint32_t e = min(z ? x * 32 + __ffs(z) - 1 : nwd * 32, span);
-        for (uint32_t a = u + 1; a < e; a++) {
-          const K xk = tab[a];
-          uint32_t j = a;
-          while (j > u && pi_lt(xk, tab[j - 1])) {
-            tab[j] = tab[j - 1];
-            j--;
-          }
-          tab[j] = xk;
-        }
+    const uint32_t nwin = span / 32;
+    // occupancy words: one warp ballot per 32-slot window
+    for (uint32_t w = warp; w < nwin; w += NW) {
+      const unsigned o = __ballot_sync(kFull, !tzero(tab[w * 32 + lane]));
+      if (lane == 0) bm[w] = o;
+    }
+    __syncthreads();
+    uint32_t tot = 0;
+    const uint32_t wex = block_excl_scan_u32(t < nwin ? __popc(bm[t]) : 0u, red, tot);
+    if (t < nwin) wbase[t] = wex;
+    __syncthreads();
+    // the occupied slots in order (the queue space is free now)
+    uint16_t* sidx = reinterpret_cast<uint16_t*>(qall);
+    for (uint32_t w = warp; w < nwin; w += NW) {
+      const uint32_t o = bm[w];
+      if ((o >> lane) & 1u) sidx[wbase[w] + __popc(o & lanemask_lt())] = (uint16_t)(w * 32 + lane);
+    }
+    __syncthreads();
+    // survivor k (rank k among the occupied slots) sits in the cluster [cs, ce);
+    // its output position = k - (slot - cs) + (keys of the cluster smaller than it)
+    const uint64_t ob = vpart ? (uint64_t)s + nk - tot : (uint64_t)s;
+    for (uint32_t kk = t; kk < tot; kk += kBU) {
+      const uint32_t slot = sidx[kk];
+      const K v = tab[slot];
+      const uint32_t w = slot >> 5, bit = slot & 31u, word = bm[w];
+      uint32_t cs;  // one past the last empty slot below (possibly in earlier windows)
+      const uint32_t below = ~word & ((1u << bit) - 1u);
+      if (below) {
+        cs = w * 32 + (32 - __clz(below));
+      } else {
+        uint32_t x = w;
+        while (x > 0 && bm[x - 1] == 0xffffffffu) x--;
+        cs = x > 0 ? (x - 1) * 32 + (32 - __clz(~bm[x - 1])) : 0u;
       }
-    }
-    uint32_t c = 0;  // occupied slots in this thread's pass-2 words
-#pragma unroll
-    for (uint32_t q = 0; q < WPT; q++) {
-      const uint32_t w = t * WPT + q;
-      if (w < nwd) c += __popc(bm[w]);
-    }
-    // exclusive prefix of the per-thread counts (warp scan + warp totals)
-    uint32_t inc = c;
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(kFull, inc, o);
-      if ((int)lane >= o) inc += y;
-    }
-    if (lane == 31) wcnt[warp] = inc;
-    __syncthreads();  // clusters sorted, per-warp counts
-    uint32_t pos = inc - c, tot = 0;
-    for (int w = 0; w < NW; w++) {
-      const uint32_t v = wcnt[w];
-      pos += w < (int)warp ? v : 0u;
-      tot += v;
-    }
-    // pass 2: the word owners list the occupied slots in order (in the last
-    // consumed input buffer), then every thread writes survivors back as keys
-    // and clears their slots
-    uint16_t* sidx = reinterpret_cast<uint16_t*>(buf);
-#pragma unroll
-    for (uint32_t q = 0; q < WPT; q++) {
-      const uint32_t w = t * WPT + q;
-      if (w >= nwd) continue;
-      uint32_t r = bm[w];
-      while (r) {
-        sidx[pos++] = (uint16_t)(w * 32 + __ffs(r) - 1);
-        r &= r - 1;
+      uint32_t ce;  // the first empty slot above
+      const uint32_t above = bit < 31 ? (~word & (~0u << (bit + 1))) : 0u;
+      if (above) {
+        ce = w * 32 + __ffs(above) - 1;
+      } else {
+        uint32_t x = w + 1;
+        while (x < nwin && bm[x] == 0xffffffffu) x++;
+        ce = x < nwin ? x * 32 + __ffs(~bm[x]) - 1 : nwin * 32;
       }
-      bm[w] = 0;
+      uint32_t rank = 0, y = cs;
+      for (; y + 1 < ce; y += 2) {  // two independent loads per step
+        const K a0 = tab[y], a1 = tab[y + 1];
+        rank += (tlt(a0, v) ? 1u : 0u) + (tlt(a1, v) ? 1u : 0u);
+      }
+      if (y < ce) rank += tlt(tab[y], v) ? 1u : 0u;
+      store_key<W>(tmp, ob + (kk - (slot - cs) + rank), from_pi(tdec(v, S, top)));
     }
-    // output region: part 0 from the bucket region's front, part 1 from its back
-    const uint64_t ob = vpart ? (uint64_t)s + nk - (tot + z) : (uint64_t)s;
-    if (z && t == 0) store_key<W>(tmp, ob, from_pi(K{}));
-    __syncthreads();  // slot list complete
-    for (uint32_t i = t; i < tot; i += kBU) {
-      const uint32_t u = sidx[i];
-      store_key<W>(tmp, ob + z + i, from_pi(tab[u]));
-      tab[u] = K{};
-    }
-    if (t == 0) {
-      surv[b] = tot + z;
-      s_zero = 0;
-    }
+    if (t == 0) surv[b] = tot;
+    __syncthreads();  // every rank computed: clear the occupied slots
+    for (uint32_t kk = t; kk < tot; kk += kBU) tab[sidx[kk]] = K{};
     __syncthreads();  // table clean for the next bucket
   }
 }
@@ -988,7 +936,7 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
   static const int use_tma = getenv("CUSCI_NO_TMA") ? 0 : 1;
   static const uint32_t lf = [] {
     const char* e = getenv("CUSCI_TABLE_LF");  // table slots per expected distinct key
-    return e ? (uint32_t)std::max(2, atoi(e)) : 4u;
+    return e ? (uint32_t)std::max(1, atoi(e)) : 3u;
   }();
   static const uint64_t dt = [] {
     const char* e = getenv("CUSCI_BUCKET_DISTINCT");  // target distinct keys per bucket
@@ -1002,7 +950,7 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
   int Bmax = 0;
   while ((n >> Bmax) > dt && Bmax < 22) Bmax++;
   int B = Bmax;
-  uint32_t dcap = 0xffffffffu;  // cap on the distinct keys a bucket is expected to hold
+  uint32_t dcap = 0xffffffffu;  // expected distinct keys per bucket (+25%; sizes the table)
   const uint32_t nb_max = 1u << Bmax;
   uint64_t *a, *b2;
   uint32_t *off, *surv, *hll;
@@ -1028,8 +976,10 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
   CUSCI_TRY(kernel_setup(ctx, (const void*)tile_scatter_kernel<W, true, 8>, kST, scatter_smem<W, 8>(), &unused));
   CUSCI_TRY(kernel_setup(ctx, (const void*)tile_scatter_kernel<W, false, 8>, kST, scatter_smem<W, 8>(), &unused));
   CUSCI_TRY(kernel_setup(ctx, (const void*)tile_scatter_kernel<W, false, 9>, kST, scatter_smem<W, 9>(), &unused));
-  CUSCI_TRY(kernel_setup(ctx, (const void*)tile_scatter_atomic_kernel<W>, kST, scatter_atomic_smem<W>(), &unused));
-  CUSCI_TRY(kernel_setup(ctx, (const void*)bucket_unique_kernel<W>, kBU, C::SMEM, &dper));
+  CUSCI_TRY(kernel_setup(ctx, (const void*)tile_scatter_atomic_kernel<W, 8>, kST, scatter_atomic_smem<W, 8>(), &unused));
+  CUSCI_TRY(kernel_setup(ctx, (const void*)tile_scatter_atomic_kernel<W, 9>, kST, scatter_atomic_smem<W, 9>(), &unused));
+  CUSCI_TRY(kernel_setup(ctx, (const void*)bucket_unique_kernel<W, false>, kBU, C::SMEM, &dper));
+  CUSCI_TRY(kernel_setup(ctx, (const void*)bucket_unique_kernel<W, true>, kBU, C::SMEM, &dper));
   const uint64_t* part = in;
   uint64_t* ibase = nullptr;  // bucket input starts when the last pass left bucket regions
   if (Bmax > 0) {
@@ -1153,7 +1103,9 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
       const int Btot = done + bits;
       const uint64_t nbk2 = 1ull << Btot;
       const uint64_t mean = n >> Btot;
-      const uint64_t cap2 = mean + mean / 5 + 1024;  // duplicates make bucket sizes spread more than keys
+      // duplicates make bucket sizes spread more than distinct keys (N2 batch, measured:
+      // max/mean 1.20 at 16 bits, 1.33 at 17): regions of 1.4 x mean + 2 Ki keys
+      const uint64_t cap2 = mean + (mean * 2) / 5 + 2048;
       const uint32_t G = (uint32_t)gstart.size() - 1;
       std::vector<PTile> tl;
       tl.reserve(n / kPTile + G + 1);
@@ -1176,7 +1128,10 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
       CUSCI_CUDA(ctx, cudaMemcpyAsync(dtl, tl.data(), nt * sizeof(PTile), cudaMemcpyHostToDevice, ctx->stream));
       CUSCI_CUDA(ctx, cudaMemsetAsync(gcur2, 0, nbk2 * sizeof(unsigned long long), ctx->stream));
       CUSCI_CUDA(ctx, cudaMemsetAsync(ovf, 0, sizeof(int), ctx->stream));
-      CUSCI_LAUNCH(ctx, PT_RADIX_DOWN, tile_scatter_atomic_kernel<W><<<nt, kST, scatter_atomic_smem<W>(), ctx->stream>>>(part, use_tma, dtl, done + bits, 1u << bits, gcur2, cap2, r2, ovf));
+      if (bits <= 8)
+        CUSCI_LAUNCH(ctx, PT_RADIX_DOWN, tile_scatter_atomic_kernel<W, 8><<<nt, kST, scatter_atomic_smem<W, 8>(), ctx->stream>>>(part, use_tma, dtl, done + bits, 1u << bits, gcur2, cap2, r2, ovf));
+      else
+        CUSCI_LAUNCH(ctx, PT_RADIX_DOWN, tile_scatter_atomic_kernel<W, 9><<<nt, kST, scatter_atomic_smem<W, 9>(), ctx->stream>>>(part, use_tma, dtl, done + bits, 1u << bits, gcur2, cap2, r2, ovf));
       std::vector<uint64_t> cnt(nbk2), ib(nbk2);
       std::vector<uint32_t> offh(nbk2 + 1);
       CUSCI_CUDA(ctx, cudaMemcpyAsync(cnt.data(), gcur2, nbk2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1235,7 +1190,7 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
       const int np = (rest + max_bits - 1) / max_bits;
       for (int pi = 0; pi < np; pi++) {
         const int bits = (rest - (done - bits1) + (np - pi) - 1) / (np - pi);  // even split
-        if (regions && np == 1 && bits <= 8 && last_regions_knob) {
+        if (regions && np == 1 && bits <= 9 && last_regions_knob) {
           const int rc = run_pass_last_regions(bits);
           if (rc == CUSCI_OK) continue;
           if (rc != -1) return rc;
@@ -1247,7 +1202,7 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
                                         ctx->stream));
         CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
       }
-      dcap = (uint32_t)std::min<double>(4e9, 2.0 * D / std::ldexp(1.0, B) + 64.0);
+      dcap = (uint32_t)std::min<double>(4e9, 1.25 * D / std::ldexp(1.0, B) + 64.0);
     }
   } else {
     const uint32_t o2[2] = {0u, (uint32_t)n};
@@ -1256,20 +1211,24 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
     CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   }
   const uint32_t nbk = 1u << B;
-  // V = 1 (knob only): each bucket is processed as two halves (by the next bit
-  // of hi), each re-reading the bucket but filling its table half as much.
-  // Measured on the N2 batch: 26 ms vs 17.5 ms for V = 0 (the table load is not
-  // what bounds the kernel), so it is off by default.
+  // V = 1: each bucket is processed as two halves (by the next bit of hi),
+  // each re-reading the bucket.  Needed when B = 0 (a table entry stores hi
+  // without its top S = B + V >= 1 fixed bits, which frees its "occupied" bit);
+  // otherwise a knob (measured slower on N2: the table load does not bound the kernel).
   static const int split_knob = [] {
     const char* e = getenv("CUSCI_BUCKET_SPLIT");  // tuning knob
     return e ? atoi(e) : 0;
   }();
-  const int V = (split_knob == 1 && B < 63) ? 1 : 0;
+  const int V = (B == 0 || (split_knob == 1 && B < 63)) ? 1 : 0;
   const uint32_t vdcap = V ? (dcap == 0xffffffffu ? dcap : dcap / 2u + 64u) : dcap;
   const uint32_t nb = nbk << V;  // work units (sub-buckets)
   uint64_t* tmp = (part == a) ? b2 : a;
   const unsigned dgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(nb, (uint64_t)ctx->num_sms * dper));
-  CUSCI_LAUNCH(ctx, PT_HASH, bucket_unique_kernel<W><<<dgrid, kBU, C::SMEM, ctx->stream>>>(part, part == in ? 1 : 0, use_tma, off, ibase, nbk, B, V, lf, vdcap, tmp, surv, flags));
+  const int raw = part == in ? 1 : 0;
+  if (raw || V)
+    CUSCI_LAUNCH(ctx, PT_HASH, bucket_unique_kernel<W, true><<<dgrid, kBU, C::SMEM, ctx->stream>>>(part, raw, off, ibase, nbk, B, V, lf, vdcap, tmp, surv, flags));
+  else
+    CUSCI_LAUNCH(ctx, PT_HASH, bucket_unique_kernel<W, false><<<dgrid, kBU, C::SMEM, ctx->stream>>>(part, raw, off, ibase, nbk, B, V, lf, vdcap, tmp, surv, flags));
   // pack the buckets' survivors in bucket order
   CUSCI_CUDA(ctx, cudaMemsetAsync(surv64, 0, (nb + 1) * sizeof(uint64_t), ctx->stream));
   CUSCI_CUDA(ctx, cudaMemcpy2DAsync(surv64, sizeof(uint64_t), surv, sizeof(uint32_t), sizeof(uint32_t), nb,
