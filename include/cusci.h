@@ -214,6 +214,14 @@ int dedup_partition(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* confi
                     int n_owners, cusci_keys* bins, uint64_t* counts);
 int dedup_finalize(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* keys, uint64_t n,
                    cusci_keys* unique_sorted);
+/* dedup_finalize for what dedup_global's owner receives: n_runs runs back to
+ * back (device keys; run r has run_counts[r] keys, HOST array), each strictly
+ * increasing in pi (a dedup_partition bin of some rank).  Same output as
+ * dedup_finalize on the concatenation, without a partition pass: every
+ * bucket's keys are located in each run by binary search (1 <= n_runs <=
+ * CUSCI_MAX_WORLD; unsorted runs give an unspecified result). */
+int dedup_finalize_runs(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* keys, const uint64_t* run_counts,
+                        int n_runs, cusci_keys* unique_sorted);
 
 /* ---- the paper's sort-based regular-sampling dedup ------
  * PAPER.md Sec 4.1.1 :448-462 ("Sort-Based Regular Sampling De-duplication",
@@ -299,8 +307,14 @@ int cusci_pool_merge(cusci_ctx* ctx, cusci_pool* space, const cusci_pool* src, c
  * EXACTLY in 128-bit integers (order independent), and e[s] is that sum
  * rounded once to fp64.  Requires |p| < 2^20 (CUSCI_E_INVALID_ARG otherwise,
  * e untouched).  A record whose key is not in the space contributes 0 and is
- * counted in *n_missing (host).  Single rank: with world > 1 records and psi
- * must first meet at the key's owner (CUSCI_E_INVALID_ARG for now). */
+ * counted in *n_missing (host).  src[r] >= n_parents: CUSCI_E_INVALID_ARG.
+ * COLLECTIVE when world > 1 (or CUSCI_OPT_FORCE_COLLECTIVE): space_keys/psi
+ * are this rank's OWNED shard (dedup_global's output on this rank), and the
+ * records' keys are looked up at their owners: each rank sends its records'
+ * distinct keys to the owners (the dedup_global partition + exchange), the
+ * owners answer with psi over a reverse exchange, and the records are
+ * contracted locally (PAPER.md :634 "just-in-time" reverse index).  Errors are
+ * agreed across ranks as in dedup_global. */
 int energy_contract(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* keys, const double* hij,
                     const uint32_t* src, uint64_t n_rec, uint64_t n_parents, const uint64_t* space_keys,
                     uint64_t n_space, const double* psi, double* e, uint64_t* n_missing);

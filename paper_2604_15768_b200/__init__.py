@@ -339,6 +339,21 @@ class Context:
         self._check(rc, "dedup_finalize")
         return self._take(k.keys, int(k.count), W)
 
+    def dedup_finalize_runs(self, space: Space, keys: torch.Tensor, run_counts) -> torch.Tensor:
+        """Owner-side unique of runs received back to back, each strictly
+        increasing in the hash order (dedup_partition bins)."""
+        W = space.words
+        cfg = _as_u64_2d(keys, W)
+        counts = (ctypes.c_uint64 * len(run_counts))(*[int(c) for c in run_counts])
+        if sum(int(c) for c in run_counts) != cfg.shape[0]:
+            raise ValueError("run_counts must sum to the number of keys")
+        k = _Keys()
+        sp = space._c()
+        rc = lib().dedup_finalize_runs(self._ctx, ctypes.byref(sp), ctypes.c_void_p(cfg.data_ptr()), counts,
+                                       len(run_counts), ctypes.byref(k))
+        self._check(rc, "dedup_finalize_runs")
+        return self._take(k.keys, int(k.count), W)
+
     # ------------------------------------------------------------------ step 3
     def pool(self, space: Space, capacity: int = 1 << 20) -> "Pool":
         return Pool(self, space, capacity)

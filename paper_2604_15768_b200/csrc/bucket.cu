@@ -696,7 +696,13 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
                                                               const uint64_t* __restrict__ ibase, uint32_t nb, int B,
                                                               int V, uint32_t lf, uint32_t dmean,
                                                               uint64_t* __restrict__ tmp, uint32_t* __restrict__ surv,
-                                                              unsigned long long* __restrict__ flags) {
+                                                              unsigned long long* __restrict__ flags,
+                                                              const uint32_t* __restrict__ lb,
+                                                              const uint64_t* __restrict__ rs, int nruns) {
+  // nruns > 0 (GEN only): the input is nruns pi-sorted runs back to back (run
+  // r starts at rs[r]); bucket b's keys are the segments [lb[r][b],
+  // lb[r][b+1]) of every run (the owner-side finalize of dedup_global: no
+  // partition pass over the received keys)
   using K = KeyT<W>;
   using C = BUCfg<W>;
   constexpr uint32_t TS = C::TS, OV = C::OV, QCAP = C::QCAP, NWIN = C::NWIN;
@@ -708,9 +714,12 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
   uint32_t* wbase = bm + NWIN;                                    // [NWIN] occupied slots before the window
   __shared__ int s_full;
   __shared__ uint32_t red[33];
+  __shared__ uint64_t sg_st[GEN ? CUSCI_MAX_WORLD : 1];       // segment starts of the current bucket
+  __shared__ uint32_t sg_pre[GEN ? CUSCI_MAX_WORLD + 1 : 1];  // bucket-local start of each segment
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5, t = threadIdx.x;
   K* q = qall + warp * QCAP;
   const int S = B + V;
+  const bool segs = GEN && nruns > 0;
   const uint32_t nsb = nb << V;
   const uint32_t bA = (uint32_t)((uint64_t)nsb * blockIdx.x / gridDim.x);
   const uint32_t bB = (uint32_t)((uint64_t)nsb * (blockIdx.x + 1) / gridDim.x);
@@ -726,6 +735,30 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
       if (t == 0) surv[b] = 0;
       continue;
     }
+    if (segs) {  // this bucket's segments (the previous bucket ended with a barrier)
+      const uint32_t bb = b >> V, nbk1 = nb + 1;
+      if (t < (uint32_t)nruns) sg_st[t] = rs[t] + lb[(size_t)t * nbk1 + bb];
+      if (t == 0) {
+        uint32_t a = 0;
+        for (int r = 0; r < nruns; r++) {
+          sg_pre[r] = a;
+          a += lb[(size_t)r * nbk1 + bb + 1] - lb[(size_t)r * nbk1 + bb];
+        }
+        sg_pre[nruns] = a;
+      }
+      __syncthreads();
+    }
+    // global index of the bucket's i-th input key
+    auto kaddr = [&](uint32_t i) -> uint64_t {
+      if (!segs) return si + i;
+      int lo = 0, hi = nruns - 1;  // last segment with sg_pre[r] <= i
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (sg_pre[mid] <= i) lo = mid;
+        else hi = mid - 1;
+      }
+      return sg_st[lo] + (i - sg_pre[lo]);
+    };
     // 2^logts home slots ~ lf x the expected distinct keys (<= nk), capped
     const uint32_t want = lf * min(nk, dmean);
     int logts = 5;
@@ -758,7 +791,7 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
       for (int u = 0; u < ILP; u++) {
         const uint32_t i = r0 + u * kBU + t;
         act[u] = i < nk;
-        if (act[u]) pv[u] = load_key<W>(part, si + i);
+        if (act[u]) pv[u] = load_key<W>(part, kaddr(i));
       }
 #pragma unroll
       for (int u = 0; u < ILP; u++) {
@@ -792,7 +825,7 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
       if (t == 0) red[0] = 0;
       __syncthreads();
       uint32_t cnt = 0;
-      for (uint32_t i = t; i < nk; i += kBU) cnt += mine(load_key<W>(part, si + i));
+      for (uint32_t i = t; i < nk; i += kBU) cnt += mine(load_key<W>(part, kaddr(i)));
       atomicAdd(&red[0], cnt);
       __syncthreads();
       const uint32_t nh = red[0];
@@ -801,7 +834,7 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
       __syncthreads();
       const uint64_t ob = vpart ? (uint64_t)s + nk - nh : (uint64_t)s;
       for (uint32_t i = t; i < nk; i += kBU) {
-        const K p = load_key<W>(part, si + i);
+        const K p = load_key<W>(part, kaddr(i));
         if (mine(p)) store_key<W>(tmp, ob + atomicAdd(&red[0], 1u), raw ? p : from_pi(p));
       }
       for (uint32_t i = t; i < span; i += kBU) tab[i] = K{};
@@ -1226,9 +1259,9 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
   const unsigned dgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(nb, (uint64_t)ctx->num_sms * dper));
   const int raw = part == in ? 1 : 0;
   if (raw || V)
-    CUSCI_LAUNCH(ctx, PT_HASH, bucket_unique_kernel<W, true><<<dgrid, kBU, C::SMEM, ctx->stream>>>(part, raw, off, ibase, nbk, B, V, lf, vdcap, tmp, surv, flags));
+    CUSCI_LAUNCH(ctx, PT_HASH, bucket_unique_kernel<W, true><<<dgrid, kBU, C::SMEM, ctx->stream>>>(part, raw, off, ibase, nbk, B, V, lf, vdcap, tmp, surv, flags, nullptr, nullptr, 0));
   else
-    CUSCI_LAUNCH(ctx, PT_HASH, bucket_unique_kernel<W, false><<<dgrid, kBU, C::SMEM, ctx->stream>>>(part, raw, off, ibase, nbk, B, V, lf, vdcap, tmp, surv, flags));
+    CUSCI_LAUNCH(ctx, PT_HASH, bucket_unique_kernel<W, false><<<dgrid, kBU, C::SMEM, ctx->stream>>>(part, raw, off, ibase, nbk, B, V, lf, vdcap, tmp, surv, flags, nullptr, nullptr, 0));
   // pack the buckets' survivors in bucket order
   CUSCI_CUDA(ctx, cudaMemsetAsync(surv64, 0, (nb + 1) * sizeof(uint64_t), ctx->stream));
   CUSCI_CUDA(ctx, cudaMemcpy2DAsync(surv64, sizeof(uint64_t), surv, sizeof(uint32_t), sizeof(uint32_t), nb,
@@ -1269,6 +1302,108 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
   return CUSCI_OK;
 }
 
+// run bounds for the owner-side finalize: lb[r][b] = first index of run r
+// (pi-sorted keys) whose top B bits of hi are >= b, b in [0, 2^B]
+template <int W>
+__global__ void run_bounds_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ rs,
+                                  const uint64_t* __restrict__ rn, int P, int B, uint32_t* __restrict__ lb) {
+  const uint32_t nbk1 = (1u << B) + 1;
+  const uint64_t id = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= (uint64_t)P * nbk1) return;
+  const uint32_t r = (uint32_t)(id / nbk1), b = (uint32_t)(id % nbk1);
+  uint64_t lo = 0, hi = rn[r];
+  if (b == nbk1 - 1) {
+    lo = hi;
+  } else {
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      const uint64_t top = B ? (hk_hi(load_key<W>(keys, rs[r] + mid)) >> (64 - B)) : 0ull;
+      if (top < b) lo = mid + 1;
+      else hi = mid;
+    }
+  }
+  lb[id] = (uint32_t)lo;
+}
+// off[b] = sum_r lb[r][b]: bucket b's offset in the virtual concatenation
+__global__ void run_offsets_kernel(const uint32_t* __restrict__ lb, int P, uint32_t nbk1, uint32_t* __restrict__ off) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nbk1) return;
+  uint32_t a = 0;
+  for (int r = 0; r < P; r++) a += lb[(size_t)r * nbk1 + b];
+  off[b] = a;
+}
+
+// owner-side finalize of dedup_global (a11): the P received runs (each
+// strictly increasing in pi, back to back) -> their distinct keys in pi order.
+// No partition pass: bucket b's keys are found in every run by binary search
+// and the bucket kernel reads the P segments directly.
+template <int W>
+int runs_dedup_impl(cusci_ctx* ctx, const uint64_t* in, const uint64_t* counts, int P, uint64_t* out, uint64_t* n_out) {
+  using C = BUCfg<W>;
+  *n_out = 0;
+  uint64_t n = 0;
+  std::vector<uint64_t> rs(P), rn(P);
+  for (int r = 0; r < P; r++) {
+    rs[r] = n;
+    rn[r] = counts[r];
+    n += counts[r];
+  }
+  if (n == 0) return CUSCI_OK;
+  if (n >= (1ull << 32)) return set_error(ctx, CUSCI_E_INVALID_ARG, "dedup: %llu received keys exceed 2^32", (unsigned long long)n);
+  int B = 0;
+  while ((n >> B) > C::DT && B < 22) B++;  // the distinct count is <= n
+  const int V = B == 0 ? 1 : 0;
+  const uint32_t nbk = 1u << B, nb = nbk << V;
+  Scratch s(ctx);
+  uint32_t *lb, *off, *surv;
+  uint64_t *drs, *surv64, *soff, *tmp;
+  unsigned long long* flags;
+  CUSCI_TRY(s.get_t((size_t)P * (nbk + 1), &lb));
+  CUSCI_TRY(s.get_t(nbk + 1, &off));
+  CUSCI_TRY(s.get_t(2 * (size_t)P, &drs));
+  CUSCI_TRY(s.get_t(nb + 1, &surv));
+  CUSCI_TRY(s.get_t(nb + 1, &surv64));
+  CUSCI_TRY(s.get_t(nb + 1, &soff));
+  CUSCI_TRY(s.get_t((n + 2) * W, &tmp));
+  CUSCI_TRY(s.get_t(2, &flags));
+  std::vector<uint64_t> hr(2 * P);
+  for (int r = 0; r < P; r++) {
+    hr[r] = rs[r];
+    hr[P + r] = rn[r];
+  }
+  CUSCI_CUDA(ctx, cudaMemcpyAsync(drs, hr.data(), 2 * P * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+  CUSCI_CUDA(ctx, cudaMemsetAsync(flags, 0, 2 * sizeof(unsigned long long), ctx->stream));
+  const uint64_t nth = (uint64_t)P * (nbk + 1);
+  CUSCI_LAUNCH(ctx, PT_SCATTER, run_bounds_kernel<W><<<(unsigned)((nth + 255) / 256), 256, 0, ctx->stream>>>(in, drs, drs + P, P, B, lb));
+  CUSCI_LAUNCH(ctx, PT_SCATTER, run_offsets_kernel<<<(nbk + 1 + 255) / 256, 256, 0, ctx->stream>>>(lb, P, nbk + 1, off));
+  int dper = 1;
+  CUSCI_TRY(kernel_setup(ctx, (const void*)bucket_unique_kernel<W, true>, kBU, C::SMEM, &dper));
+  const unsigned dgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(nb, (uint64_t)ctx->num_sms * dper));
+  static const uint32_t lf = [] {
+    const char* e = getenv("CUSCI_TABLE_LF");
+    return e ? (uint32_t)std::max(1, atoi(e)) : 3u;
+  }();
+  CUSCI_LAUNCH(ctx, PT_HASH, bucket_unique_kernel<W, true><<<dgrid, kBU, C::SMEM, ctx->stream>>>(in, 1, off, nullptr, nbk, B, V, lf, 0xffffffffu, tmp, surv, flags, lb, drs, P));
+  CUSCI_CUDA(ctx, cudaMemsetAsync(surv64, 0, (nb + 1) * sizeof(uint64_t), ctx->stream));
+  CUSCI_CUDA(ctx, cudaMemcpy2DAsync(surv64, sizeof(uint64_t), surv, sizeof(uint32_t), sizeof(uint32_t), nb,
+                                    cudaMemcpyDeviceToDevice, ctx->stream));
+  CUSCI_TRY(scan_exclusive_u64(ctx, surv64, soff, nb + 1, nullptr));
+  const unsigned cgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nb + 255) / 256, (uint64_t)ctx->num_sms * 8));
+  CUSCI_LAUNCH(ctx, PT_SCATTER, bucket_compact_kernel<W><<<cgrid, kBT, 0, ctx->stream>>>(tmp, off, surv, soff, nb, V, out));
+  uint64_t h[2];
+  CUSCI_CUDA(ctx, cudaMemcpyAsync(ctx->host_pinned, soff + nb, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  CUSCI_CUDA(ctx, cudaMemcpyAsync((char*)ctx->host_pinned + 8, flags, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  memcpy(h, ctx->host_pinned, sizeof(h));
+  ctx->dstats[0] += 1;
+  ctx->dstats[1] += n;
+  ctx->dstats[3] += h[1] ? 0 : h[0];
+  ctx->dstats[4] += nb;
+  if (h[1]) return local_dedup_impl<W>(ctx, in, n, out, n_out);  // a table overflowed: the general path
+  *n_out = h[0];
+  return CUSCI_OK;
+}
+
 template <int W>
 int owner_bounds_impl(cusci_ctx* ctx, const uint64_t* keys, uint64_t n, int P, uint64_t* counts) {
   Scratch s(ctx);
@@ -1286,6 +1421,11 @@ int owner_bounds_impl(cusci_ctx* ctx, const uint64_t* keys, uint64_t n, int P, u
 int local_dedup(cusci_ctx* ctx, int W, const uint64_t* in, uint64_t n, uint64_t* out, uint64_t* n_out) {
   if (n >= (1ull << 32)) return set_error(ctx, CUSCI_E_INVALID_ARG, "dedup: n=%llu exceeds 2^32", (unsigned long long)n);
   return W == 1 ? local_dedup_impl<1>(ctx, in, n, out, n_out) : local_dedup_impl<2>(ctx, in, n, out, n_out);
+}
+
+int runs_dedup(cusci_ctx* ctx, int W, const uint64_t* in, const uint64_t* counts, int P, uint64_t* out,
+               uint64_t* n_out) {
+  return W == 1 ? runs_dedup_impl<1>(ctx, in, counts, P, out, n_out) : runs_dedup_impl<2>(ctx, in, counts, P, out, n_out);
 }
 
 int owner_counts(cusci_ctx* ctx, int W, const uint64_t* keys, uint64_t n, int P, uint64_t* counts) {

@@ -164,12 +164,34 @@ int finalize_impl(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* keys, u
   return CUSCI_OK;
 }
 
-// a11 at the owner over P received runs (each strictly increasing in pi)
+}  // namespace
+
+int dedup_local_bins(cusci_ctx* ctx, int W, const uint64_t* configs, uint64_t n, int P, uint64_t* bins,
+                     uint64_t* counts, uint64_t* total) {
+  return W == 1 ? partition_impl<1>(ctx, configs, n, P, bins, counts, total)
+                : partition_impl<2>(ctx, configs, n, P, bins, counts, total);
+}
+
+namespace {
+
+// a11 at the owner over P received runs (each strictly increasing in pi):
+// bucket-wise unique straight from the runs (runs_dedup), no partition pass
 int finalize_runs(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* rbuf, const uint64_t* counts, int P,
                   uint64_t nrecv, cusci_keys* out) {
-  (void)counts;
-  (void)P;
-  return finalize_impl(ctx, sp, rbuf, nrecv, out);
+  const int W = sp->words;
+  out->keys = nullptr;
+  out->count = 0;
+  void* o = nullptr;
+  CUSCI_TRY(out_alloc(ctx, std::max<uint64_t>(nrecv, 1) * W * 8, &o));
+  uint64_t u = 0;
+  const int rc = runs_dedup(ctx, W, rbuf, counts, P, (uint64_t*)o, &u);
+  if (rc != CUSCI_OK) {
+    out_free(ctx, o);
+    return rc;
+  }
+  out->keys = (uint64_t*)o;
+  out->count = u;
+  return CUSCI_OK;
 }
 
 int dedup_args(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* configs, uint64_t n, const void* out) {
@@ -213,6 +235,18 @@ extern "C" int dedup_finalize(cusci_ctx* ctx, const cusci_space* sp, const uint6
   CUSCI_TRY(dedup_args(ctx, sp, keys, n, unique_sorted));
   CUSCI_CUDA(ctx, cudaSetDevice(ctx->device));
   return finalize_impl(ctx, sp, keys, n, unique_sorted);
+}
+
+extern "C" int dedup_finalize_runs(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* keys,
+                                   const uint64_t* run_counts, int n_runs, cusci_keys* unique_sorted) {
+  if (!ctx) return CUSCI_E_INVALID_ARG;
+  if (n_runs < 1 || n_runs > CUSCI_MAX_WORLD || !run_counts)
+    return set_error(ctx, CUSCI_E_INVALID_ARG, "bad n_runs/run_counts");
+  uint64_t n = 0;
+  for (int r = 0; r < n_runs; r++) n += run_counts[r];
+  CUSCI_TRY(dedup_args(ctx, sp, keys, n, unique_sorted));
+  CUSCI_CUDA(ctx, cudaSetDevice(ctx->device));
+  return finalize_runs(ctx, sp, keys, run_counts, n_runs, n, unique_sorted);
 }
 
 extern "C" int dedup_global(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* configs, uint64_t n,

@@ -167,6 +167,10 @@ __global__ void __launch_bounds__(kET) place_kernel(const uint64_t* __restrict__
   }
 }
 template <int W> __device__ __forceinline__ bool kp_empty(const KPsi<W>& r);
+// an amplitude the owner did not have (multi-rank lookup): this NaN payload
+__device__ __forceinline__ bool psi_missing(double x) {
+  return (unsigned long long)__double_as_longlong(x) == 0x7FF4DEADBEEF0001ull;
+}
 template <> __device__ __forceinline__ bool kp_empty<1>(const KPsi<1>& r) { return r.k0 == 0; }
 template <> __device__ __forceinline__ bool kp_empty<2>(const KPsi<2>& r) { return (r.k0 | r.k1) == 0; }
 
@@ -264,7 +268,7 @@ __global__ void __launch_bounds__(kET, 4) contract_kernel(const uint64_t* __rest
         KPsi<W> e = ev[u];
         for (uint64_t slot = hm[u];;) {  // probe forward until the key or an empty slot
           if (kp_eq<W>(e, kv[u])) {
-            found = true;
+            found = !psi_missing(e.psi);
             ps = e.psi;
             break;
           }
@@ -325,6 +329,51 @@ __global__ void contract_finalize_kernel(const unsigned long long* __restrict__ 
   }
 }
 
+// owner side of the multi-rank reverse index: psi of each requested key from
+// the ordered (key, psi) table of the owned shard, the missing marker if absent
+template <int W>
+__global__ void __launch_bounds__(kET) lookup_kernel(const uint64_t* __restrict__ req, uint64_t n,
+                                                    const KPsi<W>* __restrict__ table, uint64_t tslots, int k,
+                                                    double* __restrict__ out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += stride) {
+    const KeyT<W> kv = load_key<W>(req, r);
+    double ps = __longlong_as_double((long long)0x7FF4DEADBEEF0001ull);
+    for (uint64_t slot = k ? (to_pi(kv).w0 >> (64 - k)) : 0ull; slot < tslots; slot++) {
+      const KPsi<W> e = table[slot];
+      if (kp_eq<W>(e, kv)) {
+        ps = e.psi;
+        break;
+      }
+      if (kp_empty<W>(e)) break;
+    }
+    out[r] = ps;
+  }
+}
+
+// ordered (key, psi) table of a pi-sorted space (see place_kernel)
+template <int W>
+int build_table(cusci_ctx* ctx, Scratch& s, const uint64_t* space, uint64_t n_space, const double* psi, KPsi<W>** table,
+                uint64_t* tslots_out, int* k_out, unsigned long long* ovf) {
+  int k = 1;
+  while ((1ull << k) < 2 * n_space && k < 40) k++;
+  const uint64_t tslots = (1ull << k) + 4096 + n_space / 16;
+  const uint64_t nc = (n_space + kPCh - 1) / kPCh;
+  long long *cmax, *cpre;
+  CUSCI_TRY(s.get_t(tslots, table));
+  CUSCI_TRY(s.get_t(std::max<uint64_t>(nc, 1), &cmax));
+  CUSCI_TRY(s.get_t(std::max<uint64_t>(nc, 1), &cpre));
+  CUSCI_CUDA(ctx, cudaMemsetAsync(*table, 0, tslots * sizeof(KPsi<W>), ctx->stream));
+  if (n_space) {
+    CUSCI_LAUNCH(ctx, PT_ENERGY, chunk_max_kernel<W><<<(unsigned)nc, kET, 0, ctx->stream>>>(space, n_space, k, cmax));
+    CUSCI_LAUNCH(ctx, PT_ENERGY, chunk_prefix_kernel<<<1, 1024, 0, ctx->stream>>>(cmax, nc, cpre));
+    CUSCI_LAUNCH(ctx, PT_ENERGY, place_kernel<W><<<(unsigned)nc, kET, 0, ctx->stream>>>(space, psi, n_space, k, cpre, *table, tslots, ovf));
+  }
+  *tslots_out = tslots;
+  *k_out = k;
+  return CUSCI_OK;
+}
+
 template <int W>
 int contract_impl(cusci_ctx* ctx, const uint64_t* keys, const double* hij, const uint32_t* src, uint64_t n_rec,
                   uint64_t n_parents, const uint64_t* space, uint64_t n_space, const double* psi, double* e,
@@ -332,26 +381,15 @@ int contract_impl(cusci_ctx* ctx, const uint64_t* keys, const double* hij, const
   Scratch s(ctx);
   // ordered (key, psi) table: 2^k >= 2 n_space home slots + a tail for the
   // displacements at the top end
-  int k = 1;
-  while ((1ull << k) < 2 * n_space && k < 40) k++;
-  const uint64_t tslots = (1ull << k) + 4096 + n_space / 16;
-  const uint64_t nc = (n_space + kPCh - 1) / kPCh;
   KPsi<W>* table;
-  long long *cmax, *cpre;
+  uint64_t tslots;
+  int k;
   unsigned long long *acc, *flags;
-  CUSCI_TRY(s.get_t(tslots, &table));
-  CUSCI_TRY(s.get_t(std::max<uint64_t>(nc, 1), &cmax));
-  CUSCI_TRY(s.get_t(std::max<uint64_t>(nc, 1), &cpre));
   CUSCI_TRY(s.get_t(std::max<uint64_t>(4 * n_parents, 1), &acc));
   CUSCI_TRY(s.get_t(2, &flags));
-  CUSCI_CUDA(ctx, cudaMemsetAsync(table, 0, tslots * sizeof(KPsi<W>), ctx->stream));
   CUSCI_CUDA(ctx, cudaMemsetAsync(acc, 0, std::max<uint64_t>(4 * n_parents, 1) * 8, ctx->stream));
   CUSCI_CUDA(ctx, cudaMemsetAsync(flags, 0, 16, ctx->stream));
-  if (n_space) {
-    CUSCI_LAUNCH(ctx, PT_ENERGY, chunk_max_kernel<W><<<(unsigned)nc, kET, 0, ctx->stream>>>(space, n_space, k, cmax));
-    CUSCI_LAUNCH(ctx, PT_ENERGY, chunk_prefix_kernel<<<1, 1024, 0, ctx->stream>>>(cmax, nc, cpre));
-    CUSCI_LAUNCH(ctx, PT_ENERGY, place_kernel<W><<<(unsigned)nc, kET, 0, ctx->stream>>>(space, psi, n_space, k, cpre, table, tslots, flags + 1));
-  }
+  CUSCI_TRY(build_table<W>(ctx, s, space, n_space, psi, &table, &tslots, &k, flags + 1));
   if (n_rec) {
     const unsigned g2 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_rec + kET - 1) / kET, (uint64_t)ctx->num_sms * 16));
     CUSCI_LAUNCH(ctx, PT_ENERGY, contract_kernel<W><<<g2, kET, 0, ctx->stream>>>(keys, hij, src, n_rec, table, tslots, k, n_parents, acc, flags));
@@ -368,6 +406,53 @@ int contract_impl(cusci_ctx* ctx, const uint64_t* keys, const double* hij, const
   return CUSCI_OK;
 }
 
+// world > 1 (or a forced collective): records and psi meet at the key's owner
+// (PAPER.md :634 "reverse index just-in-time"): each rank sends its records'
+// locally-unique keys to their owners (the dedup_global partition + the a10
+// exchange), the owner answers every request with psi from its shard (ordered
+// table lookup; a marker when absent), the answers come back over the reverse
+// exchange aligned with the requests, and the records are contracted locally
+// against (requested keys, psi).  Two status-carrying exchanges: a failure on
+// any rank before the second one is agreed by every rank.
+template <int W>
+int contract_collective(cusci_ctx* ctx, const uint64_t* keys, const double* hij, const uint32_t* src, uint64_t n_rec,
+                        uint64_t n_parents, const uint64_t* space, uint64_t n_space, const double* psi, double* e,
+                        uint64_t* n_missing, int rc) {
+  const int P = ctx->world;
+  Scratch s(ctx);
+  uint64_t* L = nullptr;
+  uint64_t send[CUSCI_MAX_WORLD] = {0}, rcounts[CUSCI_MAX_WORLD] = {0}, nl = 0;
+  if (rc == CUSCI_OK) rc = s.get_t(std::max<uint64_t>(n_rec, 1) * W, &L);
+  if (rc == CUSCI_OK) rc = dedup_local_bins(ctx, W, keys, n_rec, P, L, send, &nl);
+  if (ctx->broken) return rc;
+  uint64_t *req, nreq;
+  CUSCI_TRY(exchange_bins(ctx, W, L, send, s, &req, &nreq, rc, rcounts));
+  // owner: psi of every requested key
+  double* ans = nullptr;
+  KPsi<W>* table;
+  uint64_t tslots;
+  int k;
+  unsigned long long* ovf = nullptr;
+  rc = s.get_t(std::max<uint64_t>(nreq, 1), &ans);
+  if (rc == CUSCI_OK) rc = s.get_t(1, &ovf);
+  if (rc == CUSCI_OK) rc = cudaMemsetAsync(ovf, 0, 8, ctx->stream) == cudaSuccess ? CUSCI_OK : CUSCI_E_CUDA;
+  if (rc == CUSCI_OK) rc = build_table<W>(ctx, s, space, n_space, psi, &table, &tslots, &k, ovf);
+  if (rc == CUSCI_OK && nreq) {
+    const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nreq + kET - 1) / kET, (uint64_t)ctx->num_sms * 16));
+    lookup_kernel<W><<<g, kET, 0, ctx->stream>>>(req, nreq, table, tslots, k, ans);
+    ctx->launches++;
+    if (cudaGetLastError() != cudaSuccess) rc = CUSCI_E_CUDA;
+  }
+  if (ctx->broken) return rc;
+  // answers back to the requesters (8-byte words), aligned with their requests
+  uint64_t *back, nback;
+  CUSCI_TRY(exchange_bins(ctx, 1, reinterpret_cast<const uint64_t*>(ans), rcounts, s, &back, &nback, rc));
+  if (nback != nl) return set_error(ctx, CUSCI_E_CUDA, "energy_contract: %llu answers for %llu requests",
+                                    (unsigned long long)nback, (unsigned long long)nl);
+  return contract_impl<W>(ctx, keys, hij, src, n_rec, n_parents, L, nl, reinterpret_cast<const double*>(back), e,
+                          n_missing);
+}
+
 }  // namespace
 }  // namespace cusci
 
@@ -378,16 +463,21 @@ extern "C" int energy_contract(cusci_ctx* ctx, const cusci_space* sp, const uint
                                uint64_t n_space, const double* psi, double* e, uint64_t* n_missing) {
   if (!ctx) return CUSCI_E_INVALID_ARG;
   if (ctx->broken) return set_error(ctx, CUSCI_E_CUDA, "context is unusable after an earlier CUDA/NCCL error");
-  CUSCI_TRY(check_space(ctx, sp));
-  if (!n_missing) return set_error(ctx, CUSCI_E_INVALID_ARG, "n_missing is NULL");
-  if (ctx->world > 1)
-    return set_error(ctx, CUSCI_E_INVALID_ARG, "energy_contract: single rank only (records and psi must meet at the owner)");
-  if (n_rec && (!keys || !hij || !src)) return set_error(ctx, CUSCI_E_INVALID_ARG, "record arrays are NULL");
-  if (n_parents && !e) return set_error(ctx, CUSCI_E_INVALID_ARG, "e is NULL");
-  if (n_space && (!space_keys || !psi)) return set_error(ctx, CUSCI_E_INVALID_ARG, "space arrays are NULL");
-  if (n_space >= (1ull << 32)) return set_error(ctx, CUSCI_E_INVALID_ARG, "n_space must be < 2^32");
+  int rc = check_space(ctx, sp);
+  if (rc == CUSCI_OK && !n_missing) rc = set_error(ctx, CUSCI_E_INVALID_ARG, "n_missing is NULL");
+  if (rc == CUSCI_OK && n_rec && (!keys || !hij || !src)) rc = set_error(ctx, CUSCI_E_INVALID_ARG, "record arrays are NULL");
+  if (rc == CUSCI_OK && n_parents && !e) rc = set_error(ctx, CUSCI_E_INVALID_ARG, "e is NULL");
+  if (rc == CUSCI_OK && n_space && (!space_keys || !psi)) rc = set_error(ctx, CUSCI_E_INVALID_ARG, "space arrays are NULL");
+  if (rc == CUSCI_OK && n_space >= (1ull << 32)) rc = set_error(ctx, CUSCI_E_INVALID_ARG, "n_space must be < 2^32");
+  if (rc == CUSCI_OK && n_rec >= (1ull << 32)) rc = set_error(ctx, CUSCI_E_INVALID_ARG, "n_rec must be < 2^32 per call");
   CUSCI_CUDA(ctx, cudaSetDevice(ctx->device));
-  *n_missing = 0;
+  if (n_missing) *n_missing = 0;
+  if (collective(ctx)) {
+    const int W = rc == CUSCI_OK ? sp->words : 1;
+    return W == 1 ? contract_collective<1>(ctx, keys, hij, src, n_rec, n_parents, space_keys, n_space, psi, e, n_missing, rc)
+                  : contract_collective<2>(ctx, keys, hij, src, n_rec, n_parents, space_keys, n_space, psi, e, n_missing, rc);
+  }
+  if (rc != CUSCI_OK) return rc;
   return sp->words == 1 ? contract_impl<1>(ctx, keys, hij, src, n_rec, n_parents, space_keys, n_space, psi, e, n_missing)
                         : contract_impl<2>(ctx, keys, hij, src, n_rec, n_parents, space_keys, n_space, psi, e, n_missing);
 }

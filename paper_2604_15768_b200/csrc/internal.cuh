@@ -412,6 +412,10 @@ int radix_sort_keys(cusci_ctx* ctx, int W, uint64_t* keys, uint64_t* alt, uint64
 // local dedup (bucket.cu): out (capacity n) receives the distinct keys of in,
 // sorted in the hash order; *n_out their number (host)
 int local_dedup(cusci_ctx* ctx, int W, const uint64_t* in, uint64_t n, uint64_t* out, uint64_t* n_out);
+// owner-side finalize: P pi-sorted runs back to back (counts HOST [P]) -> the
+// distinct keys in pi order (no partition pass)
+int runs_dedup(cusci_ctx* ctx, int W, const uint64_t* in, const uint64_t* counts, int P, uint64_t* out,
+               uint64_t* n_out);
 // owner range sizes of a hash-ordered array (host counts[P])
 int owner_counts(cusci_ctx* ctx, int W, const uint64_t* keys, uint64_t n, int P, uint64_t* counts);
 // unique compaction of sorted keys into out; count written to device *n_out_dev
@@ -425,6 +429,10 @@ int unique_sorted_keys(cusci_ctx* ctx, int W, const uint64_t* in, uint64_t n, ui
 int exchange_bins(cusci_ctx* ctx, int W, const uint64_t* bins, const uint64_t* send, Scratch& s, uint64_t** rbuf,
                   uint64_t* nrecv, int local_rc = CUSCI_OK, uint64_t* recv_counts = nullptr);
 int agree_status_all(cusci_ctx* ctx, int local);
+// a8 + a9: the distinct keys of configs in pi order, grouped into P owner
+// bins (back to back; counts HOST [P]); *total = distinct keys
+int dedup_local_bins(cusci_ctx* ctx, int W, const uint64_t* configs, uint64_t n, int P, uint64_t* bins,
+                     uint64_t* counts, uint64_t* total);
 int nccl_ok(cusci_ctx* ctx, ncclResult_t r, const char* what);
 // sync the stream and read a device u64
 int read_u64(cusci_ctx* ctx, const uint64_t* dev, uint64_t* host, int count = 1);

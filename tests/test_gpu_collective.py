@@ -81,3 +81,22 @@ def test_collective_dedup_sorted(P, cctx, W, n):
     got = cctx.dedup_sorted(sp, torch.from_numpy(keys).cuda(), 512).cpu().numpy().reshape(-1, W)
     ref = OS.from_ints(OS.sort_unique(OS.to_ints(keys, W)), W).reshape(-1, W)
     assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("wl_key,n_par,W,keep_every", [("h2o", 300, 1, 1), ("h2o", 300, 1, 3), ("c2h4", 4, 2, 2)])
+def test_collective_energy_contract(P, cctx, wl_key, n_par, W, keep_every):
+    """f1 through the owner protocol (requests -> owner lookup -> answers back)
+    vs the exact-sum oracle, with keys missing from the space."""
+    from oracle import energy
+    from tests.test_gpu_parity import assert_contract_close
+    wl, ints, par = synth.workload_inputs(wl_key, n_parents=n_par)
+    sp = P.Space(wl.m, wl.n_alpha, wl.n_beta)
+    rec = cctx.gen_coupled(sp, torch.from_numpy(par).cuda(), P.DeviceIntegrals(ints.h, ints.eri), 0.0, with_src=True)
+    uniq = cctx.dedup_global(sp, rec.keys)[::keep_every].contiguous()
+    psi = np.random.default_rng(9).uniform(-1.0, 1.0, size=uniq.shape[0])
+    e, miss = cctx.energy_contract(sp, rec, len(par), uniq, torch.from_numpy(psi).cuda())
+    src = rec.src[:rec.count].cpu().numpy()
+    ref, rmiss, _ = energy.contract(rec.keys.cpu().numpy().reshape(-1, W), rec.hij.cpu().numpy(), src, len(par),
+                                    uniq.cpu().numpy().reshape(-1, W), psi, W)
+    assert miss == rmiss and (miss > 0) == (keep_every > 1)
+    assert_contract_close(e.cpu().numpy(), ref, np.bincount(src, minlength=len(par)))

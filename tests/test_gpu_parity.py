@@ -333,12 +333,30 @@ def test_dedup_logical_ranks(P, ctx, W, Pn):
     total = 0
     for o in range(Pn):
         recv = torch.cat([bins[r][o] for r in range(Pn)])
-        got = ctx.dedup_finalize(sp, recv).cpu().numpy().reshape(-1, W)
         ref = oracle.dedup(allk, W, Pn, o)
+        got = ctx.dedup_finalize(sp, recv).cpu().numpy().reshape(-1, W)
         assert_hash_sorted_unique(got, W)
         assert np.array_equal(synth.sort_keys(got), ref.reshape(-1, W))
+        # the owner-side finalize dedup_global uses: the runs read in place, no partition pass
+        got2 = ctx.dedup_finalize_runs(sp, recv, [bins[r][o].shape[0] for r in range(Pn)]).cpu().numpy()
+        assert np.array_equal(got2.reshape(-1, W), got)
         total += len(got)
     assert total == len(oracle.dedup(allk, W))
+
+
+@pytest.mark.parametrize("W,Pn,n", [(1, 3, 3_000_000), (2, 5, 900_001), (1, 8, 20)])
+def test_dedup_finalize_runs(P, ctx, W, Pn, n):
+    """runs_dedup on runs with heavy overlap (every key on several ranks) and
+    empty runs, at sizes spanning many buckets."""
+    sp = P.Space(64 * W, 1, 1)
+    allk = synth.zipf_keys(n, W, 0.9, 1 << 21, seed=17 + Pn)
+    runs = [ctx.dedup_global(sp, torch.from_numpy(allk[r::Pn]).cuda()) for r in range(Pn)]
+    runs[1] = runs[1][:0]
+    recv = torch.cat(runs)
+    got = ctx.dedup_finalize_runs(sp, recv, [x.shape[0] for x in runs]).cpu().numpy().reshape(-1, W)
+    keep = np.concatenate([allk[r::Pn] for r in range(Pn) if r != 1]) if Pn > 1 else allk
+    assert_hash_sorted_unique(got, W)
+    assert np.array_equal(synth.sort_keys(got), oracle.dedup(keep, W).reshape(-1, W))
 
 
 # ------------------------------------------------------------------ merge
