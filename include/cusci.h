@@ -319,6 +319,62 @@ int energy_contract(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* keys,
                     const uint32_t* src, uint64_t n_rec, uint64_t n_parents, const uint64_t* space_keys,
                     uint64_t n_space, const double* psi, double* e, uint64_t* n_missing);
 
+/* ---- next row: memory-centric streaming -------------------
+ * PAPER.md Sec 4.3 :583-634 (fig:mem_flow): mini-batches with the device as a
+ * scratchpad; separate streams for host->device prefetch, compute and
+ * device->host offload, double-buffered so batch i+1 loads and batch i-1
+ * offloads while batch i computes (:617).  Host buffers should be pinned
+ * (cudaHostAlloc / torch pin_memory) for the copies to overlap. */
+typedef struct {
+  uint64_t batch_parents;  /* parents per mini-batch (stream_generate, stream_energy_regen) */
+  uint64_t batch_records;  /* records per mini-batch (stream_energy) */
+  uint64_t* host_keys;     /* HOST [host_capacity][words]: the "original set" (nullable: no offload) */
+  double* host_hij;        /* HOST [host_capacity] */
+  uint32_t* host_src;      /* HOST [host_capacity]: GLOBAL parent index (batch start + index in batch) */
+  uint64_t host_capacity;  /* records the host buffers hold */
+} cusci_stream_cfg;
+typedef struct {
+  uint64_t batches, records, unique;  /* unique: the pool's size after stream_generate */
+  double ms_wall;                     /* the stage on the device clock (events) */
+  double ms_h2d, ms_compute, ms_d2h;  /* busy time of each stream (sum of its spans): overlap = sum - wall */
+  uint64_t h2d_bytes, d2h_bytes;
+  uint64_t peak_device_bytes;         /* library-held device memory high-water mark during the stage */
+} cusci_stream_stats;
+
+/* Stage 1 (PAPER.md :628 "cold data are immediately offloaded to host memory
+ * via an asynchronous D2H stream ... global de-duplication is then performed
+ * on the retained device data"): for each parent mini-batch of parents_host
+ * (HOST [n_parents][words]): prefetch the next batch (H2D stream), gen_coupled
+ * into one of two device record slots, dedup_global of its keys and
+ * merge_space into unique_pool (compute stream), and -- if host_keys is set --
+ * offload the batch's records into the host original set (D2H stream), in
+ * batch order, src = global parent index.  Peak device memory is bounded by
+ * the batch, not by n_parents (plus the pool).  COLLECTIVE when world > 1
+ * (dedup_global; the batch count is agreed, max over ranks).  Errors: as
+ * gen_coupled / dedup_global / merge_space; E_CAPACITY when the host buffers
+ * hold fewer records than generated (stats->records = the true total, the
+ * first host_capacity records were written, the pool is complete). */
+int stream_generate(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* parents_host, uint64_t n_parents,
+                    const cusci_integrals* ints, double threshold, const cusci_stream_cfg* cfg,
+                    cusci_pool* unique_pool, cusci_stream_stats* stats);
+/* Stage 3, reload (PAPER.md :634): the original set (the cfg host buffers,
+ * n_rec records) streamed back in batches of batch_records (H2D stream,
+ * double-buffered prefetch) and contracted as energy_contract does against
+ * (space_keys, psi) (device): one table for the stage, batches accumulated
+ * exactly, so e is bit-identical to one energy_contract over all records.
+ * One rank (E_INVALID_ARG when collective). */
+int stream_energy(cusci_ctx* ctx, const cusci_space* sp, const cusci_stream_cfg* cfg, uint64_t n_rec,
+                  uint64_t n_parents, const uint64_t* space_keys, uint64_t n_space, const double* psi, double* e,
+                  uint64_t* n_missing, cusci_stream_stats* stats);
+/* Stage 3, regenerate (the B200 alternative to keeping the original set):
+ * the records of each parent mini-batch are generated again on the device
+ * (parents prefetched H2D) and contracted; same e as stream_energy, bit for
+ * bit, with no host original set at all.  One rank. */
+int stream_energy_regen(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* parents_host, uint64_t n_parents,
+                        const cusci_integrals* ints, double threshold, const cusci_stream_cfg* cfg,
+                        const uint64_t* space_keys, uint64_t n_space, const double* psi, double* e,
+                        uint64_t* n_missing, cusci_stream_stats* stats);
+
 #ifdef __cplusplus
 }
 #endif

@@ -17,7 +17,7 @@ import torch
 
 from ._lib import CUSCI_ERRORS, CusciError, lib, LIB_PATH  # noqa: F401
 
-__all__ = ["Space", "DeviceIntegrals", "Context", "Pool", "Records", "CusciError", "LIB_PATH",
+__all__ = ["Space", "DeviceIntegrals", "Context", "Pool", "Records", "HostRecords", "CusciError", "LIB_PATH",
            "gen_coupled_bound"]
 
 
@@ -37,6 +37,21 @@ class _Records(ctypes.Structure):
 
 class _Keys(ctypes.Structure):
     _fields_ = [("keys", ctypes.c_void_p), ("count", ctypes.c_uint64)]
+
+
+class _StreamCfg(ctypes.Structure):
+    _fields_ = [("batch_parents", ctypes.c_uint64), ("batch_records", ctypes.c_uint64), ("host_keys", ctypes.c_void_p),
+                ("host_hij", ctypes.c_void_p), ("host_src", ctypes.c_void_p), ("host_capacity", ctypes.c_uint64)]
+
+
+class _StreamStats(ctypes.Structure):
+    _fields_ = [("batches", ctypes.c_uint64), ("records", ctypes.c_uint64), ("unique", ctypes.c_uint64),
+                ("ms_wall", ctypes.c_double), ("ms_h2d", ctypes.c_double), ("ms_compute", ctypes.c_double),
+                ("ms_d2h", ctypes.c_double), ("h2d_bytes", ctypes.c_uint64), ("d2h_bytes", ctypes.c_uint64),
+                ("peak_device_bytes", ctypes.c_uint64)]
+
+    def as_dict(self) -> dict:
+        return {f: getattr(self, f) for f, _ in self._fields_}
 
 
 class Space:
@@ -76,6 +91,28 @@ class Records:
 
     def __init__(self, keys, hij, src, phase, count):
         self.keys, self.hij, self.src, self.phase, self.count = keys, hij, src, phase, count
+
+
+class HostRecords:
+    """The host-resident "original set" of the streaming stages:
+    pinned keys uint64 [capacity, W], hij float64 [capacity], src int32 (global
+    parent index) [capacity]; `count` = records held."""
+
+    def __init__(self, capacity: int, W: int):
+        self.capacity, self.W, self.count = int(capacity), int(W), 0
+        self.keys = torch.empty((self.capacity, W), dtype=torch.uint64, pin_memory=True)
+        self.hij = torch.empty(self.capacity, dtype=torch.float64, pin_memory=True)
+        self.src = torch.empty(self.capacity, dtype=torch.int32, pin_memory=True)
+
+    def _cfg(self, batch_parents: int = 0, batch_records: int = 0) -> "_StreamCfg":
+        return _StreamCfg(int(batch_parents), int(batch_records), self.keys.data_ptr(), self.hij.data_ptr(),
+                          self.src.data_ptr(), self.capacity)
+
+
+def _host_u64(t: torch.Tensor, W: int) -> torch.Tensor:
+    if t.dtype != torch.uint64 or t.is_cuda:
+        raise TypeError("host parents must be a CPU torch.uint64 tensor (pinned for overlap)")
+    return t.reshape(-1, W).contiguous()
 
 
 _ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
@@ -353,6 +390,63 @@ class Context:
                                        len(run_counts), ctypes.byref(k))
         self._check(rc, "dedup_finalize_runs")
         return self._take(k.keys, int(k.count), W)
+
+    # ---- memory-centric streaming (Sec 4.3)
+    def stream_generate(self, space: Space, parents_host: torch.Tensor, ints: DeviceIntegrals, threshold: float,
+                        batch_parents: int, unique_pool: "Pool", host: "HostRecords | None" = None) -> dict:
+        """Stage 1: parent mini-batches -> gen_coupled -> dedup_global -> merge_space(unique_pool),
+        with H2D prefetch and (if `host`) D2H offload of the records on their own streams."""
+        par = _host_u64(parents_host, space.words)
+        self._use_integrals(ints)
+        cfg = host._cfg(batch_parents) if host is not None else _StreamCfg(int(batch_parents), 0, None, None, None, 0)
+        st = _StreamStats()
+        sp, ci = space._c(), ints._c()
+        rc = lib().stream_generate(self._ctx, ctypes.byref(sp), ctypes.c_void_p(par.data_ptr()), par.shape[0],
+                                   ctypes.byref(ci), float(threshold), ctypes.byref(cfg), unique_pool._pool,
+                                   ctypes.byref(st))
+        if host is not None:
+            host.count = min(int(st.records), host.capacity)
+        self._check(rc, "stream_generate")
+        return st.as_dict()
+
+    def stream_energy(self, space: Space, host: "HostRecords", n_parents: int, space_keys: torch.Tensor,
+                      psi: torch.Tensor, batch_records: int, e: torch.Tensor | None = None):
+        """Stage 3 (reload): the host original set streamed back in record batches and
+        contracted; returns (e, n_missing, stats)."""
+        sk = _as_u64_2d(space_keys, space.words)
+        psi = psi.contiguous()
+        if e is None:
+            e = torch.empty(max(int(n_parents), 0), dtype=torch.float64, device=self.device)
+        miss = ctypes.c_uint64()
+        st = _StreamStats()
+        cfg = host._cfg(0, batch_records)
+        rc = lib().stream_energy(self._ctx, ctypes.byref(space._c()), ctypes.byref(cfg), host.count, int(n_parents),
+                                 ctypes.c_void_p(sk.data_ptr()), sk.shape[0], ctypes.c_void_p(psi.data_ptr()),
+                                 ctypes.c_void_p(e.data_ptr()), ctypes.byref(miss), ctypes.byref(st))
+        self._check(rc, "stream_energy")
+        return e, int(miss.value), st.as_dict()
+
+    def stream_energy_regen(self, space: Space, parents_host: torch.Tensor, ints: DeviceIntegrals, threshold: float,
+                            batch_parents: int, space_keys: torch.Tensor, psi: torch.Tensor,
+                            e: torch.Tensor | None = None):
+        """Stage 3 (regenerate): the records of each parent batch generated again on the
+        device and contracted; returns (e, n_missing, stats)."""
+        par = _host_u64(parents_host, space.words)
+        self._use_integrals(ints)
+        sk = _as_u64_2d(space_keys, space.words)
+        psi = psi.contiguous()
+        if e is None:
+            e = torch.empty(max(par.shape[0], 0), dtype=torch.float64, device=self.device)
+        miss = ctypes.c_uint64()
+        st = _StreamStats()
+        cfg = _StreamCfg(int(batch_parents), 0, None, None, None, 0)
+        sp, ci = space._c(), ints._c()
+        rc = lib().stream_energy_regen(self._ctx, ctypes.byref(sp), ctypes.c_void_p(par.data_ptr()), par.shape[0],
+                                       ctypes.byref(ci), float(threshold), ctypes.byref(cfg),
+                                       ctypes.c_void_p(sk.data_ptr()), sk.shape[0], ctypes.c_void_p(psi.data_ptr()),
+                                       ctypes.c_void_p(e.data_ptr()), ctypes.byref(miss), ctypes.byref(st))
+        self._check(rc, "stream_energy_regen")
+        return e, int(miss.value), st.as_dict()
 
     # ------------------------------------------------------------------ step 3
     def pool(self, space: Space, capacity: int = 1 << 20) -> "Pool":

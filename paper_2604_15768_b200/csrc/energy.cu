@@ -375,35 +375,53 @@ int build_table(cusci_ctx* ctx, Scratch& s, const uint64_t* space, uint64_t n_sp
 }
 
 template <int W>
+int contract_begin_t(cusci_ctx* ctx, Scratch& s, const uint64_t* space, uint64_t n_space, const double* psi,
+                     uint64_t n_parents, CState* st) {
+  st->W = W;
+  st->n_parents = n_parents;
+  CUSCI_TRY(s.get_t(std::max<uint64_t>(4 * n_parents, 1), &st->acc));
+  CUSCI_TRY(s.get_t(2, &st->flags));
+  CUSCI_CUDA(ctx, cudaMemsetAsync(st->acc, 0, std::max<uint64_t>(4 * n_parents, 1) * 8, ctx->stream));
+  CUSCI_CUDA(ctx, cudaMemsetAsync(st->flags, 0, 16, ctx->stream));
+  // ordered (key, psi) table: 2^k >= 2 n_space home slots + a tail for the
+  // displacements at the top end
+  KPsi<W>* table;
+  CUSCI_TRY(build_table<W>(ctx, s, space, n_space, psi, &table, &st->tslots, &st->k, st->flags + 1));
+  st->table = table;
+  return CUSCI_OK;
+}
+
+template <int W>
+int contract_add_t(cusci_ctx* ctx, const CState& st, const uint64_t* keys, const double* hij, const uint32_t* src,
+                   uint64_t n_rec) {
+  if (!n_rec) return CUSCI_OK;
+  const unsigned g2 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_rec + kET - 1) / kET, (uint64_t)ctx->num_sms * 16));
+  CUSCI_LAUNCH(ctx, PT_ENERGY, contract_kernel<W><<<g2, kET, 0, ctx->stream>>>(keys, hij, src, n_rec, (const KPsi<W>*)st.table, st.tslots, st.k, st.n_parents, st.acc, st.flags));
+  return CUSCI_OK;
+}
+
+int contract_end_impl(cusci_ctx* ctx, const CState& st, double* e, uint64_t* n_missing) {
+  uint64_t h[2];
+  CUSCI_TRY(read_u64(ctx, reinterpret_cast<const uint64_t*>(st.flags), h, 2));
+  if (h[1] & 2) return set_error(ctx, CUSCI_E_INVALID_ARG, "energy_contract: a record's src >= n_parents");
+  if (h[1]) return set_error(ctx, CUSCI_E_INVALID_ARG, "energy_contract: |H psi| >= 2^20 (outside the exact-sum range) or a skewed space");
+  *n_missing = h[0];
+  if (st.n_parents) {
+    const unsigned g3 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((st.n_parents + kET - 1) / kET, (uint64_t)ctx->num_sms * 8));
+    CUSCI_LAUNCH(ctx, PT_ENERGY, contract_finalize_kernel<<<g3, kET, 0, ctx->stream>>>(st.acc, st.n_parents, e));
+  }
+  return CUSCI_OK;
+}
+
+template <int W>
 int contract_impl(cusci_ctx* ctx, const uint64_t* keys, const double* hij, const uint32_t* src, uint64_t n_rec,
                   uint64_t n_parents, const uint64_t* space, uint64_t n_space, const double* psi, double* e,
                   uint64_t* n_missing) {
   Scratch s(ctx);
-  // ordered (key, psi) table: 2^k >= 2 n_space home slots + a tail for the
-  // displacements at the top end
-  KPsi<W>* table;
-  uint64_t tslots;
-  int k;
-  unsigned long long *acc, *flags;
-  CUSCI_TRY(s.get_t(std::max<uint64_t>(4 * n_parents, 1), &acc));
-  CUSCI_TRY(s.get_t(2, &flags));
-  CUSCI_CUDA(ctx, cudaMemsetAsync(acc, 0, std::max<uint64_t>(4 * n_parents, 1) * 8, ctx->stream));
-  CUSCI_CUDA(ctx, cudaMemsetAsync(flags, 0, 16, ctx->stream));
-  CUSCI_TRY(build_table<W>(ctx, s, space, n_space, psi, &table, &tslots, &k, flags + 1));
-  if (n_rec) {
-    const unsigned g2 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_rec + kET - 1) / kET, (uint64_t)ctx->num_sms * 16));
-    CUSCI_LAUNCH(ctx, PT_ENERGY, contract_kernel<W><<<g2, kET, 0, ctx->stream>>>(keys, hij, src, n_rec, table, tslots, k, n_parents, acc, flags));
-  }
-  uint64_t h[2];
-  CUSCI_TRY(read_u64(ctx, reinterpret_cast<const uint64_t*>(flags), h, 2));
-  if (h[1] & 2) return set_error(ctx, CUSCI_E_INVALID_ARG, "energy_contract: a record's src >= n_parents");
-  if (h[1]) return set_error(ctx, CUSCI_E_INVALID_ARG, "energy_contract: |H psi| >= 2^20 (outside the exact-sum range) or a skewed space");
-  *n_missing = h[0];
-  if (n_parents) {
-    const unsigned g3 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_parents + kET - 1) / kET, (uint64_t)ctx->num_sms * 8));
-    CUSCI_LAUNCH(ctx, PT_ENERGY, contract_finalize_kernel<<<g3, kET, 0, ctx->stream>>>(acc, n_parents, e));
-  }
-  return CUSCI_OK;
+  CState st;
+  CUSCI_TRY(contract_begin_t<W>(ctx, s, space, n_space, psi, n_parents, &st));
+  CUSCI_TRY(contract_add_t<W>(ctx, st, keys, hij, src, n_rec));
+  return contract_end_impl(ctx, st, e, n_missing);
 }
 
 // world > 1 (or a forced collective): records and psi meet at the key's owner
@@ -454,6 +472,20 @@ int contract_collective(cusci_ctx* ctx, const uint64_t* keys, const double* hij,
 }
 
 }  // namespace
+
+int contract_begin(cusci_ctx* ctx, Scratch& s, int W, const uint64_t* space, uint64_t n_space, const double* psi,
+                   uint64_t n_parents, CState* st) {
+  return W == 1 ? contract_begin_t<1>(ctx, s, space, n_space, psi, n_parents, st)
+                : contract_begin_t<2>(ctx, s, space, n_space, psi, n_parents, st);
+}
+int contract_add(cusci_ctx* ctx, const CState& st, const uint64_t* keys, const double* hij, const uint32_t* src,
+                 uint64_t n_rec) {
+  return st.W == 1 ? contract_add_t<1>(ctx, st, keys, hij, src, n_rec) : contract_add_t<2>(ctx, st, keys, hij, src, n_rec);
+}
+int contract_end(cusci_ctx* ctx, const CState& st, double* e, uint64_t* n_missing) {
+  return contract_end_impl(ctx, st, e, n_missing);
+}
+
 }  // namespace cusci
 
 using namespace cusci;

@@ -68,6 +68,7 @@ struct GenArgs {
   uint64_t capacity;
   unsigned long long* counter;  // [0] records, [1] unit work counter, [2] first bad parent
   int count_only;
+  uint32_t src_base;  // added to every src (streamed mini-batches write global parent indices)
 };
 
 // ---- bit helpers on W-word keys
@@ -195,7 +196,7 @@ __device__ __forceinline__ void stage_flush(const GenArgs& a, Stage<W>& st) {
       }
       if (a.src) {  // each source run is a contiguous range of the stage
         for (uint32_t j = 0; j < st.nrun; j++) {
-          const uint32_t r0 = st.run[j], r1 = j + 1 < st.nrun ? st.run[j + 1] : st.n, sv = st.run[kRuns + j];
+          const uint32_t r0 = st.run[j], r1 = j + 1 < st.nrun ? st.run[j + 1] : st.n, sv = st.run[kRuns + j] + a.src_base;
           for (uint32_t i = r0 + lane; i < r1; i += 32) a.src[base + i] = sv;
         }
       }
@@ -480,7 +481,8 @@ __global__ void __launch_bounds__(kGenThreads, 4) gen_kernel(const GenArgs a) {
 }
 
 int gen_impl(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* parents, uint64_t n_parents,
-             const cusci_integrals* ints, double threshold, cusci_records* out, bool count_only, uint64_t* count_out) {
+             const cusci_integrals* ints, double threshold, cusci_records* out, bool count_only, uint64_t* count_out,
+             uint32_t src_base = 0) {
   if (!ctx) return CUSCI_E_INVALID_ARG;
   if (ctx->broken) return set_error(ctx, CUSCI_E_CUDA, "context is unusable after an earlier CUDA/NCCL error");
   CUSCI_TRY(check_space(ctx, sp));
@@ -545,6 +547,7 @@ int gen_impl(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* parents, uin
   }
   a.counter = counter;
   a.count_only = count_only ? 1 : 0;
+  a.src_base = src_base;
   const int mode = count_only ? 0 : (out->phase ? 2 : 1);
   const size_t smem = mode == 0 ? 0 : (W == 1 ? GenCfg<1>::SMEM : GenCfg<2>::SMEM);
   void (*kern)(const GenArgs) = nullptr;
@@ -573,6 +576,16 @@ int gen_impl(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* parents, uin
 }
 
 }  // namespace
+
+int gen_records(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* parents, uint64_t n_parents,
+                const cusci_integrals* ints, double threshold, cusci_records* out, uint32_t src_base) {
+  return gen_impl(ctx, sp, parents, n_parents, ints, threshold, out, false, nullptr, src_base);
+}
+int gen_count(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* parents, uint64_t n_parents,
+              const cusci_integrals* ints, double threshold, uint64_t* count) {
+  return gen_impl(ctx, sp, parents, n_parents, ints, threshold, nullptr, true, count);
+}
+
 }  // namespace cusci
 
 using namespace cusci;

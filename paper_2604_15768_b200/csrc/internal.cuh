@@ -393,6 +393,27 @@ struct DigitSpecs {
 };
 
 // ------------------------------------------------------------------ launchers (per .cu)
+// gen_coupled with src written as src_base + (parent index in this call)
+int gen_records(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* parents, uint64_t n_parents,
+                const cusci_integrals* ints, double threshold, cusci_records* out, uint32_t src_base);
+int gen_count(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* parents, uint64_t n_parents,
+              const cusci_integrals* ints, double threshold, uint64_t* count);
+// Stage-3 contraction in pieces (energy.cu): the (key, psi) table once, any
+// number of record batches accumulated exactly, e written once
+struct CState {
+  int W = 1;
+  void* table = nullptr;
+  uint64_t tslots = 0;
+  int k = 0;
+  unsigned long long* acc = nullptr;    // [4 n_parents] exact limbs
+  unsigned long long* flags = nullptr;  // [2] missing, errors
+  uint64_t n_parents = 0;
+};
+int contract_begin(cusci_ctx* ctx, Scratch& s, int W, const uint64_t* space, uint64_t n_space, const double* psi,
+                   uint64_t n_parents, CState* st);
+int contract_add(cusci_ctx* ctx, const CState& st, const uint64_t* keys, const double* hij, const uint32_t* src,
+                 uint64_t n_rec);
+int contract_end(cusci_ctx* ctx, const CState& st, double* e, uint64_t* n_missing);
 int prep_build(cusci_ctx* ctx, const cusci_space* sp, const cusci_integrals* ints, double eps);
 
 // exclusive scan of n values (u32 or u64) in place-safe out; optional device total
