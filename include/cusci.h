@@ -375,6 +375,32 @@ int stream_energy_regen(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* p
                         const uint64_t* space_keys, uint64_t n_space, const double* psi, double* e,
                         uint64_t* n_missing, cusci_stream_stats* stats);
 
+/* ---- next row: SCI growth with a surrogate selector --------
+ * One iteration of the selected-CI loop (Sec 2.2 :308-312, Fig. 2:
+ * generate C from S, de-duplicate, select the top-K new configurations,
+ * merge them into S), with the NNQS amplitude replaced by the heat-bath
+ * surrogate (reading r16):
+ *   records (i -> j, H_ij) = gen_coupled(S); C = dedup_global(records);
+ *   score_j = max over records of |p|, p = fl(H_ij psi_i), ties between
+ *     equal |p| by sign (negative wins), for j in C \ S (score 0 excluded);
+ *   selected = the K best scores, ties in the pool hash order pi;
+ *   S <- S u selected (merge_space);  psi_out = psi over the new S in pool
+ *   order: psi_i kept for i in S, psi_j = -p_j (first-order amplitude with a
+ *   unit energy denominator) for the new j.
+ * space: the pool holding S; psi (device, [|S|]) aligned with its pi order;
+ * psi_out (device, capacity psi_out_capacity >= |S| + K) receives the new
+ * psi.  One rank (E_INVALID_ARG when collective).  E_CAPACITY if psi_out is
+ * too small (S has been merged; stats->space_after = |S|). */
+typedef struct {
+  uint64_t records, unique;         /* records of S, distinct coupled configurations */
+  uint64_t candidates, selected;    /* j in C \ S with a positive score; selected (<= K) */
+  uint64_t space_before, space_after;
+  double ms;                        /* device time of the step */
+} cusci_grow_stats;
+int sci_grow_step(cusci_ctx* ctx, const cusci_space* sp, cusci_pool* space, const double* psi,
+                  const cusci_integrals* ints, double threshold, uint64_t K, double* psi_out,
+                  uint64_t psi_out_capacity, cusci_grow_stats* stats);
+
 #ifdef __cplusplus
 }
 #endif

@@ -44,6 +44,12 @@ class _StreamCfg(ctypes.Structure):
                 ("host_hij", ctypes.c_void_p), ("host_src", ctypes.c_void_p), ("host_capacity", ctypes.c_uint64)]
 
 
+class _GrowStats(ctypes.Structure):
+    _fields_ = [("records", ctypes.c_uint64), ("unique", ctypes.c_uint64), ("candidates", ctypes.c_uint64),
+                ("selected", ctypes.c_uint64), ("space_before", ctypes.c_uint64), ("space_after", ctypes.c_uint64),
+                ("ms", ctypes.c_double)]
+
+
 class _StreamStats(ctypes.Structure):
     _fields_ = [("batches", ctypes.c_uint64), ("records", ctypes.c_uint64), ("unique", ctypes.c_uint64),
                 ("ms_wall", ctypes.c_double), ("ms_h2d", ctypes.c_double), ("ms_compute", ctypes.c_double),
@@ -390,6 +396,25 @@ class Context:
                                        len(run_counts), ctypes.byref(k))
         self._check(rc, "dedup_finalize_runs")
         return self._take(k.keys, int(k.count), W)
+
+    # ---- SCI growth with the heat-bath surrogate (Sec 2.2)
+    def sci_grow_step(self, space: Space, pool: "Pool", psi: torch.Tensor, ints: DeviceIntegrals,
+                      threshold: float, K: int):
+        """One iteration S <- S u top-K(C \\ S by heat-bath score); returns (psi over the
+        new S in pool order, stats)."""
+        psi = psi.contiguous()
+        if psi.dtype != torch.float64 or not psi.is_cuda or psi.numel() != len(pool):
+            raise ValueError("psi must be a CUDA float64 tensor aligned with the pool")
+        self._use_integrals(ints)
+        cap = len(pool) + int(K)
+        out = torch.empty(max(cap, 1), dtype=torch.float64, device=self.device)
+        st = _GrowStats()
+        sp, ci = space._c(), ints._c()
+        rc = lib().sci_grow_step(self._ctx, ctypes.byref(sp), pool._pool, ctypes.c_void_p(psi.data_ptr()),
+                                 ctypes.byref(ci), float(threshold), int(K), ctypes.c_void_p(out.data_ptr()), cap,
+                                 ctypes.byref(st))
+        self._check(rc, "sci_grow_step")
+        return out[: st.space_after], {f: getattr(st, f) for f, _ in st._fields_}
 
     # ---- SURVEY 8(f) row f3: memory-centric streaming (PAPER.md Sec 4.3)
     def stream_generate(self, space: Space, parents_host: torch.Tensor, ints: DeviceIntegrals, threshold: float,

@@ -34,19 +34,6 @@ constexpr int kET = 256;
 template <int W>
 __device__ __forceinline__ bool pi_less(const KeyT<W>& a, const KeyT<W>& b) { return pi_lt(a, b); }
 
-// T[b] = first index i with top_k(hi(space[i])) >= b, b in [0, 2^k]
-template <int W>
-__global__ void rindex_table_kernel(const uint64_t* __restrict__ space, uint64_t n, int k, uint32_t* __restrict__ T) {
-  const uint64_t nb = 1ull << k;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += stride) {
-    // buckets (prev, cur] start at i
-    const uint64_t cur = i < n ? (k ? (to_pi(load_key<W>(space, i)).w0 >> (64 - k)) : 0ull) : nb;
-    const int64_t prev = i > 0 ? (int64_t)(k ? (to_pi(load_key<W>(space, i - 1)).w0 >> (64 - k)) : 0ull) : -1;
-    for (int64_t b = prev + 1; b <= (int64_t)cur; b++) T[b] = (uint32_t)i;
-  }
-}
-
 // (key, psi) side by side: one random sector serves the match and the amplitude
 template <int W> struct KPsi;
 template <> struct __align__(16) KPsi<1> {
@@ -58,19 +45,6 @@ template <> struct __align__(32) KPsi<2> {
   double psi;
   double pad;
 };
-template <int W>
-__global__ void kpsi_kernel(const uint64_t* __restrict__ space, const double* __restrict__ psi, uint64_t n,
-                            KPsi<W>* __restrict__ kp) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    KPsi<W> r{};
-    const KeyT<W> k = load_key<W>(space, i);
-    r.k0 = k.w0;
-    if constexpr (W == 2) r.k1 = k.w1;
-    r.psi = psi[i];
-    kp[i] = r;
-  }
-}
 template <int W> __device__ __forceinline__ bool kp_eq(const KPsi<W>& r, const KeyT<W>& k);
 template <> __device__ __forceinline__ bool kp_eq<1>(const KPsi<1>& r, const KeyT<1>& k) { return r.k0 == k.w0; }
 template <> __device__ __forceinline__ bool kp_eq<2>(const KPsi<2>& r, const KeyT<2>& k) {
@@ -156,7 +130,7 @@ __global__ void __launch_bounds__(kET) place_kernel(const uint64_t* __restrict__
       const KeyT<W> kk = load_key<W>(space, i);
       r.k0 = kk.w0;
       if constexpr (W == 2) r.k1 = kk.w1;
-      r.psi = psi[i];
+      r.psi = psi ? psi[i] : __longlong_as_double((long long)i);  // no psi: the element's index
       const uint64_t slot = (uint64_t)((long long)i + full);
       if (slot < tslots) table[slot] = r;
       else *ovf = 1;  // (impossible for hash-uniform keys: displacement >> n/16)
@@ -471,6 +445,278 @@ int contract_collective(cusci_ctx* ctx, const uint64_t* keys, const double* hij,
                           n_missing);
 }
 
+
+// ---------------------------------------------------------------- f4: heat-bath selection
+// (Sec 2.2 :310-312 "selecting a subset of
+// important configurations from the newly generated candidates (e.g. top-K
+// ranked by inferred amplitudes psi) and merging them into S"; the NNQS
+// amplitude is replaced by the heat-bath surrogate, reading r16):
+//   score_j = max over records (i -> j) of |H_ij psi_i|, packed as
+//             v = bits(|p|) << 1 | [p < 0] (p the winning product: order by
+//             |p|, ties by sign), for j in C \ S;
+//   select   the K largest v > 0, ties in pi order (C is pi-sorted);
+//   psi_j   = -p (first-order amplitude with a unit energy denominator).
+template <int W>
+__global__ void __launch_bounds__(kET) hb_score_kernel(const uint64_t* __restrict__ keys, const double* __restrict__ hij,
+                                                      const uint32_t* __restrict__ src, uint64_t n_rec,
+                                                      const double* __restrict__ psi_par,
+                                                      const KPsi<W>* __restrict__ table, uint64_t tslots, int k,
+                                                      unsigned long long* __restrict__ score) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_rec; r += stride) {
+    const KeyT<W> kv = load_key<W>(keys, r);
+    const double p = __dmul_rn(hij[r], psi_par[src[r]]);
+    const unsigned long long v = ((unsigned long long)__double_as_longlong(fabs(p)) << 1) | (p < 0.0 ? 1ull : 0ull);
+    if (!v) continue;
+    for (uint64_t slot = k ? (to_pi(kv).w0 >> (64 - k)) : 0ull; slot < tslots; slot++) {
+      const KPsi<W> e = table[slot];
+      if (kp_eq<W>(e, kv)) {
+        atomicMax(&score[(uint64_t)__double_as_longlong(e.psi)], v);
+        break;
+      }
+      if (kp_empty<W>(e)) break;
+    }
+  }
+}
+// candidates already in S score 0
+template <int W>
+__global__ void __launch_bounds__(kET) hb_exclude_kernel(const uint64_t* __restrict__ S, uint64_t nS,
+                                                        const KPsi<W>* __restrict__ table, uint64_t tslots, int k,
+                                                        unsigned long long* __restrict__ score) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nS; r += stride) {
+    const KeyT<W> kv = load_key<W>(S, r);
+    for (uint64_t slot = k ? (to_pi(kv).w0 >> (64 - k)) : 0ull; slot < tslots; slot++) {
+      const KPsi<W> e = table[slot];
+      if (kp_eq<W>(e, kv)) {
+        score[(uint64_t)__double_as_longlong(e.psi)] = 0ull;
+        break;
+      }
+      if (kp_empty<W>(e)) break;
+    }
+  }
+}
+// radix-select step: histogram of digit (v >> shift) & 255 over the v > 0 that
+// match `prefix` on the bits of pmask
+__global__ void __launch_bounds__(kET) hb_hist_kernel(const unsigned long long* __restrict__ v, uint64_t n,
+                                                     unsigned long long prefix, unsigned long long pmask, int shift,
+                                                     unsigned long long* __restrict__ hist) {
+  __shared__ uint32_t h[256];
+  for (int i = threadIdx.x; i < 256; i += kET) h[i] = 0;
+  __syncthreads();
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const unsigned long long x = v[i];
+    if (x && (x & pmask) == prefix) atomicAdd(&h[(x >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += kET)
+    if (h[i]) atomicAdd(&hist[i], (unsigned long long)h[i]);
+}
+constexpr uint32_t kHB = 1024;  // elements per compaction block
+// per block: elements with v > T (cnt[2b]) and v == T (cnt[2b + 1])
+__global__ void __launch_bounds__(kET) hb_count_kernel(const unsigned long long* __restrict__ v, uint64_t n,
+                                                      unsigned long long T, uint64_t* __restrict__ gt,
+                                                      uint64_t* __restrict__ eq) {
+  __shared__ uint32_t a, b;
+  if (threadIdx.x == 0) a = b = 0;
+  __syncthreads();
+  const uint64_t i0 = (uint64_t)blockIdx.x * kHB;
+  uint32_t ca = 0, cb = 0;
+  for (uint64_t i = i0 + threadIdx.x; i < min(n, i0 + kHB); i += kET) {
+    const unsigned long long x = v[i];
+    ca += x > T;
+    cb += x == T && x;
+  }
+  atomicAdd(&a, ca);
+  atomicAdd(&b, cb);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    gt[blockIdx.x] = a;
+    eq[blockIdx.x] = b;
+  }
+}
+// stable compaction: element x is kept iff v > T, or v == T among the first
+// `need` such elements (index order = pi order); position = (kept before x)
+template <int W>
+__global__ void __launch_bounds__(kET) hb_compact_kernel(const unsigned long long* __restrict__ v, uint64_t n,
+                                                        unsigned long long T, uint64_t need,
+                                                        const uint64_t* __restrict__ gt_off,
+                                                        const uint64_t* __restrict__ eq_off,
+                                                        const uint64_t* __restrict__ cand, uint64_t* __restrict__ out,
+                                                        double* __restrict__ psi_out) {
+  __shared__ uint32_t red[33];
+  const uint64_t i0 = (uint64_t)blockIdx.x * kHB;
+  uint32_t gbase = 0, ebase = 0;
+  for (uint32_t c = 0; c < kHB; c += kET) {
+    const uint64_t i = i0 + c + threadIdx.x;
+    const unsigned long long x = i < n ? v[i] : 0ull;
+    const uint32_t fg = x > T, fe = x == T && x;
+    uint32_t tg, te;
+    const uint32_t pg = block_excl_scan_u32(fg, red, tg);
+    const uint32_t pe = block_excl_scan_u32(fe, red, te);
+    const uint64_t eb = eq_off[blockIdx.x] + ebase + pe;  // equal elements before x
+    if (fg || (fe && eb < need)) {
+      const uint64_t pos = gt_off[blockIdx.x] + gbase + pg + min(eb, need);
+      store_key<W>(out, pos, load_key<W>(cand, i));
+      const double a = __longlong_as_double((long long)(x >> 1));
+      psi_out[pos] = (x & 1ull) ? a : -a;  // psi_j = -p
+    }
+    gbase += tg;
+    ebase += te;
+  }
+}
+// psi of the merged space: from S_old (binary search in pi order) or the selection
+template <int W>
+__device__ __forceinline__ bool pi_find(const uint64_t* keys, uint64_t n, const KeyT<W>& x, uint64_t* pos) {
+  uint64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (hk_lt<W>(load_key<W>(keys, mid), x)) lo = mid + 1;
+    else hi = mid;
+  }
+  *pos = lo;
+  return lo < n && key_eq(load_key<W>(keys, lo), x);
+}
+template <int W>
+__global__ void __launch_bounds__(kET) realign_kernel(const uint64_t* __restrict__ merged, uint64_t n,
+                                                     const uint64_t* __restrict__ s_old, uint64_t ns,
+                                                     const double* __restrict__ psi_old,
+                                                     const uint64_t* __restrict__ sel, uint64_t nsel,
+                                                     const double* __restrict__ psi_sel, double* __restrict__ psi_out,
+                                                     unsigned long long* __restrict__ bad) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const KeyT<W> x = load_key<W>(merged, i);
+    uint64_t p;
+    if (pi_find<W>(s_old, ns, x, &p)) psi_out[i] = psi_old[p];
+    else if (pi_find<W>(sel, nsel, x, &p)) psi_out[i] = psi_sel[p];
+    else atomicAdd(bad, 1ull);
+  }
+}
+
+template <int W>
+int grow_step_t(cusci_ctx* ctx, const cusci_space* sp, cusci_pool* pool, const double* psi,
+                const cusci_integrals* ints, double threshold, uint64_t K, double* psi_out, uint64_t cap,
+                cusci_grow_stats* st) {
+  Scratch s(ctx);
+  const uint64_t nS = pool->count;
+  st->space_before = nS;
+  // S_t (the merge replaces the pool's buffers)
+  uint64_t* Sold;
+  CUSCI_TRY(s.get_t(std::max<uint64_t>(nS, 1) * W, &Sold));
+  if (nS) CUSCI_CUDA(ctx, cudaMemcpyAsync(Sold, pool->buf[pool->cur], nS * W * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  // records of S_t, then the candidates C_t
+  uint64_t nrec = 0;
+  CUSCI_TRY(gen_count(ctx, sp, Sold, nS, ints, threshold, &nrec));
+  uint64_t *rk;
+  double* rh;
+  uint32_t* rs;
+  CUSCI_TRY(s.get_t(std::max<uint64_t>(nrec, 1) * W, &rk));
+  CUSCI_TRY(s.get_t(std::max<uint64_t>(nrec, 1), &rh));
+  CUSCI_TRY(s.get_t(std::max<uint64_t>(nrec, 1), &rs));
+  cusci_records rec{rk, rh, rs, nullptr, nrec, 0};
+  CUSCI_TRY(gen_records(ctx, sp, Sold, nS, ints, threshold, &rec, 0));
+  st->records = rec.count;
+  cusci_keys C{nullptr, 0};
+  CUSCI_TRY(dedup_global(ctx, sp, rk, rec.count, &C));
+  struct OutGuard {
+    cusci_ctx* c;
+    void* p;
+    ~OutGuard() { out_free(c, p); }
+  } cg{ctx, C.keys};
+  const uint64_t nC = C.count;
+  st->unique = nC;
+  // index table over C_t, heat-bath scores, S_t excluded
+  KPsi<W>* table;
+  uint64_t tslots;
+  int k;
+  unsigned long long *score, *flags, *hist;
+  CUSCI_TRY(s.get_t(std::max<uint64_t>(nC, 1), &score));
+  CUSCI_TRY(s.get_t(2, &flags));
+  CUSCI_TRY(s.get_t(256, &hist));
+  CUSCI_CUDA(ctx, cudaMemsetAsync(score, 0, std::max<uint64_t>(nC, 1) * 8, ctx->stream));
+  CUSCI_CUDA(ctx, cudaMemsetAsync(flags, 0, 16, ctx->stream));
+  CUSCI_TRY(build_table<W>(ctx, s, C.keys, nC, nullptr, &table, &tslots, &k, flags + 1));
+  const unsigned g = (unsigned)ctx->num_sms * 8;
+  if (rec.count) CUSCI_LAUNCH(ctx, PT_ENERGY, hb_score_kernel<W><<<g, kET, 0, ctx->stream>>>(rk, rh, rs, rec.count, psi, table, tslots, k, score));
+  if (nS) CUSCI_LAUNCH(ctx, PT_ENERGY, hb_exclude_kernel<W><<<g, kET, 0, ctx->stream>>>(Sold, nS, table, tslots, k, score));
+  // radix select of the K-th largest score (8 x 8-bit digits, most significant first)
+  unsigned long long prefix = 0, pmask = 0;
+  uint64_t remaining = K, positive = 0;
+  for (int d = 7; d >= 0 && remaining; d--) {
+    CUSCI_CUDA(ctx, cudaMemsetAsync(hist, 0, 256 * 8, ctx->stream));
+    CUSCI_LAUNCH(ctx, PT_ENERGY, hb_hist_kernel<<<g, kET, 0, ctx->stream>>>(score, nC, prefix, pmask, 8 * d, hist));
+    uint64_t hh[256];
+    CUSCI_TRY(read_u64(ctx, reinterpret_cast<const uint64_t*>(hist), hh, 256));
+    uint64_t tot = 0;
+    for (int x = 0; x < 256; x++) tot += hh[x];
+    if (d == 7) positive = tot;
+    if (tot <= remaining) {  // every matching value is taken: threshold = the smallest of them
+      for (int x = 0; x < 256; x++)
+        if (hh[x]) {
+          prefix |= (unsigned long long)x << (8 * d);
+          break;
+        }
+      pmask |= 0xffull << (8 * d);
+      if (tot == 0) remaining = 0;
+      continue;
+    }
+    uint64_t above = 0;
+    int x = 255;
+    for (; x > 0 && above + hh[x] < remaining; x--) above += hh[x];
+    remaining -= above;
+    prefix |= (unsigned long long)x << (8 * d);
+    pmask |= 0xffull << (8 * d);
+  }
+  st->candidates = positive;
+  uint64_t nsel = 0;
+  uint64_t* sel = nullptr;
+  double* psel = nullptr;
+  if (K && positive) {
+    unsigned long long T;
+    uint64_t need;
+    if (positive <= K) {  // every candidate: threshold 1, all equal-or-above taken
+      T = 1ull;
+      need = ~0ull;
+    } else {
+      T = prefix;
+      need = remaining;
+    }
+    const uint64_t nb = (nC + kHB - 1) / kHB;
+    uint64_t *gt, *eq, *gto, *eqo;
+    CUSCI_TRY(s.get_t(nb + 1, &gt));
+    CUSCI_TRY(s.get_t(nb + 1, &eq));
+    CUSCI_TRY(s.get_t(nb + 1, &gto));
+    CUSCI_TRY(s.get_t(nb + 1, &eqo));
+    CUSCI_CUDA(ctx, cudaMemsetAsync(gt + nb, 0, 8, ctx->stream));
+    CUSCI_CUDA(ctx, cudaMemsetAsync(eq + nb, 0, 8, ctx->stream));
+    CUSCI_LAUNCH(ctx, PT_ENERGY, hb_count_kernel<<<(unsigned)nb, kET, 0, ctx->stream>>>(score, nC, T, gt, eq));
+    CUSCI_TRY(scan_exclusive_u64(ctx, gt, gto, nb + 1, nullptr));
+    CUSCI_TRY(scan_exclusive_u64(ctx, eq, eqo, nb + 1, nullptr));
+    uint64_t tot[2];
+    CUSCI_TRY(read_u64(ctx, gto + nb, &tot[0], 1));
+    CUSCI_TRY(read_u64(ctx, eqo + nb, &tot[1], 1));
+    nsel = tot[0] + std::min(tot[1], need);
+    CUSCI_TRY(s.get_t(std::max<uint64_t>(nsel, 1) * W, &sel));
+    CUSCI_TRY(s.get_t(std::max<uint64_t>(nsel, 1), &psel));
+    CUSCI_LAUNCH(ctx, PT_ENERGY, hb_compact_kernel<W><<<(unsigned)nb, kET, 0, ctx->stream>>>(score, nC, T, need, gto, eqo, C.keys, sel, psel));
+  }
+  st->selected = nsel;
+  // S <- S u selected, psi re-aligned with the new pool order
+  CUSCI_TRY(merge_space(ctx, pool, sel, nsel, nullptr));
+  const uint64_t nN = pool->count;
+  st->space_after = nN;
+  if (nN > cap) return set_error(ctx, CUSCI_E_CAPACITY, "sci_grow_step: the space grew to %llu > psi_out capacity %llu",
+                                 (unsigned long long)nN, (unsigned long long)cap);
+  if (nN)
+    CUSCI_LAUNCH(ctx, PT_ENERGY, realign_kernel<W><<<g, kET, 0, ctx->stream>>>(pool->buf[pool->cur], nN, Sold, nS, psi, sel, nsel, psel, psi_out, flags));
+  uint64_t h[2];
+  CUSCI_TRY(read_u64(ctx, reinterpret_cast<const uint64_t*>(flags), h, 2));
+  if (h[0] || h[1]) return set_error(ctx, CUSCI_E_CUDA, "sci_grow_step: internal inconsistency (%llu, %llu)",
+                                     (unsigned long long)h[0], (unsigned long long)h[1]);
+  return CUSCI_OK;
+}
 }  // namespace
 
 int contract_begin(cusci_ctx* ctx, Scratch& s, int W, const uint64_t* space, uint64_t n_space, const double* psi,
@@ -512,4 +758,34 @@ extern "C" int energy_contract(cusci_ctx* ctx, const cusci_space* sp, const uint
   if (rc != CUSCI_OK) return rc;
   return sp->words == 1 ? contract_impl<1>(ctx, keys, hij, src, n_rec, n_parents, space_keys, n_space, psi, e, n_missing)
                         : contract_impl<2>(ctx, keys, hij, src, n_rec, n_parents, space_keys, n_space, psi, e, n_missing);
+}
+
+extern "C" int sci_grow_step(cusci_ctx* ctx, const cusci_space* sp, cusci_pool* space, const double* psi,
+                             const cusci_integrals* ints, double threshold, uint64_t K, double* psi_out,
+                             uint64_t psi_out_capacity, cusci_grow_stats* stats) {
+  if (!ctx) return CUSCI_E_INVALID_ARG;
+  if (ctx->broken) return set_error(ctx, CUSCI_E_CUDA, "context is unusable after an earlier CUDA/NCCL error");
+  CUSCI_TRY(check_space(ctx, sp));
+  if (!space || space->ctx != ctx || space->sp.m != sp->m || space->sp.n_alpha != sp->n_alpha ||
+      space->sp.n_beta != sp->n_beta)
+    return set_error(ctx, CUSCI_E_INVALID_ARG, "sci_grow_step: pool of another context or space");
+  if (!stats || (space->count && !psi) || !psi_out) return set_error(ctx, CUSCI_E_INVALID_ARG, "sci_grow_step: NULL argument");
+  if (collective(ctx)) return set_error(ctx, CUSCI_E_INVALID_ARG, "sci_grow_step: one rank");
+  if (space->count >= (1ull << 32)) return set_error(ctx, CUSCI_E_INVALID_ARG, "sci_grow_step: |S| must be < 2^32");
+  CUSCI_CUDA(ctx, cudaSetDevice(ctx->device));
+  memset(stats, 0, sizeof(*stats));
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a, ctx->stream);
+  const int rc = sp->words == 1 ? grow_step_t<1>(ctx, sp, space, psi, ints, threshold, K, psi_out, psi_out_capacity, stats)
+                                : grow_step_t<2>(ctx, sp, space, psi, ints, threshold, K, psi_out, psi_out_capacity, stats);
+  cudaEventRecord(b, ctx->stream);
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  stats->ms = ms;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return rc;
 }

@@ -100,3 +100,36 @@ def test_stream_collective(P):
     assert st["batches"] == 4 and np.array_equal(synth.sort_keys(pool.keys().cpu().numpy()), ref)
     pool.close()
     c.close()
+
+
+# ------------------------------------------------------------------ f4: SCI growth (heat-bath surrogate)
+@pytest.mark.parametrize("key,n_par,K,iters", [("lih", None, 40, 3), ("h2o", 50, 2000, 3), ("n2", 20, 800, 2),
+                                               ("c2h4", 3, 300, 2)])
+def test_sci_grow_steps(P, ctx, key, n_par, K, iters):
+    """sci_grow_step from a small start space vs the oracle step by step: the
+    space, the selection and every amplitude bit for bit."""
+    from oracle import heatbath as HB
+    wl, ints, par = synth.workload_inputs(key, n_parents=n_par)
+    W = wl.words
+    if key == "lih":
+        par = par[:5]
+    sp = P.Space(wl.m, wl.n_alpha, wl.n_beta)
+    di = P.DeviceIntegrals(ints.h, ints.eri)
+    pool = ctx.pool(sp, 1024)
+    ctx.merge_space(pool, ctx.dedup_global(sp, torch.from_numpy(par).cuda()))
+    keys = pool.keys().cpu().numpy().reshape(-1, W)
+    psi = np.random.default_rng(5).uniform(-1, 1, size=len(keys))
+    ref = {tuple(int(x) for x in k): p for k, p in zip(keys, psi)}
+    psi_d = torch.from_numpy(psi).cuda()
+    for it in range(iters):
+        S = np.array(list(ref.keys()), dtype=np.uint64).reshape(-1, W)
+        rec = oracle.gen_coupled(wl.m, wl.n_alpha, wl.n_beta, S, ints, 0.0)
+        ref, sel, ncand = HB.grow_step(S, np.array(list(ref.values())), rec, K, W)
+        psi_d, st = ctx.sci_grow_step(sp, pool, psi_d, di, 0.0, K)
+        assert st["records"] == len(rec["src"]) and st["candidates"] == ncand
+        assert st["selected"] == len(sel) == min(K, ncand) and st["space_after"] == len(ref)
+        got = pool.keys().cpu().numpy().reshape(-1, W)
+        assert_hash_sorted_unique(got, W)
+        gp = psi_d.cpu().numpy()
+        assert {tuple(int(x) for x in k): p for k, p in zip(got, gp)} == ref, f"iteration {it}"
+    pool.close()
