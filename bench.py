@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-stage3", action="store_true", help="skip the Stage-3 contraction measurement (SURVEY 8(f) f1)")
     ap.add_argument("--no-f2", action="store_true", help="skip the regular-sampling dedup measurement (SURVEY 8(f) f2)")
+    ap.add_argument("--no-f3", action="store_true", help="skip the streaming-stage measurement (SURVEY 8(f) f3)")
+    ap.add_argument("--f3-parents", type=int, default=100_000, help="parents of the f3 offload measurement")
+    ap.add_argument("--no-f4", action="store_true", help="skip the SCI growth measurement (SURVEY 8(f) f4)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=None, help="parents in the oracle's bounded sample")
     return ap.parse_args()
@@ -338,38 +341,6 @@ def main():
     value = recs_all / (ms / 1e3)
     unique_rate = uni_all / (ms / 1e3)
 
-    # ---------------- e2e: host parents (pinned) -> device inside the region, count read back
-    e2e = None
-    if not args.no_e2e:
-        for _ in range(max(1, min(args.warmup, 2))):  # warm the host-input path (allocator, pinned copies)
-            pd = torch.empty_like(shard)
-            pd.copy_(shard_pinned, non_blocking=True)
-            step(pd, e2e=True)
-            torch.tensor([0], dtype=torch.int64).to(dev).cpu()
-        del pd
-        barrier(pg)
-        torch.cuda.synchronize()
-        eclocks = ClockSampler(local)
-        eclocks.start()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        er = 0
-        for _ in range(args.steps):
-            pd = torch.empty_like(shard)
-            pd.copy_(shard_pinned, non_blocking=True)
-            r, u, s = step(pd, e2e=True)
-            res = torch.tensor([r, u, s], dtype=torch.int64).to(dev).cpu()   # result read back (D2H)
-            er += int(res[0])
-        e1.record(stream)
-        torch.cuda.synchronize()
-        eclk = eclocks.stop()
-        barrier(pg)
-        ems = allreduce_max(pg, e0.elapsed_time(e1))
-        e2e = {"value": allreduce_sum(pg, er) / (ems / 1e3), "unit": "coupled configs/s",
-               "h2d_bytes_per_step": int(shard_pinned.numel() * 8 + ints.h.nbytes * 0),
-               "d2h_bytes_per_step": 24, "ms_per_step": ems / args.steps, "clocks": eclk}
-
     # ---------------- Stage-3 contraction (not part of the headline step):
     # e[s] = sum_j H_sj psi_j over every batch's records, psi synthetic and
     # aligned with the unique set C (the upool), reverse index just in time
@@ -450,6 +421,97 @@ def main():
                             "regular_sampling": bal([bnd[r + 1] - bnd[r] for r in range(Pv)]),
                             "hash_owner": bal(hcounts)}}
 
+    # ---------------- f3: memory-centric streaming (Sec 4.3; not in the headline step)
+    # Stage 1 with the original set offloaded to pinned host memory (3 streams), then
+    # Stage 3 both ways: reload the original set H2D, or regenerate it on the device
+    f3 = None
+    if not args.no_f3 and world == 1:
+        ctx.release_cached()   # the step's scratch peak: the stage runs in a fresh device budget
+        nf = min(args.f3_parents, n_par)
+        sh_h = torch.from_numpy(shard_host[:nf].copy()).pin_memory()
+        tot_f = ctx.gen_coupled_count(sp, shard[:nf], di, args.eps)
+        host = P.HostRecords(tot_f, W)
+        fpool = ctx.pool(sp, 1 << 20)
+        fb = max(1, nf // 4)
+        ctx.stream_generate(sp, sh_h, di, args.eps, fb, fpool, host)      # warm-up (allocator, pinned pages)
+        fpool.clear()
+        st1 = ctx.stream_generate(sp, sh_h, di, args.eps, fb, fpool, host)
+        fk = fpool.keys()
+        g = torch.Generator(device=dev).manual_seed(13)
+        fpsi = torch.rand(fk.shape[0], dtype=torch.float64, device=dev, generator=g) * 2.0 - 1.0
+        ctx.stream_energy(sp, host, nf, fk, fpsi, batch_records=max(1, tot_f // 4))
+        e_r, _, st3 = ctx.stream_energy(sp, host, nf, fk, fpsi, batch_records=max(1, tot_f // 4))
+        e_g, _, st3g = ctx.stream_energy_regen(sp, sh_h, di, args.eps, fb, fk, fpsi)
+        rb = 8 * W + 12
+        f3 = {"parents": nf, "batches": st1["batches"], "records": st1["records"], "unique": st1["unique"],
+              "stage1_offload": {**st1, "overlap_ms": st1["ms_h2d"] + st1["ms_compute"] + st1["ms_d2h"] - st1["ms_wall"],
+                                 "d2h_GBs": st1["d2h_bytes"] / max(st1["ms_d2h"], 1e-9) / 1e6},
+              "stage3_reload": {**st3, "h2d_GBs": st3["h2d_bytes"] / max(st3["ms_h2d"], 1e-9) / 1e6,
+                                "records_per_s": st3["records"] / (st3["ms_wall"] / 1e3)},
+              "stage3_regenerate": {**st3g, "records_per_s": st3g["records"] / (st3g["ms_wall"] / 1e3)},
+              "stage3_identical": bool(torch.equal(e_r, e_g)), "record_bytes": rb}
+        del host, fk, fpsi, e_r, e_g, sh_h
+        fpool.close()
+
+    # ---------------- f4: SCI growth with the heat-bath surrogate (SURVEY 8(f) f4; Sec 2.2, :822-833)
+    f4 = None
+    if not args.no_f4 and world == 1:
+        gpool = ctx.pool(sp, 1 << 20)
+        s0 = shard[: min(2000, n_par)]
+        ctx.merge_space(gpool, ctx.dedup_global(sp, s0))
+        g = torch.Generator(device=dev).manual_seed(17)
+        gpsi = torch.rand(len(gpool), dtype=torch.float64, device=dev, generator=g) * 2.0 - 1.0
+        curve = []
+        for it in range(4):
+            gpsi, gst = ctx.sci_grow_step(sp, gpool, gpsi, di, args.eps, 4 * len(gpool))
+            curve.append({**gst, "redundancy": 1.0 - gst["unique"] / max(gst["records"], 1),
+                          "records_per_s": gst["records"] / (gst["ms"] / 1e3)})
+        f4 = {"start_space": int(s0.shape[0]), "K": "4 x |S| per iteration", "iterations": curve}
+        gpool.close()
+
+    # ---------------- e2e through the public streaming API (f3's stream_generate): the
+    # parents come from pinned HOST memory every step (H2D prefetch on the copy stream,
+    # gen -> dedup_global -> merge_space per mini-batch), then S <- S u C with the
+    # parents copied in again, and the step's counts read back to the host
+    e2e = None
+    if not args.no_e2e:
+        del out, keys_buf, hij_buf, src_buf      # stream_generate keeps its own record slot
+        torch.cuda.empty_cache()
+        ctx.release_cached()                     # the earlier sections' scratch peaks
+
+        def e2e_step():
+            upool.clear()
+            spool.clear()
+            st = ctx.stream_generate(sp, shard_pinned, di, args.eps, batch, upool, None, batch_records=cap)
+            pd = shard_pinned.to(dev, non_blocking=True)
+            ctx.merge_space(spool, pd)
+            ctx.merge_pool(spool, upool)
+            res = torch.tensor([st["records"], len(upool), len(spool)], dtype=torch.int64).to(dev).cpu()  # D2H
+            return int(res[0])
+
+        for _ in range(max(1, min(args.warmup, 2))):  # warm the host-input path (allocator, pinned copies)
+            e2e_step()
+        barrier(pg)
+        torch.cuda.synchronize()
+        eclocks = ClockSampler(local)
+        eclocks.start()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        er = 0
+        for _ in range(args.steps):
+            er += e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        eclk = eclocks.stop()
+        barrier(pg)
+        ems = allreduce_max(pg, e0.elapsed_time(e1))
+        e2e = {"value": allreduce_sum(pg, er) / (ems / 1e3), "unit": "coupled configs/s",
+               "h2d_bytes_per_step": int(2 * shard_pinned.numel() * 8), "d2h_bytes_per_step": 24,
+               "ms_per_step": ems / args.steps, "clocks": eclk,
+               "path": "stream_generate (pinned host parents, H2D prefetch stream) + merge_space + merge_pool; "
+                       "the unique set stays GPU-resident (the pool), counts read back"}
+
     # ---------------- roofline of the dominant kernel class
     peaks = {}
     try:
@@ -487,15 +549,17 @@ def main():
     dname = max(prof.items(), key=lambda kv: kv[1][0])[0] if prof else None
     rname = dname if dname in kernels else (max(kernels, key=lambda k: kernels[k]["ms_per_step"]) if kernels else None)
     # measured DRAM traffic per launch of each class: the committed ncu launch list
-    # of this command (profiles/*_traffic.json, newest round) -- null if absent
+    # of this command for THIS workload (profiles/<round>_<workload>_traffic.json,
+    # newest round) -- null if absent
     traffic, traffic_src = {}, None
     try:
         import glob
-        tj = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")))
+        tj = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_{args.workload}_traffic.json")))
         if tj:
             d = json.load(open(tj[-1]))
-            traffic = d.get("classes", {})
-            traffic_src = os.path.relpath(tj[-1], ROOT)
+            if d.get("parents") in (None, len(par_all)) and d.get("eps", 0.0) == args.eps:
+                traffic = d.get("classes", {})
+                traffic_src = os.path.relpath(tj[-1], ROOT)
     except (OSError, ValueError):
         pass
     roof = None
@@ -511,6 +575,26 @@ def main():
         for k in kernels:
             kernels[k]["dram_bytes_per_launch_ncu"] = traffic.get(k, {}).get("dram_bytes_per_launch")
             kernels[k]["alg_bytes_per_launch"] = alg[k] / (timing[k][1] / args.steps)
+    # the dedup as a whole against what ANY dedup must move: read the N
+    # input keys, write the U distinct ones; the partition passes and the pack are
+    # implementation overhead, reported as traffic amplification (measured DRAM bytes
+    # of every dedup kernel / these algorithmic bytes)
+    dedup_roof = None
+    dcls = [c for c in ("part_scatter", "part_hist", "bucket_unique", "pack") if c in prof]
+    if dcls:
+        d_ms = sum(prof[c][0] for c in dcls) / args.steps
+        d_alg = (ds["keys_in"] + ds["keys_out"]) * 8 * W / args.steps
+        d_dram = None
+        if traffic and all(c in traffic for c in dcls):
+            d_dram = sum(traffic[c]["dram_bytes_per_launch"] * prof[c][1] / args.steps for c in dcls)
+        dedup_roof = {"bound": "hbm", "alg_bytes_per_step": d_alg, "ms_per_step": d_ms,
+                      "achieved": d_alg / (d_ms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                      "frac": d_alg / (d_ms / 1e3) / 1e9 / hbm_peak, "kernels": dcls,
+                      "dram_bytes_per_step_ncu": d_dram,
+                      "traffic_amplification": (d_dram / d_alg) if d_dram else None,
+                      "keys_per_s": ds["keys_in"] / args.steps / (d_ms / 1e3)}
+    if "part_scatter" in kernels:
+        kernels["part_scatter"]["bytes"] = "the pass's own read + write of every key (implementation overhead of the dedup, see dedup_roofline)"
     gen_roof = None
     if "gen" in kernels:
         gen_roof = {"achieved": kernels["gen"]["achieved_GBs"], "frac": kernels["gen"]["frac"],
@@ -549,11 +633,14 @@ def main():
             "unique_configs_per_s": unique_rate,
             "redundancy": 1.0 - uni_all / max(recs_all, 1),
             "roofline": roof,
+            "dedup_roofline": dedup_roof,
             "gen_kernel": gen_roof,
             "kernel_roofline": kernels,
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])},
             "stage3_contract": stage3,
             "f2_regular_sampling": f2,
+            "f3_streaming": f3,
+            "f4_sci_growth": f4,
             "cpu_baseline": cpu,
             "cpu_baseline_mt": cpu_mt,
             "e2e": e2e,

@@ -126,6 +126,13 @@ int cusci_set_option(cusci_ctx* ctx, int option, int64_t value);
 /* Drop the cached Hamiltonian prep (call after mutating or freeing the
  * integrals the cache was built from). */
 void cusci_invalidate_integrals(cusci_ctx* ctx);
+/* Return the context's cached device memory to the driver: the scratch
+ * arena (it grows to the peak of the calls made so far and is kept) and the
+ * freed blocks of its stream-ordered memory pool (stream-stage buffers).
+ * Synchronises the context stream.  Pools and outputs stay valid.  Use
+ * between phases with different memory profiles (Sec 4.3: the
+ * device as a scratchpad). */
+int cusci_release_cached(cusci_ctx* ctx);
 /* Free a library-allocated output when the context has no free callback. */
 void cusci_free(cusci_ctx* ctx, void* ptr);
 /* Number of kernels this context has launched (instrumentation). */
@@ -327,7 +334,9 @@ int energy_contract(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* keys,
  * (cudaHostAlloc / torch pin_memory) for the copies to overlap. */
 typedef struct {
   uint64_t batch_parents;  /* parents per mini-batch (stream_generate, stream_energy_regen) */
-  uint64_t batch_records;  /* records per mini-batch (stream_energy) */
+  uint64_t batch_records;  /* stream_energy: records per mini-batch; stream_generate: record-slot capacity
+                              hint (0 = count every batch exactly first; a batch above the hint is
+                              counted and generated again) */
   uint64_t* host_keys;     /* HOST [host_capacity][words]: the "original set" (nullable: no offload) */
   double* host_hij;        /* HOST [host_capacity] */
   uint32_t* host_src;      /* HOST [host_capacity]: GLOBAL parent index (batch start + index in batch) */
@@ -348,7 +357,8 @@ typedef struct {
  * into one of two device record slots, dedup_global of its keys and
  * merge_space into unique_pool (compute stream), and -- if host_keys is set --
  * offload the batch's records into the host original set (D2H stream), in
- * batch order, src = global parent index.  Peak device memory is bounded by
+ * batch order, src = global parent index (two record slots; one without
+ * offload).  Peak device memory is bounded by
  * the batch, not by n_parents (plus the pool).  COLLECTIVE when world > 1
  * (dedup_global; the batch count is agreed, max over ranks).  Errors: as
  * gen_coupled / dedup_global / merge_space; E_CAPACITY when the host buffers

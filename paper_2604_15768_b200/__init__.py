@@ -223,6 +223,10 @@ class Context:
         return dict(zip(("calls", "keys_in", "key_passes", "keys_out", "buckets", "slow_path_calls", "hist_keys",
                          "hist_free_keys"), (int(x) for x in st)))
 
+    def release_cached(self):
+        """Return the library's cached device memory (scratch arena, freed pool blocks)."""
+        self._check(lib().cusci_release_cached(self._ctx), "cusci_release_cached")
+
     def invalidate_integrals(self):
         lib().cusci_invalidate_integrals(self._ctx)
         self._ints = None
@@ -418,12 +422,15 @@ class Context:
 
     # ---- memory-centric streaming (Sec 4.3)
     def stream_generate(self, space: Space, parents_host: torch.Tensor, ints: DeviceIntegrals, threshold: float,
-                        batch_parents: int, unique_pool: "Pool", host: "HostRecords | None" = None) -> dict:
+                        batch_parents: int, unique_pool: "Pool", host: "HostRecords | None" = None,
+                        batch_records: int = 0) -> dict:
         """Stage 1: parent mini-batches -> gen_coupled -> dedup_global -> merge_space(unique_pool),
-        with H2D prefetch and (if `host`) D2H offload of the records on their own streams."""
+        with H2D prefetch and (if `host`) D2H offload of the records on their own streams.
+        batch_records: record-slot capacity hint (0: count every batch first)."""
         par = _host_u64(parents_host, space.words)
         self._use_integrals(ints)
-        cfg = host._cfg(batch_parents) if host is not None else _StreamCfg(int(batch_parents), 0, None, None, None, 0)
+        cfg = host._cfg(batch_parents, batch_records) if host is not None else \
+            _StreamCfg(int(batch_parents), int(batch_records), None, None, None, 0)
         st = _StreamStats()
         sp, ci = space._c(), ints._c()
         rc = lib().stream_generate(self._ctx, ctypes.byref(sp), ctypes.c_void_p(par.data_ptr()), par.shape[0],

@@ -17,7 +17,7 @@ EXPORTS = ["cusci_nccl_unique_id", "cusci_init", "cusci_finalize", "cusci_last_e
            "cusci_pool_copy", "cusci_pool_clear", "cusci_pool_destroy", "merge_space", "energy_contract",
            "dedup_sorted", "sort_unique", "regular_samples", "select_splitters", "split_bounds",
            "cusci_pool_merge", "cusci_set_option", "dedup_finalize_runs", "stream_generate", "stream_energy",
-           "stream_energy_regen", "sci_grow_step"]
+           "stream_energy_regen", "sci_grow_step", "cusci_release_cached"]
 
 CUSCI_OPT_FORCE_COLLECTIVE = 1
 
@@ -80,6 +80,8 @@ def lib():
     L.dedup_partition.restype = i32
     L.dedup_finalize.argtypes = [vp, vp, vp, u64, vp]
     L.dedup_finalize.restype = i32
+    L.cusci_release_cached.argtypes = [vp]
+    L.cusci_release_cached.restype = i32
     L.sci_grow_step.argtypes = [vp, vp, vp, vp, vp, ctypes.c_double, u64, vp, u64, vp]
     L.sci_grow_step.restype = i32
     L.stream_generate.argtypes = [vp, vp, vp, u64, vp, ctypes.c_double, vp, vp, vp]

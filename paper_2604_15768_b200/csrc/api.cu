@@ -270,6 +270,17 @@ int cusci_set_option(cusci_ctx* ctx, int option, int64_t value) {
   }
 }
 
+int cusci_release_cached(cusci_ctx* ctx) {
+  if (!ctx) return CUSCI_E_INVALID_ARG;
+  if (ctx->arena.depth) return set_error(ctx, CUSCI_E_INVALID_ARG, "cusci_release_cached inside a library call");
+  cudaSetDevice(ctx->device);
+  CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  arena_release_all(ctx);
+  ctx->arena.peak = 0;
+  CUSCI_CUDA(ctx, cudaMemPoolTrimTo(ctx->pool, 0));
+  return CUSCI_OK;
+}
+
 void cusci_invalidate_integrals(cusci_ctx* ctx) {
   if (!ctx) return;
   cudaStreamSynchronize(ctx->stream);

@@ -187,18 +187,32 @@ extern "C" int stream_generate(cusci_ctx* ctx, const cusci_space* sp, const uint
     if (i + 1 < nb) CUSCI_TRY(prefetch(i + 1));
     uint64_t a, n;
     batch(i, &a, &n);
-    const int sl = (int)(i % 2);
+    const int ps = (int)(i % 2);               // parent slot
+    const int sl = offload ? (int)(i % 2) : 0;  // record slot: one suffices when nothing is offloaded
     CUSCI_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ev_h2d[i], 0));
     span(bc, ctx->stream);
-    uint64_t cnt = 0;
-    CUSCI_TRY(gen_count(ctx, sp, (const uint64_t*)par[sl].p, n, ints, threshold, &cnt));
-    if (i >= 2) CUSCI_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ev_d2h[i - 2], 0));  // slot free: its offload done
-    if (rk[sl].bytes < cnt * W * 8) CUSCI_CUDA(ctx, cudaStreamSynchronize(ss.d2h));   // (re)allocation of a slot
-    CUSCI_TRY(rk[sl].ensure(ctx, std::max<uint64_t>(cnt, 1) * W * 8));
-    CUSCI_TRY(rh[sl].ensure(ctx, std::max<uint64_t>(cnt, 1) * 8));
-    CUSCI_TRY(rs[sl].ensure(ctx, std::max<uint64_t>(cnt, 1) * 4));
-    cusci_records rec{(uint64_t*)rk[sl].p, (double*)rh[sl].p, (uint32_t*)rs[sl].p, nullptr, cnt, 0};
-    CUSCI_TRY(gen_records(ctx, sp, (const uint64_t*)par[sl].p, n, ints, threshold, &rec, (uint32_t)a));
+    if (offload && i >= 2) CUSCI_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ev_d2h[i - 2], 0));  // slot free: its offload done
+    // record capacity: the caller's hint (cfg->batch_records) or an exact count;
+    // a batch that exceeds the hint is counted and generated again
+    uint64_t cnt = cfg->batch_records;
+    if (!cnt) CUSCI_TRY(gen_count(ctx, sp, (const uint64_t*)par[ps].p, n, ints, threshold, &cnt));
+    cusci_records rec{};
+    for (int attempt = 0;; attempt++) {
+      if (rk[sl].bytes < cnt * W * 8 && offload) CUSCI_CUDA(ctx, cudaStreamSynchronize(ss.d2h));  // (re)allocation
+      CUSCI_TRY(rk[sl].ensure(ctx, std::max<uint64_t>(cnt, 1) * W * 8));
+      CUSCI_TRY(rh[sl].ensure(ctx, std::max<uint64_t>(cnt, 1) * 8));
+      CUSCI_TRY(rs[sl].ensure(ctx, std::max<uint64_t>(cnt, 1) * 4));
+      rec = cusci_records{(uint64_t*)rk[sl].p, (double*)rh[sl].p, (uint32_t*)rs[sl].p, nullptr,
+                          rk[sl].bytes / (W * 8), 0};
+      const int rc = gen_records(ctx, sp, (const uint64_t*)par[ps].p, n, ints, threshold, &rec, (uint32_t)a);
+      if (rc == CUSCI_E_CAPACITY && attempt == 0) {
+        cnt = rec.count;
+        ctx->err.clear();
+        continue;
+      }
+      CUSCI_TRY(rc);
+      break;
+    }
     CUSCI_CUDA(ctx, cudaEventRecord(ev_gen[i], ctx->stream));
     st->records += rec.count;
     if (offload) {  // the original set -> host memory while the next batch computes

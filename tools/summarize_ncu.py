@@ -65,10 +65,11 @@ CLASS = {"tile_scatter_kernel": "part_scatter", "tile_hist_kernel": "part_hist",
          "scatter1_kernel": "part_scatter", "tile_scatter_atomic_kernel": "part_scatter",
          "sparse_copy_kernel": "merge_tile", "sparse_place_kernel": "merge_tile",
          "sparse_locate_kernel": "merge_split", "sparse_bounds_kernel": "merge_split",
-         "copy_check_kernel": "sorted_check", "check_sorted_kernel": "sorted_check"}
+         "copy_check_kernel": "sorted_check", "check_sorted_kernel": "sorted_check",
+         "run_bounds_kernel": "pack", "run_offsets_kernel": "pack"}
 
 
-def traffic_json(path, out_json):
+def traffic_json(path, out_json, meta=None):
     """per profiler class: DRAM bytes per launch from the launch list (timed step)."""
     rows = list(csv.reader(open(path)))
     hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
@@ -92,13 +93,17 @@ def traffic_json(path, out_json):
             a[2] += d.get("gpu__time_duration.sum", 0)
     out = {c: {"launches": a[0], "dram_bytes_per_launch": a[1] / a[0], "ncu_ms_per_launch": a[2] / a[0] / 1e6}
            for c, a in agg.items() if a[0]}
-    json.dump({"source": path, "classes": out}, open(out_json, "w"), indent=1)
+    json.dump({"source": path, **(meta or {}), "classes": out}, open(out_json, "w"), indent=1)
     return out
 
 
 if __name__ == "__main__":
+    # python tools/summarize_ncu.py TAG [WORKLOAD PARENTS EPS]
     tag = sys.argv[1]
-    print(json.dumps(traffic_json(f"gpurun_out/{tag}_launches.csv", f"profiles/{tag}_traffic.json"), indent=1))
+    wl = sys.argv[2] if len(sys.argv) > 2 else "n2"
+    meta = {"workload": wl, "parents": int(sys.argv[3]) if len(sys.argv) > 3 else 1_000_000,
+            "eps": float(sys.argv[4]) if len(sys.argv) > 4 else 0.0}
+    print(json.dumps(traffic_json(f"gpurun_out/{tag}_launches.csv", f"profiles/{tag}_{wl}_traffic.json", meta), indent=1))
     tbl, tot = launches(f"gpurun_out/{tag}_launches.csv", f"profiles/{tag}_launches.csv")
     print(tbl)
     print()
