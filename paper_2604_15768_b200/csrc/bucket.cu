@@ -15,14 +15,16 @@
 //           partition passes a call needs: high redundancy -> fewer, larger
 //           buckets);
 //   pass k  (0-2 more) segmented passes of <= 9 bits;
-//   dedup   one CTA per run of buckets: each bucket streams through shared
-//           memory in TMA pieces (the next piece is always in flight) into an
-//           ORDER-PRESERVING open-addressing table (home = the bits of hi
+//   dedup   one CTA per SM takes buckets in order from a ticket counter;
+//           each bucket's keys are loaded ILP-wide into an ORDER-PRESERVING
+//           open-addressing table in shared memory (home = the bits of hi
 //           below the bucket id scaled to the table, linear probing, no wrap):
 //           every cluster holds exactly the keys whose homes fall inside it,
-//           so sorting each short cluster in place sorts the table; the
-//           survivors are mapped back to keys (exact inverse mix);
-//   pack    buckets are concatenated in bucket order.
+//           so a survivor's rank is its cluster's start + the keys of its
+//           cluster smaller than it; the survivors are mapped back to keys (exact inverse mix) and
+//           written at their final positions: each bucket's output offset
+//           comes from a decoupled look-back over the buckets' counts (no
+//           pack pass).
 // The result is unique and sorted in the hash order.  A bucket with more
 // distinct keys than its table holds is flagged; the host then finishes with
 // a full LSD sort over the hash digits + unique (exact, rare slow path).
@@ -621,8 +623,8 @@ __device__ __forceinline__ void cas_slot(KeyT<2>* slot, const KeyT<2>& k, KeyT<2
 }
 
 // ---------------------------------------------------------------- per-bucket dedup (ordered table)
-// One CTA per SM (the table takes the shared memory) owns a contiguous run of
-// (sub-)buckets.  A (sub-)bucket is a contiguous run of pi-values whose top
+// One CTA per SM (the table takes the shared memory) takes (sub-)buckets in
+// order from a ticket counter.  A (sub-)bucket is a contiguous run of pi-values whose top
 // S = B + V bits of hi are fixed, so a table slot stores the remaining bits
 // exactly as T = (hi << S) | 1 (never 0: 0 marks an empty slot, and a zero
 // pi-value needs no special case), next to lo at W = 2.  The keys go into an
@@ -656,7 +658,8 @@ template <int W> struct BUCfg {
   static constexpr uint32_t QCAP = 32u * ILP + 32u;       // per-warp slow-path queue (keys)
   static constexpr uint32_t DT = W == 1 ? 6144 : 3072;    // plan: target distinct keys per bucket
   static constexpr size_t QBYTES = (size_t)(kBU / 32) * QCAP * sizeof(KeyT<W>);
-  static constexpr size_t SMEM = (size_t)(TS + OV) * sizeof(KeyT<W>) + QBYTES + 2 * (size_t)NWIN * sizeof(uint32_t);
+  static constexpr size_t SMEM = (size_t)(TS + OV) * sizeof(KeyT<W>) + QBYTES + 2 * (size_t)NWIN * sizeof(uint32_t) +
+                                 (size_t)(TS + OV) * sizeof(uint16_t);
   static_assert(NWIN <= kBU, "one window count per thread in the block scan");
   static_assert(QBYTES >= (TS + OV) * sizeof(uint16_t), "the occupied-slot list reuses the queue space");
   static_assert(SMEM <= 227 * 1024 - 1024, "shared memory budget");
@@ -689,13 +692,42 @@ __device__ __forceinline__ bool tprobe(KeyT<W>* tab, uint32_t s, const KeyT<W>& 
   return tzero(old) || key_eq(old, p);
 }
 
+// Output offsets without a pack pass: units (sub-buckets) are taken in order
+// from a ticket counter, and each publishes its survivor count as soon as its
+// table is complete; warp 0 then resolves the unit's output offset by a
+// decoupled look-back over the predecessors' status words (aggregate, or
+// inclusive prefix) while the other warps rank their survivors.  Every
+// predecessor of a unit holds its ticket already and publishes its count
+// before it looks back itself, so the wait cannot deadlock, resident or not.
+constexpr unsigned long long kBFlagA = 1ull << 62, kBFlagP = 2ull << 62, kBVal = (1ull << 62) - 1;
+__device__ __forceinline__ uint64_t bucket_lookback(volatile unsigned long long* st, uint32_t u) {
+  const unsigned lane = lane_id();
+  uint64_t ex = 0;
+  for (int64_t q0 = (int64_t)u - 1; q0 >= 0; q0 -= 32) {
+    const int64_t q = q0 - (int64_t)lane;
+    unsigned long long v = kBFlagP;  // before unit 0: an inclusive prefix of 0
+    if (q >= 0) v = st[q];
+    while (__any_sync(kFull, (v >> 62) == 0))
+      if ((v >> 62) == 0) v = st[q];
+    const unsigned bp = __ballot_sync(kFull, (v >> 62) == 2);
+    const unsigned L = bp ? (unsigned)(__ffs(bp) - 1) : 32u;  // nearest inclusive prefix
+    uint64_t sum = lane <= L ? (v & kBVal) : 0ull;
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o);
+    ex += sum;
+    if (bp) break;
+  }
+  return ex;
+}
+
 // GEN: raw (caller) input or split buckets (V = 1); the common case compiles without them
 template <int W, bool GEN>
 __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* __restrict__ part, int raw,
                                                               const uint32_t* __restrict__ off,
                                                               const uint64_t* __restrict__ ibase, uint32_t nb, int B,
                                                               int V, uint32_t lf, uint32_t dmean,
-                                                              uint64_t* __restrict__ tmp, uint32_t* __restrict__ surv,
+                                                              uint64_t* __restrict__ out,
+                                                              unsigned long long* __restrict__ lbst,
+                                                              unsigned int* __restrict__ ticket,
                                                               unsigned long long* __restrict__ flags,
                                                               const uint32_t* __restrict__ lb,
                                                               const uint64_t* __restrict__ rs, int nruns) {
@@ -712,7 +744,10 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
   K* qall = tab + TS + OV;                                        // [NW][QCAP]
   uint32_t* bm = reinterpret_cast<uint32_t*>(qall + NW * QCAP);   // [NWIN] occupancy words
   uint32_t* wbase = bm + NWIN;                                    // [NWIN] occupied slots before the window
+  uint16_t* pos = reinterpret_cast<uint16_t*>(wbase + NWIN);      // [TS + OV] survivor rank in the unit
   __shared__ int s_full;
+  __shared__ uint32_t s_unit;
+  __shared__ unsigned long long s_ex;
   __shared__ uint32_t red[33];
   __shared__ uint64_t sg_st[GEN ? CUSCI_MAX_WORLD : 1];       // segment starts of the current bucket
   __shared__ uint32_t sg_pre[GEN ? CUSCI_MAX_WORLD + 1 : 1];  // bucket-local start of each segment
@@ -721,21 +756,21 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
   const int S = B + V;
   const bool segs = GEN && nruns > 0;
   const uint32_t nsb = nb << V;
-  const uint32_t bA = (uint32_t)((uint64_t)nsb * blockIdx.x / gridDim.x);
-  const uint32_t bB = (uint32_t)((uint64_t)nsb * (blockIdx.x + 1) / gridDim.x);
+  volatile unsigned long long* vst = lbst;
   // the table is cleared once here and after every bucket's output
   for (uint32_t i = t; i < TS + OV; i += kBU) tab[i] = K{};
-  if (t == 0) s_full = 0;
+  if (t == 0) {
+    s_full = 0;
+    s_unit = atomicAdd(ticket, 1u);
+  }
   __syncthreads();
-  for (uint32_t b = bA; b < bB; b++) {
-    const uint32_t s = off[b >> V], nk = off[(b >> V) + 1] - s;  // s: survivor (tmp) offset
+  for (;;) {
+    const uint32_t b = s_unit;
+    if (b >= nsb) break;
+    const uint32_t s = off[b >> V], nk = off[(b >> V) + 1] - s;
     const uint64_t si = ibase ? ibase[b >> V] : (uint64_t)s;       // input offset
     const uint64_t vpart = (uint64_t)(b & ((1u << V) - 1u));
-    if (nk == 0) {
-      if (t == 0) surv[b] = 0;
-      continue;
-    }
-    if (segs) {  // this bucket's segments (the previous bucket ended with a barrier)
+    if (segs && nk) {  // this bucket's segments (the previous bucket ended with a barrier)
       const uint32_t bb = b >> V, nbk1 = nb + 1;
       if (t < (uint32_t)nruns) sg_st[t] = rs[t] + lb[(size_t)t * nbk1 + bb];
       if (t == 0) {
@@ -758,6 +793,20 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
         else hi = mid - 1;
       }
       return sg_st[lo] + (i - sg_pre[lo]);
+    };
+    // publish this unit's count (inclusive at unit 0) and resolve its output
+    // offset: warp 0 looks back, the caller's other warps keep working
+    auto publish = [&](uint32_t cnt) {
+      if (t == 0) vst[b] = (b == 0 ? kBFlagP : kBFlagA) | (unsigned long long)cnt;
+    };
+    auto resolve = [&](uint32_t cnt) {
+      if (warp == 0) {
+        const uint64_t ex = b == 0 ? 0ull : bucket_lookback(vst, b);
+        if (t == 0) {
+          if (b) vst[b] = kBFlagP | (unsigned long long)(ex + cnt);
+          s_ex = ex;
+        }
+      }
     };
     // 2^logts home slots ~ lf x the expected distinct keys (<= nk), capped
     const uint32_t want = lf * min(nk, dmean);
@@ -819,8 +868,7 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
     if (s_full) {
       // table overflow (pathological bucket): pass this (sub-)bucket's keys
       // through unfiltered (the host finishes with a full sort + unique) and
-      // restore a clean table.  Part 0 fills its bucket region from the front,
-      // part 1 from the back.
+      // restore a clean table
       auto mine = [&](const K& kk) { return !V || (((raw ? to_pi(kk) : kk).w0 << B) >> (64 - V)) == vpart; };
       if (t == 0) red[0] = 0;
       __syncthreads();
@@ -829,20 +877,23 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
       atomicAdd(&red[0], cnt);
       __syncthreads();
       const uint32_t nh = red[0];
+      publish(nh);
+      resolve(nh);
       __syncthreads();
       if (t == 0) red[0] = 0;
       __syncthreads();
-      const uint64_t ob = vpart ? (uint64_t)s + nk - nh : (uint64_t)s;
+      const uint64_t ob = s_ex;
       for (uint32_t i = t; i < nk; i += kBU) {
         const K p = load_key<W>(part, kaddr(i));
-        if (mine(p)) store_key<W>(tmp, ob + atomicAdd(&red[0], 1u), raw ? p : from_pi(p));
+        if (mine(p)) store_key<W>(out, ob + atomicAdd(&red[0], 1u), raw ? p : from_pi(p));
       }
       for (uint32_t i = t; i < span; i += kBU) tab[i] = K{};
       if (t == 0) {
-        surv[b] = nh;
         atomicAdd(&flags[0], 1ull);
         s_full = 0;
       }
+      __syncthreads();
+      if (t == 0) s_unit = atomicAdd(ticket, 1u);
       __syncthreads();
       continue;
     }
@@ -855,6 +906,7 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
     __syncthreads();
     uint32_t tot = 0;
     const uint32_t wex = block_excl_scan_u32(t < nwin ? __popc(bm[t]) : 0u, red, tot);
+    publish(tot);
     if (t < nwin) wbase[t] = wex;
     __syncthreads();
     // the occupied slots in order (the queue space is free now)
@@ -864,9 +916,9 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
       if ((o >> lane) & 1u) sidx[wbase[w] + __popc(o & lanemask_lt())] = (uint16_t)(w * 32 + lane);
     }
     __syncthreads();
+    resolve(tot);  // warp 0: the look-back first, then its share of the ranks
     // survivor k (rank k among the occupied slots) sits in the cluster [cs, ce);
-    // its output position = k - (slot - cs) + (keys of the cluster smaller than it)
-    const uint64_t ob = vpart ? (uint64_t)s + nk - tot : (uint64_t)s;
+    // its rank in the unit = k - (slot - cs) + (keys of the cluster smaller than it)
     for (uint32_t kk = t; kk < tot; kk += kBU) {
       const uint32_t slot = sidx[kk];
       const K v = tab[slot];
@@ -895,39 +947,18 @@ __global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* _
         rank += (tlt(a0, v) ? 1u : 0u) + (tlt(a1, v) ? 1u : 0u);
       }
       if (y < ce) rank += tlt(tab[y], v) ? 1u : 0u;
-      store_key<W>(tmp, ob + (kk - (slot - cs) + rank), from_pi(tdec(v, S, top)));
+      pos[kk] = (uint16_t)(kk - (slot - cs) + rank);
     }
-    if (t == 0) surv[b] = tot;
-    __syncthreads();  // every rank computed: clear the occupied slots
+    __syncthreads();  // ranks and the unit's output offset known
+    const uint64_t ob = s_ex;
+    for (uint32_t kk = t; kk < tot; kk += kBU) {
+      const uint32_t slot = sidx[kk];
+      store_key<W>(out, ob + pos[kk], from_pi(tdec(tab[slot], S, top)));
+    }
+    __syncthreads();  // every survivor written: clear the occupied slots
     for (uint32_t kk = t; kk < tot; kk += kBU) tab[sidx[kk]] = K{};
-    __syncthreads();  // table clean for the next bucket
-  }
-}
-
-// pack the buckets' survivors: one warp per 32 consecutive buckets (metadata
-// loaded lane-parallel, then each bucket copied by the whole warp)
-template <int W>
-__global__ void __launch_bounds__(kBT) bucket_compact_kernel(const uint64_t* __restrict__ tmp,
-                                                            const uint32_t* __restrict__ off,
-                                                            const uint32_t* __restrict__ surv,
-                                                            const uint64_t* __restrict__ soff, uint32_t nb, int V,
-                                                            uint64_t* __restrict__ out) {
-  const uint32_t lane = lane_id();
-  const uint32_t gw = (blockIdx.x * kBT + threadIdx.x) >> 5, nw = (gridDim.x * kBT) >> 5;
-  for (uint32_t g = gw * 32; g < nb; g += nw * 32) {
-    const uint32_t b = g + lane;
-    uint32_t st = 0, ns = 0;
-    uint64_t o = 0;
-    if (b < nb) {  // nb = sub-buckets; part 1 of a bucket sits at the back of its region
-      ns = surv[b];
-      st = (V && (b & 1u)) ? off[(b >> V) + 1] - ns : off[b >> V];
-      o = soff[b];
-    }
-    for (int l = 0; l < 32; l++) {
-      const uint32_t sl = __shfl_sync(kFull, st, l), nl = __shfl_sync(kFull, ns, l);
-      const uint64_t ol = __shfl_sync(kFull, o, l);
-      for (uint32_t i = lane; i < nl; i += 32) store_key<W>(out, ol + i, load_key<W>(tmp, (uint64_t)sl + i));
-    }
+    if (t == 0) s_unit = atomicAdd(ticket, 1u);
+    __syncthreads();  // table clean for the next unit
   }
 }
 
@@ -986,9 +1017,8 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
   uint32_t dcap = 0xffffffffu;  // expected distinct keys per bucket (+25%; sizes the table)
   const uint32_t nb_max = 1u << Bmax;
   uint64_t *a, *b2;
-  uint32_t *off, *surv, *hll;
-  uint64_t *surv64, *soff;
-  unsigned long long* flags;
+  uint32_t *off, *hll;
+  unsigned long long *flags, *lbst;
   // hist-free first pass (large calls): 256 group regions of `cap` keys in `a`
   static const int hist_free_knob = [] {
     const char* e = getenv("CUSCI_HIST_FREE_PASS1");  // tuning knob (0 disables)
@@ -999,9 +1029,7 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
   CUSCI_TRY(s.get_t((std::max<uint64_t>(n, hist_free ? 256 * cap1 : 0) + 2) * W, &a));  // + slack: 16-byte TMA pieces
   CUSCI_TRY(s.get_t((n + 2) * W, &b2));
   CUSCI_TRY(s.get_t(nb_max + 1, &off));
-  CUSCI_TRY(s.get_t(2 * (size_t)nb_max + 1, &surv));   // x2: sub-buckets (V = 1)
-  CUSCI_TRY(s.get_t(2 * (size_t)nb_max + 1, &surv64));
-  CUSCI_TRY(s.get_t(2 * (size_t)nb_max + 1, &soff));
+  CUSCI_TRY(s.get_t(2 * (size_t)nb_max + 1, &lbst));   // x2: sub-buckets (V = 1); + the ticket
   CUSCI_TRY(s.get_t(kHllM, &hll));
   CUSCI_TRY(s.get_t(2, &flags));
   CUSCI_CUDA(ctx, cudaMemsetAsync(flags, 0, 2 * sizeof(unsigned long long), ctx->stream));
@@ -1255,25 +1283,21 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
   const int V = (B == 0 || (split_knob == 1 && B < 63)) ? 1 : 0;
   const uint32_t vdcap = V ? (dcap == 0xffffffffu ? dcap : dcap / 2u + 64u) : dcap;
   const uint32_t nb = nbk << V;  // work units (sub-buckets)
-  uint64_t* tmp = (part == a) ? b2 : a;
   const unsigned dgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(nb, (uint64_t)ctx->num_sms * dper));
   const int raw = part == in ? 1 : 0;
+  CUSCI_CUDA(ctx, cudaMemsetAsync(lbst, 0, (nb + 1) * sizeof(unsigned long long), ctx->stream));  // + the ticket
+  unsigned int* ticket = reinterpret_cast<unsigned int*>(lbst + nb);
   if (raw || V)
-    CUSCI_LAUNCH(ctx, PT_HASH, bucket_unique_kernel<W, true><<<dgrid, kBU, C::SMEM, ctx->stream>>>(part, raw, off, ibase, nbk, B, V, lf, vdcap, tmp, surv, flags, nullptr, nullptr, 0));
+    CUSCI_LAUNCH(ctx, PT_HASH, bucket_unique_kernel<W, true><<<dgrid, kBU, C::SMEM, ctx->stream>>>(part, raw, off, ibase, nbk, B, V, lf, vdcap, out, lbst, ticket, flags, nullptr, nullptr, 0));
   else
-    CUSCI_LAUNCH(ctx, PT_HASH, bucket_unique_kernel<W, false><<<dgrid, kBU, C::SMEM, ctx->stream>>>(part, raw, off, ibase, nbk, B, V, lf, vdcap, tmp, surv, flags, nullptr, nullptr, 0));
-  // pack the buckets' survivors in bucket order
-  CUSCI_CUDA(ctx, cudaMemsetAsync(surv64, 0, (nb + 1) * sizeof(uint64_t), ctx->stream));
-  CUSCI_CUDA(ctx, cudaMemcpy2DAsync(surv64, sizeof(uint64_t), surv, sizeof(uint32_t), sizeof(uint32_t), nb,
-                                    cudaMemcpyDeviceToDevice, ctx->stream));
-  CUSCI_TRY(scan_exclusive_u64(ctx, surv64, soff, nb + 1, nullptr));
-  const unsigned cgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nb + 255) / 256, (uint64_t)ctx->num_sms * 8));
-  CUSCI_LAUNCH(ctx, PT_SCATTER, bucket_compact_kernel<W><<<cgrid, kBT, 0, ctx->stream>>>(tmp, off, surv, soff, nb, V, out));
+    CUSCI_LAUNCH(ctx, PT_HASH, bucket_unique_kernel<W, false><<<dgrid, kBU, C::SMEM, ctx->stream>>>(part, raw, off, ibase, nbk, B, V, lf, vdcap, out, lbst, ticket, flags, nullptr, nullptr, 0));
+  // the last unit's inclusive prefix is the survivor count
   uint64_t h[2];
-  CUSCI_CUDA(ctx, cudaMemcpyAsync(ctx->host_pinned, soff + nb, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  CUSCI_CUDA(ctx, cudaMemcpyAsync(ctx->host_pinned, lbst + nb - 1, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
   CUSCI_CUDA(ctx, cudaMemcpyAsync((char*)ctx->host_pinned + 8, flags, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
   CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   memcpy(h, ctx->host_pinned, sizeof(h));
+  h[0] &= kBVal;
   *n_out = h[0];
   ctx->dstats[0] += 1;
   ctx->dstats[1] += n;
@@ -1355,16 +1379,13 @@ int runs_dedup_impl(cusci_ctx* ctx, const uint64_t* in, const uint64_t* counts, 
   const int V = B == 0 ? 1 : 0;
   const uint32_t nbk = 1u << B, nb = nbk << V;
   Scratch s(ctx);
-  uint32_t *lb, *off, *surv;
-  uint64_t *drs, *surv64, *soff, *tmp;
-  unsigned long long* flags;
+  uint32_t *lb, *off;
+  uint64_t* drs;
+  unsigned long long *flags, *lbst;
   CUSCI_TRY(s.get_t((size_t)P * (nbk + 1), &lb));
   CUSCI_TRY(s.get_t(nbk + 1, &off));
   CUSCI_TRY(s.get_t(2 * (size_t)P, &drs));
-  CUSCI_TRY(s.get_t(nb + 1, &surv));
-  CUSCI_TRY(s.get_t(nb + 1, &surv64));
-  CUSCI_TRY(s.get_t(nb + 1, &soff));
-  CUSCI_TRY(s.get_t((n + 2) * W, &tmp));
+  CUSCI_TRY(s.get_t(nb + 1, &lbst));
   CUSCI_TRY(s.get_t(2, &flags));
   std::vector<uint64_t> hr(2 * P);
   for (int r = 0; r < P; r++) {
@@ -1383,18 +1404,14 @@ int runs_dedup_impl(cusci_ctx* ctx, const uint64_t* in, const uint64_t* counts, 
     const char* e = getenv("CUSCI_TABLE_LF");
     return e ? (uint32_t)std::max(1, atoi(e)) : 3u;
   }();
-  CUSCI_LAUNCH(ctx, PT_HASH, bucket_unique_kernel<W, true><<<dgrid, kBU, C::SMEM, ctx->stream>>>(in, 1, off, nullptr, nbk, B, V, lf, 0xffffffffu, tmp, surv, flags, lb, drs, P));
-  CUSCI_CUDA(ctx, cudaMemsetAsync(surv64, 0, (nb + 1) * sizeof(uint64_t), ctx->stream));
-  CUSCI_CUDA(ctx, cudaMemcpy2DAsync(surv64, sizeof(uint64_t), surv, sizeof(uint32_t), sizeof(uint32_t), nb,
-                                    cudaMemcpyDeviceToDevice, ctx->stream));
-  CUSCI_TRY(scan_exclusive_u64(ctx, surv64, soff, nb + 1, nullptr));
-  const unsigned cgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nb + 255) / 256, (uint64_t)ctx->num_sms * 8));
-  CUSCI_LAUNCH(ctx, PT_SCATTER, bucket_compact_kernel<W><<<cgrid, kBT, 0, ctx->stream>>>(tmp, off, surv, soff, nb, V, out));
+  CUSCI_CUDA(ctx, cudaMemsetAsync(lbst, 0, (nb + 1) * sizeof(unsigned long long), ctx->stream));
+  CUSCI_LAUNCH(ctx, PT_HASH, bucket_unique_kernel<W, true><<<dgrid, kBU, C::SMEM, ctx->stream>>>(in, 1, off, nullptr, nbk, B, V, lf, 0xffffffffu, out, lbst, reinterpret_cast<unsigned int*>(lbst + nb), flags, lb, drs, P));
   uint64_t h[2];
-  CUSCI_CUDA(ctx, cudaMemcpyAsync(ctx->host_pinned, soff + nb, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  CUSCI_CUDA(ctx, cudaMemcpyAsync(ctx->host_pinned, lbst + nb - 1, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
   CUSCI_CUDA(ctx, cudaMemcpyAsync((char*)ctx->host_pinned + 8, flags, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
   CUSCI_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   memcpy(h, ctx->host_pinned, sizeof(h));
+  h[0] &= kBVal;
   ctx->dstats[0] += 1;
   ctx->dstats[1] += n;
   ctx->dstats[3] += h[1] ? 0 : h[0];
