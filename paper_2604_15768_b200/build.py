@@ -33,18 +33,22 @@ def _newest_input(paths):
     return max(os.path.getmtime(p) for p in paths)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str | None = None, extra: list[str] | None = None) -> str:
+    """extra: additional nvcc flags (A/B variants, tools/build_variant.py); out: the .so path"""
+    lib = out or LIB
+    extra = list(extra or [])
+    build_dir = BUILD if not extra else BUILD + "_" + str(abs(hash(tuple(extra))))
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     hdrs = sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(ROOT, "include", "cusci.h")]
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= _newest_input(srcs + hdrs + [__file__]):
-        return LIB
-    os.makedirs(BUILD, exist_ok=True)
+    if not force and not extra and os.path.exists(lib) and os.path.getmtime(lib) >= _newest_input(srcs + hdrs + [__file__]):
+        return lib
+    os.makedirs(build_dir, exist_ok=True)
     inc, libdir = nccl_dirs()
     common = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-I", inc,
-                     "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr", "-Xptxas", "-v"]
+                     "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr", "-Xptxas", "-v"] + extra
 
     def compile_one(src):
-        obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+        obj = os.path.join(build_dir, os.path.basename(src) + ".o")
         cmd = [NVCC] + common + ["-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
@@ -55,17 +59,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
         objs = list(ex.map(compile_one, srcs))
-    tmp = LIB + f".{os.getpid()}.tmp"
+    tmp = lib + f".{os.getpid()}.tmp"
     cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-L", libdir, "-l:libnccl.so.2",
                                                          "-Xlinker", f"-rpath={libdir}", "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     if verbose:
         for o in objs:
             print(open(o + ".ptxas.txt").read())
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -38,10 +38,19 @@ namespace {
 constexpr int kGenThreads = 256;
 constexpr int kGenWarps = kGenThreads / 32;
 constexpr unsigned long long kNoError = ~0ull;
-constexpr int kChunks = 4;  // 32-entry chunks (128-bit loads per lane) in flight per step
+#ifndef CUSCI_GEN_CHUNKS
+#define CUSCI_GEN_CHUNKS 4  // (macros: A/B variants, tools/build_variant.py)
+#endif
+#ifndef CUSCI_GEN_MINB
+#define CUSCI_GEN_MINB 4
+#endif
+#ifndef CUSCI_GEN_STAGE1
+#define CUSCI_GEN_STAGE1 256
+#endif
+constexpr int kChunks = CUSCI_GEN_CHUNKS;  // 32-entry chunks (128-bit loads per lane) in flight per step
 
 template <int W> struct GenCfg {
-  static constexpr int STAGE = W == 1 ? 256 : 192;  // staged records per warp (4 CTAs/SM)
+  static constexpr int STAGE = W == 1 ? CUSCI_GEN_STAGE1 : 192;  // staged records per warp (4 CTAs/SM)
   static constexpr size_t BYTES_PER_REC = (W == 1 ? 16 : 24) + 1;
   static constexpr size_t SMEM = (size_t)kGenWarps * STAGE * BYTES_PER_REC;
 };
@@ -426,7 +435,7 @@ __device__ __forceinline__ uint32_t do_pairs(const GenArgs& a, const KeyT<W>& pa
 }
 
 template <int W, int MODE>
-__global__ void __launch_bounds__(kGenThreads, 4) gen_kernel(const GenArgs a) {
+__global__ void __launch_bounds__(kGenThreads, CUSCI_GEN_MINB) gen_kernel(const GenArgs a) {
   extern __shared__ __align__(16) unsigned char gsm[];
   __shared__ uint8_t occ_s[kGenWarps][128];
   __shared__ RowInfo<W> ri_s[kGenWarps][kRowBatch + 1];   // pair-row descriptors of the current batch

@@ -1,5 +1,5 @@
 """Per-source-line instruction / stall-sample breakdown of an ncu report
-(--import-source on, -lineinfo): python tools/ncu_lines.py REPORT [kernel-regex] [N]."""
+(--import-source on, -lineinfo): python tools/ncu_lines.py REPORT [kernel-regex] [N] [skip]."""
 import csv
 import io
 import subprocess
@@ -8,8 +8,10 @@ import sys
 rep = sys.argv[1]
 kre = sys.argv[2] if len(sys.argv) > 2 else "."
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
+skip = int(sys.argv[4]) if len(sys.argv) > 4 else 0  # matching launches to skip
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass", "--kernel-name",
-                      f"regex:{kre}"], capture_output=True, text=True).stdout
+                      f"regex:{kre}", "--launch-skip", str(skip), "--launch-count", "1"], capture_output=True,
+                     text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hi = [i for i, r in enumerate(rows) if r and r[0] == "Line No"][0]
 hdr = rows[hi]
