@@ -6,9 +6,10 @@
 // (reading r13).  The merged sequence of S (sorted unique) and U (sorted
 // unique), ties S-first, is cut into tiles of kTile outputs by a diagonal
 // binary search per tile boundary; each CTA stages its S and U runs in shared
-// memory, merges them (serial merge of ITEMS outputs per thread from one
-// in-tile diagonal search), drops an element equal to its predecessor (an
-// element of U already in S), validates U's order, and writes S' and
+// memory, maps them to their pi-values, merges them (ITEMS outputs per thread
+// in registers from one in-tile diagonal search), drops an element equal to
+// its predecessor (an element of U already in S), validates U's order, and
+// writes S' and
 // inserted = U \ S at offsets found by decoupled look-back -- ONE sweep over
 // S and U.  S' goes to the pool's second buffer (grown geometrically to the
 // upper bound |S| + |U| when needed) and the buffers are swapped.
@@ -21,12 +22,15 @@ namespace {
 
 constexpr int kMergeThreads = 256;
 template <int W> struct MergeCfg {
-  static constexpr int ITEMS = W == 1 ? 8 : 4;  // outputs per thread (<= 32: bit masks)
+#ifndef CUSCI_MERGE_ITEMS1
+#define CUSCI_MERGE_ITEMS1 8
+#endif
+  static constexpr int ITEMS = W == 1 ? CUSCI_MERGE_ITEMS1 : 4;  // outputs per thread (<= 32: bit masks)
   static constexpr int TILE = kMergeThreads * ITEMS;
   static constexpr int BUFE = TILE + 4;          // + parity slack of the two runs (W = 1)
-  // dynamic shared memory: two TMA input buffers, abh (hi; later the
-  // compacted output lists), mrg (merged order as buffer indices)
-  static constexpr size_t SMEM = 2 * (size_t)BUFE * sizeof(KeyT<W>) + (size_t)TILE * (8 + 2);
+  // dynamic shared memory: two TMA input buffers, the tile's pi-values
+  // (later its kept keys), the inserted outputs' buffer indices
+  static constexpr size_t SMEM = 2 * (size_t)BUFE * sizeof(KeyT<W>) + (size_t)TILE * (sizeof(KeyT<W>) + 2);
 };
 
 template <int W>
@@ -203,12 +207,14 @@ __device__ __forceinline__ bool mtile_issued(const MTile& g) {
 // Persistent merge: CTA c owns tiles c, c + G, ... (G = resident CTAs, so a
 // tile's predecessors are always being processed: the look-back cannot
 // deadlock).  While tile t is merged, the S and U runs of tile t + G stream
-// into the other buffer by TMA.  Per tile: merge path in shared memory (ties
-// S-first), drop an element equal to its predecessor (an element of U already
-// in S), check that the U run is strictly increasing in the hash order, count
-// kept / inserted outputs with one block scan, publish the counts and resolve
-// the output offsets by a warp-parallel decoupled look-back, compact the
-// outputs into shared-memory lists and write them with coalesced stores.
+// into the other buffer by TMA.  Per tile: the keys are mapped once to their
+// pi-values (an exact bijection, so pi equality is key equality); each thread
+// merges ITEMS outputs in registers from one merge-path diagonal search (ties
+// S-first) and drops an output equal to its predecessor (an element of U
+// already in S) as it goes; one block scan counts the kept and inserted
+// outputs together; warp 0 publishes the counts and resolves the output
+// offsets by a warp-parallel decoupled look-back while the kept keys are
+// staged in order in shared memory; they leave with coalesced stores.
 template <int W>
 __global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(const uint64_t* __restrict__ S, uint64_t nS,
                                                                   const uint64_t* __restrict__ U, uint64_t nU,
@@ -217,16 +223,16 @@ __global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(const uint64_
                                                                   int* __restrict__ bad,
                                                                   uint64_t* __restrict__ out, uint64_t* __restrict__ ins,
                                                                   int check_u) {
-  constexpr int kMergeItems = MergeCfg<W>::ITEMS;
+  using K = KeyT<W>;
+  constexpr int IT = MergeCfg<W>::ITEMS;
   constexpr int kTile = MergeCfg<W>::TILE;
   constexpr int BUFE = MergeCfg<W>::BUFE;
   extern __shared__ __align__(16) unsigned char msm[];
-  KeyT<W>* bufs = reinterpret_cast<KeyT<W>*>(msm);                // [2][BUFE]
-  uint64_t* abh = reinterpret_cast<uint64_t*>(bufs + 2 * BUFE);   // hi by logical index (S run, then U run)
-  uint16_t* mrg = reinterpret_cast<uint16_t*>(abh + kTile);       // merged tile as buffer indices
-  uint16_t* lk = reinterpret_cast<uint16_t*>(abh);                // kept outputs (compacted; aliases abh)
-  uint16_t* li = lk + kTile;                                      // inserted outputs (compacted)
-  __shared__ uint32_t red[33], red2[33];
+  K* bufs = reinterpret_cast<K*>(msm);                        // [2][BUFE] keys (TMA targets)
+  K* hv = bufs + 2 * BUFE;                                    // [TILE] pi-values by logical index (S run, then U run);
+                                                              // after the merge: the kept keys in output order
+  uint16_t* li = reinterpret_cast<uint16_t*>(hv + kTile);     // [TILE] inserted outputs (buffer indices)
+  __shared__ uint32_t red[33];
   __shared__ uint64_t run_k, run_i;
   __shared__ __align__(8) uint64_t bar[2];
   if (threadIdx.x == 0) {
@@ -242,7 +248,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(const uint64_
     mtile_issue<W>(mtile<W>(split, blockIdx.x, nS, nU), S, U, bufs, &bar[0]);
   for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, cb ^= 1) {
     const MTile g = mtile<W>(split, t, nS, nU);
-    KeyT<W>* buf = bufs + cb * BUFE;
+    K* buf = bufs + cb * BUFE;
     if (tma && threadIdx.x == 0 && t + gridDim.x < ntiles) {  // prefetch the next tile into the other buffer
       fence_proxy_async_smem();
       mtile_issue<W>(mtile<W>(split, t + gridDim.x, nS, nU), S, U, bufs + (cb ^ 1) * BUFE, &bar[cb ^ 1]);
@@ -253,85 +259,112 @@ __global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(const uint64_
       mbar_wait(&bar[cb], (phase >> cb) & 1u);
       phase ^= 1u << cb;
     }
-    // keys outside the TMA cores (odd head / tail at W = 1, everything without
-    // TMA) come from plain loads; hi once per key
-    for (int x = threadIdx.x; x < len; x += kMergeThreads) {
-      const bool fromS = x < na;
-      const uint64_t gi = fromS ? g.i0 + x : g.j0 + (x - na);
-      const uint64_t gs = fromS ? g.i0 : g.j0, ge = fromS ? g.i0 + na : g.j0 + nb;
-      const uint32_t bi = fromS ? g.sl + x : g.ul + (x - na);
-      bool core = tma;
-      if (W == 1) core = core && gi >= ((gs + 1) & ~1ull) && gi < (ge & ~1ull);
-      KeyT<W> k;
-      if (core) {
-        k = buf[bi];
-      } else {
-        k = load_key<W>(fromS ? S : U, gi);
-        buf[bi] = k;
+    // keys -> pi-values; keys outside the TMA cores (odd head / tail at W = 1,
+    // everything without TMA) come from plain loads
+    {
+      int s0 = 0, s1 = 0, u0 = 0, u1 = 0;  // TMA core of each run, local indices
+      if (tma) {
+        if (W == 1) {
+          s0 = (int)(((g.i0 + 1) & ~1ull) - g.i0);
+          s1 = (int)(((g.i0 + na) & ~1ull) - g.i0);
+          u0 = (int)(((g.j0 + 1) & ~1ull) - g.j0);
+          u1 = (int)(((g.j0 + nb) & ~1ull) - g.j0);
+        } else {
+          s1 = na;
+          u1 = nb;
+        }
       }
-      abh[x] = hk_hi(k);
+      for (int x = threadIdx.x; x < na; x += kMergeThreads) {
+        K k;
+        if (x >= s0 && x < s1) {
+          k = buf[g.sl + x];
+        } else {
+          k = load_key<W>(S, g.i0 + x);
+          buf[g.sl + x] = k;
+        }
+        hv[x] = to_pi(k);
+      }
+      for (int y = threadIdx.x; y < nb; y += kMergeThreads) {
+        K k;
+        if (y >= u0 && y < u1) {
+          k = buf[g.ul + y];
+        } else {
+          k = load_key<W>(U, g.j0 + y);
+          buf[g.ul + y] = k;
+        }
+        hv[na + y] = to_pi(k);
+      }
     }
     __syncthreads();
-    // hash-order comparisons by logical index: hi first, lo only on a tie (W = 2)
-    auto bidx = [&](int x) -> uint32_t { return x < na ? g.sl + x : g.ul + (x - na); };
-    auto le = [&](int x, int y) -> bool {
-      const uint64_t hx = abh[x], hy = abh[y];
-      if (W == 1 || hx != hy) return hx <= hy;
-      return hk_lo(buf[bidx(x)]) <= hk_lo(buf[bidx(y)]);
-    };
     if (check_u) {  // input check: U strictly increasing in the hash order (tile run + left boundary)
       bool badu = false;
-      for (int x = threadIdx.x; x < nb; x += kMergeThreads) {
-        if (x > 0) badu |= le(na + x, na + x - 1);
-        else if (g.j0 > 0 && g.j0 <= nU) badu |= !hk_lt<W>(load_key<W>(U, g.j0 - 1), buf[g.ul]);
+      for (int y = threadIdx.x; y < nb; y += kMergeThreads) {
+        if (y > 0) badu |= !pi_lt(hv[na + y - 1], hv[na + y]);
+        else if (g.j0 > 0 && g.j0 <= nU) badu |= !pi_lt(to_pi(load_key<W>(U, g.j0 - 1)), hv[na]);
       }
       if (badu) *bad = 1;
     }
-    // each thread merges outputs [k0, k0 + ITEMS)
-    const int k0 = threadIdx.x * kMergeItems;
+    // this thread's outputs [k0, k0 + IT): merged in registers, duplicates of
+    // the predecessor dropped (bit r of km: output k0 + r kept; of im: kept
+    // and from U = inserted)
+    const int k0 = threadIdx.x * IT;
+    uint32_t km = 0, im = 0;
+    uint32_t idx[IT];
     if (k0 < len) {
-      int lo = k0 > nb ? k0 - nb : 0, hi = std::min(k0, na);
+      int lo = k0 > nb ? k0 - nb : 0, hi = min(k0, na);
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
-        if (le(mid, na + k0 - mid - 1)) lo = mid + 1;
+        if (!pi_lt(hv[na + k0 - mid - 1], hv[mid])) lo = mid + 1;  // S[mid] <= U[k0 - mid - 1]
         else hi = mid;
       }
       int i = lo, j = k0 - lo;
-      for (int k = k0; k < std::min(k0 + kMergeItems, len); k++) {
-        const bool takeA = i < na && (j >= nb || le(i, na + j));
-        mrg[k] = (uint16_t)(takeA ? g.sl + i++ : g.ul + j++);
+      K prev{};
+      bool hp = false;
+      if (k0 > 0) {
+        hp = true;
+        if (i == 0) prev = hv[na + j - 1];
+        else if (j == 0) prev = hv[i - 1];
+        else prev = pi_lt(hv[i - 1], hv[na + j - 1]) ? hv[na + j - 1] : hv[i - 1];
+      } else if (!g.inval) {  // the tile's predecessor: the larger of S[i0 - 1], U[j0 - 1]
+        if (g.i0 > 0) {
+          prev = to_pi(load_key<W>(S, g.i0 - 1));
+          hp = true;
+        }
+        if (g.j0 > 0) {
+          const K u = to_pi(load_key<W>(U, g.j0 - 1));
+          if (!hp || pi_lt(prev, u)) prev = u;
+          hp = true;
+        }
       }
-    }
-    // predecessor of the tile's first output: the larger of S[i0-1], U[j0-1]
-    KeyT<W> prev0{};
-    bool has_prev0 = false;
-    if (threadIdx.x == 0 && !g.inval) {
-      if (g.i0 > 0) {
-        prev0 = load_key<W>(S, g.i0 - 1);
-        has_prev0 = true;
-      }
-      if (g.j0 > 0) {
-        const KeyT<W> u = load_key<W>(U, g.j0 - 1);
-        if (!has_prev0 || hk_lt<W>(prev0, u)) prev0 = u;
-        has_prev0 = true;
-      }
-    }
-    __syncthreads();
-    // this thread's kept / inserted outputs (bit r = output k0 + r)
-    uint32_t km = 0, im = 0;
-    for (int r = 0; r < kMergeItems; r++) {
-      const int k = k0 + r;
-      if (k < len) {
-        const bool dup = k > 0 ? key_eq(buf[mrg[k]], buf[mrg[k - 1]]) : (has_prev0 && key_eq(buf[mrg[0]], prev0));
-        if (!dup) {
-          km |= 1u << r;
-          if (mrg[k] >= g.ul) im |= 1u << r;
+      K a = i < na ? hv[i] : K{}, b = j < nb ? hv[na + j] : K{};
+#pragma unroll
+      for (int r = 0; r < IT; r++) {
+        idx[r] = 0;
+        if (k0 + r < len) {
+          const bool takeA = i < na && (j >= nb || !pi_lt(b, a));
+          const K v = takeA ? a : b;
+          idx[r] = takeA ? g.sl + i : g.ul + j;
+          if (takeA) {
+            i++;
+            if (i < na) a = hv[i];
+          } else {
+            j++;
+            if (j < nb) b = hv[na + j];
+          }
+          if (!(hp && key_eq(v, prev))) {
+            km |= 1u << r;
+            if (!takeA) im |= 1u << r;
+          }
+          prev = v;
+          hp = true;
         }
       }
     }
-    uint32_t tk, ti;
-    uint32_t pk = block_excl_scan_u32(__popc(km), red, tk);
-    uint32_t pi = block_excl_scan_u32(__popc(im), red2, ti);
+    // kept (low 16 bits) and inserted (high 16 bits) counted by one scan; its
+    // barriers also end every thread's merge (hv is free from here on)
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan_u32((uint32_t)__popc(km) | ((uint32_t)__popc(im) << 16), red, tot);
+    const uint32_t tk = tot & 0xffffu, ti = tot >> 16;
     if (threadIdx.x < 32) {  // publish + warp-parallel look-back
       volatile unsigned long long* st = status;
       if (threadIdx.x == 0) {
@@ -351,16 +384,20 @@ __global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(const uint64_
         run_i = ei;
       }
     }
-    for (int r = 0; r < kMergeItems; r++) {
-      if ((km >> r) & 1u) lk[pk++] = mrg[k0 + r];
-      if ((im >> r) & 1u) li[pi++] = mrg[k0 + r];
+    {  // stage the kept keys (in output order) and the inserted indices
+      uint32_t pk = ex & 0xffffu, pin = ex >> 16;
+#pragma unroll
+      for (int r = 0; r < IT; r++) {
+        if ((km >> r) & 1u) hv[pk++] = buf[idx[r]];
+        if ((im >> r) & 1u) li[pin++] = (uint16_t)idx[r];
+      }
     }
     __syncthreads();
     const uint64_t rk = run_k, rin = run_i;
-    for (uint32_t x = threadIdx.x; x < tk; x += kMergeThreads) store_key<W>(out, rk + x, buf[lk[x]]);
+    for (uint32_t x = threadIdx.x; x < tk; x += kMergeThreads) store_key<W>(out, rk + x, hv[x]);
     if (ins)
       for (uint32_t x = threadIdx.x; x < ti; x += kMergeThreads) store_key<W>(ins, rin + x, buf[li[x]]);
-    __syncthreads();  // buffer, lists and run offsets free for the next tile
+    __syncthreads();  // buffers, lists and run offsets free for the next tile
   }
 }
 
