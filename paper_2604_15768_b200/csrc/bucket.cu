@@ -648,15 +648,21 @@ __device__ __forceinline__ void cas_slot(KeyT<2>* slot, const KeyT<2>& k, KeyT<2
 // cluster with a smaller T): the table is never sorted in place (no serial
 // insertion sort on the critical path); survivors are written as keys (exact
 // inverse mix) at the bucket offset + rank.
-constexpr int kBU = 1024;  // dedup threads; one CTA per SM
+#ifndef CUSCI_BU_THREADS  // (tuning macros: A/B variants, tools/build_variant.py)
+#define CUSCI_BU_THREADS 1024
+#define CUSCI_BU_LOGTS1 14
+#define CUSCI_BU_OV1 1024
+#define CUSCI_BU_DT1 6144
+#endif
+constexpr int kBU = CUSCI_BU_THREADS;  // dedup threads (the table fills the shared memory: 1024 -> one CTA per SM)
 template <int W> struct BUCfg {
   static constexpr int ILP = W == 1 ? 4 : 2;              // keys per thread per round
-  static constexpr int LOGTS = W == 1 ? 14 : 13;          // max home slots 2^LOGTS
+  static constexpr int LOGTS = W == 1 ? CUSCI_BU_LOGTS1 : CUSCI_BU_LOGTS1 - 1;  // max home slots 2^LOGTS
   static constexpr uint32_t TS = 1u << LOGTS;
-  static constexpr uint32_t OV = W == 1 ? 1024 : 512;     // overflow tail
+  static constexpr uint32_t OV = W == 1 ? CUSCI_BU_OV1 : CUSCI_BU_OV1 / 2;  // overflow tail
   static constexpr uint32_t NWIN = (TS + OV) / 32;        // 32-slot windows
   static constexpr uint32_t QCAP = 32u * ILP + 32u;       // per-warp slow-path queue (keys)
-  static constexpr uint32_t DT = W == 1 ? 6144 : 3072;    // plan: target distinct keys per bucket
+  static constexpr uint32_t DT = W == 1 ? CUSCI_BU_DT1 : CUSCI_BU_DT1 / 2;  // plan: target distinct keys per bucket
   static constexpr size_t QBYTES = (size_t)(kBU / 32) * QCAP * sizeof(KeyT<W>);
   static constexpr size_t SMEM = (size_t)(TS + OV) * sizeof(KeyT<W>) + QBYTES + 2 * (size_t)NWIN * sizeof(uint32_t) +
                                  (size_t)(TS + OV) * sizeof(uint16_t);
@@ -721,7 +727,7 @@ __device__ __forceinline__ uint64_t bucket_lookback(volatile unsigned long long*
 
 // GEN: raw (caller) input or split buckets (V = 1); the common case compiles without them
 template <int W, bool GEN>
-__global__ void __launch_bounds__(kBU, 1) bucket_unique_kernel(const uint64_t* __restrict__ part, int raw,
+__global__ void __launch_bounds__(kBU, 1024 / kBU) bucket_unique_kernel(const uint64_t* __restrict__ part, int raw,
                                                               const uint32_t* __restrict__ off,
                                                               const uint64_t* __restrict__ ibase, uint32_t nb, int B,
                                                               int V, uint32_t lf, uint32_t dmean,
@@ -1039,8 +1045,9 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
   CUSCI_TRY(kernel_setup(ctx, (const void*)tile_scatter_kernel<W, false, 9>, kST, scatter_smem<W, 9>(), &unused));
   CUSCI_TRY(kernel_setup(ctx, (const void*)tile_scatter_atomic_kernel<W, 8>, kST, scatter_atomic_smem<W, 8>(), &unused));
   CUSCI_TRY(kernel_setup(ctx, (const void*)tile_scatter_atomic_kernel<W, 9>, kST, scatter_atomic_smem<W, 9>(), &unused));
+  int dper_g = 1;
   CUSCI_TRY(kernel_setup(ctx, (const void*)bucket_unique_kernel<W, false>, kBU, C::SMEM, &dper));
-  CUSCI_TRY(kernel_setup(ctx, (const void*)bucket_unique_kernel<W, true>, kBU, C::SMEM, &dper));
+  CUSCI_TRY(kernel_setup(ctx, (const void*)bucket_unique_kernel<W, true>, kBU, C::SMEM, &dper_g));
   const uint64_t* part = in;
   uint64_t* ibase = nullptr;  // bucket input starts when the last pass left bucket regions
   if (Bmax > 0) {
@@ -1283,8 +1290,9 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
   const int V = (B == 0 || (split_knob == 1 && B < 63)) ? 1 : 0;
   const uint32_t vdcap = V ? (dcap == 0xffffffffu ? dcap : dcap / 2u + 64u) : dcap;
   const uint32_t nb = nbk << V;  // work units (sub-buckets)
-  const unsigned dgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(nb, (uint64_t)ctx->num_sms * dper));
   const int raw = part == in ? 1 : 0;
+  const unsigned dgrid =
+      (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(nb, (uint64_t)ctx->num_sms * ((raw || V) ? dper_g : dper)));
   CUSCI_CUDA(ctx, cudaMemsetAsync(lbst, 0, (nb + 1) * sizeof(unsigned long long), ctx->stream));  // + the ticket
   unsigned int* ticket = reinterpret_cast<unsigned int*>(lbst + nb);
   if (raw || V)
