@@ -736,11 +736,13 @@ __global__ void __launch_bounds__(kBU, 1024 / kBU) bucket_unique_kernel(const ui
                                                               unsigned int* __restrict__ ticket,
                                                               unsigned long long* __restrict__ flags,
                                                               const uint32_t* __restrict__ lb,
-                                                              const uint64_t* __restrict__ rs, int nruns) {
+                                                              const uint64_t* __restrict__ rs, int nruns,
+                                                              uint64_t ubase) {
   // nruns > 0 (GEN only): the input is nruns pi-sorted runs back to back (run
   // r starts at rs[r]); bucket b's keys are the segments [lb[r][b],
   // lb[r][b+1]) of every run (the owner-side finalize of dedup_global: no
-  // partition pass over the received keys)
+  // partition pass over the received keys).  ubase: global id of unit 0 (the
+  // units cover only the input's hash range; bucket id = (ubase + b) >> V)
   using K = KeyT<W>;
   using C = BUCfg<W>;
   constexpr uint32_t TS = C::TS, OV = C::OV, QCAP = C::QCAP, NWIN = C::NWIN;
@@ -870,7 +872,7 @@ __global__ void __launch_bounds__(kBU, 1024 / kBU) bucket_unique_kernel(const ui
     if (qn) drain(qn);
     if (full) s_full = 1;
     __syncthreads();  // table complete
-    const uint64_t top = (uint64_t)b << (64 - S);  // the sub-bucket's fixed top S bits of hi
+    const uint64_t top = (ubase + b) << (64 - S);  // the sub-bucket's fixed top S bits of hi
     if (s_full) {
       // table overflow (pathological bucket): pass this (sub-)bucket's keys
       // through unfiltered (the host finishes with a full sort + unique) and
@@ -1296,9 +1298,9 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
   CUSCI_CUDA(ctx, cudaMemsetAsync(lbst, 0, (nb + 1) * sizeof(unsigned long long), ctx->stream));  // + the ticket
   unsigned int* ticket = reinterpret_cast<unsigned int*>(lbst + nb);
   if (raw || V)
-    CUSCI_LAUNCH(ctx, PT_HASH, bucket_unique_kernel<W, true><<<dgrid, kBU, C::SMEM, ctx->stream>>>(part, raw, off, ibase, nbk, B, V, lf, vdcap, out, lbst, ticket, flags, nullptr, nullptr, 0));
+    CUSCI_LAUNCH(ctx, PT_HASH, bucket_unique_kernel<W, true><<<dgrid, kBU, C::SMEM, ctx->stream>>>(part, raw, off, ibase, nbk, B, V, lf, vdcap, out, lbst, ticket, flags, nullptr, nullptr, 0, 0ull));
   else
-    CUSCI_LAUNCH(ctx, PT_HASH, bucket_unique_kernel<W, false><<<dgrid, kBU, C::SMEM, ctx->stream>>>(part, raw, off, ibase, nbk, B, V, lf, vdcap, out, lbst, ticket, flags, nullptr, nullptr, 0));
+    CUSCI_LAUNCH(ctx, PT_HASH, bucket_unique_kernel<W, false><<<dgrid, kBU, C::SMEM, ctx->stream>>>(part, raw, off, ibase, nbk, B, V, lf, vdcap, out, lbst, ticket, flags, nullptr, nullptr, 0, 0ull));
   // the last unit's inclusive prefix is the survivor count
   uint64_t h[2];
   CUSCI_CUDA(ctx, cudaMemcpyAsync(ctx->host_pinned, lbst + nb - 1, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1335,11 +1337,13 @@ int local_dedup_impl(cusci_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* o
 }
 
 // run bounds for the owner-side finalize: lb[r][b] = first index of run r
-// (pi-sorted keys) whose top B bits of hi are >= b, b in [0, 2^B]
+// (pi-sorted keys) whose top B bits of hi are >= b0 + b, b in [0, nu]
+// (lb[r][nu] = the run's length: every key's bucket is <= b0 + nu - 1)
 template <int W>
 __global__ void run_bounds_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ rs,
-                                  const uint64_t* __restrict__ rn, int P, int B, uint32_t* __restrict__ lb) {
-  const uint32_t nbk1 = (1u << B) + 1;
+                                  const uint64_t* __restrict__ rn, int P, int B, uint64_t b0, uint32_t nu,
+                                  uint32_t* __restrict__ lb) {
+  const uint32_t nbk1 = nu + 1;
   const uint64_t id = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= (uint64_t)P * nbk1) return;
   const uint32_t r = (uint32_t)(id / nbk1), b = (uint32_t)(id % nbk1);
@@ -1350,11 +1354,21 @@ __global__ void run_bounds_kernel(const uint64_t* __restrict__ keys, const uint6
     while (lo < hi) {
       const uint64_t mid = (lo + hi) >> 1;
       const uint64_t top = B ? (hk_hi(load_key<W>(keys, rs[r] + mid)) >> (64 - B)) : 0ull;
-      if (top < b) lo = mid + 1;
+      if (top < b0 + b) lo = mid + 1;
       else hi = mid;
     }
   }
   lb[id] = (uint32_t)lo;
+}
+// the hash range of P pi-sorted runs: ends[0] = min hi (over the runs' first
+// keys), ends[1] = max hi (over their last keys); ends pre-set to (~0, 0)
+template <int W>
+__global__ void run_ends_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ rs,
+                                const uint64_t* __restrict__ rn, int P, unsigned long long* __restrict__ ends) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= P || rn[r] == 0) return;
+  atomicMin(&ends[0], (unsigned long long)hk_hi(load_key<W>(keys, rs[r])));
+  atomicMax(&ends[1], (unsigned long long)hk_hi(load_key<W>(keys, rs[r] + rn[r] - 1)));
 }
 // off[b] = sum_r lb[r][b]: bucket b's offset in the virtual concatenation
 __global__ void run_offsets_kernel(const uint32_t* __restrict__ lb, int P, uint32_t nbk1, uint32_t* __restrict__ off) {
@@ -1382,28 +1396,47 @@ int runs_dedup_impl(cusci_ctx* ctx, const uint64_t* in, const uint64_t* counts, 
   }
   if (n == 0) return CUSCI_OK;
   if (n >= (1ull << 32)) return set_error(ctx, CUSCI_E_INVALID_ARG, "dedup: %llu received keys exceed 2^32", (unsigned long long)n);
-  int B = 0;
-  while ((n >> B) > C::DT && B < 22) B++;  // the distinct count is <= n
-  const int V = B == 0 ? 1 : 0;
-  const uint32_t nbk = 1u << B, nb = nbk << V;
   Scratch s(ctx);
-  uint32_t *lb, *off;
   uint64_t* drs;
-  unsigned long long *flags, *lbst;
-  CUSCI_TRY(s.get_t((size_t)P * (nbk + 1), &lb));
-  CUSCI_TRY(s.get_t(nbk + 1, &off));
+  unsigned long long* ends;
   CUSCI_TRY(s.get_t(2 * (size_t)P, &drs));
-  CUSCI_TRY(s.get_t(nb + 1, &lbst));
-  CUSCI_TRY(s.get_t(2, &flags));
+  CUSCI_TRY(s.get_t(2, &ends));
   std::vector<uint64_t> hr(2 * P);
   for (int r = 0; r < P; r++) {
     hr[r] = rs[r];
     hr[P + r] = rn[r];
   }
   CUSCI_CUDA(ctx, cudaMemcpyAsync(drs, hr.data(), 2 * P * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+  // the received keys' hash range: an owner's runs all lie in its range
+  // [r 2^64 / P, (r + 1) 2^64 / P), so bucketing by the top bits of hi over the
+  // whole space would put everything into 1/P of the buckets (tables overflow);
+  // the bucket bits are widened by the range's leading zero bits and only the
+  // buckets inside [min, max] become work units
+  {
+    const unsigned long long e0[2] = {~0ull, 0ull};
+    memcpy(ctx->host_pinned, e0, sizeof(e0));
+    CUSCI_CUDA(ctx, cudaMemcpyAsync(ends, ctx->host_pinned, sizeof(e0), cudaMemcpyHostToDevice, ctx->stream));
+    CUSCI_LAUNCH(ctx, PT_SCATTER, run_ends_kernel<W><<<(P + 127) / 128, 128, 0, ctx->stream>>>(in, drs, drs + P, P, ends));
+  }
+  uint64_t hmm[2];
+  CUSCI_TRY(read_u64(ctx, reinterpret_cast<const uint64_t*>(ends), hmm, 2));
+  int B = 0;
+  while ((n >> B) > C::DT && B < 22) B++;  // the distinct count is <= n
+  const uint64_t span = hmm[1] - hmm[0];
+  const int extra = span ? __builtin_clzll(span) : 63;  // the range fits in 2^(64 - extra)
+  const int Bt = std::min(B + extra, 63);
+  const uint64_t b0 = Bt ? hmm[0] >> (64 - Bt) : 0ull, b1 = Bt ? hmm[1] >> (64 - Bt) : 0ull;
+  const int V = Bt == 0 ? 1 : 0;
+  const uint32_t nbk = (uint32_t)(b1 - b0 + 1), nb = nbk << V;  // <= 2^(B + 1) buckets
+  uint32_t *lb, *off;
+  unsigned long long *flags, *lbst;
+  CUSCI_TRY(s.get_t((size_t)P * (nbk + 1), &lb));
+  CUSCI_TRY(s.get_t(nbk + 1, &off));
+  CUSCI_TRY(s.get_t(nb + 1, &lbst));
+  CUSCI_TRY(s.get_t(2, &flags));
   CUSCI_CUDA(ctx, cudaMemsetAsync(flags, 0, 2 * sizeof(unsigned long long), ctx->stream));
   const uint64_t nth = (uint64_t)P * (nbk + 1);
-  CUSCI_LAUNCH(ctx, PT_SCATTER, run_bounds_kernel<W><<<(unsigned)((nth + 255) / 256), 256, 0, ctx->stream>>>(in, drs, drs + P, P, B, lb));
+  CUSCI_LAUNCH(ctx, PT_SCATTER, run_bounds_kernel<W><<<(unsigned)((nth + 255) / 256), 256, 0, ctx->stream>>>(in, drs, drs + P, P, Bt, b0, nbk, lb));
   CUSCI_LAUNCH(ctx, PT_SCATTER, run_offsets_kernel<<<(nbk + 1 + 255) / 256, 256, 0, ctx->stream>>>(lb, P, nbk + 1, off));
   int dper = 1;
   CUSCI_TRY(kernel_setup(ctx, (const void*)bucket_unique_kernel<W, true>, kBU, C::SMEM, &dper));
@@ -1413,7 +1446,7 @@ int runs_dedup_impl(cusci_ctx* ctx, const uint64_t* in, const uint64_t* counts, 
     return e ? (uint32_t)std::max(1, atoi(e)) : 3u;
   }();
   CUSCI_CUDA(ctx, cudaMemsetAsync(lbst, 0, (nb + 1) * sizeof(unsigned long long), ctx->stream));
-  CUSCI_LAUNCH(ctx, PT_HASH, bucket_unique_kernel<W, true><<<dgrid, kBU, C::SMEM, ctx->stream>>>(in, 1, off, nullptr, nbk, B, V, lf, 0xffffffffu, out, lbst, reinterpret_cast<unsigned int*>(lbst + nb), flags, lb, drs, P));
+  CUSCI_LAUNCH(ctx, PT_HASH, bucket_unique_kernel<W, true><<<dgrid, kBU, C::SMEM, ctx->stream>>>(in, 1, off, nullptr, nbk, Bt, V, lf, 0xffffffffu, out, lbst, reinterpret_cast<unsigned int*>(lbst + nb), flags, lb, drs, P, b0 << V));
   uint64_t h[2];
   CUSCI_CUDA(ctx, cudaMemcpyAsync(ctx->host_pinned, lbst + nb - 1, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
   CUSCI_CUDA(ctx, cudaMemcpyAsync((char*)ctx->host_pinned + 8, flags, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
