@@ -106,5 +106,8 @@ if __name__ == "__main__":
     print(json.dumps(traffic_json(f"gpurun_out/{tag}_launches.csv", f"profiles/{tag}_{wl}_traffic.json", meta), indent=1))
     tbl, tot = launches(f"gpurun_out/{tag}_launches.csv", f"profiles/{tag}_launches.csv")
     print(tbl)
-    print()
-    print(full(f"gpurun_out/{tag}_full.ncu-rep"))
+    import glob
+    for rep in sorted(glob.glob(f"gpurun_out/{tag}_full*.ncu-rep")):
+        print()
+        print(f"### {os.path.basename(rep)}")
+        print(full(rep))
