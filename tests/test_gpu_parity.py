@@ -359,6 +359,29 @@ def test_dedup_finalize_runs(P, ctx, W, Pn, n):
     assert np.array_equal(synth.sort_keys(got), oracle.dedup(keep, W).reshape(-1, W))
 
 
+@pytest.mark.parametrize("W,Pn,n", [(1, 8, 4_000_000), (2, 3, 1_500_000), (1, 6, 2_000_000)])
+def test_dedup_finalize_runs_owner_range(P, ctx, W, Pn, n):
+    """What dedup_global's owner r receives at P ranks: every rank's bin for
+    owner r, i.e. keys from 1/P of the hash space (owner(j) = floor(hi P / 2^64)).
+    The finalize must bucket over that range -- the exact slow path (a full
+    LSD sort) is not taken -- and give the oracle's set for the owner."""
+    sp = P.Space(64 * W, 1, 1)
+    allk = synth.zipf_keys(n, W, 0.9, 1 << 22, seed=29 + Pn)
+    r_own = Pn // 2
+    runs = []
+    for r in range(Pn):
+        bins, counts = ctx.dedup_partition(sp, torch.from_numpy(allk[r::Pn]).cuda(), Pn)
+        off = sum(counts[:r_own])
+        runs.append(bins[off:off + counts[r_own]].clone())
+    recv = torch.cat(runs)
+    ctx.dedup_stats(reset=True)
+    got = ctx.dedup_finalize_runs(sp, recv, [x.shape[0] for x in runs]).cpu().numpy().reshape(-1, W)
+    st = ctx.dedup_stats(reset=True)
+    assert st["slow_path_calls"] == 0
+    assert_hash_sorted_unique(got, W)
+    assert np.array_equal(synth.sort_keys(got), oracle.dedup(allk, W, Pn, r_own).reshape(-1, W))
+
+
 # ------------------------------------------------------------------ merge
 @pytest.mark.parametrize("W", [1, 2])
 def test_merge_parity(P, ctx, W):
