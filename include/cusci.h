@@ -216,7 +216,10 @@ int dedup_global(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* configs,
  *     bins->keys holds the bins back to back (bin r first at offset
  *     sum_{r'<r} counts[r']); counts (HOST, [n_owners]) receives the sizes.
  *   dedup_finalize: unique of a received buffer (device, [n][words]) into
- *     the pool hash order pi. */
+ *     the pool hash order pi.  Its buckets are planned for keys spread over
+ *     the whole hash space; on one owner's keys (1/P of the space) it is
+ *     exact but may take the slow path (a full sort) -- dedup_global uses
+ *     dedup_finalize_runs, which buckets over the received keys' range. */
 int dedup_partition(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* configs, uint64_t n,
                     int n_owners, cusci_keys* bins, uint64_t* counts);
 int dedup_finalize(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* keys, uint64_t n,
@@ -225,7 +228,9 @@ int dedup_finalize(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* keys, 
  * back (device keys; run r has run_counts[r] keys, HOST array), each strictly
  * increasing in pi (a dedup_partition bin of some rank).  Same output as
  * dedup_finalize on the concatenation, without a partition pass: every
- * bucket's keys are located in each run by binary search (1 <= n_runs <=
+ * bucket's keys are located in each run by binary search, and the buckets
+ * cover only the runs' hash range [min, max] (an owner's runs lie in 1/P of
+ * the space), so they hold the planned number of keys (1 <= n_runs <=
  * CUSCI_MAX_WORLD; unsorted runs give an unspecified result). */
 int dedup_finalize_runs(cusci_ctx* ctx, const cusci_space* sp, const uint64_t* keys, const uint64_t* run_counts,
                         int n_runs, cusci_keys* unique_sorted);
