@@ -770,6 +770,52 @@ def test_dedup_at_scale(distinct_target, passes):
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
 
 
+_N2_BATCH = r"""
+import sys, torch
+sys.path.insert(0, %r)
+import paper_2604_15768_b200 as P, synth
+wl, ints, par = synth.workload_inputs("n2", n_parents=1_000_000)
+ctx = P.Context(0)
+sp = P.Space(wl.m, 7, 7)
+di = P.DeviceIntegrals(ints.h, ints.eri)
+shard = ctx.dedup_global(sp, torch.from_numpy(par).cuda())
+rec = ctx.gen_coupled(sp, shard[:500_000], di, 0.0, with_src=False)
+assert rec.count == 1_938_044_316, rec.count
+ctx.dedup_stats(reset=True)
+u = ctx.dedup_global(sp, rec.keys)
+st = ctx.dedup_stats(reset=True)
+assert st["hist_free_keys"] == rec.count and st["slow_path_calls"] == 0, st   # the bench's hist-free plan ran
+# strict hash order on the device (hi = fmix64(key), W = 1)
+def srl(x, k):  # logical shift right of int64 bit patterns
+    return (x >> k) & ((1 << (64 - k)) - 1)
+def fmix(x):  # splitmix64 finalizer on int64 bit patterns (multiplications wrap mod 2^64)
+    x = x ^ srl(x, 30); x = x * -4658895280553007687; x = x ^ srl(x, 27); x = x * -7723592293110705685
+    return x ^ srl(x, 31)
+hi = fmix(u.view(torch.int64).reshape(-1)) ^ (-(2 ** 63))   # unsigned order as signed order
+assert bool((hi[1:] > hi[:-1]).all()), "not strictly increasing in the hash order"
+del hi
+# the set: torch's sort-based unique of the same 1.94e9 keys (library code, independent of libcusci)
+ref = torch.unique(rec.keys.view(torch.int64).reshape(-1))
+del rec
+got = torch.sort(u.view(torch.int64).reshape(-1)).values
+assert got.shape == ref.shape and bool(torch.equal(got, ref)), (got.shape, ref.shape)
+print("OK", int(ref.shape[0]))
+"""
+
+
+def test_dedup_n2_bench_batch():
+    """The bench's own dedup call at full size: the first N2 batch (5e5 parents ->
+    1,938,044,316 generated keys, 86% redundant) through the histogram-free
+    plan, against torch.unique of the same keys (set equality) with strict
+    hash order checked on the device."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _N2_BATCH % root], capture_output=True, text=True, timeout=1200, cwd=root)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
+
+
 # ------------------------------------------------------------------ Stage-3 contraction (SURVEY 8(f) f1)
 def _contract_case(P, ctx, wl_key, n_par, W, seed, keep_every=1):
     from oracle import energy
