@@ -799,6 +799,24 @@ ref = torch.unique(rec.keys.view(torch.int64).reshape(-1))
 del rec
 got = torch.sort(u.view(torch.int64).reshape(-1)).values
 assert got.shape == ref.shape and bool(torch.equal(got, ref)), (got.shape, ref.shape)
+del got, ref
+# the bench's merges at full size: the unique pool over both batches (the general
+# merge), then S <- S u C from the parents (the sparse path), against torch.unique
+pool = ctx.pool(sp, 1 << 20)
+ctx.merge_space(pool, u)
+rec2 = ctx.gen_coupled(sp, shard[500_000:], di, 0.0, with_src=False)
+u2 = ctx.dedup_global(sp, rec2.keys)
+del rec2
+ctx.merge_space(pool, u2)
+ref = torch.unique(torch.cat([u.view(torch.int64).reshape(-1), u2.view(torch.int64).reshape(-1)]))
+got = torch.sort(pool.keys().view(torch.int64).reshape(-1)).values
+assert got.shape == ref.shape and bool(torch.equal(got, ref)), (got.shape, ref.shape)
+spool = ctx.pool(sp, 1 << 20)
+ctx.merge_space(spool, shard)
+ctx.merge_pool(spool, pool)
+ref = torch.unique(torch.cat([ref, shard.view(torch.int64).reshape(-1)]))
+got = torch.sort(spool.keys().view(torch.int64).reshape(-1)).values
+assert got.shape == ref.shape and bool(torch.equal(got, ref)), (got.shape, ref.shape)
 print("OK", int(ref.shape[0]))
 """
 
@@ -807,7 +825,8 @@ def test_dedup_n2_bench_batch():
     """The bench's own dedup call at full size: the first N2 batch (5e5 parents ->
     1,938,044,316 generated keys, 86% redundant) through the histogram-free
     plan, against torch.unique of the same keys (set equality) with strict
-    hash order checked on the device."""
+    hash order checked on the device; then the bench's merges at full size
+    (the unique pool over both batches, S <- S u C from the parents)."""
     import os
     import subprocess
     import sys
