@@ -44,6 +44,9 @@ constexpr unsigned long long kNoError = ~0ull;
 #ifndef CUSCI_GEN_MINB
 #define CUSCI_GEN_MINB 4
 #endif
+#ifndef CUSCI_GEN_IFLOAD
+#define CUSCI_GEN_IFLOAD 1
+#endif
 #ifndef CUSCI_GEN_STAGE1
 #define CUSCI_GEN_STAGE1 256
 #endif
@@ -409,7 +412,11 @@ __device__ __forceinline__ uint32_t do_pairs(const GenArgs& a, const KeyT<W>& pa
 #pragma unroll
         for (int u = 0; u < kChunks; u++) {
           const uint32_t i = e + 32 * u + lane;
+#if CUSCI_GEN_IFLOAD
+          if (i < len) raw[u] = __ldg(rowp + i);  // lanes past the row are masked out of `keep`
+#else
           raw[u] = i < len ? __ldg(rowp + i) : make_ulonglong2(~0ull, 0ull);
+#endif
         }
 #pragma unroll
         for (int u = 0; u < kChunks; u++) {
