@@ -802,11 +802,15 @@ assert got.shape == ref.shape and bool(torch.equal(got, ref)), (got.shape, ref.s
 del got, ref
 # the bench's merges at full size: the unique pool over both batches (the general
 # merge), then S <- S u C from the parents (the sparse path), against torch.unique
+ctx.release_cached()
+torch.cuda.empty_cache()
 pool = ctx.pool(sp, 1 << 20)
 ctx.merge_space(pool, u)
 rec2 = ctx.gen_coupled(sp, shard[500_000:], di, 0.0, with_src=False)
 u2 = ctx.dedup_global(sp, rec2.keys)
 del rec2
+ctx.release_cached()
+torch.cuda.empty_cache()
 ctx.merge_space(pool, u2)
 ref = torch.unique(torch.cat([u.view(torch.int64).reshape(-1), u2.view(torch.int64).reshape(-1)]))
 got = torch.sort(pool.keys().view(torch.int64).reshape(-1)).values
@@ -821,7 +825,7 @@ print("OK", int(ref.shape[0]))
 """
 
 
-def test_dedup_n2_bench_batch():
+def test_dedup_n2_bench_batch(P, ctx):
     """The bench's own dedup call at full size: the first N2 batch (5e5 parents ->
     1,938,044,316 generated keys, 86% redundant) through the histogram-free
     plan, against torch.unique of the same keys (set equality) with strict
@@ -831,6 +835,8 @@ def test_dedup_n2_bench_batch():
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    ctx.release_cached()          # this process's cached device memory: the subprocess needs ~100 GB
+    torch.cuda.empty_cache()
     r = subprocess.run([sys.executable, "-c", _N2_BATCH % root], capture_output=True, text=True, timeout=1200, cwd=root)
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
 
