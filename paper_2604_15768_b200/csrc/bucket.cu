@@ -51,6 +51,11 @@ template <int W>
 __device__ __forceinline__ uint32_t top_bits(const KeyT<W>& p, int bits) {
   return bits ? (uint32_t)(p.w0 >> (64 - bits)) : 0u;
 }
+// the top `bits` (>= 1) bits of hi: no zero-width case on the hot paths
+template <int W>
+__device__ __forceinline__ uint32_t top_bits_nz(const KeyT<W>& p, int bits) {
+  return (uint32_t)(p.w0 >> (64 - bits));
+}
 // key i of the pass input as a pi-value (RAW: the caller's keys, mixed here once)
 template <int W, bool RAW>
 __device__ __forceinline__ KeyT<W> load_pi(const uint64_t* in, uint64_t i) {
@@ -289,7 +294,7 @@ __global__ void __launch_bounds__(kST, 2) tile_scatter_kernel(const uint64_t* __
 }
 
 template <int W, int RB> constexpr size_t scatter_atomic_smem() {
-  return kSRing * ((size_t)SSCfg<W>::SUB + 2) * sizeof(KeyT<W>) + 2 * (1u << RB) * 8 + 3 * (1u << RB) * 4;
+  return kSRing * ((size_t)SSCfg<W>::SUB + 2) * sizeof(KeyT<W>);  // the ring (digit tables: static)
 }
 
 // The last (bucket-forming) pass after a hist-free first pass, also without a
@@ -310,9 +315,10 @@ __global__ void __launch_bounds__(kST, 2) tile_scatter_atomic_kernel(const uint6
   static_assert(RMAX <= (uint32_t)kST, "one thread per digit");
   extern __shared__ __align__(16) unsigned char ssm[];  // scatter_atomic_smem<W, RB>() bytes
   KeyT<W>* ring = reinterpret_cast<KeyT<W>*>(ssm);       // [kSRing][SUB + 2]
-  unsigned long long* dl = reinterpret_cast<unsigned long long*>(ring + kSRing * (SUB + 2));  // [2][256]
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(dl + 2 * RMAX);
-  uint32_t* lst = cnt + RMAX;  // [2][256]
+  // digit tables in static shared memory (compile-time addresses on the per-key paths)
+  __shared__ unsigned long long dl[2 * RMAX];  // [2][RMAX] run starts (round parity)
+  __shared__ uint32_t cnt[RMAX];
+  __shared__ uint32_t lst[2 * RMAX];           // [2][RMAX] stage starts
   __shared__ __align__(8) uint64_t bar[kSRing];
   const PTile t = tiles[blockIdx.x];
   const uint64_t gbase = t.mbase * R;  // first bucket of the tile's group (R = 2^bits <= RMAX digits)
@@ -341,7 +347,7 @@ __global__ void __launch_bounds__(kST, 2) tile_scatter_atomic_kernel(const uint6
     const KeyT<W>* stage = ring + (r % kSRing) * (SUB + 2);
     for (uint32_t j = threadIdx.x; j < m; j += kST) {
       const KeyT<W> x = stage[j];
-      const uint32_t d = top_bits<W>(x, bsel) & (R - 1);
+      const uint32_t d = top_bits_nz<W>(x, bsel) & (R - 1);
       const unsigned long long bd = dl[q * RMAX + d];
       if (bd != ~0ull) store_key<W>(out, bd + (j - lst[q * RMAX + d]), x);
     }
@@ -369,13 +375,22 @@ __global__ void __launch_bounds__(kST, 2) tile_scatter_atomic_kernel(const uint6
     uint32_t dr[ITEMS];
     const uint32_t c0 = (W == 1 && tma) ? (uint32_t)((t.start + r0) & 1u) : 0u;
     const uint32_t c1 = !tma ? 0u : (W == 1 ? m - (uint32_t)((t.start + r0 + m) & 1u) : m);
+    if (m == (uint32_t)SUB && c0 == 0 && c1 == (uint32_t)SUB) {  // full sub-round in the ring: no guards
 #pragma unroll
-    for (int u = 0; u < ITEMS; u++) {
-      const uint32_t i = u * kST + threadIdx.x;
-      if (i < m) {
-        k[u] = (i >= c0 && i < c1) ? buf[i + c0] : load_key<W>(in, t.start + r0 + i);
-        const uint32_t d = top_bits<W>(k[u], bsel) & (R - 1);
+      for (int u = 0; u < ITEMS; u++) {
+        k[u] = buf[u * kST + threadIdx.x];
+        const uint32_t d = top_bits_nz<W>(k[u], bsel) & (R - 1);
         dr[u] = (d << 16) | atomicAdd(&cnt[d], 1u);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < ITEMS; u++) {
+        const uint32_t i = u * kST + threadIdx.x;
+        if (i < m) {
+          k[u] = (i >= c0 && i < c1) ? buf[i + c0] : load_key<W>(in, t.start + r0 + i);
+          const uint32_t d = top_bits_nz<W>(k[u], bsel) & (R - 1);
+          dr[u] = (d << 16) | atomicAdd(&cnt[d], 1u);
+        }
       }
     }
     __syncthreads();  // counts final; the slot's keys are in registers: it becomes the stage
@@ -407,10 +422,15 @@ __global__ void __launch_bounds__(kST, 2) tile_scatter_atomic_kernel(const uint6
     }
     __syncthreads();
     KeyT<W>* stage = buf;
+    if (m == (uint32_t)SUB) {
 #pragma unroll
-    for (int u = 0; u < ITEMS; u++) {
-      const uint32_t i = u * kST + threadIdx.x;
-      if (i < m) stage[lst[q * RMAX + (dr[u] >> 16)] + (dr[u] & 0xffffu)] = k[u];
+      for (int u = 0; u < ITEMS; u++) stage[lst[q * RMAX + (dr[u] >> 16)] + (dr[u] & 0xffffu)] = k[u];
+    } else {
+#pragma unroll
+      for (int u = 0; u < ITEMS; u++) {
+        const uint32_t i = u * kST + threadIdx.x;
+        if (i < m) stage[lst[q * RMAX + (dr[u] >> 16)] + (dr[u] & 0xffffu)] = k[u];
+      }
     }
     if (r > 0) store_round(r - 1);
     for (uint32_t d = threadIdx.x; d < RMAX; d += kST) cnt[d] = 0;
@@ -443,10 +463,11 @@ __global__ void __launch_bounds__(kST, 2) scatter1_kernel(const uint64_t* __rest
   constexpr uint32_t RMAX = 256;
   extern __shared__ __align__(16) unsigned char ssm[];  // scatter1_smem<W>() bytes
   KeyT<W>* ring = reinterpret_cast<KeyT<W>*>(ssm);       // [kSRing][SUB + 2]
-  unsigned long long* dl = reinterpret_cast<unsigned long long*>(ring + kSRing * (SUB + 2));  // [2][256]
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(dl + 2 * RMAX);
-  uint32_t* lst = cnt + RMAX;                              // [2][256]
-  uint8_t* reg = reinterpret_cast<uint8_t*>(lst + 2 * RMAX);  // [kHllM] HLL registers, one byte each
+  // digit tables and HLL registers in static shared memory (compile-time addresses)
+  __shared__ unsigned long long dl[2 * RMAX];           // [2][256]
+  __shared__ uint32_t cnt[RMAX];
+  __shared__ uint32_t lst[2 * RMAX];                    // [2][256]
+  __shared__ __align__(4) uint8_t reg[kHllM];           // HLL registers, one byte each
   __shared__ __align__(8) uint64_t bar[kSRing];
   const bool tma = use_tma && ((reinterpret_cast<uintptr_t>(in) & 15u) == 0);
   const uint64_t nsub = (n + SUB - 1) / SUB;
@@ -511,29 +532,35 @@ __global__ void __launch_bounds__(kST, 2) scatter1_kernel(const uint64_t* __rest
     uint32_t dr[ITEMS];
     const uint32_t c0 = (W == 1 && tma) ? (uint32_t)(s0 & 1u) : 0u;
     const uint32_t c1 = !tma ? 0u : (W == 1 ? m - (uint32_t)((s0 + m) & 1u) : m);
-#pragma unroll
-    for (int u = 0; u < ITEMS; u++) {
-      const uint32_t i = u * kST + threadIdx.x;
-      if (i < m) {
-        k[u] = to_pi((i >= c0 && i < c1) ? buf[i + c0] : load_key<W>(in, s0 + i));
-        const uint32_t d = (uint32_t)(k[u].w0 >> 56);
-        dr[u] = (d << 16) | atomicAdd(&cnt[d], 1u);
-        const uint64_t hv = k[u].w0;  // hash-sampled HLL (see tile_hist_kernel)
-        if (((hv >> kHllLog) & (kHllSample - 1)) == 0) {
-          const uint32_t idx = (uint32_t)hv & (kHllM - 1);
-          const uint32_t rho = (uint32_t)min(__clzll(hv), 64 - kHllLog - 4) + 1;
-          if (rho > reg[idx]) {  // rare: byte max by a CAS on the containing word
-            uint32_t* wp = reinterpret_cast<uint32_t*>(reg) + (idx >> 2);
-            const uint32_t sh = (idx & 3u) * 8u;
-            uint32_t old = *wp;
-            while (((old >> sh) & 0xffu) < rho) {
-              const uint32_t nw = (old & ~(0xffu << sh)) | (rho << sh);
-              const uint32_t got = atomicCAS(wp, old, nw);
-              if (got == old) break;
-              old = got;
-            }
+    auto rank_key = [&](int u, const KeyT<W>& key) {
+      k[u] = to_pi(key);
+      const uint32_t d = (uint32_t)(k[u].w0 >> 56);
+      dr[u] = (d << 16) | atomicAdd(&cnt[d], 1u);
+      const uint64_t hv = k[u].w0;  // hash-sampled HLL (see tile_hist_kernel)
+      if (((hv >> kHllLog) & (kHllSample - 1)) == 0) {
+        const uint32_t idx = (uint32_t)hv & (kHllM - 1);
+        const uint32_t rho = (uint32_t)min(__clzll(hv), 64 - kHllLog - 4) + 1;
+        if (rho > reg[idx]) {  // rare: byte max by a CAS on the containing word
+          uint32_t* wp = reinterpret_cast<uint32_t*>(reg) + (idx >> 2);
+          const uint32_t sh = (idx & 3u) * 8u;
+          uint32_t old = *wp;
+          while (((old >> sh) & 0xffu) < rho) {
+            const uint32_t nw = (old & ~(0xffu << sh)) | (rho << sh);
+            const uint32_t got = atomicCAS(wp, old, nw);
+            if (got == old) break;
+            old = got;
           }
         }
+      }
+    };
+    if (m == (uint32_t)SUB && c0 == 0 && c1 == (uint32_t)SUB) {  // full sub-round in the ring: no guards
+#pragma unroll
+      for (int u = 0; u < ITEMS; u++) rank_key(u, buf[u * kST + threadIdx.x]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < ITEMS; u++) {
+        const uint32_t i = u * kST + threadIdx.x;
+        if (i < m) rank_key(u, (i >= c0 && i < c1) ? buf[i + c0] : load_key<W>(in, s0 + i));
       }
     }
     __syncthreads();  // counts final; the slot's keys are in registers: it becomes the stage
@@ -565,10 +592,15 @@ __global__ void __launch_bounds__(kST, 2) scatter1_kernel(const uint64_t* __rest
     }
     __syncthreads();  // lst[q], dl[q ^ 1] ready; cnt read out
     KeyT<W>* stage = buf;
+    if (m == (uint32_t)SUB) {
 #pragma unroll
-    for (int u = 0; u < ITEMS; u++) {
-      const uint32_t i = u * kST + threadIdx.x;
-      if (i < m) stage[lst[q * RMAX + (dr[u] >> 16)] + (dr[u] & 0xffffu)] = k[u];
+      for (int u = 0; u < ITEMS; u++) stage[lst[q * RMAX + (dr[u] >> 16)] + (dr[u] & 0xffffu)] = k[u];
+    } else {
+#pragma unroll
+      for (int u = 0; u < ITEMS; u++) {
+        const uint32_t i = u * kST + threadIdx.x;
+        if (i < m) stage[lst[q * RMAX + (dr[u] >> 16)] + (dr[u] & 0xffffu)] = k[u];
+      }
     }
     if (kk > 0) store_round(kk - 1);
     for (uint32_t d = threadIdx.x; d < RMAX; d += kST) cnt[d] = 0;
@@ -584,7 +616,7 @@ __global__ void __launch_bounds__(kST, 2) scatter1_kernel(const uint64_t* __rest
     if (reg[i]) atomicMax(&hll[i], reg[i]);
 }
 template <int W> constexpr size_t scatter1_smem() {
-  return kSRing * ((size_t)SSCfg<W>::SUB + 2) * sizeof(KeyT<W>) + 2 * 256 * 8 + 3 * 256 * 4 + kHllM;
+  return kSRing * ((size_t)SSCfg<W>::SUB + 2) * sizeof(KeyT<W>);  // the ring (tables: static)
 }
 
 // group offsets after a pass: for old group g with meta {start, tiles, mbase},
