@@ -209,7 +209,21 @@ __device__ __forceinline__ void stage_flush(const GenArgs& a, Stage<W>& st) {
       if (a.src) {  // each source run is a contiguous range of the stage
         for (uint32_t j = 0; j < st.nrun; j++) {
           const uint32_t r0 = st.run[j], r1 = j + 1 < st.nrun ? st.run[j + 1] : st.n, sv = st.run[kRuns + j] + a.src_base;
-          for (uint32_t i = r0 + lane; i < r1; i += 32) a.src[base + i] = sv;
+          if (W == 1 && (reinterpret_cast<uintptr_t>(a.src) & 7u) == 0) {
+            // two src per lane (8-byte stores) from an even global index; an odd
+            // head / tail alone (at W = 2 the extra registers cost more than they save)
+            uint32_t i0 = r0;
+            if (((base + r0) & 1ull) && r0 < r1) {
+              if (lane == 0) a.src[base + r0] = sv;
+              i0++;
+            }
+            uint2* s2 = reinterpret_cast<uint2*>(a.src + base + i0);
+            const uint32_t np = (r1 - i0) >> 1;
+            for (uint32_t q = lane; q < np; q += 32) s2[q] = make_uint2(sv, sv);
+            if (((r1 - i0) & 1u) && lane == 0) a.src[base + r1 - 1] = sv;
+          } else {
+            for (uint32_t i = r0 + lane; i < r1; i += 32) a.src[base + i] = sv;
+          }
         }
       }
       if (MODE == 2)
