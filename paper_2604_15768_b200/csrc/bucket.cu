@@ -293,6 +293,13 @@ __global__ void __launch_bounds__(kST, 2) tile_scatter_kernel(const uint64_t* __
   }
 }
 
+// a digit's stage -> output delta for the hist-free scatters: run start - stage
+// start + SUB (never ~0: the run start is < 2^63), or ~0 for "no write"
+template <int W>
+__device__ __forceinline__ unsigned long long stage_delta(unsigned long long b, uint32_t l) {
+  return b == ~0ull ? ~0ull : b + (unsigned long long)SSCfg<W>::SUB - l;
+}
+
 template <int W, int RB> constexpr size_t scatter_atomic_smem() {
   return kSRing * ((size_t)SSCfg<W>::SUB + 2) * sizeof(KeyT<W>);  // the ring (digit tables: static)
 }
@@ -345,11 +352,12 @@ __global__ void __launch_bounds__(kST, 2) tile_scatter_atomic_kernel(const uint6
   auto store_round = [&](uint32_t r) {
     const uint32_t q = r & 1, m = sub_len(r);
     const KeyT<W>* stage = ring + (r % kSRing) * (SUB + 2);
+    uint64_t* const outb = out - (size_t)SUB * W;  // dl holds run start - stage start + SUB
     for (uint32_t j = threadIdx.x; j < m; j += kST) {
       const KeyT<W> x = stage[j];
       const uint32_t d = top_bits_nz<W>(x, bsel) & (R - 1);
       const unsigned long long bd = dl[q * RMAX + d];
-      if (bd != ~0ull) store_key<W>(out, bd + (j - lst[q * RMAX + d]), x);
+      if (bd != ~0ull) store_key<W>(outb, bd + j, x);
     }
   };
   if (tma && threadIdx.x == 0)
@@ -416,7 +424,7 @@ __global__ void __launch_bounds__(kST, 2) tile_scatter_atomic_kernel(const uint6
     }
     if (threadIdx.x < RMAX) {  // publish the previous round's runs, reserve this round's
       const uint32_t d = threadIdx.x;
-      if (r > 0) dl[(q ^ 1) * RMAX + d] = resolve(d, pcd, bres);
+      if (r > 0) dl[(q ^ 1) * RMAX + d] = stage_delta<W>(resolve(d, pcd, bres), lst[(q ^ 1) * RMAX + d]);
       pcd = cnt[d];
       bres = pcd ? atomicAdd(&gcur[gbase + d], (unsigned long long)pcd) : 0ull;
     }
@@ -438,7 +446,8 @@ __global__ void __launch_bounds__(kST, 2) tile_scatter_atomic_kernel(const uint6
     if (tma && threadIdx.x == 0 && r + kSRing - 1 < nsub) issue(r + kSRing - 1);  // into round r-1's slot
   }
   if (nsub > 0) {
-    if (threadIdx.x < RMAX) dl[((nsub - 1) & 1) * RMAX + threadIdx.x] = resolve(threadIdx.x, pcd, bres);
+    const uint32_t q = (nsub - 1) & 1;
+    if (threadIdx.x < RMAX) dl[q * RMAX + threadIdx.x] = stage_delta<W>(resolve(threadIdx.x, pcd, bres), lst[q * RMAX + threadIdx.x]);
     __syncthreads();
     store_round(nsub - 1);
   }
@@ -498,11 +507,12 @@ __global__ void __launch_bounds__(kST, 2) scatter1_kernel(const uint64_t* __rest
     const uint32_t q = (uint32_t)(k & 1);
     const uint32_t m = sub_len(k);
     const KeyT<W>* stage = ring + (uint32_t)(k % kSRing) * (SUB + 2);
+    uint64_t* const outb = out - (size_t)SUB * W;  // dl holds run start - stage start + SUB
     for (uint32_t j = threadIdx.x; j < m; j += kST) {
       const KeyT<W> x = stage[j];
       const uint32_t d = (uint32_t)(x.w0 >> 56);
       const unsigned long long bd = dl[q * RMAX + d];
-      if (bd != ~0ull) store_key<W>(out, bd + (j - lst[q * RMAX + d]), x);
+      if (bd != ~0ull) store_key<W>(outb, bd + j, x);
     }
   };
   uint64_t nk = 0;  // local sub-rounds
@@ -586,7 +596,7 @@ __global__ void __launch_bounds__(kST, 2) scatter1_kernel(const uint64_t* __rest
     }
     if (threadIdx.x < RMAX) {  // publish the previous round's runs, reserve this round's
       const uint32_t d = threadIdx.x;
-      if (kk > 0) dl[(q ^ 1) * RMAX + d] = resolve(d, pcd, bres);
+      if (kk > 0) dl[(q ^ 1) * RMAX + d] = stage_delta<W>(resolve(d, pcd, bres), lst[(q ^ 1) * RMAX + d]);
       pcd = cnt[d];
       bres = pcd ? atomicAdd(&gcur[d], (unsigned long long)pcd) : 0ull;
     }
@@ -608,7 +618,8 @@ __global__ void __launch_bounds__(kST, 2) scatter1_kernel(const uint64_t* __rest
     if (tma && threadIdx.x == 0 && kk + kSRing - 1 < nk) issue(kk + kSRing - 1);  // into round kk-1's slot
   }
   if (nk > 0) {
-    if (threadIdx.x < RMAX) dl[((nk - 1) & 1) * RMAX + threadIdx.x] = resolve(threadIdx.x, pcd, bres);
+    const uint32_t q = (uint32_t)((nk - 1) & 1);
+    if (threadIdx.x < RMAX) dl[q * RMAX + threadIdx.x] = stage_delta<W>(resolve(threadIdx.x, pcd, bres), lst[q * RMAX + threadIdx.x]);
     __syncthreads();
     store_round(nk - 1);
   }
@@ -686,6 +697,9 @@ __device__ __forceinline__ void cas_slot(KeyT<2>* slot, const KeyT<2>& k, KeyT<2
 #define CUSCI_BU_OV1 1024
 #define CUSCI_BU_DT1 6144
 #endif
+#ifndef CUSCI_BU_CASFIRST
+#define CUSCI_BU_CASFIRST 1  // W = 1: probe with the CAS itself (no load first: 11.66 -> 10.56 ms per N2 batch)
+#endif
 constexpr int kBU = CUSCI_BU_THREADS;  // dedup threads (the table fills the shared memory: 1024 -> one CTA per SM)
 template <int W> struct BUCfg {
   static constexpr int ILP = W == 1 ? 4 : 2;              // keys per thread per round
@@ -721,7 +735,7 @@ __device__ __forceinline__ uint32_t thome(const KeyT<2>& t, int logts) { return 
 template <int W>
 __device__ __forceinline__ bool tprobe(KeyT<W>* tab, uint32_t s, const KeyT<W>& p) {
   KeyT<W> old;
-  if (W == 1) {
+  if (W == 1 && !CUSCI_BU_CASFIRST) {
     const KeyT<W> c = tab[s];
     if (key_eq(c, p)) return true;
     if (!tzero(c)) return false;
@@ -850,8 +864,7 @@ __global__ void __launch_bounds__(kBU, 1024 / kBU) bucket_unique_kernel(const ui
     };
     // 2^logts home slots ~ lf x the expected distinct keys (<= nk), capped
     const uint32_t want = lf * min(nk, dmean);
-    int logts = 5;
-    while (logts < C::LOGTS && (1u << logts) < want) logts++;
+    const int logts = want <= 32u ? 5 : min(C::LOGTS, 32 - __clz(want - 1u));
     const uint32_t span = (1u << logts) + OV;
     bool full = false;
     uint32_t qn = 0;  // warp-uniform queue fill
@@ -955,8 +968,7 @@ __global__ void __launch_bounds__(kBU, 1024 / kBU) bucket_unique_kernel(const ui
       const uint32_t o = bm[w];
       if ((o >> lane) & 1u) sidx[wbase[w] + __popc(o & lanemask_lt())] = (uint16_t)(w * 32 + lane);
     }
-    __syncthreads();
-    resolve(tot);  // warp 0: the look-back first, then its share of the ranks
+    __syncthreads();    resolve(tot);  // warp 0: the look-back first, then its share of the ranks
     // survivor k (rank k among the occupied slots) sits in the cluster [cs, ce);
     // its rank in the unit = k - (slot - cs) + (keys of the cluster smaller than it)
     for (uint32_t kk = t; kk < tot; kk += kBU) {
@@ -991,12 +1003,11 @@ __global__ void __launch_bounds__(kBU, 1024 / kBU) bucket_unique_kernel(const ui
     }
     __syncthreads();  // ranks and the unit's output offset known
     const uint64_t ob = s_ex;
-    for (uint32_t kk = t; kk < tot; kk += kBU) {
+    for (uint32_t kk = t; kk < tot; kk += kBU) {  // each survivor's slot is read once here: clear it as it goes
       const uint32_t slot = sidx[kk];
       store_key<W>(out, ob + pos[kk], from_pi(tdec(tab[slot], S, top)));
+      tab[slot] = K{};
     }
-    __syncthreads();  // every survivor written: clear the occupied slots
-    for (uint32_t kk = t; kk < tot; kk += kBU) tab[sidx[kk]] = K{};
     if (t == 0) s_unit = atomicAdd(ticket, 1u);
     __syncthreads();  // table clean for the next unit
   }
