@@ -101,7 +101,11 @@ __device__ __forceinline__ bool kdisjoint(const KeyT<1>& a, const KeyT<1>& b) { 
 __device__ __forceinline__ bool kdisjoint(const KeyT<2>& a, const KeyT<2>& b) {
   return ((a.w0 & b.w0) | (a.w1 & b.w1)) == 0;
 }
-__device__ __forceinline__ uint32_t kparity_and(const KeyT<1>& a, const KeyT<1>& b) { return __popcll(a.w0 & b.w0) & 1u; }
+__device__ __forceinline__ uint32_t kparity_and(const KeyT<1>& a, const KeyT<1>& b) {
+  // parity of popc(a & b) = parity of popc of the two halves xor-folded (two LOP3 + one POPC)
+  const uint64_t x = a.w0 & b.w0;
+  return __popc((uint32_t)x ^ (uint32_t)(x >> 32)) & 1u;
+}
 __device__ __forceinline__ uint32_t kparity_and(const KeyT<2>& a, const KeyT<2>& b) {
   return (__popcll(a.w0 & b.w0) ^ __popcll(a.w1 & b.w1)) & 1u;
 }
@@ -347,15 +351,36 @@ __device__ __forceinline__ uint32_t do_singles(const GenArgs& a, const KeyT<W>& 
 constexpr int kRowBatch = 96;  // rows per descriptor batch (N2-like parents: one batch)
 template <int W> struct RowInfo;
 template <> struct __align__(8) RowInfo<1> {
-  uint32_t rs;  // first entry of the row in the flattened stream
-  uint32_t rb;  // table index of the row's first entry | phase constant << 31
+  uint32_t rb;   // table index of the row's first entry | phase constant << 31
+  uint32_t len;  // entries in the row
   uint64_t base, M;
 };
-template <> struct __align__(8) RowInfo<2> {
-  uint32_t rs, rb;
+template <> struct __align__(16) RowInfo<2> {
+  uint32_t rb, len;
   uint32_t pq;  // p | q << 8
   uint32_t pad;
 };
+
+// the row loop reads its descriptors through a pinned 32-bit shared address
+// (an asm result cannot be rematerialised: without the pin the compiler
+// recomputes the warp's descriptor base from %tid and the CTA window every row)
+__device__ __forceinline__ uint32_t pin_u32(uint32_t v) {
+  uint32_t r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
+__device__ __forceinline__ RowInfo<1> ld_rowinfo(uint32_t sa, const RowInfo<1>*) {
+  RowInfo<1> r;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(r.rb), "=r"(r.len) : "r"(sa));
+  asm volatile("ld.shared.u64 %0, [%1+8];" : "=l"(r.base) : "r"(sa));
+  asm volatile("ld.shared.u64 %0, [%1+16];" : "=l"(r.M) : "r"(sa));
+  return r;
+}
+__device__ __forceinline__ RowInfo<2> ld_rowinfo(uint32_t sa, const RowInfo<2>*) {
+  RowInfo<2> r;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r.rb), "=r"(r.len), "=r"(r.pq), "=r"(r.pad) : "r"(sa));
+  return r;
+}
 
 template <int W, int MODE>
 __device__ __forceinline__ uint32_t do_pairs(const GenArgs& a, const KeyT<W>& par, const KeyT<W>& PP,
@@ -367,11 +392,9 @@ __device__ __forceinline__ uint32_t do_pairs(const GenArgs& a, const KeyT<W>& pa
   const ulonglong2* ent = reinterpret_cast<const ulonglong2*>(a.ent);
   for (uint32_t b0 = r0; b0 < r1; b0 += kRowBatch) {
     const uint32_t nr = min((uint32_t)kRowBatch, r1 - b0);
-    // ---- row descriptors (lane-parallel) + exclusive scan of the row lengths
-    uint32_t carry = 0;
+    // ---- row descriptors (lane-parallel)
     for (uint32_t j0 = 0; j0 < nr; j0 += 32) {
       const uint32_t j = j0 + lane;
-      uint32_t len = 0;
       if (j < nr) {
         uint32_t k = b0 + j - 1;  // pair index -> (x, y), x < y
         int x = 0;
@@ -383,8 +406,8 @@ __device__ __forceinline__ uint32_t do_pairs(const GenArgs& a, const KeyT<W>& pa
         const int p = occ[x], q = occ[y];
         const uint32_t row = (uint32_t)q * (q - 1) / 2 + p;
         const uint32_t e0 = __ldg(a.rowptr + row);
-        len = __ldg(a.rowptr + row + 1) - e0;
         RowInfo<W> r;
+        r.len = __ldg(a.rowptr + row + 1) - e0;
         r.rb = e0 | ((uint32_t)((x + y + 1) & 1) << 31);
         if constexpr (W == 1) {
           r.base = par.w0 ^ (1ull << p) ^ (1ull << q);
@@ -393,23 +416,16 @@ __device__ __forceinline__ uint32_t do_pairs(const GenArgs& a, const KeyT<W>& pa
           r.pq = (uint32_t)p | ((uint32_t)q << 8);
           r.pad = 0;
         }
-        const uint32_t incl = warp_incl_scan_u32(len);
-        r.rs = carry + incl - len;
         ri[j] = r;
-        carry += __shfl_sync(kFull, incl, 31);
-      } else {
-        const uint32_t incl = warp_incl_scan_u32(0u);
-        carry += __shfl_sync(kFull, incl, 31);
       }
     }
-    if (lane == 0) ri[nr].rs = carry;  // sentinel
     __syncwarp();
-    const uint32_t T = carry;
-    // ---- rows: warp-uniform descriptor (one broadcast load), kChunks 32-entry
+    // ---- rows: warp-uniform descriptor (broadcast loads), kChunks 32-entry
     // chunks (128-bit loads) in flight per step
+    const uint32_t ri_sa = pin_u32((uint32_t)__cvta_generic_to_shared(ri));
     for (uint32_t j = 0; j < nr; j++) {
-      const RowInfo<W> R = ri[j];
-      const uint32_t len = ri[j + 1].rs - R.rs;
+      const RowInfo<W> R = ld_rowinfo(ri_sa + j * (uint32_t)sizeof(RowInfo<W>), ri);
+      const uint32_t len = R.len;
       const ulonglong2* rowp = ent + (R.rb & 0x7fffffffu);
       KeyT<W> base, M;
       if constexpr (W == 1) {
@@ -459,7 +475,7 @@ template <int W, int MODE>
 __global__ void __launch_bounds__(kGenThreads, CUSCI_GEN_MINB) gen_kernel(const GenArgs a) {
   extern __shared__ __align__(16) unsigned char gsm[];
   __shared__ uint8_t occ_s[kGenWarps][128];
-  __shared__ RowInfo<W> ri_s[kGenWarps][kRowBatch + 1];   // pair-row descriptors of the current batch
+  __shared__ RowInfo<W> ri_s[kGenWarps][kRowBatch];       // pair-row descriptors of the current batch
   __shared__ uint32_t run_s[kGenWarps][2 * kRuns];          // stage source runs
   __shared__ unsigned long long unit_s[kGenWarps];
   if (a.counter[2] != kNoError) return;  // invalid parent: write nothing
