@@ -697,17 +697,23 @@ __device__ __forceinline__ void cas_slot(KeyT<2>* slot, const KeyT<2>& k, KeyT<2
 #define CUSCI_BU_OV1 1024
 #define CUSCI_BU_DT1 6144
 #endif
+#ifndef CUSCI_BU_ILP1
+#define CUSCI_BU_ILP1 4
+#endif
+#ifndef CUSCI_BU_PROBE2
+#define CUSCI_BU_PROBE2 0  // the fast path also probes home + 1 before queueing a key
+#endif
 #ifndef CUSCI_BU_CASFIRST
 #define CUSCI_BU_CASFIRST 1  // W = 1: probe with the CAS itself (no load first: 11.66 -> 10.56 ms per N2 batch)
 #endif
 constexpr int kBU = CUSCI_BU_THREADS;  // dedup threads (the table fills the shared memory: 1024 -> one CTA per SM)
 template <int W> struct BUCfg {
-  static constexpr int ILP = W == 1 ? 4 : 2;              // keys per thread per round
+  static constexpr int ILP = W == 1 ? CUSCI_BU_ILP1 : 2;  // keys per thread per round
   static constexpr int LOGTS = W == 1 ? CUSCI_BU_LOGTS1 : CUSCI_BU_LOGTS1 - 1;  // max home slots 2^LOGTS
   static constexpr uint32_t TS = 1u << LOGTS;
   static constexpr uint32_t OV = W == 1 ? CUSCI_BU_OV1 : CUSCI_BU_OV1 / 2;  // overflow tail
   static constexpr uint32_t NWIN = (TS + OV) / 32;        // 32-slot windows
-  static constexpr uint32_t QCAP = 32u * ILP + 32u;       // per-warp slow-path queue (keys)
+  static constexpr uint32_t QCAP = 32u * (ILP < 4 ? ILP : 4) + 32u;  // per-warp slow-path queue (keys; drained mid-round when ILP > 4)
   static constexpr uint32_t DT = W == 1 ? CUSCI_BU_DT1 : CUSCI_BU_DT1 / 2;  // plan: target distinct keys per bucket
   static constexpr size_t QBYTES = (size_t)(kBU / 32) * QCAP * sizeof(KeyT<W>);
   static constexpr size_t SMEM = (size_t)(TS + OV) * sizeof(KeyT<W>) + QBYTES + 2 * (size_t)NWIN * sizeof(uint32_t) +
@@ -873,7 +879,7 @@ __global__ void __launch_bounds__(kBU, 1024 / kBU) bucket_unique_kernel(const ui
       const uint32_t q0 = qn - cnt;
       if (lane < cnt) {
         const K p = q[q0 + lane];
-        uint32_t sidx = thome(p, logts) + 1;  // the home slot holds another key
+        uint32_t sidx = thome(p, logts) + 1 + CUSCI_BU_PROBE2;  // the first probed slot(s) hold other keys
         for (;;) {
           if (sidx >= span) {
             full = true;
@@ -904,12 +910,18 @@ __global__ void __launch_bounds__(kBU, 1024 / kBU) bucket_unique_kernel(const ui
           if (!GEN || !V || ((p.w0 << B) >> (64 - V)) == vpart) {  // (V: the other sub-bucket is skipped)
             p = tenc(p, S);
             pv[u] = p;
-            slow = !tprobe<W>(tab, thome(p, logts), p);
+            const uint32_t h = thome(p, logts);
+            slow = !tprobe<W>(tab, h, p);
+            if (CUSCI_BU_PROBE2 && slow) slow = !tprobe<W>(tab, h + 1, p);  // (h + 1 < TS + OV: no bound check)
           }
         }
         const unsigned sb = __ballot_sync(kFull, slow);
         if (slow) q[qn + __popc(sb & lanemask_lt())] = pv[u];
         qn += __popc(sb);
+        if (ILP > 4 && qn > QCAP - 32) {  // (warp-uniform) room for the next append
+          __syncwarp();
+          drain(32);
+        }
       }
       __syncwarp();
       while (qn >= 32) drain(32);
