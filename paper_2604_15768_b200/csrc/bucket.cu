@@ -44,7 +44,10 @@ constexpr int kBI = 8;          // keys per thread per hist round
 constexpr int kBTile = kBT * kBI;
 constexpr int kHllLog = 11;     // HyperLogLog: 2^11 registers (~2.3% standard error)
 constexpr uint32_t kHllM = 1u << kHllLog;
-constexpr uint32_t kHllSample = 16;  // the sketch sees a 1/16 hash sample of the keys
+#ifndef CUSCI_HLL_SAMPLE
+#define CUSCI_HLL_SAMPLE 256  // 16 -> 256: a warp rarely holds a sampled key (part_scatter 15.16 -> 14.39 ms per N2 batch, same plan)
+#endif
+constexpr uint32_t kHllSample = CUSCI_HLL_SAMPLE;  // the sketch sees a 1/kHllSample hash sample of the keys
 
 // digit source: the top bits of the pi-value's hi word (w0)
 template <int W>
