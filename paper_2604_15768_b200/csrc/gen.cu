@@ -205,10 +205,13 @@ __device__ __forceinline__ void stage_flush(const GenArgs& a, Stage<W>& st) {
     if (lane == 0) base = atomicAdd(&a.counter[0], (unsigned long long)st.n);
     base = __shfl_sync(kFull, base, 0);
     if (base + st.n <= a.capacity) {
-      for (uint32_t i = lane; i < st.n; i += 32) {
+      // lane pointers advanced by 32 records per step (no 64-bit index arithmetic per record)
+      uint64_t* kp = a.keys + (base + lane) * W;
+      double* hp = a.hij + base + lane;
+      for (uint32_t i = lane; i < st.n; i += 32, kp += 32 * W, hp += 32) {
         const StRec<W> r = st.kh[i];
-        store_key<W>(a.keys, base + i, st_key(r));
-        a.hij[base + i] = r.h;
+        store_key<W>(kp, 0, st_key(r));
+        *hp = r.h;
       }
       if (a.src) {  // each source run is a contiguous range of the stage
         for (uint32_t j = 0; j < st.nrun; j++) {
