@@ -703,6 +703,9 @@ __device__ __forceinline__ void cas_slot(KeyT<2>* slot, const KeyT<2>& k, KeyT<2
 #ifndef CUSCI_BU_ILP1
 #define CUSCI_BU_ILP1 4
 #endif
+#ifndef CUSCI_BU_PF
+#define CUSCI_BU_PF 131072  // bytes of the next unit's input prefetched into L2 (0: off; 64 / 128 / 192 / 256 KiB: 10.24 / 10.04 / 10.06 / 10.63 ms vs 10.27 ms per N2 batch)
+#endif
 #ifndef CUSCI_BU_PROBE2
 #define CUSCI_BU_PROBE2 0  // the fast path also probes home + 1 before queueing a key
 #endif
@@ -809,7 +812,7 @@ __global__ void __launch_bounds__(kBU, 1024 / kBU) bucket_unique_kernel(const ui
   uint32_t* wbase = bm + NWIN;                                    // [NWIN] occupied slots before the window
   uint16_t* pos = reinterpret_cast<uint16_t*>(wbase + NWIN);      // [TS + OV] survivor rank in the unit
   __shared__ int s_full;
-  __shared__ uint32_t s_unit;
+  __shared__ uint32_t s_unit, s_next;
   __shared__ unsigned long long s_ex;
   __shared__ uint32_t red[33];
   __shared__ uint64_t sg_st[GEN ? CUSCI_MAX_WORLD : 1];       // segment starts of the current bucket
@@ -820,6 +823,24 @@ __global__ void __launch_bounds__(kBU, 1024 / kBU) bucket_unique_kernel(const ui
   const bool segs = GEN && nruns > 0;
   const uint32_t nsb = nb << V;
   volatile unsigned long long* vst = lbst;
+  // L2 prefetch of the head of a unit's input (CUSCI_BU_PF bytes; 0 = off):
+  // the next unit's ticket is taken when a unit starts, so its first loads
+  // find L2 lines.  A unit held as "next" follows a smaller unit of the same
+  // CTA, so the smallest unpublished unit is always being processed: the
+  // look-back still cannot deadlock.
+  auto l2_prefetch = [&](uint32_t u) {
+#if CUSCI_BU_PF
+    if (segs || u >= nsb) return;
+    const uint32_t s0 = off[u >> V], n0 = off[(u >> V) + 1] - s0;
+    const uint64_t i0 = ibase ? ibase[u >> V] : (uint64_t)s0;
+    const uint64_t a0 = reinterpret_cast<uint64_t>(part + i0 * W) & ~15ull;
+    uint64_t a1 = (reinterpret_cast<uint64_t>(part + (i0 + n0) * W) + 15ull) & ~15ull;
+    if (a1 > a0 + CUSCI_BU_PF) a1 = a0 + CUSCI_BU_PF;
+    if (a1 > a0) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
+#else
+    (void)u;
+#endif
+  };
   // the table is cleared once here and after every bucket's output
   for (uint32_t i = t; i < TS + OV; i += kBU) tab[i] = K{};
   if (t == 0) {
@@ -830,6 +851,10 @@ __global__ void __launch_bounds__(kBU, 1024 / kBU) bucket_unique_kernel(const ui
   for (;;) {
     const uint32_t b = s_unit;
     if (b >= nsb) break;
+    if (CUSCI_BU_PF && t == 0) {
+      s_next = atomicAdd(ticket, 1u);
+      l2_prefetch(s_next);
+    }
     const uint32_t s = off[b >> V], nk = off[(b >> V) + 1] - s;
     const uint64_t si = ibase ? ibase[b >> V] : (uint64_t)s;       // input offset
     const uint64_t vpart = (uint64_t)(b & ((1u << V) - 1u));
@@ -961,7 +986,7 @@ __global__ void __launch_bounds__(kBU, 1024 / kBU) bucket_unique_kernel(const ui
         s_full = 0;
       }
       __syncthreads();
-      if (t == 0) s_unit = atomicAdd(ticket, 1u);
+      if (t == 0) s_unit = CUSCI_BU_PF ? s_next : atomicAdd(ticket, 1u);
       __syncthreads();
       continue;
     }
@@ -1023,7 +1048,7 @@ __global__ void __launch_bounds__(kBU, 1024 / kBU) bucket_unique_kernel(const ui
       store_key<W>(out, ob + pos[kk], from_pi(tdec(tab[slot], S, top)));
       tab[slot] = K{};
     }
-    if (t == 0) s_unit = atomicAdd(ticket, 1u);
+    if (t == 0) s_unit = CUSCI_BU_PF ? s_next : atomicAdd(ticket, 1u);
     __syncthreads();  // table clean for the next unit
   }
 }
