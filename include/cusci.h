@@ -122,6 +122,14 @@ const char* cusci_last_error(const cusci_ctx* ctx);
  * identical to the world = 1 shortcut.  Errors: E_INVALID_ARG (unknown
  * option, or no communicator). */
 #define CUSCI_OPT_FORCE_COLLECTIVE 1
+/* CUSCI_OPT_CONTRACT_PARTITION (value -1 / 0 / 1): energy_contract and the
+ * Stage-3 stream paths first scatter the records by the top 8 bits of their
+ * key's hash-order value into 256 regions, so the reverse-index probes of a
+ * region stay inside an L2-resident slice of the (key, psi) table: 1 on,
+ * 0 (default) / -1 off (on one N2 batch the partition cuts the contraction's
+ * DRAM reads 4x but costs more than it saves).  Results are
+ * identical either way (exact sums). */
+#define CUSCI_OPT_CONTRACT_PARTITION 2
 int cusci_set_option(cusci_ctx* ctx, int option, int64_t value);
 /* Drop the cached Hamiltonian prep (call after mutating or freeing the
  * integrals the cache was built from). */

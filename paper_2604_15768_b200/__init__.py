@@ -244,6 +244,11 @@ class Context:
         from ._lib import CUSCI_OPT_FORCE_COLLECTIVE
         self._check(lib().cusci_set_option(self._ctx, CUSCI_OPT_FORCE_COLLECTIVE, 1 if on else 0), "cusci_set_option")
 
+    def contract_partition(self, mode: int = 0):
+        """energy_contract's pi-partition of the records: 1 on, 0 (default) / -1 off."""
+        from ._lib import CUSCI_OPT_CONTRACT_PARTITION
+        self._check(lib().cusci_set_option(self._ctx, CUSCI_OPT_CONTRACT_PARTITION, int(mode)), "cusci_set_option")
+
     @staticmethod
     def nccl_unique_id() -> bytes:
         buf = ctypes.create_string_buffer(128)

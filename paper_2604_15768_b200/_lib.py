@@ -20,6 +20,7 @@ EXPORTS = ["cusci_nccl_unique_id", "cusci_init", "cusci_finalize", "cusci_last_e
            "stream_energy_regen", "sci_grow_step", "cusci_release_cached"]
 
 CUSCI_OPT_FORCE_COLLECTIVE = 1
+CUSCI_OPT_CONTRACT_PARTITION = 2
 
 
 PROFILE_TAGS = ["prep", "validate", "gen", "bucket_unique", "pack", "part_hist", "part_scatter",

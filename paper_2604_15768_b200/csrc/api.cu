@@ -265,6 +265,10 @@ int cusci_set_option(cusci_ctx* ctx, int option, int64_t value) {
         return set_error(ctx, CUSCI_E_INVALID_ARG, "CUSCI_OPT_FORCE_COLLECTIVE needs a communicator (pass an NCCL id to cusci_init)");
       ctx->force_collective = value ? 1 : 0;
       return CUSCI_OK;
+    case CUSCI_OPT_CONTRACT_PARTITION:
+      if (value < -1 || value > 1) return set_error(ctx, CUSCI_E_INVALID_ARG, "CUSCI_OPT_CONTRACT_PARTITION takes -1, 0 or 1");
+      ctx->contract_partition = (int)value;
+      return CUSCI_OK;
     default:
       return set_error(ctx, CUSCI_E_INVALID_ARG, "unknown option %d", option);
   }

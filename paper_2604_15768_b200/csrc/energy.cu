@@ -198,7 +198,22 @@ __global__ void __launch_bounds__(kET, 4) contract_kernel(const uint64_t* __rest
                                                       const uint32_t* __restrict__ src, uint64_t n_rec,
                                                       const KPsi<W>* __restrict__ table, uint64_t tslots,
                                                       int k, uint64_t n_parents, unsigned long long* __restrict__ acc,
-                                                      unsigned long long* __restrict__ flags) {
+                                                      unsigned long long* __restrict__ flags,
+                                                      const unsigned long long* __restrict__ rcnt, uint64_t rcap,
+                                                      const int* __restrict__ rovf, const uint64_t* __restrict__ fkeys,
+                                                      const double* __restrict__ fhij, const uint32_t* __restrict__ fsrc,
+                                                      uint64_t fn, unsigned long long* __restrict__ tick) {
+  // region mode (rcnt != null): the records were partitioned by rec_partition_kernel
+  // into regions of rcap slots (rcap % 64 == 0), region g holding rcnt[g] records;
+  // if that partition overflowed (*rovf), the flat records (f*) are contracted instead
+  if (rcnt && *rovf) {
+    keys = fkeys;
+    hij = fhij;
+    src = fsrc;
+    n_rec = fn;
+    rcnt = nullptr;
+    tick = nullptr;
+  }
   const unsigned lane = lane_id();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   uint64_t missing = 0;
@@ -208,7 +223,9 @@ __global__ void __launch_bounds__(kET, 4) contract_kernel(const uint64_t* __rest
   constexpr int kU = 2;
   const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = stride >> 5;
-  for (uint64_t w0 = wid * 32 * kU; w0 < n_rec; w0 += nw * 32 * kU) {
+  auto group = [&](const uint64_t w0) {
+    // records of this 64-record group that exist (a group never straddles a region)
+    const uint64_t lim = rcnt ? (w0 / rcap) * rcap + min((uint64_t)rcnt[w0 / rcap], rcap) : n_rec;
     uint32_t sv[kU];
     KeyT<W> kv[kU];
     uint64_t hm[kU];
@@ -218,14 +235,18 @@ __global__ void __launch_bounds__(kET, 4) contract_kernel(const uint64_t* __rest
     for (int u = 0; u < kU; u++) {
       const uint64_t r = w0 + u * 32 + lane;
       sv[u] = 0xffffffffu;
-      if (r < n_rec) {
-        sv[u] = src[r];
+      if (r < lim) {
+        sv[u] = __ldcs(src + r);  // streamed once: evict-first, the table slice keeps L2
         if (sv[u] >= n_parents) {  // out-of-range parent index: flagged, never accumulated
           badsrc = true;
           sv[u] = 0xffffffffu;
         }
-        hv[u] = hij[r];
-        kv[u] = load_key<W>(keys, r);
+        hv[u] = __ldcs(hij + r);
+        if constexpr (W == 1) kv[u] = KeyT<W>{__ldcs(reinterpret_cast<const unsigned long long*>(keys) + r)};
+        else {
+          const ulonglong2 x = __ldcs(reinterpret_cast<const ulonglong2*>(keys) + r);
+          kv[u] = KeyT<W>{x.x, x.y};
+        }
         // home slot of the key in the ordered (key, psi) table
         hm[u] = k ? (to_pi(kv[u]).w0 >> (64 - k)) : 0ull;
         ev[u] = table[hm[u]];
@@ -236,7 +257,7 @@ __global__ void __launch_bounds__(kET, 4) contract_kernel(const uint64_t* __rest
     for (int u = 0; u < kU; u++) {
       qv[u] = 0;
       const uint64_t r = w0 + u * 32 + lane;
-      if (r < n_rec) {
+      if (r < lim) {
         bool found = false;
         double ps = 0.0;
         KPsi<W> e = ev[u];
@@ -261,7 +282,7 @@ __global__ void __launch_bounds__(kET, 4) contract_kernel(const uint64_t* __rest
 #pragma unroll
     for (int u = 0; u < kU; u++) {
       const uint32_t s = sv[u];
-      const bool valid = w0 + u * 32 + lane < n_rec;
+      const bool valid = w0 + u * 32 + lane < lim;
       // segmented inclusive sum over runs of equal src (lanes in record order)
       const uint32_t sprev = __shfl_up_sync(kFull, s, 1);
       const unsigned heads = __ballot_sync(kFull, lane == 0 || sprev != s);
@@ -286,11 +307,129 @@ __global__ void __launch_bounds__(kET, 4) contract_kernel(const uint64_t* __rest
         atomicAdd(a4 + 3, (unsigned long long)l3);
       }
     }
+  };
+  if (tick) {  // region mode: 512-record chunks in order from a ticket (the grid's chunks in flight stay
+               // within one or two regions, so their table slices stay in L2)
+    for (;;) {
+      unsigned long long c = 0;
+      if (lane == 0) c = atomicAdd(tick, 1ull);
+      const uint64_t cb = __shfl_sync(kFull, c, 0) * 512ull;
+      if (cb >= n_rec) break;
+      for (uint64_t w0 = cb; w0 < cb + 512 && w0 < n_rec; w0 += 32 * kU) group(w0);
+    }
+  } else {
+    for (uint64_t w0 = wid * 32 * kU; w0 < n_rec; w0 += nw * 32 * kU) group(w0);
   }
   for (int o = 16; o; o >>= 1) missing += __shfl_xor_sync(kFull, missing, o);
   if (lane == 0 && missing) atomicAdd(&flags[0], (unsigned long long)missing);
   if (__any_sync(kFull, big) && lane == 0) atomicOr(&flags[1], 1ull);
   if (__any_sync(kFull, badsrc) && lane == 0) atomicOr(&flags[1], 2ull);
+}
+
+// ---- pi-partition of the records (f1 at scale): the (key, psi) table is far
+// larger than L2 and a record's probe is a random sector (ncu: ~130 DRAM bytes
+// per probe).  Records are first scattered by the top 8 bits of their key's
+// pi-value into 256 regions (hist-free: regions of rcap slots, runs reserved
+// per (sub-round, digit) with one global atomic, as dedup's first pass); the
+// contraction then sweeps the regions in order with a persistent grid, so the
+// table slice the probes touch (1/256 of the table) stays in L2.  Within a
+// region a sub-round's records of one digit stay together, so a parent's
+// records still arrive in runs for the warp-level src reduction.
+constexpr int kRPT = 512;
+template <int W> struct RPCfg {
+  static constexpr int SUB = W == 1 ? 4096 : 2048;  // records per sub-round
+  static constexpr size_t SMEM = (size_t)SUB * (8 * W + 8 + 4 + 1);
+};
+template <int W>
+__global__ void __launch_bounds__(kRPT, 2) rec_partition_kernel(const uint64_t* __restrict__ keys,
+                                                               const double* __restrict__ hij,
+                                                               const uint32_t* __restrict__ src, uint64_t n,
+                                                               uint64_t rcap, unsigned long long* __restrict__ gcur,
+                                                               uint64_t* __restrict__ okeys, double* __restrict__ oh,
+                                                               uint32_t* __restrict__ osrc, int* __restrict__ ovf) {
+  constexpr int SUB = RPCfg<W>::SUB, IT = SUB / kRPT, R = 256;
+  extern __shared__ __align__(16) unsigned char rsm[];
+  KeyT<W>* sk = reinterpret_cast<KeyT<W>*>(rsm);
+  double* sh = reinterpret_cast<double*>(sk + SUB);
+  uint32_t* ss = reinterpret_cast<uint32_t*>(sh + SUB);
+  uint8_t* sd = reinterpret_cast<uint8_t*>(ss + SUB);
+  __shared__ uint32_t cnt[R], lst[R];
+  __shared__ unsigned long long dl[R];
+  const uint32_t t = threadIdx.x;
+  const uint64_t nsub = (n + SUB - 1) / SUB;
+  for (uint64_t sb = blockIdx.x; sb < nsub; sb += gridDim.x) {
+    for (uint32_t d = t; d < R; d += kRPT) cnt[d] = 0;
+    __syncthreads();
+    const uint64_t r0 = sb * SUB;
+    const uint32_t m = (uint32_t)min((uint64_t)SUB, n - r0);
+    KeyT<W> kv[IT];
+    double hv[IT];
+    uint32_t sv[IT], dr[IT];
+#pragma unroll
+    for (int u = 0; u < IT; u++) {
+      const uint32_t i = u * kRPT + t;
+      if (i < m) {
+        kv[u] = load_key<W>(keys, r0 + i);
+        hv[u] = hij[r0 + i];
+        sv[u] = src[r0 + i];
+        const uint32_t d = (uint32_t)(to_pi(kv[u]).w0 >> 56);
+        dr[u] = (d << 16) | atomicAdd(&cnt[d], 1u);
+      }
+    }
+    __syncthreads();
+    if (t < 32) {  // exclusive scan of the digit counts (8 per lane)
+      uint32_t c[R / 32], loc = 0;
+#pragma unroll
+      for (int j = 0; j < R / 32; j++) {
+        c[j] = cnt[t * (R / 32) + j];
+        loc += c[j];
+      }
+      uint32_t inc = loc;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, inc, o);
+        if ((int)t >= o) inc += y;
+      }
+      uint32_t ex = inc - loc;
+#pragma unroll
+      for (int j = 0; j < R / 32; j++) {
+        lst[t * (R / 32) + j] = ex;
+        ex += c[j];
+      }
+    }
+    if (t < R) {  // reserve this sub-round's run in region t
+      const uint32_t c = cnt[t];
+      unsigned long long b = c ? atomicAdd(&gcur[t], (unsigned long long)c) : 0ull;
+      if (c && b + c > rcap) {
+        *ovf = 1;
+        b = ~0ull;
+      }
+      dl[t] = c ? (b == ~0ull ? ~0ull : (unsigned long long)t * rcap + b) : ~0ull;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < IT; u++) {
+      const uint32_t i = u * kRPT + t;
+      if (i < m) {
+        const uint32_t d = dr[u] >> 16, p = lst[d] + (dr[u] & 0xffffu);
+        sk[p] = kv[u];
+        sh[p] = hv[u];
+        ss[p] = sv[u];
+        sd[p] = (uint8_t)d;
+      }
+    }
+    __syncthreads();
+    for (uint32_t j = t; j < m; j += kRPT) {  // runs of consecutive addresses per digit
+      const uint32_t d = sd[j];
+      const unsigned long long b = dl[d];
+      if (b != ~0ull) {
+        const uint64_t o = b + (j - lst[d]);
+        store_key<W>(okeys, o, sk[j]);
+        oh[o] = sh[j];
+        osrc[o] = ss[j];
+      }
+    }
+    __syncthreads();
+  }
 }
 
 __global__ void contract_finalize_kernel(const unsigned long long* __restrict__ acc, uint64_t n, double* __restrict__ e) {
@@ -369,8 +508,47 @@ template <int W>
 int contract_add_t(cusci_ctx* ctx, const CState& st, const uint64_t* keys, const double* hij, const uint32_t* src,
                    uint64_t n_rec) {
   if (!n_rec) return CUSCI_OK;
-  const unsigned g2 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_rec + kET - 1) / kET, (uint64_t)ctx->num_sms * 16));
-  CUSCI_LAUNCH(ctx, PT_ENERGY, contract_kernel<W><<<g2, kET, 0, ctx->stream>>>(keys, hij, src, n_rec, (const KPsi<W>*)st.table, st.tslots, st.k, st.n_parents, st.acc, st.flags));
+  const uint64_t tbytes = st.tslots * sizeof(KPsi<W>);
+  // Measured on one N2 batch (1.94e9 records, 4.24e8-key space, 17 GB table): the
+  // flat kernel reads ~150 DRAM bytes per record (a random probe pulls whole
+  // lines) and takes 73 ms; partitioned, the contraction reads 38 B per record
+  // (73 GB; the slices stay in L2) but becomes bound by its per-record integer
+  // work (65 ms) and the partition costs 35 ms -- so automatic mode keeps the
+  // flat kernel; CUSCI_OPT_CONTRACT_PARTITION = 1 selects the partitioned one.
+  (void)tbytes;
+  const bool part = ctx->contract_partition > 0;
+  if (!part) {
+    const unsigned g2 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_rec + kET - 1) / kET, (uint64_t)ctx->num_sms * 16));
+    CUSCI_LAUNCH(ctx, PT_ENERGY, contract_kernel<W><<<g2, kET, 0, ctx->stream>>>(keys, hij, src, n_rec, (const KPsi<W>*)st.table, st.tslots, st.k, st.n_parents, st.acc, st.flags, nullptr, 0, nullptr, nullptr, nullptr, nullptr, 0, nullptr));
+    return CUSCI_OK;
+  }
+  // pi-partitioned: regions of rcap slots (mean + 2% + 4 Ki, a multiple of 64)
+  Scratch s(ctx);
+  const uint64_t rcap = ((n_rec / 256 + n_rec / 256 / 50 + 4096) + 63) & ~63ull;
+  uint64_t* pk;
+  double* ph;
+  uint32_t* ps;
+  unsigned long long *gcur, *tick;
+  int* ovf;
+  CUSCI_TRY(s.get_t(256 * rcap * W, &pk));
+  CUSCI_TRY(s.get_t(1, &tick));
+  CUSCI_TRY(s.get_t(256 * rcap, &ph));
+  CUSCI_TRY(s.get_t(256 * rcap, &ps));
+  CUSCI_TRY(s.get_t(256, &gcur));
+  CUSCI_TRY(s.get_t(1, &ovf));
+  CUSCI_CUDA(ctx, cudaMemsetAsync(gcur, 0, 256 * sizeof(unsigned long long), ctx->stream));
+  CUSCI_CUDA(ctx, cudaMemsetAsync(ovf, 0, sizeof(int), ctx->stream));
+  CUSCI_CUDA(ctx, cudaMemsetAsync(tick, 0, sizeof(unsigned long long), ctx->stream));
+  int pper = 1, cper = 1;
+  CUSCI_TRY(kernel_setup(ctx, (const void*)rec_partition_kernel<W>, kRPT, RPCfg<W>::SMEM, &pper));
+  CUSCI_TRY(kernel_setup(ctx, (const void*)contract_kernel<W>, kET, 0, &cper));
+  const uint64_t nsub = (n_rec + RPCfg<W>::SUB - 1) / RPCfg<W>::SUB;
+  const unsigned gp = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(nsub, (uint64_t)ctx->num_sms * pper));
+  CUSCI_LAUNCH(ctx, PT_ENERGY, rec_partition_kernel<W><<<gp, kRPT, RPCfg<W>::SMEM, ctx->stream>>>(keys, hij, src, n_rec, rcap, gcur, pk, ph, ps, ovf));
+  // persistent grid: every warp sweeps the regions in step with the others, so
+  // the probes of the whole grid stay inside one or two table slices
+  const unsigned gc = (unsigned)(ctx->num_sms * std::max(1, cper));
+  CUSCI_LAUNCH(ctx, PT_ENERGY, contract_kernel<W><<<gc, kET, 0, ctx->stream>>>(pk, ph, ps, 256 * rcap, (const KPsi<W>*)st.table, st.tslots, st.k, st.n_parents, st.acc, st.flags, gcur, rcap, ovf, keys, hij, src, n_rec, tick));
   return CUSCI_OK;
 }
 

@@ -117,6 +117,7 @@ struct cusci_ctx {
   std::vector<cudaEvent_t> ev_free;
   std::vector<cusci::KSetup> ksetup;  // kernel_setup cache (this context's device)
   int force_collective = 0;           // CUSCI_OPT_FORCE_COLLECTIVE
+  int contract_partition = 0;         // CUSCI_OPT_CONTRACT_PARTITION: -1 off, 0 auto, 1 on
   std::string err;
 };
 

@@ -885,6 +885,29 @@ def test_contract_c2h4_w2(P, ctx):
     assert _contract_case(P, ctx, "c2h4", 4, 2, 4, keep_every=3) > 0
 
 
+@pytest.mark.parametrize("wl_key,n_par,W,keep_every", [("lih", None, 1, 1), ("h2o", 2000, 1, 1), ("h2o", 2000, 1, 3),
+                                                        ("c2h4", 6, 2, 3)])
+def test_contract_partitioned(P, ctx, wl_key, n_par, W, keep_every):
+    """the pi-partitioned contraction (records scattered into 256 regions first,
+    CUSCI_OPT_CONTRACT_PARTITION = 1) against the exact-sum definition, incl.
+    absent amplitudes; and bit-identical to the unpartitioned kernel"""
+    try:
+        ctx.contract_partition(1)
+        miss = _contract_case(P, ctx, wl_key, n_par, W, 11, keep_every=keep_every)
+        assert (miss > 0) == (keep_every > 1)
+        wl, ints, par = synth.workload_inputs(wl_key, n_parents=n_par)
+        sp = P.Space(wl.m, wl.n_alpha, wl.n_beta)
+        rec = ctx.gen_coupled(sp, torch.from_numpy(par).cuda(), P.DeviceIntegrals(ints.h, ints.eri), 0.0, with_src=True)
+        uniq = ctx.dedup_global(sp, rec.keys)
+        psi = torch.from_numpy(np.random.default_rng(5).uniform(-1, 1, uniq.shape[0])).cuda()
+        e1, m1 = ctx.energy_contract(sp, rec, len(par), uniq, psi)
+        ctx.contract_partition(-1)
+        e0, m0 = ctx.energy_contract(sp, rec, len(par), uniq, psi)
+        assert m0 == m1 and torch.equal(e0, e1)
+    finally:
+        ctx.contract_partition(0)
+
+
 def test_contract_rejects_bad_src(P, ctx):
     wl, ints, par = synth.workload_inputs("lih")
     sp = P.Space(wl.m, wl.n_alpha, wl.n_beta)
