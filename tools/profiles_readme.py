@@ -24,14 +24,14 @@ L = [f"## Round {int(tag[1:])}\n",
      f"* `{tag}_bench.json`: the bench line (CUDA events, {d['steps']} timed steps after {d['warmup']} warm-up, clocks sampled during the run).",
      f"* `{tag}_launches.csv`, `{tag}_n2_traffic.json`: every launch of the ncu-profiled step (time, DRAM bytes) and DRAM bytes per\n  launch per kernel class (read by `bench.py` as `traffic`).",
      f"* `{tag}_ncu_full_raw.csv`: raw counters of the five `--set full` captures (gen, both partition passes, bucket_unique, merge_tile).",
-     f"* `{tag}_sanitizer_{{memcheck,racecheck,synccheck,memcheck_large}}.log`: compute-sanitizer over every kernel path: 0 errors, 0 hazards.",
+     f"* `{tag}_sanitizer_{{memcheck,racecheck,synccheck,memcheck_large}}.log`: compute-sanitizer over every kernel path (mid-round-2 code, see Reading): 0 errors, 0 hazards.",
      f"* `{tag}_gpu_tests.log`, `{tag}_smoke.log`: the GPU test suite and the smoke run.",
      f"* `{tag}_{{eps,m120,c2h4,h2o}}_bench.json`: the other BASELINE configurations.\n",
      "### Bench line (N2 cc-pVDZ-like: 56 spin orbitals, 14 electrons, 10^6 parents, eps = 0)\n",
      f"* **{d['value']:.3g} coupled configs/s** ({d['ms_per_step']:.1f} ms/step, {d['config']['records_per_step']:,} records/step),",
      f"  **{d['unique_configs_per_s']:.3g} unique configs/s** ({d['config']['unique_per_step']:,} unique; redundancy {d['redundancy']:.3f});",
      f"  e2e through `stream_generate` from pinned host parents: {d['e2e']['value']:.3g}/s ({d['e2e']['ms_per_step']:.1f} ms/step).",
-     f"* Round history: 171.4 (round-1 start) → 105.2 (round-1 end) → 96.1 (round-2 start) → {d['ms_per_step']:.1f} ms/step.",
+     f"* Round history: 171.4 (round-1 start) → 105.2 (round-1 end) → 96.1 (round-2 start) → 92.4 (mid round 2) → {d['ms_per_step']:.1f} ms/step.",
      f"* `roofline` (headline): `{rf['kernel']}` at {rf['frac']:.3f} of the {rf['peak']:,.0f} GB/s measured copy peak ({rf['achieved']:,.0f} GB/s of algorithmic bytes;\n"
      f"  DRAM traffic {rf['traffic']/1e9:.2f} GB per launch vs {rf['alg_bytes_per_launch']/1e9:.2f} GB algorithmic).",
      f"* clocks {d['clocks']['sm_mhz']:.0f} MHz median under load (max {d['clocks']['sm_max_mhz']:.0f}), throttle reasons {d['clocks']['reasons']}; {d['gpu_launches']} library launches in the timed region.",
