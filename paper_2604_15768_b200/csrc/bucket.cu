@@ -681,10 +681,11 @@ __device__ __forceinline__ void cas_slot(KeyT<2>* slot, const KeyT<2>& k, KeyT<2
 // among themselves.
 //
 // Insertion: each round a thread loads ILP keys straight from global memory
-// (coalesced, all in flight together) and takes them through the FAST path:
-// one shared load of the home slot -- equal: duplicate; empty: one CAS (W = 2
-// probes with the 128-bit CAS itself).  Keys that miss (home held by another
-// key, a lost CAS) are appended BY VALUE to a per-warp queue (ballot
+// (coalesced, all in flight together; the first 128 KiB of the NEXT unit are
+// bulk-prefetched into L2 when a unit starts) and takes them through the FAST
+// path: one shared CAS of the home slot (64-bit at W = 1, 128-bit at W = 2)
+// -- it returns empty: inserted, equal: duplicate, anything else: a miss.
+// Keys that miss are appended BY VALUE to a per-warp queue (ballot
 // compaction); whenever 32 are queued the warp drains them with every lane
 // probing, so the divergent probe loop runs on full warps.
 // Output: occupancy words by warp ballots over 32-slot windows, one block scan
