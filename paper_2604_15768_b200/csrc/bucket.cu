@@ -704,6 +704,9 @@ __device__ __forceinline__ void cas_slot(KeyT<2>* slot, const KeyT<2>& k, KeyT<2
 #ifndef CUSCI_BU_ILP1
 #define CUSCI_BU_ILP1 4
 #endif
+#ifndef CUSCI_BU_DB
+#define CUSCI_BU_DB 1  // double-buffered insert rounds (10.03 -> 9.79 ms per N2 batch)
+#endif
 #ifndef CUSCI_BU_PF
 #define CUSCI_BU_PF 131072  // bytes of the next unit's input prefetched into L2 (0: off; 64 / 128 / 192 / 256 KiB: 10.24 / 10.04 / 10.06 / 10.63 ms vs 10.27 ms per N2 batch)
 #endif
@@ -921,15 +924,35 @@ __global__ void __launch_bounds__(kBU, 1024 / kBU) bucket_unique_kernel(const ui
       qn = q0;
       __syncwarp();
     };
+#if CUSCI_BU_DB
+    // double-buffered rounds: the next round's keys are loaded before this
+    // round's probes, so their latency overlaps the probing
+    K nx[ILP];
+#pragma unroll
+    for (int u = 0; u < ILP; u++) {
+      const uint32_t i = u * kBU + t;
+      if (i < nk) nx[u] = load_key<W>(part, kaddr(i));
+    }
+#endif
     for (uint32_t r0 = 0; r0 < nk; r0 += ILP * kBU) {
       K pv[ILP];
       bool act[ILP];
+#if CUSCI_BU_DB
+#pragma unroll
+      for (int u = 0; u < ILP; u++) {
+        act[u] = r0 + u * kBU + t < nk;
+        pv[u] = nx[u];
+        const uint32_t i = r0 + ILP * kBU + u * kBU + t;
+        if (i < nk) nx[u] = load_key<W>(part, kaddr(i));
+      }
+#else
 #pragma unroll
       for (int u = 0; u < ILP; u++) {
         const uint32_t i = r0 + u * kBU + t;
         act[u] = i < nk;
         if (act[u]) pv[u] = load_key<W>(part, kaddr(i));
       }
+#endif
 #pragma unroll
       for (int u = 0; u < ILP; u++) {
         bool slow = false;
